@@ -1,0 +1,250 @@
+/*
+ * walkforge_b200.h — C-ABI of the B200-native random-walk engine.
+ *
+ * Drop-in boundary for the reference's step-centric Gather–Move–Update path
+ * (walkforge, /root/reference/proj).  Every entry point below replaces one
+ * reference interface; the citation is on each declaration.  Plain pointers and
+ * sizes only — no C++ or torch types cross this line.  A header-only C++ shim
+ * with the reference's own template signatures sits on top of it
+ * (include/walkforge_b200/engine.hpp); a Python ctypes mirror lives in
+ * paper_2107_11983_b200/engine.py.
+ *
+ * Error model: every function returns a wf_status.  Status codes map 1:1 onto
+ * the reference exception classes (proj/include/walkforge/error.hpp:8-48); the
+ * message of the last failure on the calling thread is wf_last_error().
+ */
+#ifndef WALKFORGE_B200_H
+#define WALKFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WF_ABI_VERSION 1
+
+/* ---- status codes: proj/include/walkforge/error.hpp:8-48 ------------------ */
+typedef enum wf_status {
+    WF_OK = 0,
+    WF_ERR_PARSE = 1,         /* ParseError        error.hpp:14-16 */
+    WF_ERR_FORMAT = 2,        /* FormatError       error.hpp:19-21 */
+    WF_ERR_CONFIG = 3,        /* ConfigError       error.hpp:25-27 */
+    WF_ERR_DISTRIBUTION = 4,  /* DistributionError error.hpp:31-33 */
+    WF_ERR_CONTRACT = 5,      /* ContractError     error.hpp:36-38 */
+    WF_ERR_REJECTION_CAP = 6, /* RejectionCapError error.hpp:42-44 */
+    WF_ERR_IO = 7,            /* IoError           error.hpp:47-49 */
+    WF_ERR_CUDA = 8,          /* device fault / no device (no reference class) */
+    WF_ERR_OOM = 9,           /* device allocation failed */
+    WF_ERR_INVALID_ARG = 10   /* null handle / bad pointer at the ABI */
+} wf_status;
+
+/* ---- enums mirrored from the reference ------------------------------------ */
+/* SamplerKind, proj/include/walkforge/sampler.hpp:21 */
+typedef enum wf_sampler {
+    WF_SAMPLER_DEFAULT = -1, /* resolve_default_sampler, program.hpp:68-75 */
+    WF_SAMPLER_NAIVE = 0,
+    WF_SAMPLER_ITS = 1,
+    WF_SAMPLER_ALIAS = 2,
+    WF_SAMPLER_REJ = 3,
+    WF_SAMPLER_OREJ = 4
+} wf_sampler;
+
+/* The built-in programs, proj/include/walkforge/algorithms.hpp:20-193 */
+typedef enum wf_program_kind {
+    WF_PROGRAM_PPR = 0,      /* PprProgram       algorithms.hpp:20-37   */
+    WF_PROGRAM_DEEPWALK = 1, /* DeepWalkProgram  algorithms.hpp:41-67   */
+    WF_PROGRAM_NODE2VEC = 2, /* Node2VecProgram  algorithms.hpp:79-133  */
+    WF_PROGRAM_METAPATH = 3, /* MetaPathProgram  algorithms.hpp:141-173 */
+    WF_PROGRAM_UNIFORM = 4   /* UniformProgram   algorithms.hpp:177-193 */
+} wf_program_kind;
+
+/* WalkStatus, proj/include/walkforge/walker.hpp:12 (0 complete, 1 dead end) */
+typedef enum wf_walk_status { WF_WALK_COMPLETE = 0, WF_WALK_DEAD_END = 1 } wf_walk_status;
+
+/* QuerySpec::Mode, proj/include/walkforge/walker.hpp:61-84 */
+typedef enum wf_query_mode {
+    WF_QUERY_ONE_PER_VERTEX = 0,
+    WF_QUERY_FROM_SOURCE = 1,
+    WF_QUERY_FROM_LIST = 2 /* QuerySpec::from_file after parsing: explicit sources */
+} wf_query_mode;
+
+/* ---- plain-data descriptors ----------------------------------------------- */
+
+/* One program and its constructor arguments.  Validation follows each
+ * reference constructor (e.g. PprProgram: termination in (0, 1],
+ * algorithms.hpp:22-27; Node2Vec a, b > 0 finite, algorithms.hpp:81-96). */
+typedef struct wf_program_desc {
+    int32_t kind;           /* wf_program_kind */
+    uint32_t target_length; /* DeepWalk / Node2Vec / Uniform: vertices per walk */
+    int32_t weighted;       /* DeepWalk / Node2Vec: scale by edge weight */
+    int32_t reserved0;
+    double termination;     /* PPR stop probability */
+    double a;               /* Node2Vec return parameter */
+    double b;               /* Node2Vec in-out parameter */
+    const uint32_t* schema; /* MetaPath label schema (host pointer) */
+    uint32_t schema_len;
+    uint32_t reserved1;
+} wf_program_desc;
+
+/* ExecOptions, proj/include/walkforge/engine.hpp:81-89.  `threads` is the
+ * reference's worker count; on the device it is ignored (lanes replace
+ * workers).  k / k_prime (interleave ring sizes, interleave.hpp:391-393) are
+ * accepted and validated like the reference, then used as launch hints. */
+typedef struct wf_exec_options {
+    uint64_t seed;
+    int32_t sampler;           /* wf_sampler */
+    int32_t use_static_tables; /* default 1 */
+    uint32_t rej_trial_cap;    /* default 1<<20 (sampler.hpp:27) */
+    uint32_t threads;
+    uint32_t k;
+    uint32_t k_prime;
+    uint32_t path_stride;      /* device row capacity for unbounded walks (0 = auto) */
+    uint32_t reserved;
+} wf_exec_options;
+
+typedef struct wf_query_spec {
+    int32_t mode; /* wf_query_mode */
+    uint32_t source;
+    uint64_t count;
+    const uint32_t* sources; /* FROM_LIST: host or device pointer, `count` entries */
+} wf_query_spec;
+
+/* RunMetrics, proj/include/walkforge/engine.hpp:64-69 */
+typedef struct wf_run_metrics {
+    double preprocess_seconds;
+    double exec_seconds;
+    uint64_t total_steps;
+    uint32_t max_in_flight;
+    uint32_t reserved;
+} wf_run_metrics;
+
+typedef struct wf_graph_info {
+    uint32_t vertex_count;
+    uint32_t max_degree_lo; /* max degree fits in 32 bits (graph.cpp:165-168) */
+    uint64_t edge_count;
+    double max_weight;      /* 0 when unweighted (graph.hpp:56) */
+    int32_t has_weights;
+    int32_t has_labels;
+    int32_t adjacency_sorted;
+    int32_t device;
+    uint32_t label_count; /* max label + 1 (0 if unlabeled) */
+    uint32_t reserved;
+} wf_graph_info;
+
+/* Synthetic R-MAT generator (ingest; SURVEY §8 d).  Symmetrised,
+ * de-duplicated, self-loops dropped, sorted adjacency.  Weights f32 =
+ * synthetic_weight(seed, e) rounded to f32 and labels = synthetic_label(seed,
+ * e, label_count), keyed on the final CSR edge index like the reference's
+ * synthetic attributes (graph.cpp:279-287, synthetic.cpp:11-39). */
+typedef struct wf_rmat_params {
+    uint32_t scale;
+    uint32_t edge_factor;
+    double a, b, c; /* d = 1 - a - b - c */
+    uint64_t seed;
+    int32_t weighted;
+    uint32_t label_count; /* 0 = unlabeled */
+} wf_rmat_params;
+
+typedef struct wf_graph wf_graph;     /* device-resident CSR (Graph, graph.hpp:17-107) */
+typedef struct wf_session wf_session; /* program + resolved sampler + static tables (ResolvedRun, engine.hpp:275-294) */
+typedef struct wf_walkset wf_walkset; /* WalkSet + RunMetrics (engine.hpp:71-74, walker.hpp:47-55) */
+
+/* ---- library ---------------------------------------------------------------- */
+int wf_abi_version(void);
+const char* wf_last_error(void);
+/* Number of engine kernel launches since load (evidence for bench's gpu_launches). */
+uint64_t wf_kernel_launches(void);
+
+/* ---- graph residency: Graph::from_csr, graph.cpp:118-159 ---------------------
+ * Validates like from_csr (monotone offsets, ids in range, finite non-negative
+ * weights, matching lengths) and uploads.  Host pointers.  weights/labels may
+ * be NULL (absent).  Labels must be < 256 (stored as u8 on the device). */
+int wf_graph_create(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
+                    const uint32_t* labels, uint32_t vertex_count, uint64_t edge_count, int device,
+                    wf_graph** out);
+/* Same from DEVICE pointers (already resident, e.g. torch tensors); copies. */
+int wf_graph_create_device(const uint64_t* offsets, const uint32_t* neighbors,
+                           const float* weights, const uint8_t* labels, uint32_t vertex_count,
+                           uint64_t edge_count, int device, wf_graph** out);
+int wf_graph_generate_rmat(const wf_rmat_params* params, int device, wf_graph** out);
+int wf_graph_info_get(const wf_graph* g, wf_graph_info* out);
+/* Copies CSR arrays back to HOST buffers (any may be NULL to skip). */
+int wf_graph_download(const wf_graph* g, uint64_t* offsets, uint32_t* neighbors, float* weights,
+                      uint8_t* labels);
+/* Membership test, Graph::has_edge (graph.cpp:182-188), batched on the device. */
+int wf_graph_has_edge(const wf_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                      uint8_t* out);
+void wf_graph_destroy(wf_graph* g);
+
+/* ---- sessions: ResolvedRun (engine.hpp:275-294) ------------------------------
+ * Resolves the sampler (program default or override), checks the
+ * program/sampler pairing (resolve_flow, engine.hpp:255-272), and builds the
+ * static tables on the device (preprocess_static, engine.hpp:190-251). */
+int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_exec_options* opts,
+                      wf_session** out);
+/* Resolved sampler and flow (0 Direct, 1 Tables, 2 Gathered). */
+int wf_session_describe(const wf_session* s, int32_t* sampler, int32_t* flow,
+                        double* preprocess_seconds);
+void wf_session_destroy(wf_session* s);
+
+/* Runs every query of `spec` (run_sequential / run_interleaved,
+ * engine.hpp:440-504, interleave.hpp:391-556 — identical outputs).  Result
+ * owned by the returned walkset (device memory). */
+int wf_session_run(wf_session* s, const wf_query_spec* spec, wf_walkset** out,
+                   wf_run_metrics* metrics);
+
+/* Low-level launch into caller-owned DEVICE buffers on a caller stream (bench
+ * and streaming paths).  Queries [qid_begin, qid_end) of `spec`.
+ *   paths   u32[(qid_end-qid_begin) * stride]   row r = query qid_begin + r
+ *   lengths u32[(qid_end-qid_begin)]            true path length (may exceed stride)
+ *   status  u8 [(qid_end-qid_begin)]            wf_walk_status
+ *   visit_counts u32[V] or NULL                 += occurrences of each vertex
+ *   steps_out u64[1] or NULL                    += moves (device counter)
+ * Rows whose walk outgrows `stride` hold the first `stride` vertices; their
+ * count is accumulated in overflow_out (u64, device, may be NULL).  Async: no
+ * host synchronisation; errors flagged on the device surface at the next
+ * wf_session_sync. */
+int wf_session_launch(wf_session* s, const wf_query_spec* spec, uint64_t qid_begin,
+                      uint64_t qid_end, uint32_t* paths, uint32_t stride, uint32_t* lengths,
+                      uint8_t* status, uint32_t* visit_counts, unsigned long long* steps_out,
+                      unsigned long long* overflow_out, void* stream);
+/* Synchronises `stream` and raises any device-side error (RejectionCapError,
+ * ContractError) recorded by launches since the last sync. */
+int wf_session_sync(wf_session* s, void* stream);
+
+/* ---- walk sets: WalkSet (walker.hpp:47-55) -------------------------------- */
+int wf_walkset_info(const wf_walkset* w, uint64_t* n_queries, uint64_t* total_vertices,
+                    uint32_t* max_length);
+/* Ragged copy-out of queries [qid_begin, qid_end): offsets u64[n+1] (relative
+ * to the first), vertices u32[sum], status u8[n].  HOST or DEVICE pointers
+ * (detected); any may be NULL. */
+int wf_walkset_copy(const wf_walkset* w, uint64_t qid_begin, uint64_t qid_end, uint64_t* offsets,
+                    uint32_t* vertices, uint8_t* status);
+/* Occurrences of each vertex over all paths (sources included): u32[V]. */
+int wf_walkset_visit_counts(const wf_walkset* w, uint32_t* counts);
+void wf_walkset_destroy(wf_walkset* w);
+
+/* ---- convenience: run_sequential in one call -------------------------------- */
+int wf_run(const wf_graph* g, const wf_program_desc* prog, const wf_query_spec* spec,
+           const wf_exec_options* opts, wf_walkset** out, wf_run_metrics* metrics);
+
+/* ---- device RNG probes (RngStream, rng.hpp:19-67), for parity tests --------- */
+/* out[i*draws + j] = j-th next_u64() of RngStream(seed, streams[i]) */
+int wf_rng_probe(uint64_t seed, const uint64_t* streams, uint64_t n_streams, uint32_t draws,
+                 uint64_t* out);
+
+/* ---- static tables probe (preprocess_static, engine.hpp:190-251) -------------
+ * Copies the session's ALIAS buckets to HOST: thr u64[E] = ceil(split*2^53),
+ * first_dst/second_dst u32[E]; exhausted u8[V].  ITS: cumulative f64[E]. REJ:
+ * p_star f64[V]. Pointers may be NULL to skip. */
+int wf_session_tables(const wf_session* s, uint64_t* alias_thr, uint32_t* alias_first_dst,
+                      uint32_t* alias_second_dst, double* its_cumulative, double* rej_p_star,
+                      uint8_t* exhausted);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WALKFORGE_B200_H */

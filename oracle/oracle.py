@@ -1,0 +1,332 @@
+"""TEST INFRASTRUCTURE — ctypes front-ends for the two CPU checkers.
+
+* ``RefOracle``  — the UNMODIFIED reference engine (oracle/_ref/libwfref.so, built
+  by ``make -C oracle ref`` from /root/reference/proj sources + ref_harness.cpp).
+* ``PortOracle`` — the plain-C restatement (oracle/liboracle.so, wf_oracle.c).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from paper_2107_11983_b200.abi import RunMetricsC, raise_for
+from paper_2107_11983_b200.host import (ExecOptions, Graph, QuerySpec, RunMetrics, RunResult,
+                                        WalkSet)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_LIB = os.path.join(HERE, "_ref", "libwfref.so")
+PORT_LIB = os.path.join(HERE, "liboracle.so")
+
+_u64p = C.POINTER(C.c_uint64)
+_u32p = C.POINTER(C.c_uint32)
+_u8p = C.POINTER(C.c_uint8)
+_f64p = C.POINTER(C.c_double)
+_f32p = C.POINTER(C.c_float)
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_LIB)
+
+
+class _WfoGraph(C.Structure):
+    _fields_ = [("offsets", _u64p), ("neighbors", _u32p), ("weights", _f32p),
+                ("labels", _u8p), ("vertex_count", C.c_uint32), ("edge_count", C.c_uint64)]
+
+
+class _WfoResult(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("offsets", _u64p), ("vertices", _u32p), ("status", _u8p),
+                ("total_steps", C.c_uint64), ("exec_seconds", C.c_double),
+                ("preprocess_seconds", C.c_double)]
+
+
+class PortOracle:
+    """The C restatement (wf_oracle.c)."""
+
+    def __init__(self, path: str = PORT_LIB):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        lib = C.CDLL(path)
+        lib.wfo_run.restype = C.c_int
+        lib.wfo_static_tables.restype = C.c_int
+        lib.wfo_alias_init.restype = C.c_int
+        self.lib = lib
+
+    def _graph(self, g: Graph) -> _WfoGraph:
+        cg = _WfoGraph()
+        cg.offsets = _ptr(g.offsets, _u64p)
+        cg.neighbors = _ptr(g.neighbors, _u32p)
+        cg.weights = _ptr(g.weights, _f32p)
+        cg.labels = _ptr(g.labels, _u8p)
+        cg.vertex_count = g.vertex_count
+        cg.edge_count = g.edge_count
+        return cg
+
+    def rng_probe(self, seed: int, stream: int, draws: int) -> np.ndarray:
+        out = np.zeros(draws, dtype=np.uint64)
+        self.lib.wfo_rng_probe(C.c_uint64(seed), C.c_uint64(stream), C.c_uint32(draws),
+                               _ptr(out, _u64p))
+        return out
+
+    def rng_index_real(self, seed, stream, n, bound):
+        idx = C.c_uint32()
+        real = C.c_double()
+        self.lib.wfo_rng_index_real(C.c_uint64(seed), C.c_uint64(stream), C.c_uint32(n),
+                                    C.c_double(bound), C.byref(idx), C.byref(real))
+        return idx.value, real.value
+
+    def alias_init(self, weights):
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        n = w.size
+        split = np.zeros(n, np.float64)
+        first = np.zeros(n, np.uint32)
+        second = np.zeros(n, np.uint32)
+        err = C.create_string_buffer(256)
+        rc = self.lib.wfo_alias_init(_ptr(w, _f64p), C.c_uint32(n), _ptr(split, _f64p),
+                                     _ptr(first, _u32p), _ptr(second, _u32p), err, 256)
+        raise_for(rc, err.value.decode())
+        return split, first, second
+
+    def run(self, g: Graph, spec: QuerySpec, prog, opts: ExecOptions,
+            qids: Optional[np.ndarray] = None, threads: int = 1, discard: bool = False) -> RunResult:
+        cg = self._graph(g)
+        desc = prog.to_c()
+        cspec = spec.to_c()
+        copts = opts.to_c()
+        res = _WfoResult()
+        err = C.create_string_buffer(256)
+        q = None if qids is None else np.ascontiguousarray(qids, dtype=np.uint64)
+        rc = self.lib.wfo_run(C.byref(cg), C.byref(desc), C.byref(cspec), C.byref(copts),
+                              _ptr(q, _u64p), C.c_uint64(0 if q is None else q.size),
+                              C.c_int(threads), C.c_int(1 if discard else 0), C.byref(res),
+                              err, 256)
+        raise_for(rc, err.value.decode())
+        try:
+            n = res.n
+            metrics = RunMetrics(res.preprocess_seconds, res.exec_seconds, res.total_steps, 1)
+            if discard:
+                ws = WalkSet(np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.uint8))
+            else:
+                offsets = np.ctypeslib.as_array(res.offsets, shape=(n + 1,)).copy()
+                verts = (np.ctypeslib.as_array(res.vertices, shape=(int(offsets[-1]),)).copy()
+                         if offsets[-1] else np.zeros(0, np.uint32))
+                status = (np.ctypeslib.as_array(res.status, shape=(n,)).copy()
+                          if n else np.zeros(0, np.uint8))
+                ws = WalkSet(offsets, verts, status, q)
+        finally:
+            self.lib.wfo_result_free(C.byref(res))
+        return RunResult(ws, metrics)
+
+    def static_tables(self, g: Graph, prog, sampler: int):
+        v, e = g.vertex_count, g.edge_count
+        out = dict(alias_split=np.zeros(e, np.float64), alias_first_dst=np.zeros(e, np.uint32),
+                   alias_second_dst=np.zeros(e, np.uint32), its=np.zeros(e, np.float64),
+                   rej_p_star=np.zeros(v, np.float64), exhausted=np.zeros(v, np.uint8))
+        cg = self._graph(g)
+        desc = prog.to_c()
+        err = C.create_string_buffer(256)
+        rc = self.lib.wfo_static_tables(C.byref(cg), C.byref(desc), C.c_int(sampler),
+                                        _ptr(out["alias_split"], _f64p),
+                                        _ptr(out["alias_first_dst"], _u32p),
+                                        _ptr(out["alias_second_dst"], _u32p),
+                                        _ptr(out["its"], _f64p), _ptr(out["rej_p_star"], _f64p),
+                                        _ptr(out["exhausted"], _u8p), err, 256)
+        raise_for(rc, err.value.decode())
+        return out
+
+
+class RefOracle:
+    """The unmodified reference, through oracle/_ref/libwfref.so."""
+
+    def __init__(self, path: str = REF_LIB):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where "
+                                    "/root/reference is mounted")
+        lib = C.CDLL(path)
+        lib.wfref_last_error.restype = C.c_char_p
+        lib.wfref_synthetic_weight.restype = C.c_double
+        lib.wfref_synthetic_label.restype = C.c_uint32
+        lib.wfref_hardware_threads.restype = C.c_uint
+        self.lib = lib
+
+    def _check(self, rc):
+        raise_for(rc, (self.lib.wfref_last_error() or b"").decode())
+
+    # -- graphs ------------------------------------------------------------------
+    def graph(self, g: Graph) -> "RefGraph":
+        w64 = None if g.weights is None else g.weights.astype(np.float64)
+        lab = None if g.labels is None else g.labels.astype(np.uint32)
+        h = C.c_void_p()
+        self._check(self.lib.wfref_graph_create(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
+                                                _ptr(w64, _f64p), _ptr(lab, _u32p),
+                                                C.c_uint32(g.vertex_count),
+                                                C.c_uint64(g.edge_count), C.byref(h)))
+        return RefGraph(self, h)
+
+    def power_law(self, vertex_count, edge_count, seed, exponent=0.8, weighted=False,
+                  label_count=0) -> "RefGraph":
+        h = C.c_void_p()
+        self._check(self.lib.wfref_graph_power_law(C.c_uint32(vertex_count),
+                                                   C.c_uint64(edge_count), C.c_double(exponent),
+                                                   C.c_uint64(seed), C.c_int(int(weighted)),
+                                                   C.c_uint32(label_count), C.byref(h)))
+        return RefGraph(self, h)
+
+    def ring(self, n, seed=0, weighted=False, label_count=0) -> "RefGraph":
+        h = C.c_void_p()
+        self._check(self.lib.wfref_graph_ring(C.c_uint32(n), C.c_uint64(seed),
+                                              C.c_int(int(weighted)), C.c_uint32(label_count),
+                                              C.byref(h)))
+        return RefGraph(self, h)
+
+    def build(self, vertex_count, edges, weights=None, labels=None) -> "RefGraph":
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint32)
+        h = C.c_void_p()
+        self._check(self.lib.wfref_graph_build(C.c_uint32(vertex_count), _ptr(e, _u32p),
+                                               C.c_uint64(e.shape[0]), _ptr(w, _f64p),
+                                               _ptr(lab, _u32p), C.byref(h)))
+        return RefGraph(self, h)
+
+    # -- RNG ---------------------------------------------------------------------
+    def rng_probe(self, seed, stream, draws):
+        out = np.zeros(draws, dtype=np.uint64)
+        self.lib.wfref_rng_probe(C.c_uint64(seed), C.c_uint64(stream), C.c_uint32(draws),
+                                 _ptr(out, _u64p))
+        return out
+
+    def rng_index_real(self, seed, stream, n, bound):
+        idx = C.c_uint32()
+        real = C.c_double()
+        self.lib.wfref_rng_index_real(C.c_uint64(seed), C.c_uint64(stream), C.c_uint32(n),
+                                      C.c_double(bound), C.byref(idx), C.byref(real))
+        return idx.value, real.value
+
+    def alias_init(self, weights):
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        n = w.size
+        split = np.zeros(n, np.float64)
+        first = np.zeros(n, np.uint32)
+        second = np.zeros(n, np.uint32)
+        self._check(self.lib.wfref_alias_init(_ptr(w, _f64p), C.c_uint32(n), _ptr(split, _f64p),
+                                              _ptr(first, _u32p), _ptr(second, _u32p)))
+        return split, first, second
+
+    def synthetic_weight(self, seed, edge):
+        return self.lib.wfref_synthetic_weight(C.c_uint64(seed), C.c_uint64(edge))
+
+    def synthetic_label(self, seed, edge, count):
+        return self.lib.wfref_synthetic_label(C.c_uint64(seed), C.c_uint64(edge),
+                                              C.c_uint32(count))
+
+    def hardware_threads(self) -> int:
+        return int(self.lib.wfref_hardware_threads())
+
+
+class RefGraph:
+    def __init__(self, ref: RefOracle, handle: C.c_void_p):
+        self.ref = ref
+        self.h = handle
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ref.lib.wfref_graph_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self):
+        v = C.c_uint32()
+        e = C.c_uint64()
+        hw = C.c_int()
+        hl = C.c_int()
+        md = C.c_uint64()
+        mw = C.c_double()
+        so = C.c_int()
+        self.ref.lib.wfref_graph_info(self.h, C.byref(v), C.byref(e), C.byref(hw), C.byref(hl),
+                                      C.byref(md), C.byref(mw), C.byref(so))
+        return dict(V=v.value, E=e.value, has_weights=bool(hw.value), has_labels=bool(hl.value),
+                    max_degree=md.value, max_weight=mw.value, sorted=bool(so.value))
+
+    def export(self):
+        """CSR arrays (weights f64, labels u32) as the reference holds them."""
+        i = self.info()
+        off = np.zeros(i["V"] + 1, np.uint64)
+        nbr = np.zeros(i["E"], np.uint32)
+        w = np.zeros(i["E"], np.float64) if i["has_weights"] else None
+        lab = np.zeros(i["E"], np.uint32) if i["has_labels"] else None
+        self.ref.lib.wfref_graph_export(self.h, _ptr(off, _u64p), _ptr(nbr, _u32p),
+                                        _ptr(w, _f64p), _ptr(lab, _u32p))
+        return off, nbr, w, lab
+
+    def has_edge(self, u, v) -> bool:
+        return bool(self.ref.lib.wfref_has_edge(self.h, C.c_uint32(u), C.c_uint32(v)))
+
+    def _collect(self, h, metrics: RunMetricsC, qids_given) -> RunResult:
+        lib = self.ref.lib
+        n = C.c_uint64()
+        tv = C.c_uint64()
+        lib.wfref_result_info(h, C.byref(n), C.byref(tv))
+        qids = np.zeros(n.value, np.uint64)
+        offsets = np.zeros(n.value + 1, np.uint64)
+        verts = np.zeros(tv.value, np.uint32)
+        status = np.zeros(n.value, np.uint8)
+        lib.wfref_result_copy(h, _ptr(qids, _u64p), _ptr(offsets, _u64p), _ptr(verts, _u32p),
+                              _ptr(status, _u8p))
+        lib.wfref_result_destroy(h)
+        m = RunMetrics(metrics.preprocess_seconds, metrics.exec_seconds, metrics.total_steps,
+                       metrics.max_in_flight)
+        return RunResult(WalkSet(offsets, verts, status, qids), m)
+
+    def run(self, spec: QuerySpec, prog, opts: ExecOptions, interleaved: bool = False,
+            discard: bool = False) -> RunResult:
+        desc = prog.to_c()
+        cspec = spec.to_c()
+        copts = opts.to_c()
+        h = C.c_void_p()
+        m = RunMetricsC()
+        self.ref._check(self.ref.lib.wfref_run(self.h, C.byref(desc), C.byref(cspec),
+                                               C.byref(copts), C.c_int(int(interleaved)),
+                                               C.c_int(int(discard)), C.byref(h), C.byref(m)))
+        return self._collect(h, m, None)
+
+    def run_qids(self, spec: QuerySpec, prog, opts: ExecOptions, qids) -> RunResult:
+        desc = prog.to_c()
+        cspec = spec.to_c()
+        copts = opts.to_c()
+        q = np.ascontiguousarray(qids, dtype=np.uint64)
+        h = C.c_void_p()
+        m = RunMetricsC()
+        self.ref._check(self.ref.lib.wfref_run_qids(self.h, C.byref(desc), C.byref(cspec),
+                                                    C.byref(copts), _ptr(q, _u64p),
+                                                    C.c_uint64(q.size), C.byref(h), C.byref(m)))
+        return self._collect(h, m, q)
+
+    def static_tables(self, prog, sampler: int):
+        i = self.info()
+        e, v = i["E"], i["V"]
+        out = dict(alias_split=np.zeros(e, np.float64), alias_first=np.zeros(e, np.uint32),
+                   alias_second=np.zeros(e, np.uint32), alias_first_dst=np.zeros(e, np.uint32),
+                   alias_second_dst=np.zeros(e, np.uint32), its=np.zeros(e, np.float64),
+                   rej_p_star=np.zeros(v, np.float64), exhausted=np.zeros(v, np.uint8))
+        secs = C.c_double()
+        desc = prog.to_c()
+        self.ref._check(self.ref.lib.wfref_static_tables(
+            self.h, C.byref(desc), C.c_int(sampler), _ptr(out["alias_split"], _f64p),
+            _ptr(out["alias_first"], _u32p), _ptr(out["alias_second"], _u32p),
+            _ptr(out["alias_first_dst"], _u32p), _ptr(out["alias_second_dst"], _u32p),
+            _ptr(out["its"], _f64p), _ptr(out["rej_p_star"], _f64p), _ptr(out["exhausted"], _u8p),
+            C.byref(secs)))
+        out["seconds"] = secs.value
+        return out
