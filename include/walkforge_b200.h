@@ -214,6 +214,20 @@ int wf_session_launch(wf_session* s, const wf_query_spec* spec, uint64_t qid_beg
  * ContractError) recorded by launches since the last sync. */
 int wf_session_sync(wf_session* s, void* stream);
 
+/* Runs every query of `spec` and streams the walk set straight into HOST
+ * buffers (the reference returns RunResult::walks in host memory,
+ * engine.hpp:448-452, or streams blocks to a BlockSink, engine.hpp:76-79):
+ *   offsets  u64[n+1]   path of query i = vertices[offsets[i] .. offsets[i+1])
+ *   vertices u32[vertices_capacity]
+ *   status   u8[n]
+ * Queries run in chunks of `chunk_queries` (0 = auto); chunk k's walks are
+ * compacted and copied to the host while chunk k+1 runs.  Pinned host memory
+ * gives full copy bandwidth.  A FROM_LIST spec takes a HOST source list.
+ * WF_ERR_INVALID_ARG if the walks need more than vertices_capacity entries. */
+int wf_session_run_host(wf_session* s, const wf_query_spec* spec, uint64_t* offsets,
+                        uint32_t* vertices, uint64_t vertices_capacity, uint8_t* status,
+                        uint64_t chunk_queries, wf_run_metrics* metrics);
+
 /* ---- walk sets: WalkSet (walker.hpp:47-55) -------------------------------- */
 int wf_walkset_info(const wf_walkset* w, uint64_t* n_queries, uint64_t* total_vertices,
                     uint32_t* max_length);

@@ -1,0 +1,628 @@
+// extern "C" boundary (include/walkforge_b200.h).  Every entry point catches
+// wf::Error and maps it to a wf_status + wf_last_error(); nothing here falls
+// back to the CPU: without a device every call fails with WF_ERR_CUDA.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "runtime.hpp"
+
+using namespace wf;
+
+struct wf_graph {
+    std::unique_ptr<GraphStore> g;
+};
+struct wf_session {
+    std::unique_ptr<Session> s;
+    DeviceBuffer<unsigned long long> counters;  // steps, overflow
+};
+struct wf_walkset {
+    std::unique_ptr<WalkSetStore> w;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return WF_OK;
+    } catch (const wf::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return WF_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return WF_ERR_INVALID_ARG;
+    }
+}
+
+void require(bool ok, const char* what) {
+    if (!ok) raise(WF_ERR_INVALID_ARG, what);
+}
+
+const char* type_name(int t) {
+    return t == kUnbiased ? "unbiased" : (t == kStatic ? "static" : "dynamic");
+}
+
+int walker_type(int prog) {
+    switch (prog) {
+        case WF_PROGRAM_PPR:
+        case WF_PROGRAM_UNIFORM: return kUnbiased;
+        case WF_PROGRAM_DEEPWALK: return kStatic;
+        default: return kDynamic;
+    }
+}
+
+std::string fmt_double(double x) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%f", x);
+    return buf;
+}
+
+// Program constructors' validation (algorithms.hpp:22-27, 43-51, 81-96,
+// 143-160, 179-182) and the resolved run (resolve_default_sampler,
+// program.hpp:68-75; resolve_flow, engine.hpp:255-272; resolve_orej_bound,
+// engine.hpp:103-114).
+void resolve_program(Session& s, const wf_program_desc& d, const wf_exec_options* o) {
+    GraphStore& g = *s.g;
+    ProgParams& p = s.params;
+    p = ProgParams{};
+    s.desc = d;
+    bool has_max_weight = true;
+    switch (d.kind) {
+        case WF_PROGRAM_PPR:
+            if (!(d.termination > 0.0 && d.termination <= 1.0))
+                config_error("termination probability must be in (0, 1], got " + fmt_double(d.termination));
+            p.stop_thr = unit_threshold(d.termination);
+            p.bound = 1.0;
+            s.unbounded = true;
+            break;
+        case WF_PROGRAM_DEEPWALK:
+            if (d.target_length < 1) config_error("target length must be >= 1");
+            if (d.weighted && !g.has_weights()) config_error("weighted walks need a graph with edge weights");
+            p.length = d.target_length;
+            p.weighted = d.weighted ? 1 : 0;
+            p.bound = d.weighted ? g.max_weight : 1.0;
+            break;
+        case WF_PROGRAM_NODE2VEC: {
+            if (!(std::isfinite(d.a) && d.a > 0.0)) config_error("return parameter a must be positive and finite");
+            if (!(std::isfinite(d.b) && d.b > 0.0)) config_error("in-out parameter b must be positive and finite");
+            if (d.target_length < 1) config_error("target length must be >= 1");
+            if (d.weighted && !g.has_weights()) config_error("weighted walks need a graph with edge weights");
+            p.length = d.target_length;
+            p.weighted = d.weighted ? 1 : 0;
+            p.inv_a = 1.0 / d.a;
+            p.inv_b = 1.0 / d.b;
+            p.first = std::max({p.inv_a, 1.0, p.inv_b});
+            p.bound = d.weighted ? p.first * g.max_weight : p.first;
+            p.lo_w = std::min(1.0, p.inv_b);
+            p.hi_w = std::max(1.0, p.inv_b);
+            break;
+        }
+        case WF_PROGRAM_METAPATH: {
+            if (!g.has_labels()) config_error("meta-path walks need a graph with edge labels");
+            if (d.schema_len == 0 || d.schema == nullptr) config_error("meta-path schema must be non-empty");
+            s.schema.assign(d.schema, d.schema + d.schema_len);
+            for (uint32_t l : s.schema)
+                if (l > 255 || !g.label_present[l])
+                    config_error("schema label " + std::to_string(l) + " does not occur in the graph");
+            s.schema_dev.allocate(s.schema.size());
+            WF_CUDA(cudaMemcpy(s.schema_dev.get(), s.schema.data(), s.schema.size() * 4, cudaMemcpyHostToDevice));
+            p.schema = s.schema_dev.get();
+            p.schema_len = d.schema_len;
+            has_max_weight = false;
+            break;
+        }
+        case WF_PROGRAM_UNIFORM:
+            if (d.target_length < 1) config_error("target length must be >= 1");
+            p.length = d.target_length;
+            p.bound = 1.0;
+            break;
+        default:
+            config_error("unknown program kind " + std::to_string(d.kind));
+    }
+    s.desc.schema = nullptr;
+    const int type = walker_type(d.kind);
+    int kind = o && o->sampler >= 0 ? o->sampler
+               : d.kind == WF_PROGRAM_NODE2VEC ? WF_SAMPLER_OREJ
+               : type == kUnbiased ? WF_SAMPLER_NAIVE
+               : type == kStatic ? WF_SAMPLER_ALIAS : WF_SAMPLER_ITS;
+    if (kind < WF_SAMPLER_NAIVE || kind > WF_SAMPLER_OREJ) config_error("unknown sampler");
+    const bool use_tables = o ? o->use_static_tables != 0 : true;
+    int flow;
+    if (kind == WF_SAMPLER_NAIVE) {
+        if (type != kUnbiased)
+            config_error(std::string("NAIVE assumes a uniform distribution; the program is ") + type_name(type));
+        flow = kDirect;
+    } else if (kind == WF_SAMPLER_OREJ) {
+        flow = kDirect;
+    } else if (type == kDynamic) {
+        flow = kGathered;
+    } else {
+        flow = use_tables ? kTables : kGathered;
+    }
+    s.kind = kind;
+    s.flow = flow;
+    s.trial_cap = o && o->rej_trial_cap ? o->rej_trial_cap : (1u << 20);
+    s.seed = o ? o->seed : 0;
+    if (kind == WF_SAMPLER_OREJ) {
+        if (!has_max_weight) config_error("O-REJ needs a program with max_weight()");
+        if (!std::isfinite(p.bound) || p.bound <= 0.0)
+            raise(WF_ERR_CONTRACT, "max_weight() must be positive and finite");
+    }
+    if (o && (o->k != 0 || o->k_prime != 0)) {  // interleave.hpp:395-400
+        if (o->k == 0) config_error("task ring size must be >= 1");
+        if (o->k_prime == 0 || o->k_prime > o->k) config_error("search ring size must be in [1, k]");
+    }
+    // row capacity: fixed-length programs hold their whole walk
+    uint32_t fixed = d.kind == WF_PROGRAM_METAPATH ? d.schema_len + 1
+                     : d.kind == WF_PROGRAM_PPR ? 0 : d.target_length;
+    if (fixed) s.default_stride = fixed;
+    else s.default_stride = o && o->path_stride ? o->path_stride : 64;
+}
+
+struct ResolvedSpec {
+    wf_query_spec spec{};
+    uint64_t n = 0;
+    DeviceBuffer<uint32_t> sources;
+    const uint32_t* dev_sources = nullptr;
+};
+
+// QuerySpec::total + validate (walker.cpp:80-109), sources made device-resident.
+void resolve_spec(const GraphStore& g, const wf_query_spec* q, ResolvedSpec& r) {
+    require(q != nullptr, "null query spec");
+    r.spec = *q;
+    switch (q->mode) {
+        case WF_QUERY_ONE_PER_VERTEX:
+            r.n = g.V;
+            break;
+        case WF_QUERY_FROM_SOURCE:
+            if (q->source >= g.V)
+                config_error("query source " + std::to_string(q->source) + " is not a vertex (V=" +
+                             std::to_string(g.V) + ")");
+            r.n = q->count;
+            break;
+        case WF_QUERY_FROM_LIST: {
+            r.n = q->count;
+            if (r.n == 0) break;
+            require(q->sources != nullptr, "null source list");
+            std::vector<uint32_t> host;
+            const uint32_t* hp = q->sources;
+            if (is_device_pointer(q->sources)) {
+                host.resize(r.n);
+                WF_CUDA(cudaMemcpy(host.data(), q->sources, r.n * 4, cudaMemcpyDeviceToHost));
+                hp = host.data();
+                r.dev_sources = q->sources;
+            }
+            for (uint64_t i = 0; i < r.n; ++i)
+                if (hp[i] >= g.V)
+                    config_error("query source " + std::to_string(hp[i]) + " is not a vertex (V=" +
+                                 std::to_string(g.V) + ")");
+            if (!r.dev_sources) {
+                r.sources.allocate(r.n);
+                WF_CUDA(cudaMemcpy(r.sources.get(), q->sources, r.n * 4, cudaMemcpyHostToDevice));
+                r.dev_sources = r.sources.get();
+            }
+            break;
+        }
+        default:
+            config_error("unknown query mode");
+    }
+}
+
+void check_device_error(Session& s) {
+    int h = 0;
+    WF_CUDA(cudaMemcpy(&h, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
+    if (h != 0) {
+        WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
+        if (h == WF_ERR_REJECTION_CAP)
+            raise(h, "rejection sampling exceeded " + std::to_string(s.trial_cap) +
+                         " trials; asserted bound does not match the weights");
+        raise(h, "device-side contract violation");
+    }
+}
+
+__global__ void k_rng_probe(uint64_t premixed, const uint64_t* streams, uint64_t n, uint32_t draws,
+                            uint64_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        Rng r{stream_state(premixed, streams[i])};
+        for (uint32_t j = 0; j < draws; ++j) out[i * draws + j] = r.next();
+    }
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ x, uint64_t n, unsigned* out) {
+    unsigned m = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        m = max(m, x[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+int current_device() {
+    int d = 0;
+    WF_CUDA(cudaGetDevice(&d));
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wf_abi_version(void) { return WF_ABI_VERSION; }
+const char* wf_last_error(void) { return g_last_error.c_str(); }
+uint64_t wf_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int wf_graph_create(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
+                    const uint32_t* labels, uint32_t vertex_count, uint64_t edge_count, int device,
+                    wf_graph** out) {
+    return guarded([&] {
+        require(out && offsets && (neighbors || edge_count == 0), "null argument");
+        auto h = std::make_unique<wf_graph>();
+        h->g.reset(graph_from_host(offsets, neighbors, weights, labels, vertex_count, edge_count,
+                                   device < 0 ? current_device() : device));
+        *out = h.release();
+    });
+}
+
+int wf_graph_create_device(const uint64_t* offsets, const uint32_t* neighbors,
+                           const float* weights, const uint8_t* labels, uint32_t vertex_count,
+                           uint64_t edge_count, int device, wf_graph** out) {
+    return guarded([&] {
+        require(out && offsets && (neighbors || edge_count == 0), "null argument");
+        auto h = std::make_unique<wf_graph>();
+        h->g.reset(graph_from_device(offsets, neighbors, weights, labels, vertex_count, edge_count,
+                                     device < 0 ? current_device() : device));
+        *out = h.release();
+    });
+}
+
+int wf_graph_generate_rmat(const wf_rmat_params* params, int device, wf_graph** out) {
+    return guarded([&] {
+        require(out && params, "null argument");
+        auto h = std::make_unique<wf_graph>();
+        h->g.reset(graph_generate_rmat(*params, device < 0 ? current_device() : device));
+        *out = h.release();
+    });
+}
+
+int wf_graph_info_get(const wf_graph* g, wf_graph_info* out) {
+    return guarded([&] {
+        require(g && out, "null argument");
+        const GraphStore& s = *g->g;
+        std::memset(out, 0, sizeof(*out));
+        out->vertex_count = s.V;
+        out->edge_count = s.E;
+        out->max_degree_lo = s.max_degree;
+        out->max_weight = s.max_weight;
+        out->has_weights = s.has_weights();
+        out->has_labels = s.has_labels();
+        out->adjacency_sorted = s.sorted;
+        out->device = s.device;
+        out->label_count = s.label_count;
+    });
+}
+
+int wf_graph_download(const wf_graph* g, uint64_t* offsets, uint32_t* neighbors, float* weights,
+                      uint8_t* labels) {
+    return guarded([&] {
+        require(g != nullptr, "null graph");
+        const GraphStore& s = *g->g;
+        DeviceGuard guard(s.device);
+        if (offsets) WF_CUDA(cudaMemcpy(offsets, s.offsets.get(), (s.V + 1ull) * 8, cudaMemcpyDefault));
+        if (neighbors && s.E) WF_CUDA(cudaMemcpy(neighbors, s.nbr.get(), s.E * 4, cudaMemcpyDefault));
+        if (weights && s.has_weights() && s.E)
+            WF_CUDA(cudaMemcpy(weights, s.weights.get(), s.E * 4, cudaMemcpyDefault));
+        if (labels && s.has_labels() && s.E)
+            WF_CUDA(cudaMemcpy(labels, s.labels.get(), s.E, cudaMemcpyDefault));
+    });
+}
+
+int wf_graph_has_edge(const wf_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                      uint8_t* out) {
+    return guarded([&] {
+        require(g && src && dst && out, "null argument");
+        if (n) graph_has_edge(*g->g, src, dst, n, out);
+    });
+}
+
+void wf_graph_destroy(wf_graph* g) {
+    if (g) {
+        DeviceGuard guard(g->g->device);
+        delete g;
+    }
+}
+
+int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_exec_options* opts,
+                      wf_session** out) {
+    return guarded([&] {
+        require(g && prog && out, "null argument");
+        DeviceGuard guard(g->g->device);
+        auto h = std::make_unique<wf_session>();
+        h->s = std::make_unique<Session>();
+        Session& s = *h->s;
+        s.g = g->g.get();
+        resolve_program(s, *prog, opts);
+        s.error_word.allocate(1);
+        WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
+        s.cursor.allocate(1);
+        h->counters.allocate(2);
+        if (s.flow == kTables) s.build_tables(nullptr);
+        if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) s.g->ensure_label_index(nullptr);
+        s.grid = occupancy_grid(s);
+        *out = h.release();
+    });
+}
+
+int wf_session_describe(const wf_session* s, int32_t* sampler, int32_t* flow,
+                        double* preprocess_seconds) {
+    return guarded([&] {
+        require(s != nullptr, "null session");
+        if (sampler) *sampler = s->s->kind;
+        if (flow) *flow = s->s->flow;
+        if (preprocess_seconds) *preprocess_seconds = s->s->preprocess_seconds;
+    });
+}
+
+void wf_session_destroy(wf_session* s) {
+    if (s) {
+        DeviceGuard guard(s->s->g->device);
+        delete s;
+    }
+}
+
+int wf_session_launch(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin,
+                      uint64_t qid_end, uint32_t* paths, uint32_t stride, uint32_t* lengths,
+                      uint8_t* status, uint32_t* visit_counts, unsigned long long* steps_out,
+                      unsigned long long* overflow_out, void* stream) {
+    return guarded([&] {
+        require(sh && spec && paths && lengths && status, "null argument");
+        Session& s = *sh->s;
+        DeviceGuard guard(s.g->device);
+        require(spec->mode != WF_QUERY_FROM_LIST || is_device_pointer(spec->sources),
+                "wf_session_launch needs a device-resident source list");
+        if (spec->mode == WF_QUERY_FROM_SOURCE && spec->source >= s.g->V)
+            config_error("query source " + std::to_string(spec->source) + " is not a vertex");
+        unsigned long long* steps = steps_out ? steps_out : sh->counters.get();
+        unsigned long long* over = overflow_out ? overflow_out : sh->counters.get() + 1;
+        launch_walk(s, *spec, spec->sources, qid_begin, qid_end, nullptr, paths, stride, lengths,
+                    status, visit_counts, steps, over, s.cursor.get(),
+                    static_cast<cudaStream_t>(stream));
+    });
+}
+
+int wf_session_sync(wf_session* sh, void* stream) {
+    return guarded([&] {
+        require(sh != nullptr, "null session");
+        DeviceGuard guard(sh->s->g->device);
+        WF_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        check_device_error(*sh->s);
+    });
+}
+
+int wf_session_run(wf_session* sh, const wf_query_spec* spec, wf_walkset** out,
+                   wf_run_metrics* metrics) {
+    return guarded([&] {
+        require(sh && spec && out, "null argument");
+        Session& s = *sh->s;
+        GraphStore& g = *s.g;
+        DeviceGuard guard(g.device);
+        ResolvedSpec rs;
+        resolve_spec(g, spec, rs);
+        auto wh = std::make_unique<wf_walkset>();
+        wh->w = std::make_unique<WalkSetStore>();
+        WalkSetStore& w = *wh->w;
+        w.device = g.device;
+        w.n = rs.n;
+        w.V = g.V;
+        w.stride = s.default_stride;
+        w.paths.allocate(std::max<uint64_t>(w.n * w.stride, 1));
+        w.lengths.allocate(std::max<uint64_t>(w.n, 1));
+        w.status.allocate(std::max<uint64_t>(w.n, 1));
+        const bool counts = s.desc.kind == WF_PROGRAM_PPR;
+        if (counts) {
+            w.visit_counts.allocate(g.V);
+            WF_CUDA(cudaMemset(w.visit_counts.get(), 0, g.V * 4ull));
+        }
+        unsigned long long* ctr = sh->counters.get();
+        WF_CUDA(cudaMemset(ctr, 0, 16));
+        cudaEvent_t e0, e1;
+        WF_CUDA(cudaEventCreate(&e0));
+        WF_CUDA(cudaEventCreate(&e1));
+        WF_CUDA(cudaEventRecord(e0, nullptr));
+        launch_walk(s, rs.spec, rs.dev_sources, 0, w.n, nullptr, w.paths.get(), w.stride,
+                    w.lengths.get(), w.status.get(), counts ? w.visit_counts.get() : nullptr, ctr,
+                    ctr + 1, s.cursor.get(), nullptr);
+        WF_CUDA(cudaEventRecord(e1, nullptr));
+        WF_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        WF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        check_device_error(s);
+        unsigned long long hc[2] = {0, 0};
+        WF_CUDA(cudaMemcpy(hc, ctr, 16, cudaMemcpyDeviceToHost));
+        if (hc[1] > 0) {
+            // re-run the walks that outgrew their row; same (seed, qid) streams
+            std::vector<uint32_t> lens(w.n);
+            WF_CUDA(cudaMemcpy(lens.data(), w.lengths.get(), w.n * 4, cudaMemcpyDeviceToHost));
+            std::vector<uint64_t> qids;
+            uint32_t mx = 0;
+            for (uint64_t r = 0; r < w.n; ++r)
+                if (lens[r] > w.stride) {
+                    w.over_rows.push_back(r);
+                    qids.push_back(r);
+                    mx = std::max(mx, lens[r]);
+                }
+            w.over_stride = mx;
+            DeviceBuffer<uint64_t> dq(qids.size());
+            WF_CUDA(cudaMemcpy(dq.get(), qids.data(), qids.size() * 8, cudaMemcpyHostToDevice));
+            w.over_paths.allocate(qids.size() * static_cast<uint64_t>(mx));
+            DeviceBuffer<uint32_t> tl(qids.size());
+            DeviceBuffer<uint8_t> ts(qids.size());
+            DeviceBuffer<unsigned long long> tc(2);
+            WF_CUDA(cudaMemset(tc.get(), 0, 16));
+            launch_walk(s, rs.spec, rs.dev_sources, 0, qids.size(), dq.get(), w.over_paths.get(), mx,
+                        tl.get(), ts.get(), nullptr, tc.get(), tc.get() + 1, s.cursor.get(), nullptr);
+            WF_CUDA(cudaDeviceSynchronize());
+            check_device_error(s);
+        }
+        w.metrics.preprocess_seconds = s.preprocess_seconds;
+        w.metrics.exec_seconds = ms * 1e-3;
+        w.metrics.total_steps = hc[0];
+        w.metrics.max_in_flight = static_cast<uint32_t>(
+            std::min<uint64_t>(static_cast<uint64_t>(s.grid) * kBlock, std::max<uint64_t>(w.n, 1)));
+        w.total_vertices = w.n + hc[0];
+        if (w.n) {
+            DeviceBuffer<unsigned> m(1);
+            WF_CUDA(cudaMemset(m.get(), 0, 4));
+            k_max_u32<<<256, 256>>>(w.lengths.get(), w.n, m.get());
+            WF_LAUNCHED();
+            WF_CUDA(cudaMemcpy(&w.max_length, m.get(), 4, cudaMemcpyDeviceToHost));
+        }
+        if (metrics) *metrics = w.metrics;
+        *out = wh.release();
+    });
+}
+
+int wf_session_run_host(wf_session* sh, const wf_query_spec* spec, uint64_t* offsets,
+                        uint32_t* vertices, uint64_t vertices_capacity, uint8_t* status,
+                        uint64_t chunk_queries, wf_run_metrics* metrics) {
+    return guarded([&] {
+        require(sh && spec && vertices, "null argument");
+        Session& s = *sh->s;
+        GraphStore& g = *s.g;
+        DeviceGuard guard(g.device);
+        uint64_t n = spec->mode == WF_QUERY_ONE_PER_VERTEX ? g.V : spec->count;
+        if (spec->mode == WF_QUERY_FROM_SOURCE && spec->source >= g.V)
+            config_error("query source " + std::to_string(spec->source) + " is not a vertex (V=" +
+                         std::to_string(g.V) + ")");
+        if (spec->mode == WF_QUERY_FROM_LIST) {
+            require(spec->sources != nullptr || n == 0, "null source list");
+            require(!is_device_pointer(spec->sources), "wf_session_run_host takes a host source list");
+            for (uint64_t i = 0; i < n; ++i)
+                if (spec->sources[i] >= g.V)
+                    config_error("query source " + std::to_string(spec->sources[i]) +
+                                 " is not a vertex (V=" + std::to_string(g.V) + ")");
+        }
+        run_to_host(s, *spec, spec->sources, n, offsets, vertices, vertices_capacity, status,
+                    chunk_queries, metrics);
+    });
+}
+
+int wf_walkset_info(const wf_walkset* w, uint64_t* n_queries, uint64_t* total_vertices,
+                    uint32_t* max_length) {
+    return guarded([&] {
+        require(w != nullptr, "null walkset");
+        if (n_queries) *n_queries = w->w->n;
+        if (total_vertices) *total_vertices = w->w->total_vertices;
+        if (max_length) *max_length = w->w->max_length;
+    });
+}
+
+int wf_walkset_copy(const wf_walkset* w, uint64_t qid_begin, uint64_t qid_end, uint64_t* offsets,
+                    uint32_t* vertices, uint8_t* status) {
+    return guarded([&] {
+        require(w != nullptr, "null walkset");
+        walkset_copy(*w->w, qid_begin, qid_end, offsets, vertices, status);
+    });
+}
+
+int wf_walkset_visit_counts(const wf_walkset* wh, uint32_t* counts) {
+    return guarded([&] {
+        require(wh && counts, "null argument");
+        const WalkSetStore& w = *wh->w;
+        DeviceGuard guard(w.device);
+        const bool dev = is_device_pointer(counts);
+        if (w.visit_counts.get()) {
+            WF_CUDA(cudaMemcpy(counts, w.visit_counts.get(), w.V * 4ull, cudaMemcpyDefault));
+            return;
+        }
+        DeviceBuffer<uint32_t> tmp;
+        uint32_t* dc = counts;
+        if (!dev) {
+            tmp.allocate(w.V);
+            dc = tmp.get();
+        }
+        walkset_visit_counts(w, dc, nullptr);
+        WF_CUDA(cudaDeviceSynchronize());
+        if (!dev) WF_CUDA(cudaMemcpy(counts, dc, w.V * 4ull, cudaMemcpyDeviceToHost));
+    });
+}
+
+void wf_walkset_destroy(wf_walkset* w) {
+    if (w) {
+        DeviceGuard guard(w->w->device);
+        delete w;
+    }
+}
+
+int wf_run(const wf_graph* g, const wf_program_desc* prog, const wf_query_spec* spec,
+           const wf_exec_options* opts, wf_walkset** out, wf_run_metrics* metrics) {
+    wf_session* s = nullptr;
+    int rc = guarded([&] {
+        require(g && spec, "null argument");
+        ResolvedSpec rs;
+        resolve_spec(*g->g, spec, rs);  // run_sequential validates the spec first (engine.hpp:443)
+    });
+    if (rc != WF_OK) return rc;
+    rc = wf_session_create(g, prog, opts, &s);
+    if (rc != WF_OK) return rc;
+    rc = wf_session_run(s, spec, out, metrics);
+    wf_session_destroy(s);
+    return rc;
+}
+
+int wf_rng_probe(uint64_t seed, const uint64_t* streams, uint64_t n_streams, uint32_t draws,
+                 uint64_t* out) {
+    return guarded([&] {
+        require(streams && out, "null argument");
+        if (!n_streams || !draws) return;
+        DeviceBuffer<uint64_t> ds(n_streams), dout(n_streams * draws);
+        WF_CUDA(cudaMemcpy(ds.get(), streams, n_streams * 8, cudaMemcpyHostToDevice));
+        k_rng_probe<<<64, 256>>>(seed_premix(seed), ds.get(), n_streams, draws, dout.get());
+        WF_LAUNCHED();
+        WF_CUDA(cudaMemcpy(out, dout.get(), n_streams * draws * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int wf_session_tables(const wf_session* sh, uint64_t* alias_thr, uint32_t* alias_first_dst,
+                      uint32_t* alias_second_dst, double* its_cumulative, double* rej_p_star,
+                      uint8_t* exhausted) {
+    return guarded([&] {
+        require(sh != nullptr, "null session");
+        const Session& s = *sh->s;
+        const GraphStore& g = *s.g;
+        DeviceGuard guard(g.device);
+        if (s.alias.get() && (alias_thr || alias_first_dst || alias_second_dst)) {
+            std::vector<uint4> b(g.E);
+            WF_CUDA(cudaMemcpy(b.data(), s.alias.get(), g.E * 16, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < g.E; ++i) {
+                if (alias_thr) alias_thr[i] = (static_cast<uint64_t>(b[i].y) << 32) | b[i].x;
+                if (alias_first_dst) alias_first_dst[i] = b[i].z;
+                if (alias_second_dst) alias_second_dst[i] = b[i].w;
+            }
+        }
+        if (s.its.get() && its_cumulative)
+            WF_CUDA(cudaMemcpy(its_cumulative, s.its.get(), g.E * 8, cudaMemcpyDeviceToHost));
+        if (s.rej.get() && rej_p_star)
+            WF_CUDA(cudaMemcpy(rej_p_star, s.rej.get(), g.V * 8ull, cudaMemcpyDeviceToHost));
+        if (s.exhausted.get() && exhausted)
+            WF_CUDA(cudaMemcpy(exhausted, s.exhausted.get(), g.V, cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"

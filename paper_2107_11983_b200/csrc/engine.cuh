@@ -1,0 +1,555 @@
+// Device side of the walk engine: graph view, the built-in programs as
+// templated device functors, the samplers, and the persistent step kernel.
+//
+// Reference map (paths under /root/reference/proj):
+//   GraphView            include/walkforge/graph.hpp:17-107 (CSR) + packed vertex words
+//   Program<K>           include/walkforge/algorithms.hpp:20-193 via the WalkProgram
+//                        concept (program.hpp:49-93): weight / update / finished / max_weight
+//   move<P,S,F>          StepDriver::step, engine.hpp:342-426 (Direct / Tables / Gathered)
+//   walk_kernel          run_sequential / run_interleaved (engine.hpp:440-504,
+//                        interleave.hpp:391-556): a lane per walker, a global
+//                        atomic query cursor refilling lanes (the GPU analogue of
+//                        admit/refill, interleave.hpp:436-456, 531-538).
+#pragma once
+
+#include <cstdint>
+
+#include "rng.cuh"
+
+namespace wf {
+
+constexpr uint32_t kDegBits = 24;
+constexpr uint32_t kDegEscape = (1u << kDegBits) - 1;  // degree >= this: read offsets
+constexpr int kBlock = 256;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kMaxIndexedLabels = 6;  // 32 B label record: u64 base + 6 u32 group ends
+
+enum Flow : int { kDirect = 0, kTables = 1, kGathered = 2 };
+enum WalkerTypeE : int { kUnbiased = 0, kStatic = 1, kDynamic = 2 };  // program.hpp:17
+enum MoveResult : int { kDead = 0, kMoved = 1, kFault = 2 };
+
+struct GraphView {
+    uint32_t V;
+    uint64_t E;
+    const uint64_t* __restrict__ offsets;  // V+1
+    const uint32_t* __restrict__ nbr;      // E, sorted per vertex when `sorted`
+    const float* __restrict__ weights;     // E or null
+    const uint8_t* __restrict__ labels;    // E or null
+    const uint64_t* __restrict__ vword;    // V: base << 24 | min(deg, escape)
+    int sorted;
+    // MetaPath label index (label-partitioned CSR): per vertex 32 B
+    // {u64 base, u32 end[6]} and the stably partitioned neighbour array.
+    const uint4* __restrict__ lab_rec;
+    const uint32_t* __restrict__ lab_nbr;
+    uint32_t label_count;
+};
+
+struct ProgParams {
+    uint64_t stop_thr;  // PPR: ceil(termination * 2^53)
+    uint32_t length;    // DeepWalk / Node2Vec / Uniform target length
+    int weighted;
+    double inv_a, inv_b, first, bound;  // Node2Vec (algorithms.hpp:87-90)
+    double lo_w, hi_w;                  // min/max(1, 1/b): lazy O-REJ thresholds
+    const uint32_t* __restrict__ schema;  // MetaPath (device copy)
+    uint32_t schema_len;
+};
+
+struct WalkLaunch {
+    GraphView g;
+    const uint64_t* __restrict__ sview;  // sampling vertex words (exhausted -> degree 0)
+    const uint4* __restrict__ alias;     // {thr lo, thr hi, first_dst, second_dst} per edge
+    const double* __restrict__ its;      // cumulative per edge
+    const double* __restrict__ rej_pstar;  // per vertex
+    ProgParams prog;
+    int qmode;
+    uint32_t qsource;
+    const uint32_t* __restrict__ qsources;
+    uint64_t qid_begin;
+    const uint64_t* __restrict__ qid_map;  // optional: row -> qid (overflow re-runs)
+    uint64_t n_rows;
+    uint64_t seed_mixed;
+    uint32_t trial_cap;
+    uint32_t stride;
+    uint32_t* __restrict__ paths;
+    uint32_t* __restrict__ lengths;
+    uint8_t* __restrict__ status;
+    uint32_t* __restrict__ visit_counts;
+    unsigned long long* steps_out;
+    unsigned long long* overflow_out;
+    unsigned long long* cursor;
+    int* error_word;
+    double* scratch;  // gathered ALIAS: per-lane park area
+    uint64_t scratch_stride;
+    int use_label_index;
+};
+
+struct Walker {
+    uint64_t row;
+    Rng rng;
+    uint64_t cur_base;
+    uint64_t prev_base;
+    uint32_t cur, prev;
+    uint32_t cur_deg, prev_deg;
+    uint32_t len;  // vertices on the path so far (moves + 1)
+};
+
+// ---- graph helpers -------------------------------------------------------------
+
+__device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t* vw, uint32_t v,
+                                              uint64_t& base, uint32_t& deg) {
+    uint64_t w = __ldg(vw + v);
+    base = w >> kDegBits;
+    deg = static_cast<uint32_t>(w & kDegEscape);
+    if (deg == kDegEscape) {  // rare: very high degree
+        base = __ldg(g.offsets + v);
+        deg = static_cast<uint32_t>(__ldg(g.offsets + v + 1) - base);
+    }
+}
+
+// Graph::has_edge (graph.cpp:182-188): std::binary_search on sorted lists,
+// linear scan otherwise.  Membership only, so any exact search is equivalent.
+__device__ __forceinline__ bool has_edge(const GraphView& g, uint64_t base, uint32_t deg,
+                                         uint32_t dst) {
+    const uint32_t* ns = g.nbr + base;
+    if (g.sorted) {
+        uint32_t lo = 0, hi = deg;
+        while (lo < hi) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(ns + mid) < dst) lo = mid + 1; else hi = mid;
+        }
+        return lo < deg && __ldg(ns + lo) == dst;
+    }
+    for (uint32_t i = 0; i < deg; ++i)
+        if (__ldg(ns + i) == dst) return true;
+    return false;
+}
+
+// cumulative_upper_index, sampler.hpp:48-60.
+__device__ __forceinline__ uint32_t upper_index(const double* cum, uint32_t n, double x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (x < __ldg(cum + mid)) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// ---- programs: the WalkProgram concept as device functors ------------------------
+// weight(q, e): q-dependent weight (gathered / O-REJ flows); weight_static(e):
+// weight(nullptr, e) for static contexts (program.hpp:39-42).
+
+template <int K>
+struct Program;
+
+template <>
+struct Program<WF_PROGRAM_PPR> {  // algorithms.hpp:20-37
+    static constexpr int type = kUnbiased;
+    static constexpr bool prechecked = false;
+    static constexpr bool has_max_weight = true;
+    __device__ static double weight(const ProgParams&, const GraphView&, const Walker&, uint64_t) {
+        return 1.0;
+    }
+    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
+        return 1.0;
+    }
+    // update draws the stop coin: uniform_real(1.0) < stop (algorithms.hpp:31)
+    __device__ static bool update(const ProgParams& p, Walker& q) {
+        return q.rng.bits53() < p.stop_thr;
+    }
+    __device__ static bool finished(const ProgParams&, const Walker&) { return false; }
+};
+
+template <>
+struct Program<WF_PROGRAM_UNIFORM> {  // algorithms.hpp:177-193
+    static constexpr int type = kUnbiased;
+    static constexpr bool prechecked = true;
+    static constexpr bool has_max_weight = true;
+    __device__ static double weight(const ProgParams&, const GraphView&, const Walker&, uint64_t) {
+        return 1.0;
+    }
+    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
+        return 1.0;
+    }
+    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len >= p.length; }
+    __device__ static bool finished(const ProgParams& p, const Walker& q) { return q.len >= p.length; }
+};
+
+template <>
+struct Program<WF_PROGRAM_DEEPWALK> {  // algorithms.hpp:41-67
+    static constexpr int type = kStatic;
+    static constexpr bool prechecked = true;
+    static constexpr bool has_max_weight = true;
+    __device__ static double weight_static(const ProgParams& p, const GraphView& g, uint64_t e) {
+        return p.weighted ? static_cast<double>(__ldg(g.weights + e)) : 1.0;
+    }
+    __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker&,
+                                    uint64_t e) {
+        return weight_static(p, g, e);
+    }
+    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len >= p.length; }
+    __device__ static bool finished(const ProgParams& p, const Walker& q) { return q.len >= p.length; }
+};
+
+template <>
+struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
+    static constexpr int type = kDynamic;
+    static constexpr bool prechecked = true;
+    static constexpr bool has_max_weight = true;
+    __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker& q,
+                                    uint64_t e) {  // algorithms.hpp:103-119
+        double w;
+        if (q.len == 1) {
+            w = p.first;
+        } else {
+            uint32_t dst = __ldg(g.nbr + e);
+            if (dst == q.prev) w = p.inv_a;
+            else if (has_edge(g, q.prev_base, q.prev_deg, dst)) w = 1.0;
+            else w = p.inv_b;
+        }
+        return p.weighted ? __dmul_rn(w, static_cast<double>(__ldg(g.weights + e))) : w;
+    }
+    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
+        return 0.0;  // never called: dynamic programs have no static tables
+    }
+    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len >= p.length; }
+    __device__ static bool finished(const ProgParams& p, const Walker& q) { return q.len >= p.length; }
+};
+
+template <>
+struct Program<WF_PROGRAM_METAPATH> {  // algorithms.hpp:141-173
+    static constexpr int type = kDynamic;
+    static constexpr bool prechecked = true;
+    static constexpr bool has_max_weight = false;
+    __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker& q,
+                                    uint64_t e) {  // algorithms.hpp:164-166
+        return static_cast<uint32_t>(__ldg(g.labels + e)) == __ldg(p.schema + (q.len - 1)) ? 1.0
+                                                                                          : 0.0;
+    }
+    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
+        return 0.0;
+    }
+    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len - 1 >= p.schema_len; }
+    __device__ static bool finished(const ProgParams& p, const Walker& q) {
+        return q.len - 1 >= p.schema_len;
+    }
+};
+
+// ---- samplers ------------------------------------------------------------------
+
+// O-REJ accept test (rej_generate, sampler.hpp:152-164 with the program weight
+// evaluated lazily, engine.hpp:356-364).  Node2Vec evaluates only as much of
+// its weight as y needs: every weight out of a vertex lies in {1/a, 1, 1/b}
+// (times w_e when weighted) so y below / above the candidates decides without
+// the adjacency search.  Same accept decisions, same draws — bit-exact.
+template <int K>
+__device__ __forceinline__ bool orej_accept(const WalkLaunch& L, const Walker& q, uint64_t e,
+                                            double y) {
+    return y < Program<K>::weight(L.prog, L.g, q, e);
+}
+
+template <>
+__device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunch& L,
+                                                                 const Walker& q, uint64_t e,
+                                                                 double y) {
+    const ProgParams& p = L.prog;
+    double ew = p.weighted ? static_cast<double>(__ldg(L.g.weights + e)) : 1.0;
+    auto scaled = [&](double w) { return p.weighted ? __dmul_rn(w, ew) : w; };
+    if (q.len == 1) return y < scaled(p.first);
+    uint32_t dst = __ldg(L.g.nbr + e);
+    if (dst == q.prev) return y < scaled(p.inv_a);
+    if (y < scaled(p.lo_w)) return true;
+    if (!(y < scaled(p.hi_w))) return false;
+    bool common = has_edge(L.g, q.prev_base, q.prev_deg, dst);
+    return y < scaled(common ? 1.0 : p.inv_b);
+}
+
+__device__ __forceinline__ void raise_device(const WalkLaunch& L, int code) {
+    atomicCAS(L.error_word, 0, code);
+}
+
+// Vose's alias construction (sampler.hpp:89-120) for ONE bucket x, over the
+// weights produced by wfn(i), without the FIFO worklists: the small queue is
+// [initial smalls ascending] ++ [larges in demotion order] and larges are
+// demoted in ascending order, so three ascending cursors replay it exactly.
+// Demoted larges park their final scaled value in park[] until consumed.
+// Returns split of bucket x and its alias index (x itself when none).
+template <typename WFn>
+__device__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double* park,
+                            double& split_out, uint32_t& second_out) {
+    auto scaled = [&](uint32_t i) { return wfn(i) * n / sum; };
+    uint32_t a = 0;        // next initial-small candidate
+    uint32_t c = 0;        // next demoted-large candidate (trails the large cursor)
+    uint32_t demoted = 0;  // larges demoted so far
+    uint32_t consumed_demoted = 0;
+    uint32_t lcur = 0;     // current large
+    auto next_large = [&](uint32_t from) {
+        while (from < n && !(scaled(from) >= 1.0)) ++from;
+        return from;
+    };
+    auto next_small = [&](uint32_t from) {
+        while (from < n && !(scaled(from) < 1.0)) ++from;
+        return from;
+    };
+    lcur = next_large(0);
+    double lval = lcur < n ? scaled(lcur) : 0.0;
+    a = next_small(0);
+    while (lcur < n) {
+        uint32_t s;
+        double sval;
+        if (a < n) {
+            s = a;
+            sval = scaled(a);
+            a = next_small(a + 1);
+        } else if (consumed_demoted < demoted) {
+            c = next_large(c);
+            s = c;
+            sval = park[c];
+            c += 1;
+            consumed_demoted += 1;
+        } else {
+            break;
+        }
+        if (s == x) {
+            split_out = sval;
+            second_out = lcur;
+            return;
+        }
+        lval -= 1.0 - sval;
+        if (lval < 1.0) {
+            park[lcur] = lval;
+            demoted += 1;
+            lcur = next_large(lcur + 1);
+            if (lcur < n) lval = scaled(lcur);
+        }
+    }
+    split_out = 1.0;  // leftover: probability exactly 1, no alias (sampler.hpp:112-119)
+    second_out = x;
+}
+
+// One move: StepDriver::step (engine.hpp:342-426).  Draw order per sampler is
+// the reference contract (engine.hpp:330-333): NAIVE x; ITS x_real; ALIAS x
+// then y; REJ / O-REJ (x, y) per trial; dead ends consume no draws.
+template <int K, int S, int F>
+__device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& dst) {
+    using P = Program<K>;
+    const uint32_t d = q.cur_deg;
+    const uint64_t base = q.cur_base;
+    if (d == 0) return kDead;
+    uint32_t pick = 0;
+    if constexpr (F == kDirect) {
+        if constexpr (S == WF_SAMPLER_NAIVE) {
+            pick = q.rng.index(d);
+        } else {  // O-REJ
+            uint32_t t = 0;
+            for (;; ++t) {
+                if (t >= L.trial_cap) {
+                    raise_device(L, WF_ERR_REJECTION_CAP);
+                    return kFault;
+                }
+                uint32_t x = q.rng.index(d);
+                double y = q.rng.real(L.prog.bound);
+                if (orej_accept<K>(L, q, base + x, y)) { pick = x; break; }
+            }
+        }
+    } else if constexpr (F == kTables) {
+        if constexpr (S == WF_SAMPLER_ALIAS) {
+            uint32_t x = q.rng.index(d);
+            uint4 b = __ldg(L.alias + base + x);
+            uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
+            dst = q.rng.bits53() < thr ? b.z : b.w;  // y < split <=> k < ceil(split 2^53)
+            return kMoved;
+        } else if constexpr (S == WF_SAMPLER_ITS) {
+            const double* cum = L.its + base;
+            double x = q.rng.real(__ldg(cum + d - 1));
+            pick = upper_index(cum, d, x);
+        } else {  // REJ with p* per vertex
+            double ps = __ldg(L.rej_pstar + q.cur);
+            uint32_t t = 0;
+            for (;; ++t) {
+                if (t >= L.trial_cap) {
+                    raise_device(L, WF_ERR_REJECTION_CAP);
+                    return kFault;
+                }
+                uint32_t x = q.rng.index(d);
+                double y = q.rng.real(ps);
+                if (y < P::weight_static(L.prog, L.g, base + x)) { pick = x; break; }
+            }
+        }
+    } else {  // Gathered: gather (engine.hpp:134-184) without the scratch table
+        if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) {
+            if (L.use_label_index) {
+                // label-partitioned CSR: q.cur_base / q.cur_deg already frame the
+                // group of edges labelled schema[moves]; the reference picks the
+                // j-th matching edge in CSR order with j = floor(uniform_real(m))
+                // (cumulative table over 0/1 weights), which is the j-th edge of
+                // the stably partitioned group.
+                double x = q.rng.real(static_cast<double>(d));
+                dst = __ldg(L.g.lab_nbr + base + static_cast<uint32_t>(x));
+                return kMoved;
+            }
+        }
+        double sum = 0.0, mx = 0.0;
+        for (uint32_t i = 0; i < d; ++i) {
+            double w = P::weight(L.prog, L.g, q, base + i);
+            sum += w;
+            mx = w > mx ? w : mx;
+        }
+        if (!(sum > 0.0)) return kDead;
+        if constexpr (S == WF_SAMPLER_ITS) {
+            double x = q.rng.real(sum);  // == cumulative[d-1]: same sequential sum
+            double run = 0.0;
+            pick = d - 1;
+            for (uint32_t i = 0; i < d; ++i) {
+                run += P::weight(L.prog, L.g, q, base + i);
+                if (x < run) { pick = i; break; }
+            }
+        } else if constexpr (S == WF_SAMPLER_ALIAS) {
+            uint32_t x = q.rng.index(d);
+            uint64_t k = q.rng.bits53();
+            double* park = L.scratch + (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * L.scratch_stride;
+            double split;
+            uint32_t second;
+            vose_bucket(d, sum, [&](uint32_t i) { return P::weight(L.prog, L.g, q, base + i); }, x,
+                        park, split, second);
+            pick = k < unit_threshold(split) ? x : second;
+        } else {  // REJ over the gathered weights, p* = max
+            uint32_t t = 0;
+            for (;; ++t) {
+                if (t >= L.trial_cap) {
+                    raise_device(L, WF_ERR_REJECTION_CAP);
+                    return kFault;
+                }
+                uint32_t x = q.rng.index(d);
+                double y = q.rng.real(mx);
+                if (y < P::weight(L.prog, L.g, q, base + x)) { pick = x; break; }
+            }
+        }
+    }
+    dst = __ldg(L.g.nbr + base + pick);
+    return kMoved;
+}
+
+// Loads what the next move out of q.cur needs into registers.
+template <int K, int S, int F>
+__device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
+    if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
+        if (L.use_label_index) {
+            const uint4* rec = L.g.lab_rec + 2 * static_cast<uint64_t>(q.cur);
+            uint4 r0 = __ldg(rec);
+            uint4 r1 = __ldg(rec + 1);
+            uint64_t base = (static_cast<uint64_t>(r0.y) << 32) | r0.x;
+            uint32_t ends[kMaxIndexedLabels] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            uint32_t l = __ldg(L.prog.schema + (q.len - 1));
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxIndexedLabels; ++i) {
+                if (static_cast<uint32_t>(i) == l) hi = ends[i];
+                if (static_cast<uint32_t>(i) + 1 == l) lo = ends[i];
+            }
+            if (l >= static_cast<uint32_t>(kMaxIndexedLabels)) lo = hi = 0;
+            q.cur_base = base + lo;
+            q.cur_deg = hi - lo;
+            return;
+        }
+    }
+    decode_vertex(L.g, L.sview, q.cur, q.cur_base, q.cur_deg);
+}
+
+__device__ __forceinline__ uint32_t source_at(const WalkLaunch& L, uint64_t qid) {  // walker.hpp:70-77
+    if (L.qmode == WF_QUERY_ONE_PER_VERTEX) return static_cast<uint32_t>(qid);
+    if (L.qmode == WF_QUERY_FROM_SOURCE) return L.qsource;
+    return __ldg(L.qsources + qid);
+}
+
+__device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int st) {
+    L.lengths[q.row] = q.len;
+    L.status[q.row] = static_cast<uint8_t>(st);
+    if (q.len > L.stride) atomicAdd(L.overflow_out, 1ULL);
+}
+
+__device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint32_t v) {
+    if (q.len < L.stride) __stcs(L.paths + q.row * L.stride + q.len, v);
+    if (L.visit_counts) atomicAdd(L.visit_counts + v, 1u);
+}
+
+// The persistent step kernel.  One walker per lane; lanes whose walk ended pull
+// the next query id from a global cursor with one atomic per warp (the GPU
+// analogue of the interleaved executor's admit/refill, interleave.hpp:436-464,
+// 531-538), so PPR's geometric terminations never idle a lane while queries
+// remain.  Every walker draws only from its own (seed, qid) stream, so the
+// output is independent of scheduling, exactly as in the reference.
+template <int K, int S, int F>
+__global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
+    using P = Program<K>;
+    const int lane = threadIdx.x & 31;
+    Walker q;
+    q.row = 0;
+    q.cur = q.prev = 0;
+    q.cur_deg = q.prev_deg = 0;
+    q.cur_base = q.prev_base = 0;
+    q.len = 0;
+    q.rng.s = 0;
+    bool active = false;
+    bool drained = false;
+    unsigned long long steps = 0;
+    for (;;) {
+        // refill lanes without a live walker
+        for (;;) {
+            unsigned need = __ballot_sync(kFull, !active && !drained);
+            if (need == 0) break;
+            int leader = __ffs(need) - 1;
+            unsigned long long first = 0;
+            if (lane == leader) first = atomicAdd(L.cursor, static_cast<unsigned long long>(__popc(need)));
+            first = __shfl_sync(kFull, first, leader);
+            if (!active && !drained) {
+                uint64_t row = first + __popc(need & ((1u << lane) - 1));
+                if (row >= L.n_rows) {
+                    drained = true;
+                } else {
+                    uint64_t qid = L.qid_map ? __ldg(L.qid_map + row) : L.qid_begin + row;
+                    q.row = row;
+                    q.rng.s = stream_state(L.seed_mixed, qid);
+                    q.cur = source_at(L, qid);
+                    q.prev = 0xFFFFFFFFu;
+                    q.len = 0;
+                    emit(L, q, q.cur);
+                    q.len = 1;
+                    if (P::prechecked && P::finished(L.prog, q)) {
+                        finish(L, q, WF_WALK_COMPLETE);  // walk_already_finished, program.hpp:86-93
+                    } else {
+                        load_current<K, S, F>(L, q);
+                        active = true;
+                    }
+                }
+            }
+        }
+        if (!__any_sync(kFull, active)) break;
+        if (active) {
+            uint32_t dst = 0;
+            int r = move<K, S, F>(L, q, dst);
+            if (r == kMoved) {
+                q.prev = q.cur;
+                q.prev_base = q.cur_base;
+                q.prev_deg = q.cur_deg;
+                q.cur = dst;
+                emit(L, q, dst);
+                q.len += 1;
+                steps += 1;
+                if (P::update(L.prog, q)) {
+                    finish(L, q, WF_WALK_COMPLETE);
+                    active = false;
+                } else {
+                    load_current<K, S, F>(L, q);
+                }
+            } else {
+                finish(L, q, WF_WALK_DEAD_END);
+                active = false;
+            }
+        }
+    }
+    // one atomic per warp for the step total
+    for (int o = 16; o > 0; o >>= 1) steps += __shfl_xor_sync(kFull, steps, o);
+    if (lane == 0 && steps) atomicAdd(L.steps_out, steps);
+}
+
+}  // namespace wf

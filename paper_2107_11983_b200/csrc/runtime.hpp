@@ -1,0 +1,146 @@
+// Host-side runtime objects behind the C-ABI handles.
+//
+//   GraphStore   device-resident Graph (graph.hpp:17-107): CSR + packed vertex
+//                words + optional label index; stats from finalize_stats
+//                (graph.cpp:161-180).
+//   Session      ResolvedRun (engine.hpp:275-294): program parameters, resolved
+//                sampler/flow, device static tables (preprocess_static).
+//   WalkSetStore RunResult (engine.hpp:71-74): device rows + lengths + status.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.cuh"
+
+namespace wf {
+
+struct GraphStore {
+    int device = 0;
+    uint32_t V = 0;
+    uint64_t E = 0;
+    DeviceBuffer<uint64_t> offsets;
+    DeviceBuffer<uint32_t> nbr;
+    DeviceBuffer<float> weights;
+    DeviceBuffer<uint8_t> labels;
+    DeviceBuffer<uint64_t> vword;
+    bool sorted = true;
+    uint32_t max_degree = 0;
+    double max_weight = 0.0;
+    uint32_t label_count = 0;
+    std::vector<uint8_t> label_present;  // 256 flags (MetaPath constructor check)
+
+    std::mutex mu;
+    bool label_index_built = false;
+    DeviceBuffer<uint4> lab_rec;
+    DeviceBuffer<uint32_t> lab_nbr;
+
+    GraphView view() const {
+        GraphView g{};
+        g.V = V;
+        g.E = E;
+        g.offsets = offsets.get();
+        g.nbr = nbr.get();
+        g.weights = weights.get();
+        g.labels = labels.get();
+        g.vword = vword.get();
+        g.sorted = sorted ? 1 : 0;
+        g.lab_rec = lab_rec.get();
+        g.lab_nbr = lab_nbr.get();
+        g.label_count = label_count;
+        return g;
+    }
+    bool has_weights() const { return weights.get() != nullptr; }
+    bool has_labels() const { return labels.get() != nullptr; }
+
+    // After offsets/nbr/weights/labels are resident: validate (from_csr),
+    // compute stats, build vertex words.  `labels_checked` = labels already u8.
+    void finalize(cudaStream_t st);
+    void ensure_label_index(cudaStream_t st);
+};
+
+struct Session {
+    GraphStore* g = nullptr;
+    wf_program_desc desc{};
+    std::vector<uint32_t> schema;
+    DeviceBuffer<uint32_t> schema_dev;
+    ProgParams params{};
+    int kind = 0;  // wf_sampler
+    int flow = 0;  // Flow
+    uint64_t seed = 0;
+    uint32_t trial_cap = 1u << 20;
+    uint32_t default_stride = 0;  // path row capacity
+    bool unbounded = false;       // PPR: geometric lengths
+    double preprocess_seconds = 0.0;
+    DeviceBuffer<uint4> alias;
+    DeviceBuffer<double> its;
+    DeviceBuffer<double> rej;
+    DeviceBuffer<uint8_t> exhausted;
+    DeviceBuffer<uint64_t> sview;  // vertex words with exhausted vertices at degree 0
+    bool any_exhausted = false;
+    DeviceBuffer<int> error_word;
+    DeviceBuffer<unsigned long long> cursor;
+    DeviceBuffer<double> scratch;
+    uint64_t scratch_stride = 0;
+    int grid = 0;
+
+    void build_tables(cudaStream_t st);
+};
+
+struct WalkSetStore {
+    int device = 0;
+    uint64_t n = 0;
+    uint32_t stride = 0;
+    uint32_t V = 0;
+    DeviceBuffer<uint32_t> paths;
+    DeviceBuffer<uint32_t> lengths;
+    DeviceBuffer<uint8_t> status;
+    DeviceBuffer<uint32_t> visit_counts;
+    // walks longer than `stride`, re-run into their own rows
+    std::vector<uint64_t> over_rows;
+    uint32_t over_stride = 0;
+    DeviceBuffer<uint32_t> over_paths;
+    wf_run_metrics metrics{};
+    uint64_t total_vertices = 0;
+    uint32_t max_length = 0;
+};
+
+// walk.cu
+void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sources,
+                 uint64_t qid_begin, uint64_t qid_end, const uint64_t* qid_map, uint32_t* paths,
+                 uint32_t stride, uint32_t* lengths, uint8_t* status, uint32_t* visit_counts,
+                 unsigned long long* steps_out, unsigned long long* overflow_out,
+                 unsigned long long* cursor, cudaStream_t st);
+int occupancy_grid(const Session& s);
+
+// graph.cu
+GraphStore* graph_from_host(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
+                            const uint32_t* labels, uint32_t V, uint64_t E, int device);
+GraphStore* graph_from_device(const uint64_t* offsets, const uint32_t* neighbors,
+                              const float* weights, const uint8_t* labels, uint32_t V, uint64_t E,
+                              int device);
+GraphStore* graph_generate_rmat(const wf_rmat_params& p, int device);
+void graph_has_edge(const GraphStore& g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                    uint8_t* out);
+
+// u32 -> u64 widening for scans over lengths / degrees
+struct WidenU64 {
+    __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+};
+
+// stream.cu: pipelined run + copy of the walk set into host buffers
+void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t n,
+                 uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
+                 uint64_t chunk, wf_run_metrics* metrics);
+
+// walk set copy-out (walk.cu)
+void walkset_visit_counts(const WalkSetStore& w, uint32_t* counts_dev, cudaStream_t st);
+void walkset_copy(const WalkSetStore& w, uint64_t qb, uint64_t qe, uint64_t* offsets,
+                  uint32_t* vertices, uint8_t* status);
+
+}  // namespace wf

@@ -1,0 +1,204 @@
+// Run + stream the walk set to host memory, overlapping the walk kernel of
+// chunk k+1 with the compaction + device->host copy of chunk k (two streams,
+// double-buffered staging).  This is the end-to-end path: the reference hands
+// its walks back in host memory (RunResult::walks, engine.hpp:448-452) or
+// through a BlockSink per worker block (engine.hpp:76-79, output.cpp:133-200).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace wf {
+
+namespace {
+
+__global__ void k_compact_chunk(const uint32_t* __restrict__ rows, uint32_t stride,
+                                const uint32_t* __restrict__ lengths,
+                                const uint64_t* __restrict__ offs, uint64_t nrows,
+                                uint32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = warp; r < nrows; r += nwarps) {
+        uint32_t len = min(lengths[r], stride);
+        const uint32_t* src = rows + r * stride;
+        uint32_t* dst = out + offs[r];
+        for (uint32_t j = lane; j < len; j += 32) dst[j] = src[j];
+    }
+}
+
+struct Streams {
+    cudaStream_t a = nullptr, b = nullptr;
+    ~Streams() {
+        if (a) cudaStreamDestroy(a);
+        if (b) cudaStreamDestroy(b);
+    }
+};
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t make() {
+        cudaEvent_t e;
+        WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+        return e;
+    }
+    ~Events() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t n,
+                 uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
+                 uint64_t chunk, wf_run_metrics* metrics) {
+    GraphStore& g = *s.g;
+    DeviceGuard guard(g.device);
+    const uint32_t stride = s.default_stride;
+    if (chunk == 0) chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (4ull * stride)));
+    chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
+    Streams st;
+    WF_CUDA(cudaStreamCreateWithFlags(&st.a, cudaStreamNonBlocking));
+    WF_CUDA(cudaStreamCreateWithFlags(&st.b, cudaStreamNonBlocking));
+    Events evs;
+    auto t0 = std::chrono::steady_clock::now();
+
+    DeviceBuffer<uint32_t> d_src;
+    if (spec.mode == WF_QUERY_FROM_LIST && n) {
+        d_src.allocate(n);
+        WF_CUDA(cudaMemcpyAsync(d_src.get(), host_sources, n * 4, cudaMemcpyHostToDevice, st.a));
+    }
+    DeviceBuffer<uint32_t> rows[2], lens[2], stage[2];
+    DeviceBuffer<uint8_t> stat[2];
+    DeviceBuffer<uint64_t> offs[2];
+    size_t scan_bytes = 0;
+    {
+        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(nullptr, WidenU64{});
+        cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, in, static_cast<uint64_t*>(nullptr),
+                                      static_cast<int64_t>(chunk), st.a);
+    }
+    DeviceBuffer<uint8_t> scan_tmp(std::max<size_t>(scan_bytes, 1));
+    for (int b = 0; b < 2; ++b) {
+        rows[b].allocate(chunk * stride);
+        lens[b].allocate(chunk);
+        stat[b].allocate(chunk);
+        offs[b].allocate(chunk + 1);
+        stage[b].allocate(chunk * stride);
+        WF_CUDA(cudaMemsetAsync(offs[b].get(), 0, 8, st.a));
+    }
+    DeviceBuffer<unsigned long long> ctr(2);
+    WF_CUDA(cudaMemsetAsync(ctr.get(), 0, 16, st.a));
+    uint64_t* h_tot = nullptr;  // per-buffer chunk totals (pinned)
+    WF_CUDA(cudaMallocHost(&h_tot, 2 * sizeof(uint64_t)));
+    struct HostFree { uint64_t* p; ~HostFree() { if (p) cudaFreeHost(p); } } hf{h_tot};
+
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    cudaEvent_t ev_comp[2] = {evs.make(), evs.make()};
+    cudaEvent_t ev_copy[2] = {evs.make(), evs.make()};
+    bool copy_pending[2] = {false, false};
+    std::vector<uint64_t> chunk_base(nchunks + 1, 0);
+
+    auto enqueue_compute = [&](uint64_t k) {
+        const int b = static_cast<int>(k & 1);
+        const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
+        // buffer b (status / offsets / staging) is free once chunk k-2's copy drained
+        if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(st.a, ev_copy[b], 0));
+        launch_walk(s, spec, d_src.get(), r0, r1, nullptr, rows[b].get(), stride, lens[b].get(),
+                    stat[b].get(), nullptr, ctr.get(), ctr.get() + 1, s.cursor.get(), st.a);
+        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(lens[b].get(), WidenU64{});
+        WF_CUDA(cub::DeviceScan::InclusiveSum(scan_tmp.get(), scan_bytes, in, offs[b].get() + 1,
+                                              static_cast<int64_t>(nr), st.a));
+        count_launch();
+        int blocks = static_cast<int>(std::min<uint64_t>((nr * 32 + 255) / 256, 65535));
+        k_compact_chunk<<<std::max(blocks, 1), 256, 0, st.a>>>(rows[b].get(), stride, lens[b].get(),
+                                                               offs[b].get(), nr, stage[b].get());
+        WF_LAUNCHED();
+        WF_CUDA(cudaMemcpyAsync(h_tot + b, offs[b].get() + nr, 8, cudaMemcpyDeviceToHost, st.a));
+        WF_CUDA(cudaEventRecord(ev_comp[b], st.a));
+    };
+
+    if (nchunks) enqueue_compute(0);
+    for (uint64_t k = 0; k < nchunks; ++k) {
+        const int b = static_cast<int>(k & 1);
+        const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
+        WF_CUDA(cudaEventSynchronize(ev_comp[b]));
+        const uint64_t cnt = h_tot[b];
+        chunk_base[k + 1] = chunk_base[k] + cnt;
+        if (chunk_base[k + 1] > capacity)
+            raise(WF_ERR_INVALID_ARG, "vertices_capacity too small for the walk set");
+        if (k + 1 < nchunks) enqueue_compute(k + 1);  // overlaps the copy below
+        WF_CUDA(cudaStreamWaitEvent(st.b, ev_comp[b], 0));
+        if (cnt)
+            WF_CUDA(cudaMemcpyAsync(vertices + chunk_base[k], stage[b].get(), cnt * 4,
+                                    cudaMemcpyDeviceToHost, st.b));
+        if (offsets)
+            WF_CUDA(cudaMemcpyAsync(offsets + r0, offs[b].get(), nr * 8, cudaMemcpyDeviceToHost, st.b));
+        if (status)
+            WF_CUDA(cudaMemcpyAsync(status + r0, stat[b].get(), nr, cudaMemcpyDeviceToHost, st.b));
+        WF_CUDA(cudaEventRecord(ev_copy[b], st.b));
+        copy_pending[b] = true;
+    }
+    WF_CUDA(cudaStreamSynchronize(st.b));
+    WF_CUDA(cudaStreamSynchronize(st.a));
+    int err = 0;
+    WF_CUDA(cudaMemcpy(&err, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
+    if (err) {
+        WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
+        raise(err, err == WF_ERR_REJECTION_CAP
+                       ? "rejection sampling exceeded " + std::to_string(s.trial_cap) +
+                             " trials; asserted bound does not match the weights"
+                       : std::string("device-side contract violation"));
+    }
+    // chunk-relative offsets -> absolute
+    if (offsets) {
+        for (uint64_t k = 0; k < nchunks; ++k) {
+            const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk);
+            const uint64_t base = chunk_base[k];
+            for (uint64_t r = r0; r < r1; ++r) offsets[r] += base;
+        }
+        offsets[n] = chunk_base[nchunks];
+    }
+    unsigned long long hc[2] = {0, 0};
+    WF_CUDA(cudaMemcpy(hc, ctr.get(), 16, cudaMemcpyDeviceToHost));
+    if (hc[1] > 0) {
+        // walks longer than a row: re-run them whole and patch their paths
+        if (!offsets) raise(WF_ERR_INVALID_ARG, "offsets are required to place overflowing walks");
+        std::vector<uint64_t> qids;
+        uint32_t mx = 0;
+        for (uint64_t r = 0; r < n; ++r) {
+            uint64_t len = offsets[r + 1] - offsets[r];
+            if (len > stride) {
+                qids.push_back(r);
+                mx = std::max<uint32_t>(mx, static_cast<uint32_t>(len));
+            }
+        }
+        DeviceBuffer<uint64_t> dq(qids.size());
+        WF_CUDA(cudaMemcpy(dq.get(), qids.data(), qids.size() * 8, cudaMemcpyHostToDevice));
+        DeviceBuffer<uint32_t> p(qids.size() * static_cast<uint64_t>(mx)), l(qids.size());
+        DeviceBuffer<uint8_t> sst(qids.size());
+        DeviceBuffer<unsigned long long> c2(2);
+        WF_CUDA(cudaMemset(c2.get(), 0, 16));
+        launch_walk(s, spec, d_src.get(), 0, qids.size(), dq.get(), p.get(), mx, l.get(), sst.get(),
+                    nullptr, c2.get(), c2.get() + 1, s.cursor.get(), nullptr);
+        std::vector<uint32_t> hp(qids.size() * static_cast<uint64_t>(mx));
+        WF_CUDA(cudaMemcpy(hp.data(), p.get(), hp.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < qids.size(); ++i) {
+            uint64_t r = qids[i];
+            std::copy(hp.begin() + i * mx, hp.begin() + i * mx + (offsets[r + 1] - offsets[r]),
+                      vertices + offsets[r]);
+        }
+    }
+    if (metrics) {
+        metrics->preprocess_seconds = s.preprocess_seconds;
+        metrics->exec_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        metrics->total_steps = hc[0];
+        metrics->max_in_flight = static_cast<uint32_t>(static_cast<uint64_t>(s.grid) * kBlock);
+    }
+}
+
+}  // namespace wf

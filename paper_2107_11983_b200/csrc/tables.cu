@@ -1,0 +1,230 @@
+// Static-Gather preprocessing on the device: preprocess_static
+// (engine.hpp:190-251) for ALIAS, ITS and REJ, one thread per vertex.
+//
+// Per vertex the reference sums the weights sequentially (engine.hpp:218-226),
+// marks the vertex exhausted when the sum is not positive, and builds
+//   ALIAS  Vose's table with FIFO worklists (sampler.hpp:89-120), decorated with
+//          destinations (engine.hpp:118-127);
+//   ITS    the running-sum cumulative table (engine.hpp:232-238);
+//   REJ    p* = max weight (engine.hpp:244-246).
+// Everything runs in fp64 in the reference's operation order, so the tables are
+// bit-identical (checked against the reference's own preprocess_static output
+// in tests/test_engine_gpu.py).  The ALIAS build replays the FIFO worklists with
+// three ascending cursors and parks demoted larges' values in their own
+// output bucket, so it needs no E-sized scratch (SURVEY §7 hard part 1).
+//
+// Device bucket (16 B): {u64 thr = ceil(split * 2^53), u32 first_dst,
+// u32 second_dst}; `y < split` with y = uniform_real(1.0) is exactly
+// `(r >> 11) < thr` (rng.cuh unit_threshold).
+#include <chrono>
+
+#include "runtime.hpp"
+
+namespace wf {
+
+namespace {
+
+struct UnitWeight {
+    __device__ __forceinline__ double operator()(uint64_t) const { return 1.0; }
+};
+struct EdgeWeight {
+    const float* __restrict__ w;
+    __device__ __forceinline__ double operator()(uint64_t e) const {
+        return static_cast<double>(__ldg(w + e));
+    }
+};
+
+__device__ __forceinline__ void store_bucket(uint4* b, double split, uint32_t first_dst,
+                                             uint32_t second_dst) {
+    uint64_t thr = unit_threshold(split);
+    *b = make_uint4(static_cast<uint32_t>(thr), static_cast<uint32_t>(thr >> 32), first_dst, second_dst);
+}
+
+__device__ __forceinline__ void park(uint4* b, double v) {
+    uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+    b->x = static_cast<uint32_t>(bits);
+    b->y = static_cast<uint32_t>(bits >> 32);
+}
+
+__device__ __forceinline__ double unpark(const uint4* b) {
+    uint64_t bits = (static_cast<uint64_t>(b->y) << 32) | b->x;
+    return __longlong_as_double(static_cast<long long>(bits));
+}
+
+template <typename WF>
+__global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                               uint32_t V, WF wf, uint4* __restrict__ bucket,
+                               uint8_t* __restrict__ exhausted, unsigned* any_exhausted) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n == 0) continue;
+        double sum = 0.0;
+        for (uint32_t i = 0; i < n; ++i) sum += wf(a0 + i);
+        if (!(sum > 0.0)) {
+            exhausted[v] = 1;
+            atomicOr(any_exhausted, 1u);
+            continue;
+        }
+        const uint32_t* dst = nbr + a0;
+        uint4* out = bucket + a0;
+        auto scaled = [&](uint32_t i) { return wf(a0 + i) * n / sum; };  // sampler.hpp:97
+        auto next_large = [&](uint32_t from) {
+            while (from < n && !(scaled(from) >= 1.0)) ++from;
+            return from;
+        };
+        auto next_small = [&](uint32_t from) {
+            while (from < n && !(scaled(from) < 1.0)) ++from;
+            return from;
+        };
+        uint32_t lcur = next_large(0);
+        double lval = lcur < n ? scaled(lcur) : 0.0;
+        uint32_t a = next_small(0);
+        uint32_t c = 0, demoted = 0, consumed = 0;
+        while (lcur < n) {  // sampler.hpp:103-111
+            uint32_t s;
+            double sval;
+            if (a < n) {
+                s = a;
+                sval = scaled(a);
+                a = next_small(a + 1);
+            } else if (consumed < demoted) {
+                c = next_large(c);
+                s = c;
+                sval = unpark(out + c);
+                ++c;
+                ++consumed;
+            } else {
+                break;
+            }
+            store_bucket(out + s, sval, dst[s], dst[lcur]);
+            lval -= 1.0 - sval;
+            if (lval < 1.0) {
+                park(out + lcur, lval);
+                ++demoted;
+                lcur = next_large(lcur + 1);
+                if (lcur < n) lval = scaled(lcur);
+            }
+        }
+        // leftovers at probability exactly 1 (sampler.hpp:112-119)
+        for (uint32_t s = a; s < n; s = next_small(s + 1)) store_bucket(out + s, 1.0, dst[s], dst[s]);
+        while (consumed < demoted) {
+            c = next_large(c);
+            store_bucket(out + c, 1.0, dst[c], dst[c]);
+            ++c;
+            ++consumed;
+        }
+        for (uint32_t l = lcur; l < n; l = next_large(l + 1)) store_bucket(out + l, 1.0, dst[l], dst[l]);
+    }
+}
+
+template <typename WF>
+__global__ void k_static_its(const uint64_t* __restrict__ off, uint32_t V, WF wf,
+                             double* __restrict__ cum, uint8_t* __restrict__ exhausted,
+                             unsigned* any_exhausted) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n == 0) continue;
+        double run = 0.0;
+        for (uint32_t i = 0; i < n; ++i) {
+            run += wf(a0 + i);
+            cum[a0 + i] = run;
+        }
+        if (!(run > 0.0)) {
+            exhausted[v] = 1;
+            atomicOr(any_exhausted, 1u);
+        }
+    }
+}
+
+template <typename WF>
+__global__ void k_static_rej(const uint64_t* __restrict__ off, uint32_t V, WF wf,
+                             double* __restrict__ pstar, uint8_t* __restrict__ exhausted,
+                             unsigned* any_exhausted) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n == 0) continue;
+        double sum = 0.0, mx = 0.0;
+        for (uint32_t i = 0; i < n; ++i) {
+            double w = wf(a0 + i);
+            sum += w;
+            mx = w > mx ? w : mx;
+        }
+        if (!(sum > 0.0)) {
+            exhausted[v] = 1;
+            atomicOr(any_exhausted, 1u);
+        } else {
+            pstar[v] = mx;
+        }
+    }
+}
+
+__global__ void k_sampling_view(const uint64_t* __restrict__ vword, const uint8_t* __restrict__ ex,
+                                uint32_t V, uint64_t* __restrict__ out) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t w = vword[v];
+        // exhausted: degree 0 (dead end, no draws).  Escaped words keep their
+        // escape only when live.
+        out[v] = ex[v] ? (w & ~static_cast<uint64_t>(kDegEscape)) : w;
+    }
+}
+
+template <typename WF>
+void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
+    GraphStore& g = *s.g;
+    const int threads = 128;
+    uint64_t blocks = (g.V + threads - 1) / threads;
+    blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, static_cast<uint64_t>(sm_count(g.device)) * 64));
+    if (s.kind == WF_SAMPLER_ALIAS) {
+        s.alias.allocate(std::max<uint64_t>(g.E, 1));
+        k_static_alias<<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
+                                                   s.alias.get(), s.exhausted.get(), any);
+    } else if (s.kind == WF_SAMPLER_ITS) {
+        s.its.allocate(std::max<uint64_t>(g.E, 1));
+        k_static_its<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.its.get(),
+                                                 s.exhausted.get(), any);
+    } else {
+        s.rej.allocate(g.V);
+        WF_CUDA(cudaMemsetAsync(s.rej.get(), 0, g.V * sizeof(double), st));
+        k_static_rej<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.rej.get(),
+                                                 s.exhausted.get(), any);
+    }
+    WF_LAUNCHED();
+}
+
+}  // namespace
+
+void Session::build_tables(cudaStream_t st) {
+    GraphStore& gs = *g;
+    DeviceGuard guard(gs.device);
+    auto t0 = std::chrono::steady_clock::now();
+    exhausted.allocate(gs.V);
+    WF_CUDA(cudaMemsetAsync(exhausted.get(), 0, gs.V, st));
+    DeviceBuffer<unsigned> any(1);
+    WF_CUDA(cudaMemsetAsync(any.get(), 0, 4, st));
+    bool edge_weight = desc.kind == WF_PROGRAM_DEEPWALK && desc.weighted;
+    if (edge_weight) launch_tables(*this, EdgeWeight{gs.weights.get()}, any.get(), st);
+    else launch_tables(*this, UnitWeight{}, any.get(), st);
+    unsigned h = 0;
+    WF_CUDA(cudaMemcpyAsync(&h, any.get(), 4, cudaMemcpyDeviceToHost, st));
+    WF_CUDA(cudaStreamSynchronize(st));
+    any_exhausted = h != 0;
+    if (any_exhausted) {
+        sview.allocate(gs.V);
+        uint64_t blocks = std::min<uint64_t>((gs.V + 255) / 256, 65535);
+        k_sampling_view<<<std::max<uint64_t>(blocks, 1), 256, 0, st>>>(gs.vword.get(), exhausted.get(), gs.V,
+                                                                     sview.get());
+        WF_LAUNCHED();
+        WF_CUDA(cudaStreamSynchronize(st));
+    }
+    preprocess_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace wf

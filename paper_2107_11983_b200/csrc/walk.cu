@@ -1,0 +1,248 @@
+// Kernel instantiation + launch for every legal (program, sampler, flow)
+// pairing (resolve_flow, engine.hpp:255-272), and the walk-set copy-out.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <map>
+#include <tuple>
+
+#include "runtime.hpp"
+
+namespace wf {
+
+using KernelFn = void (*)(const WalkLaunch);
+
+namespace {
+
+template <int K, int S, int F>
+constexpr KernelFn kfn() {
+    return &walk_kernel<K, S, F>;
+}
+
+// Every program × sampler × flow the reference accepts.
+KernelFn select_kernel(int prog, int sampler, int flow) {
+#define WF_CASE(P, S, F) \
+    if (prog == P && sampler == S && flow == F) return kfn<P, S, F>();
+#define WF_UNBIASED(P)                                             \
+    WF_CASE(P, WF_SAMPLER_NAIVE, kDirect)                          \
+    WF_CASE(P, WF_SAMPLER_OREJ, kDirect)                           \
+    WF_CASE(P, WF_SAMPLER_ITS, kTables)                            \
+    WF_CASE(P, WF_SAMPLER_ALIAS, kTables)                          \
+    WF_CASE(P, WF_SAMPLER_REJ, kTables)                            \
+    WF_CASE(P, WF_SAMPLER_ITS, kGathered)                          \
+    WF_CASE(P, WF_SAMPLER_ALIAS, kGathered)                        \
+    WF_CASE(P, WF_SAMPLER_REJ, kGathered)
+    WF_UNBIASED(WF_PROGRAM_PPR)
+    WF_UNBIASED(WF_PROGRAM_UNIFORM)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_OREJ, kDirect)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ITS, kTables)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ALIAS, kTables)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_REJ, kTables)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ITS, kGathered)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ALIAS, kGathered)
+    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_REJ, kGathered)
+    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_OREJ, kDirect)
+    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_ITS, kGathered)
+    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_ALIAS, kGathered)
+    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_REJ, kGathered)
+    WF_CASE(WF_PROGRAM_METAPATH, WF_SAMPLER_ITS, kGathered)
+    WF_CASE(WF_PROGRAM_METAPATH, WF_SAMPLER_ALIAS, kGathered)
+    WF_CASE(WF_PROGRAM_METAPATH, WF_SAMPLER_REJ, kGathered)
+#undef WF_UNBIASED
+#undef WF_CASE
+    config_error("no kernel for this program/sampler/flow combination");
+}
+
+}  // namespace
+
+int occupancy_grid(const Session& s) {
+    KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
+    int per_sm = 0;
+    WF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+    return std::max(1, per_sm) * sm_count(s.g->device);
+}
+
+void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sources,
+                 uint64_t qid_begin, uint64_t qid_end, const uint64_t* qid_map, uint32_t* paths,
+                 uint32_t stride, uint32_t* lengths, uint8_t* status, uint32_t* visit_counts,
+                 unsigned long long* steps_out, unsigned long long* overflow_out,
+                 unsigned long long* cursor, cudaStream_t st) {
+    GraphStore& g = *s.g;
+    if (qid_end <= qid_begin) return;
+    if (stride == 0) config_error("path stride must be >= 1");
+    KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
+    WalkLaunch L{};
+    L.g = g.view();
+    L.sview = s.any_exhausted ? s.sview.get() : g.vword.get();
+    L.alias = s.alias.get();
+    L.its = s.its.get();
+    L.rej_pstar = s.rej.get();
+    L.prog = s.params;
+    L.qmode = spec.mode;
+    L.qsource = spec.source;
+    L.qsources = dev_sources;
+    L.qid_begin = qid_begin;
+    L.qid_map = qid_map;
+    L.n_rows = qid_end - qid_begin;
+    L.seed_mixed = seed_premix(s.seed);
+    L.trial_cap = s.trial_cap;
+    L.stride = stride;
+    L.paths = paths;
+    L.lengths = lengths;
+    L.status = status;
+    L.visit_counts = visit_counts;
+    L.steps_out = steps_out;
+    L.overflow_out = overflow_out;
+    L.cursor = cursor;
+    L.error_word = s.error_word.get();
+    L.use_label_index = g.label_index_built ? 1 : 0;
+    int grid = s.grid > 0 ? s.grid : occupancy_grid(s);
+    uint64_t lanes_needed = (L.n_rows + 31) / 32 * 32;
+    int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));
+    grid = std::max(1, std::min(grid, grid_needed));
+    if (s.kind == WF_SAMPLER_ALIAS && s.flow == kGathered) {
+        // per-lane park area for the on-the-fly Vose construction
+        uint64_t per_lane = std::max<uint32_t>(g.max_degree, 1);
+        uint64_t budget = 4ull << 30;
+        uint64_t lanes = std::max<uint64_t>(kBlock, budget / (per_lane * 8));
+        grid = std::max(1, std::min<int>(grid, static_cast<int>(lanes / kBlock)));
+        uint64_t need = static_cast<uint64_t>(grid) * kBlock * per_lane;
+        if (s.scratch.size() < need) s.scratch.allocate(need);
+        L.scratch = s.scratch.get();
+        L.scratch_stride = per_lane;
+    }
+    WF_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+    fn<<<grid, kBlock, 0, st>>>(L);
+    WF_LAUNCHED();
+}
+
+// ---- walk-set copy-out -------------------------------------------------------------
+
+namespace {
+
+__global__ void k_compact_rows(const uint32_t* __restrict__ paths, uint32_t stride,
+                               const uint32_t* __restrict__ lengths,
+                               const uint64_t* __restrict__ offs, uint64_t r0, uint64_t nrows,
+                               uint64_t out_base, uint32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = warp; i < nrows; i += nwarps) {
+        uint64_t r = r0 + i;
+        uint32_t len = min(lengths[r], stride);
+        const uint32_t* src = paths + r * stride;
+        uint32_t* dst = out + (offs[r] - out_base);
+        for (uint32_t j = lane; j < len; j += 32) dst[j] = src[j];
+    }
+}
+
+__global__ void k_count_visits(const uint32_t* __restrict__ paths, uint32_t stride,
+                               const uint32_t* __restrict__ lengths, uint64_t n,
+                               uint32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = warp; r < n; r += nwarps) {
+        uint32_t len = min(lengths[r], stride);
+        for (uint32_t j = lane; j < len; j += 32) atomicAdd(counts + paths[r * stride + j], 1u);
+    }
+}
+
+}  // namespace
+
+// Occurrences of each vertex over all stored rows (sources included).  Walks
+// that outgrew their row are counted from their re-run rows.
+void walkset_visit_counts(const WalkSetStore& w, uint32_t* counts, cudaStream_t st) {
+    WF_CUDA(cudaMemsetAsync(counts, 0, w.V * 4ull, st));
+    if (w.n) {
+        int blocks = static_cast<int>(std::min<uint64_t>((w.n * 32 + 255) / 256, 65535));
+        k_count_visits<<<blocks, 256, 0, st>>>(w.paths.get(), w.stride, w.lengths.get(), w.n, counts);
+        WF_LAUNCHED();
+    }
+    if (!w.over_rows.empty()) {
+        // full paths of the overflowed walks replace their truncated rows
+        std::vector<uint32_t> lens(w.over_rows.size());
+        for (size_t i = 0; i < w.over_rows.size(); ++i)
+            WF_CUDA(cudaMemcpy(&lens[i], w.lengths.get() + w.over_rows[i], 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> hp(w.over_rows.size() * static_cast<size_t>(w.over_stride));
+        WF_CUDA(cudaMemcpy(hp.data(), w.over_paths.get(), hp.size() * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> hc(w.V);
+        WF_CUDA(cudaMemcpyAsync(hc.data(), counts, w.V * 4ull, cudaMemcpyDeviceToHost, st));
+        WF_CUDA(cudaStreamSynchronize(st));
+        for (size_t i = 0; i < w.over_rows.size(); ++i)
+            for (uint32_t j = w.stride; j < lens[i]; ++j) hc[hp[i * w.over_stride + j]] += 1;
+        WF_CUDA(cudaMemcpy(counts, hc.data(), w.V * 4ull, cudaMemcpyHostToDevice));
+    }
+}
+
+void walkset_copy(const WalkSetStore& w, uint64_t qb, uint64_t qe, uint64_t* offsets,
+                  uint32_t* vertices, uint8_t* status) {
+    DeviceGuard guard(w.device);
+    if (qe > w.n || qb > qe) raise(WF_ERR_INVALID_ARG, "query range out of bounds");
+    const uint64_t n = qe - qb;
+    cudaStream_t st = nullptr;
+    // offsets over [qb, qe) relative to qb
+    DeviceBuffer<uint64_t> d_off(n + 1);
+    WF_CUDA(cudaMemsetAsync(d_off.get(), 0, 8, st));
+    if (n) {
+        size_t tb = 0;
+        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(w.lengths.get() + qb, WidenU64{});
+        cub::DeviceScan::InclusiveSum(nullptr, tb, in, d_off.get() + 1, static_cast<int64_t>(n), st);
+        DeviceBuffer<uint8_t> tmp(tb);
+        WF_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, in, d_off.get() + 1, static_cast<int64_t>(n), st));
+        count_launch();
+    }
+    std::vector<uint64_t> h_off(n + 1);
+    WF_CUDA(cudaMemcpyAsync(h_off.data(), d_off.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+    WF_CUDA(cudaStreamSynchronize(st));
+    if (offsets) {
+        if (is_device_pointer(offsets)) WF_CUDA(cudaMemcpy(offsets, d_off.get(), (n + 1) * 8, cudaMemcpyDeviceToDevice));
+        else std::copy(h_off.begin(), h_off.end(), offsets);
+    }
+    if (status && n) {
+        WF_CUDA(cudaMemcpy(status, w.status.get() + qb, n, cudaMemcpyDefault));
+    }
+    if (!vertices || n == 0) return;
+    const bool dev_out = is_device_pointer(vertices);
+    const uint64_t total = h_off[n];
+    // offsets for the compaction kernel are absolute per row: shift by qb
+    const uint64_t* row_offs = d_off.get();
+    auto compact = [&](uint64_t r0, uint64_t r1, uint32_t* out, uint64_t out_base) {
+        uint64_t rows = r1 - r0;
+        if (!rows) return;
+        int blocks = static_cast<int>(std::min<uint64_t>((rows * 32 + 255) / 256, 65535));
+        k_compact_rows<<<blocks, 256, 0, st>>>(w.paths.get() + qb * w.stride, w.stride,
+                                               w.lengths.get() + qb, row_offs, r0, rows, out_base, out);
+        WF_LAUNCHED();
+    };
+    if (dev_out) {
+        compact(0, n, vertices, 0);
+    } else {
+        // bounded staging: rows in chunks of <= 64 Mi vertices
+        const uint64_t kStage = 64ull << 20;
+        DeviceBuffer<uint32_t> stage(std::min<uint64_t>(std::max<uint64_t>(total, 1), kStage));
+        uint64_t r0 = 0;
+        while (r0 < n) {
+            uint64_t r1 = r0;
+            uint64_t lo = h_off[r0];
+            while (r1 < n && (h_off[r1 + 1] - lo <= kStage || r1 == r0)) ++r1;
+            uint64_t cnt = h_off[r1] - lo;
+            if (cnt > stage.size()) stage.allocate(cnt);
+            compact(r0, r1, stage.get(), lo);
+            WF_CUDA(cudaMemcpyAsync(vertices + lo, stage.get(), cnt * 4, cudaMemcpyDeviceToHost, st));
+            WF_CUDA(cudaStreamSynchronize(st));
+            r0 = r1;
+        }
+    }
+    WF_CUDA(cudaStreamSynchronize(st));
+    // walks that outgrew the row capacity: their full paths from the re-run
+    for (size_t i = 0; i < w.over_rows.size(); ++i) {
+        uint64_t r = w.over_rows[i];
+        if (r < qb || r >= qe) continue;
+        uint64_t len = h_off[r - qb + 1] - h_off[r - qb];
+        WF_CUDA(cudaMemcpy(vertices + h_off[r - qb], w.over_paths.get() + i * w.over_stride,
+                           len * 4, cudaMemcpyDefault));
+    }
+}
+
+}  // namespace wf

@@ -1,0 +1,344 @@
+"""Python mirror of the reference's engine interface over the CUDA C-ABI.
+
+    run_sequential(g, spec, prog, opts)            engine.hpp:440-504
+    run_interleaved(g, spec, prog, k, k', opts)    interleave.hpp:391-556
+    Session  ~ detail::ResolvedRun                 engine.hpp:275-294
+    DeviceGraph ~ Graph resident in HBM            graph.hpp:17-107
+
+All compute goes through paper_2107_11983_b200/libwalkforge_b200.so (sm_100a
+kernels).  There is no CPU fallback: if the library or a device is missing,
+every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import abi
+from . import host as host_mod
+from .abi import (ExecOptionsC, GraphInfoC, ProgramDesc, QuerySpecC, RmatParamsC, RunMetricsC,
+                  raise_for)
+from .host import ExecOptions, Graph, QuerySpec, RunMetrics, RunResult, WalkSet
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwalkforge_b200.so")
+
+_u64p = C.POINTER(C.c_uint64)
+_u32p = C.POINTER(C.c_uint32)
+_u8p = C.POINTER(C.c_uint8)
+_f32p = C.POINTER(C.c_float)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads the engine; raises if it was not built (no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: run paper_2107_11983_b200/build.py "
+                           "(or __graft_entry__.build())")
+    lib = C.CDLL(path)
+    lib.wf_last_error.restype = C.c_char_p
+    lib.wf_kernel_launches.restype = C.c_uint64
+    for name in abi.EXPORTED_SYMBOLS:
+        getattr(lib, name)  # every declared symbol must resolve
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise_for(rc, (_lib.wf_last_error() or b"").decode())
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def kernel_launches() -> int:
+    return int(load_library().wf_kernel_launches())
+
+
+class DeviceGraph:
+    """A Graph resident in HBM (wf_graph)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.h = handle
+        self._info = None
+
+    @classmethod
+    def from_host(cls, g: Graph, device: int = 0) -> "DeviceGraph":
+        lib = load_library()
+        h = _vp()
+        lab = None if g.labels is None else g.labels.astype(np.uint32)
+        _check(lib.wf_graph_create(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
+                                   _ptr(g.weights, _f32p), _ptr(lab, _u32p),
+                                   C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),
+                                   C.c_int(device), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, offsets_ptr: int, neighbors_ptr: int, weights_ptr: int, labels_ptr: int,
+                    vertex_count: int, edge_count: int, device: int = 0) -> "DeviceGraph":
+        """From device pointers (e.g. torch tensor .data_ptr()); 0 = absent."""
+        lib = load_library()
+        h = _vp()
+        _check(lib.wf_graph_create_device(_vp(offsets_ptr), _vp(neighbors_ptr),
+                                          _vp(weights_ptr or None), _vp(labels_ptr or None),
+                                          C.c_uint32(vertex_count), C.c_uint64(edge_count),
+                                          C.c_int(device), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def rmat(cls, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
+             c: float = 0.19, seed: int = 1, weighted: bool = False, label_count: int = 0,
+             device: int = 0) -> "DeviceGraph":
+        """Synthetic R-MAT (SURVEY §8 d), generated and CSR-built on the device."""
+        lib = load_library()
+        p = RmatParamsC(scale, edge_factor, a, b, c, seed, 1 if weighted else 0, label_count)
+        h = _vp()
+        _check(lib.wf_graph_generate_rmat(C.byref(p), C.c_int(device), C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.wf_graph_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        if self._info is None:
+            i = GraphInfoC()
+            _check(load_library().wf_graph_info_get(self.h, C.byref(i)))
+            self._info = dict(V=i.vertex_count, E=i.edge_count, max_degree=i.max_degree,
+                              max_weight=i.max_weight, has_weights=bool(i.has_weights),
+                              has_labels=bool(i.has_labels), sorted=bool(i.adjacency_sorted),
+                              device=i.device, label_count=i.label_count)
+        return self._info
+
+    @property
+    def vertex_count(self) -> int:
+        return self.info()["V"]
+
+    @property
+    def edge_count(self) -> int:
+        return self.info()["E"]
+
+    def download(self) -> Graph:
+        i = self.info()
+        off = np.zeros(i["V"] + 1, np.uint64)
+        nbr = np.zeros(i["E"], np.uint32)
+        w = np.zeros(i["E"], np.float32) if i["has_weights"] else None
+        lab = np.zeros(i["E"], np.uint8) if i["has_labels"] else None
+        _check(load_library().wf_graph_download(self.h, _ptr(off, _u64p), _ptr(nbr, _u32p),
+                                                _ptr(w, _f32p), _ptr(lab, _u8p)))
+        return Graph(off, nbr, w, lab)
+
+    def has_edge(self, src, dst) -> np.ndarray:
+        s = np.ascontiguousarray(src, dtype=np.uint32)
+        d = np.ascontiguousarray(dst, dtype=np.uint32)
+        out = np.zeros(s.size, np.uint8)
+        _check(load_library().wf_graph_has_edge(self.h, _ptr(s, _u32p), _ptr(d, _u32p),
+                                                C.c_uint64(s.size), _ptr(out, _u8p)))
+        return out.astype(bool)
+
+
+class DeviceWalkSet:
+    """RunResult's WalkSet kept in HBM (wf_walkset)."""
+
+    def __init__(self, handle, metrics: RunMetrics, n_queries: int, vertex_count: int):
+        self.h = handle
+        self.metrics = metrics
+        self.n = n_queries
+        self.V = vertex_count
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.wf_walkset_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self):
+        n = C.c_uint64()
+        tv = C.c_uint64()
+        ml = C.c_uint32()
+        _check(load_library().wf_walkset_info(self.h, C.byref(n), C.byref(tv), C.byref(ml)))
+        return dict(n=n.value, total_vertices=tv.value, max_length=ml.value)
+
+    def to_host(self, qid_begin: int = 0, qid_end: Optional[int] = None) -> WalkSet:
+        qe = self.n if qid_end is None else qid_end
+        n = qe - qid_begin
+        off = np.zeros(n + 1, np.uint64)
+        st = np.zeros(n, np.uint8)
+        lib = load_library()
+        _check(lib.wf_walkset_copy(self.h, C.c_uint64(qid_begin), C.c_uint64(qe),
+                                   _ptr(off, _u64p), None, _ptr(st, _u8p)))
+        verts = np.zeros(int(off[-1]), np.uint32)
+        _check(lib.wf_walkset_copy(self.h, C.c_uint64(qid_begin), C.c_uint64(qe), None,
+                                   _ptr(verts, _u32p), None))
+        return WalkSet(off, verts, st, np.arange(qid_begin, qe, dtype=np.uint64))
+
+    def copy_into(self, offsets_ptr: int, vertices_ptr: int, status_ptr: int,
+                  qid_begin: int = 0, qid_end: Optional[int] = None) -> None:
+        """Raw copy into caller buffers (host or device pointers)."""
+        qe = self.n if qid_end is None else qid_end
+        _check(load_library().wf_walkset_copy(self.h, C.c_uint64(qid_begin), C.c_uint64(qe),
+                                              _vp(offsets_ptr or None), _vp(vertices_ptr or None),
+                                              _vp(status_ptr or None)))
+
+    def visit_counts(self) -> np.ndarray:
+        out = np.zeros(self.V, np.uint32)
+        _check(load_library().wf_walkset_visit_counts(self.h, _ptr(out, _u32p)))
+        return out
+
+
+class Session:
+    """A program bound to a device graph with its sampler resolved and static
+    tables built (ResolvedRun)."""
+
+    def __init__(self, graph: DeviceGraph, prog, opts: Optional[ExecOptions] = None):
+        self.graph = graph
+        self.prog = prog
+        self.opts = opts or ExecOptions()
+        self._desc = prog.to_c()
+        self._copts = self.opts.to_c()
+        h = _vp()
+        _check(load_library().wf_session_create(graph.h, C.byref(self._desc),
+                                                C.byref(self._copts), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.wf_session_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def describe(self):
+        s = C.c_int32()
+        f = C.c_int32()
+        p = C.c_double()
+        _check(load_library().wf_session_describe(self.h, C.byref(s), C.byref(f), C.byref(p)))
+        return abi.Sampler(s.value), abi.Flow(f.value), p.value
+
+    def run(self, spec: QuerySpec) -> DeviceWalkSet:
+        cs = spec.to_c()
+        m = RunMetricsC()
+        h = _vp()
+        _check(load_library().wf_session_run(self.h, C.byref(cs), C.byref(h), C.byref(m)))
+        metrics = RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
+        n = spec.total(self.graph) if spec.mode == abi.QueryMode.ONE_PER_VERTEX else spec.count
+        return DeviceWalkSet(h, metrics, n, self.graph.vertex_count)
+
+    def launch(self, spec: QuerySpec, qid_begin: int, qid_end: int, paths_ptr: int, stride: int,
+               lengths_ptr: int, status_ptr: int, visit_counts_ptr: int = 0,
+               steps_ptr: int = 0, overflow_ptr: int = 0, stream: int = 0,
+               sources_dev_ptr: int = 0) -> None:
+        """wf_session_launch into caller-owned device buffers (async)."""
+        cs = spec.to_c()
+        if sources_dev_ptr:
+            cs.sources = C.cast(_vp(sources_dev_ptr), _u32p)
+        _check(load_library().wf_session_launch(
+            self.h, C.byref(cs), C.c_uint64(qid_begin), C.c_uint64(qid_end), _vp(paths_ptr),
+            C.c_uint32(stride), _vp(lengths_ptr), _vp(status_ptr), _vp(visit_counts_ptr or None),
+            _vp(steps_ptr or None), _vp(overflow_ptr or None), _vp(stream or None)))
+
+    def run_host(self, spec: QuerySpec, offsets_ptr: int, vertices_ptr: int, capacity: int,
+                 status_ptr: int, chunk: int = 0) -> RunMetrics:
+        """wf_session_run_host: run and stream the walk set into HOST buffers
+        (pointers; pinned memory for full bandwidth)."""
+        cs = spec.to_c()
+        m = RunMetricsC()
+        _check(load_library().wf_session_run_host(
+            self.h, C.byref(cs), _vp(offsets_ptr or None), _vp(vertices_ptr), C.c_uint64(capacity),
+            _vp(status_ptr or None), C.c_uint64(chunk), C.byref(m)))
+        return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
+
+    def run_to_numpy(self, spec: QuerySpec, chunk: int = 0) -> RunResult:
+        """Convenience over run_host with numpy (pageable) buffers."""
+        n = self.graph.vertex_count if spec.mode == abi.QueryMode.ONE_PER_VERTEX else spec.count
+        stride = self.row_capacity()
+        # fixed-length programs fit n * stride exactly; unbounded (PPR) walks get headroom
+        cap = n * stride if not isinstance(self.prog, host_mod.PprProgram) else n * stride * 4 + 4096
+        off = np.zeros(n + 1, np.uint64)
+        verts = np.zeros(max(cap, 1), np.uint32)
+        st = np.zeros(max(n, 1), np.uint8)
+        m = self.run_host(spec, off.ctypes.data, verts.ctypes.data, cap, st.ctypes.data, chunk)
+        return RunResult(WalkSet(off, verts[:int(off[-1])], st[:n]), m)
+
+    def row_capacity(self) -> int:
+        p = self.prog
+        if isinstance(p, host_mod.MetaPathProgram):
+            return len(p.schema) + 1
+        if isinstance(p, host_mod.PprProgram):
+            return self.opts.path_stride or 64
+        return p.target_length
+
+    def sync(self, stream: int = 0) -> None:
+        _check(load_library().wf_session_sync(self.h, _vp(stream or None)))
+
+    def tables(self) -> dict:
+        i = self.graph.info()
+        e, v = i["E"], i["V"]
+        out = dict(alias_thr=np.zeros(e, np.uint64), alias_first_dst=np.zeros(e, np.uint32),
+                   alias_second_dst=np.zeros(e, np.uint32), its=np.zeros(e, np.float64),
+                   rej_p_star=np.zeros(v, np.float64), exhausted=np.zeros(v, np.uint8))
+        _check(load_library().wf_session_tables(
+            self.h, _ptr(out["alias_thr"], _u64p), _ptr(out["alias_first_dst"], _u32p),
+            _ptr(out["alias_second_dst"], _u32p), _ptr(out["its"], _f64p),
+            _ptr(out["rej_p_star"], _f64p), _ptr(out["exhausted"], _u8p)))
+        return out
+
+
+def _as_device(g) -> DeviceGraph:
+    return g if isinstance(g, DeviceGraph) else DeviceGraph.from_host(g)
+
+
+def run_sequential(g, spec: QuerySpec, prog, opts: Optional[ExecOptions] = None) -> RunResult:
+    """run_sequential (engine.hpp:440-504): every query to completion; the walk
+    set is a pure function of (graph, spec, program, seed)."""
+    dg = _as_device(g)
+    cs = spec.to_c()
+    # validate the spec before resolving the program, like the reference
+    desc = prog.to_c()
+    copts = (opts or ExecOptions()).to_c()
+    m = RunMetricsC()
+    h = _vp()
+    _check(load_library().wf_run(dg.h, C.byref(desc), C.byref(cs), C.byref(copts), C.byref(h),
+                                 C.byref(m)))
+    n = dg.vertex_count if spec.mode == abi.QueryMode.ONE_PER_VERTEX else spec.count
+    ws = DeviceWalkSet(h, RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps,
+                                     m.max_in_flight), n, dg.vertex_count)
+    return RunResult(ws.to_host(), ws.metrics)
+
+
+def run_interleaved(g, spec: QuerySpec, prog, k: int, k_prime: int,
+                    opts: Optional[ExecOptions] = None) -> RunResult:
+    """run_interleaved (interleave.hpp:391-556): same walks as run_sequential;
+    k / k' are validated like the reference and otherwise only launch hints."""
+    o = opts or ExecOptions()
+    o = ExecOptions(**{**o.__dict__, "k": k, "k_prime": k_prime})
+    if k == 0:
+        raise abi.ConfigError("task ring size must be >= 1")
+    if k_prime == 0 or k_prime > k:
+        raise abi.ConfigError("search ring size must be in [1, k]")
+    return run_sequential(g, spec, prog, o)
+
+
+def rng_probe(seed: int, streams, draws: int) -> np.ndarray:
+    s = np.ascontiguousarray(streams, dtype=np.uint64)
+    out = np.zeros((s.size, draws), np.uint64)
+    _check(load_library().wf_rng_probe(C.c_uint64(seed), _ptr(s, _u64p), C.c_uint64(s.size),
+                                       C.c_uint32(draws), _ptr(out, _u64p)))
+    return out

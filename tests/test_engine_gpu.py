@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the reference.
+
+* golden fixtures made by the unmodified reference (tests/golden/): RNG vectors,
+  every program x sampler x flow combination, edge cases, error classes, static
+  tables — bit-exact;
+* synthetic R-MAT graphs generated on the device, compared with the reference
+  engine (oracle/_ref) or the C restatement on the same CSR — bit-exact walks;
+* size-independent properties at full BASELINE sizes (tests/test_configs_gpu.py).
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import PortOracle, RefOracle, ref_available
+from paper_2107_11983_b200 import abi
+from paper_2107_11983_b200 import engine as E
+from paper_2107_11983_b200.host import (DeepWalkProgram, ExecOptions, MetaPathProgram,
+                                        Node2VecProgram, PprProgram, QuerySpec, UniformProgram)
+from tests import golden_util as gu
+from tests.rmat_ref import rmat_csr
+
+pytestmark = pytest.mark.gpu
+
+CASES = gu.cases()
+_graphs = {}
+
+
+def dgraph(name):
+    if name not in _graphs:
+        _graphs[name] = E.DeviceGraph.from_host(gu.graph(name))
+    return _graphs[name]
+
+
+def oracle():
+    return RefOracle() if ref_available() else None
+
+
+def test_rng_matches_reference_vectors():
+    z = gu.rng()
+    for (s, q), draws in zip(z["pairs"], z["draws"]):
+        got = E.rng_probe(int(s), [int(q)], 16)[0]
+        assert np.array_equal(got, draws)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_golden_case(case):
+    g = dgraph(case["graph"])
+    if "error" in case:
+        with pytest.raises(getattr(abi, case["error"])):
+            E.run_sequential(g, gu.spec(case), gu.program(case), gu.opts(case))
+        return
+    res = E.run_sequential(g, gu.spec(case), gu.program(case), gu.opts(case))
+    want = gu.walks(case)
+    bad = res.walks.first_mismatch(want)
+    assert bad is None, (bad, res.walks.path(bad) if bad is not None and bad < len(res.walks) else None,
+                         want.path(bad) if bad is not None and bad < len(want) else None)
+    assert res.metrics.total_steps == case["total_steps"]
+
+
+def test_golden_cases_interleaved_entry_point():
+    case = next(c for c in CASES if c["name"] == "pl_node2vec_w_orej")
+    res = E.run_interleaved(dgraph(case["graph"]), gu.spec(case), gu.program(case), 64, 32,
+                            gu.opts(case))
+    assert res.walks.equals(gu.walks(case))
+    with pytest.raises(abi.ConfigError):
+        E.run_interleaved(dgraph(case["graph"]), gu.spec(case), gu.program(case), 4, 8,
+                          gu.opts(case))
+
+
+@pytest.mark.parametrize("gname", ["powerlaw", "zeroweights", "ring"])
+def test_static_tables_bit_exact(gname):
+    t = gu.tables()
+    g = dgraph(gname)
+    prog = DeepWalkProgram(20, True)
+    for s in [abi.Sampler.ALIAS, abi.Sampler.ITS, abi.Sampler.REJ]:
+        sess = E.Session(g, prog, ExecOptions(sampler=s))
+        out = sess.tables()
+        key = f"{gname}/{s.name.lower()}"
+        ex = t[f"{key}/exhausted"]
+        assert np.array_equal(out["exhausted"], ex)
+        if s == abi.Sampler.ALIAS:
+            split = t[f"{key}/alias_split"]
+            thr = np.array([_ceil53(x) for x in split], dtype=np.uint64)
+            # slots of exhausted vertices are never read (the reference leaves them zeroed)
+            live = np.repeat(ex == 0, np.diff(gu.graph(gname).offsets).astype(np.int64))
+            assert np.array_equal(out["alias_thr"][live], thr[live])
+            assert np.array_equal(out["alias_first_dst"][live], t[f"{key}/alias_first_dst"][live])
+            assert np.array_equal(out["alias_second_dst"][live], t[f"{key}/alias_second_dst"][live])
+        elif s == abi.Sampler.ITS:
+            assert np.array_equal(out["its"], t[f"{key}/its"])
+        else:
+            assert np.array_equal(out["rej_p_star"], t[f"{key}/rej_p_star"])
+
+
+def _ceil53(split: float) -> int:
+    from fractions import Fraction
+    x = Fraction(split) * (1 << 53)
+    n = x.numerator // x.denominator
+    return n + (1 if n < x else 0)
+
+
+def test_unit_threshold_equivalence():
+    """(r >> 11) < ceil(c * 2^53) <=> uniform_real(1.0) < c, over random r and
+    adversarial c next to the draw."""
+    rng = np.random.default_rng(0)
+    port = PortOracle()
+    for _ in range(2000):
+        seed, stream = (int(x) for x in rng.integers(0, 2 ** 63, 2))
+        r = int(port.rng_probe(seed, stream, 1)[0])
+        k = r >> 11
+        u = k * 2.0 ** -53
+        for c in [u, np.nextafter(u, 0), np.nextafter(u, 1), 0.2, 1.0, 0.5]:
+            if not (0 < c <= 1):
+                continue
+            assert (k < _ceil53(c)) == (u < c)
+
+
+@pytest.mark.parametrize("scale,weighted,labels", [(6, False, 0), (9, True, 5), (10, True, 3)])
+def test_rmat_generator_matches_reference_restatement(scale, weighted, labels):
+    g = E.DeviceGraph.rmat(scale, 16, seed=7, weighted=weighted, label_count=labels).download()
+    off, nbr, w, lab = rmat_csr(scale, 16, seed=7, weighted=weighted, label_count=labels)
+    assert np.array_equal(g.offsets, off)
+    assert np.array_equal(g.neighbors, nbr)
+    if weighted:
+        assert np.array_equal(g.weights, w)
+    if labels:
+        assert np.array_equal(g.labels, lab)
+
+
+def test_rmat_weights_are_reference_synthetic_weights():
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefOracle()
+    g = E.DeviceGraph.rmat(8, 16, seed=3, weighted=True, label_count=5).download()
+    for e in range(0, g.edge_count, 97):
+        assert g.weights[e] == np.float32(ref.synthetic_weight(3, e))
+        assert g.labels[e] == ref.synthetic_label(3, e, 5)
+
+
+def _compare_with_reference(dg, hg, spec, prog, opts, qids=None):
+    ref = RefOracle() if ref_available() else None
+    if ref is not None:
+        rg = ref.graph(hg)
+        want = rg.run_qids(spec, prog, opts, qids) if qids is not None else rg.run(spec, prog, opts)
+    else:
+        want = PortOracle().run(hg, spec, prog, opts, qids=qids, threads=4)
+    got = E.run_sequential(dg, spec, prog, opts)
+    if qids is not None:
+        gw = got.walks
+        for i, q in enumerate(qids):
+            assert gw.status[q] == want.walks.status[i]
+            assert np.array_equal(gw.path(int(q)), want.walks.path(i)), int(q)
+    else:
+        bad = got.walks.first_mismatch(want.walks)
+        assert bad is None, bad
+        assert got.metrics.total_steps == want.metrics.total_steps
+    return got
+
+
+RMAT_PROGRAMS = [
+    ("ppr_naive", lambda: PprProgram(0.2), None),
+    ("ppr_alias", lambda: PprProgram(0.2), abi.Sampler.ALIAS),
+    ("deepwalk_alias_w", lambda: DeepWalkProgram(80, True), None),
+    ("deepwalk_its_w", lambda: DeepWalkProgram(40, True), abi.Sampler.ITS),
+    ("deepwalk_rej_w", lambda: DeepWalkProgram(40, True), abi.Sampler.REJ),
+    ("node2vec_orej", lambda: Node2VecProgram(2.0, 0.5, 80, False), None),
+    ("node2vec_orej_w", lambda: Node2VecProgram(2.0, 0.5, 40, True), None),
+    ("node2vec_its", lambda: Node2VecProgram(2.0, 0.5, 12, False), abi.Sampler.ITS),
+    ("metapath_its", lambda: MetaPathProgram([i % 5 for i in range(79)]), None),
+    ("metapath_rej", lambda: MetaPathProgram([i % 5 for i in range(20)]), abi.Sampler.REJ),
+    ("metapath_alias", lambda: MetaPathProgram([i % 5 for i in range(10)]), abi.Sampler.ALIAS),
+    ("uniform_naive", lambda: UniformProgram(30), None),
+]
+
+
+@pytest.fixture(scope="module")
+def rmat12():
+    dg = E.DeviceGraph.rmat(12, 16, seed=1, weighted=True, label_count=5)
+    return dg, dg.download()
+
+
+@pytest.mark.parametrize("name,mk,sampler", RMAT_PROGRAMS, ids=[p[0] for p in RMAT_PROGRAMS])
+def test_rmat12_all_walks_match_reference(rmat12, name, mk, sampler):
+    dg, hg = rmat12
+    spec = QuerySpec.one_per_vertex()
+    if name.startswith("ppr"):
+        spec = QuerySpec.from_list(np.random.default_rng(5).integers(0, hg.vertex_count, 20000))
+    _compare_with_reference(dg, hg, spec, mk(), ExecOptions(seed=11, sampler=sampler))
+
+
+def test_ppr_row_overflow_rerun_is_exact(rmat12):
+    """Walks longer than the row capacity are re-run into their own rows."""
+    dg, hg = rmat12
+    spec = QuerySpec.from_list(np.random.default_rng(9).integers(0, hg.vertex_count, 5000))
+    opts = ExecOptions(seed=3, path_stride=2)
+    got = _compare_with_reference(dg, hg, spec, PprProgram(0.1), opts)
+    assert got.walks.lengths().max() > 2
+
+
+def test_visit_counts_match_paths(rmat12):
+    dg, hg = rmat12
+    spec = QuerySpec.from_list(np.random.default_rng(2).integers(0, hg.vertex_count, 30000))
+    sess = E.Session(dg, PprProgram(0.2), ExecOptions(seed=5, path_stride=4))
+    ws = sess.run(spec)
+    host = ws.to_host()
+    want = np.bincount(host.vertices, minlength=hg.vertex_count).astype(np.uint32)
+    assert np.array_equal(ws.visit_counts(), want)
+    sess2 = E.Session(dg, DeepWalkProgram(10, True), ExecOptions(seed=5))
+    ws2 = sess2.run(QuerySpec.one_per_vertex())
+    h2 = ws2.to_host()
+    assert np.array_equal(ws2.visit_counts(),
+                          np.bincount(h2.vertices, minlength=hg.vertex_count).astype(np.uint32))
+
+
+def test_label_index_path_equals_label_scan_path(rmat12):
+    """MetaPath through the label-partitioned CSR equals the generic per-step
+    label scan (the reference's gather) on the same queries."""
+    dg, hg = rmat12
+    schema = [i % 5 for i in range(40)]
+    fast = E.run_sequential(dg, QuerySpec.one_per_vertex(), MetaPathProgram(schema),
+                            ExecOptions(seed=4))
+    want = PortOracle().run(hg, QuerySpec.one_per_vertex(), MetaPathProgram(schema),
+                            ExecOptions(seed=4), threads=4)
+    assert fast.walks.equals(want.walks)
+
+
+def test_results_independent_of_launch_and_repeat(rmat12):
+    dg, _ = rmat12
+    prog = Node2VecProgram(2.0, 0.5, 30, False)
+    a = E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, ExecOptions(seed=8))
+    b = E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, ExecOptions(seed=8, k=1, k_prime=1))
+    assert a.walks.equals(b.walks)
+
+
+def test_session_launch_chunks_equal_whole_run(rmat12):
+    """Query ranges launched separately (the multi-GPU shard path) reproduce the
+    whole run: walks depend only on (seed, qid)."""
+    import torch
+    dg, hg = rmat12
+    prog = DeepWalkProgram(20, True)
+    opts = ExecOptions(seed=13)
+    whole = E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, opts).walks
+    sess = E.Session(dg, prog, opts)
+    n = hg.vertex_count
+    paths = torch.zeros(n * 20, dtype=torch.int32, device="cuda")
+    lens = torch.zeros(n, dtype=torch.int32, device="cuda")
+    st = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bounds = [0, 1000, 1001, 2500, n]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        sess.launch(QuerySpec.one_per_vertex(), lo, hi, paths.data_ptr() + lo * 20 * 4, 20,
+                    lens.data_ptr() + lo * 4, st.data_ptr() + lo, 0, steps.data_ptr())
+    sess.sync()
+    rows = paths.view(n, 20).cpu().numpy().view(np.uint32)
+    L = lens.cpu().numpy()
+    assert np.array_equal(L, whole.lengths())
+    for q in range(0, n, 7):
+        assert np.array_equal(rows[q, :L[q]], whole.path(q))
+    assert int(steps.item()) == int(whole.lengths().sum() - n)
+
+
+def test_errors_surface_as_reference_classes(rmat12):
+    dg, hg = rmat12
+    with pytest.raises(abi.ConfigError):
+        E.Session(dg, MetaPathProgram([0, 1]), ExecOptions(sampler=abi.Sampler.OREJ))
+    with pytest.raises(abi.ConfigError):
+        E.Session(dg, DeepWalkProgram(5, True), ExecOptions(sampler=abi.Sampler.NAIVE))
+    with pytest.raises(abi.ConfigError):
+        E.run_sequential(dg, QuerySpec.from_source(hg.vertex_count + 3, 4), PprProgram(0.2))
+    # a trial cap the bound cannot meet: RejectionCapError raised after the sync
+    with pytest.raises(abi.RejectionCapError):
+        E.run_sequential(dg, QuerySpec.one_per_vertex(), Node2VecProgram(0.01, 0.5, 10, False),
+                         ExecOptions(seed=1, rej_trial_cap=1))
+
+
+def test_graph_validation_like_from_csr():
+    from paper_2107_11983_b200.host import Graph
+    bad = Graph(np.array([0, 2, 1], np.uint64), np.array([1, 0], np.uint32))
+    with pytest.raises(abi.ConfigError):
+        E.DeviceGraph.from_host(bad)
+    bad2 = Graph(np.array([0, 1, 2], np.uint64), np.array([1, 5], np.uint32))
+    with pytest.raises(abi.ConfigError):
+        E.DeviceGraph.from_host(bad2)
+    bad3 = Graph(np.array([0, 1, 2], np.uint64), np.array([1, 0], np.uint32),
+                 np.array([1.0, -2.0], np.float32))
+    with pytest.raises(abi.ConfigError):
+        E.DeviceGraph.from_host(bad3)
+
+
+def test_has_edge_matches_reference(rmat12):
+    dg, hg = rmat12
+    rng = np.random.default_rng(1)
+    src = rng.integers(0, hg.vertex_count, 5000)
+    dst = np.where(rng.random(5000) < 0.5, rng.integers(0, hg.vertex_count, 5000),
+                   [hg.neighbors_of(int(s))[0] if hg.degree(int(s)) else 0 for s in src])
+    got = dg.has_edge(src, dst)
+    want = np.array([d in set(hg.neighbors_of(int(s)).tolist()) for s, d in zip(src, dst)])
+    assert np.array_equal(got, want)
