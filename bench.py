@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark: RW steps/sec of the B200 walk engine (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+                    [--impl ours|reference] [--no-extras]
+
+One "step" = one pass of the hot path over one batch of queries of the named
+configuration (BASELINE.json `configs`, SURVEY §8 d shorthand):
+
+  c1  DeepWalk s16 weighted ALIAS, one walk per vertex, L=80
+  c2  PPR s20, NAIVE, 2^20 uniform random sources, stop 0.2, + visit counts  [default]
+  c3  Node2Vec s22 (a=2, b=0.5) O-REJ, one walk per vertex, L=80
+  c4  MetaPath s22, 5 labels, schema [i%5]x79, one walk per vertex
+  c5  DeepWalk s26 weighted ALIAS, 2^26 walks, L=80
+
+Graphs are synthetic R-MAT (a,b,c,d = .57/.19/.19/.05, edge factor 16, seed 1)
+generated on the device; the paper's real graphs are not in this container.
+
+value     device-resident throughput: moves / s, inputs in HBM, CUDA events on
+          the launching stream, max over ranks.
+e2e       same metric through the C-ABI call that returns walks in HOST memory
+          (wf_session_run_host): H2D of the step's source list from pinned host
+          memory + D2H of the whole walk set (ragged) into pinned host memory.
+roofline  algorithmic bytes per launch (S_alg x moves) / mean launch time vs the
+          measured HBM copy bandwidth (MEASURED_PEAKS.json).
+cpu_baseline  the unmodified reference (oracle/_ref, run_interleaved k=64 k'=32,
+          all host threads, no-op sink) on a bounded sample, rank 0 at N=1.
+
+Multi-GPU (torchrun): graph replicated per rank, queries sharded in contiguous
+qid blocks (worker_range, engine.hpp:296-298); every rank walks its own batch of
+the configured size (weak scaling); PPR visit counts are summed with one NCCL
+all-reduce inside the timed step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RW steps/sec at 1/2/4/8 B200 per algorithm; % of HBM random-access roofline"
+SECTOR = 32
+
+CONFIGS = {
+    "c1": dict(workload="C1 DeepWalk R-MAT s16 ef16, weighted f32 [1,5), ALIAS tables, one walk "
+                        "per vertex, length 80, seed 1", scale=16, program="deepwalk", length=80,
+               weighted=True, labels=0, queries="per_vertex"),
+    "c2": dict(workload="C2 PPR R-MAT s20 ef16, unweighted, NAIVE, 2^20 uniform random sources, "
+                        "stop 0.2, walks + visit counts", scale=20, program="ppr", weighted=False,
+               labels=0, queries="random", n_queries=1 << 20),
+    "c3": dict(workload="C3 Node2Vec R-MAT s22 ef16, p=a=2 q=b=0.5, O-REJ, one walk per vertex, "
+                        "length 80", scale=22, program="node2vec", length=80, weighted=False,
+               labels=0, queries="per_vertex"),
+    "c4": dict(workload="C4 MetaPath R-MAT s22 ef16, labels u8 {0..4}, f32 weights (unused), "
+                        "schema [i%5]x79, one walk per vertex", scale=22, program="metapath",
+               weighted=True, labels=5, queries="per_vertex"),
+    "c5": dict(workload="C5 DeepWalk R-MAT s26 ef16, weighted f32 [1,5), ALIAS tables, 2^26 walks, "
+                        "length 80", scale=26, program="deepwalk", length=80, weighted=True,
+               labels=0, queries="per_vertex"),
+}
+
+# CPU-baseline samples (queries), sized for ~10-30 s of reference work on 16 cores
+CPU_SAMPLE = {"c1": 1 << 16, "c2": 1 << 20, "c3": 1 << 20, "c4": 1 << 15, "c5": 1 << 22}
+
+
+def program_of(cfg):
+    from paper_2107_11983_b200.host import (DeepWalkProgram, MetaPathProgram, Node2VecProgram,
+                                            PprProgram)
+    p = cfg["program"]
+    if p == "deepwalk":
+        return DeepWalkProgram(cfg["length"], cfg["weighted"])
+    if p == "ppr":
+        return PprProgram(0.2)
+    if p == "node2vec":
+        return Node2VecProgram(2.0, 0.5, cfg["length"], False)
+    return MetaPathProgram([i % 5 for i in range(79)])
+
+
+def row_capacity(cfg):
+    if cfg["program"] == "ppr":
+        return 64
+    if cfg["program"] == "metapath":
+        return 80
+    return cfg["length"]
+
+
+def query_plan(cfg, V, rank, world):
+    """(QuerySpec over the whole job, qid_begin, qid_end) for this rank."""
+    from paper_2107_11983_b200.host import QuerySpec
+    if cfg["queries"] == "random":
+        per = cfg["n_queries"]
+        total = per * world  # weak scaling: each rank its own batch of 2^20
+        src = np.random.default_rng(1).integers(0, V, total, dtype=np.uint32)
+        spec = QuerySpec.from_list(src)
+        lo, hi = per * rank, per * (rank + 1)
+    else:
+        # one walk per vertex; the vertex list is sharded (C5: 2^26 walks split
+        # evenly).  FROM_LIST with sources[q] = q is the same walk set as
+        # one_per_vertex and gives the e2e path a real H2D input.
+        spec = QuerySpec.from_list(np.arange(V, dtype=np.uint32))
+        lo, hi = V * rank // world, V * (rank + 1) // world
+    return spec, lo, hi
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def s_alg_bytes(cfg, stats, moves):
+    """Algorithmic bytes per move (SURVEY §8 d, restated for our layout):
+    packed 8 B vertex word = 1 sector (never straddles), 16 B alias bucket = 1
+    sector, neighbour id = 1 sector, 32 B MetaPath label record = 1 sector,
+    path entry 4 B = 1/8 sector; O-REJ adds 1 sector per trial's neighbour load
+    and 1 per adjacency-search probe (instrumented counts)."""
+    p = cfg["program"]
+    if p in ("deepwalk", "ppr", "metapath"):
+        return 2.125 * SECTOR, "vertex word + bucket/neighbour (+label record) + path, 2.125 sectors"
+    trials = stats["trials"] / max(moves, 1)
+    probes = stats["probes"] / max(moves, 1)
+    sectors = 1.0 + trials + probes + 0.125
+    return sectors * SECTOR, (f"vertex word + {trials:.3f} trial neighbour loads + {probes:.3f} "
+                              f"search probes + path = {sectors:.3f} sectors")
+
+
+def flush_l2(buf):
+    buf.add_(1)
+
+
+def run_ours(args, cfg, rank, world, local_rank, dist):
+    import torch
+
+    from paper_2107_11983_b200 import engine as E
+    from paper_2107_11983_b200.host import ExecOptions
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    t_setup = time.time()
+    dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
+                            label_count=cfg["labels"], device=dev)
+    info = dg.info()
+    V = info["V"]
+    prog = program_of(cfg)
+    opts = ExecOptions(seed=1, path_stride=row_capacity(cfg))
+    sess = E.Session(dg, prog, opts)
+    sampler, flow, pre_s = sess.describe()
+    spec, lo, hi = query_plan(cfg, V, rank, world)
+    n = hi - lo
+    stride = row_capacity(cfg)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    d_src = torch.from_numpy(spec.sources.view(np.int32)).to(f"cuda:{dev}")
+    paths = torch.empty(n * stride, dtype=torch.int32, device=dev)
+    lens = torch.empty(n, dtype=torch.int32, device=dev)
+    stat = torch.empty(n, dtype=torch.uint8, device=dev)
+    steps = torch.zeros(1, dtype=torch.int64, device=dev)
+    over = torch.zeros(1, dtype=torch.int64, device=dev)
+    counts = torch.zeros(V, dtype=torch.int32, device=dev) if cfg["program"] == "ppr" else None
+    small = cfg["scale"] <= 20  # working set near L2 size: flush between steps
+    l2buf = torch.zeros((256 << 20) // 4, dtype=torch.float32, device=dev) if small else None
+
+    def one_step():
+        steps.zero_()
+        if counts is not None:
+            counts.zero_()
+        sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), stat.data_ptr(),
+                    counts.data_ptr() if counts is not None else 0, steps.data_ptr(),
+                    over.data_ptr(), sptr, sources_dev_ptr=d_src.data_ptr())
+        if counts is not None and world > 1:
+            dist.all_reduce(counts)  # NCCL: the one collective of the path
+
+    # logical access counts for S_alg (one instrumented pass, untimed)
+    sess.set_stats(True)
+    one_step()
+    sess.sync(sptr)
+    stats = sess.stats()
+    moves_per_step = int(steps.item())
+    sess.set_stats(False)
+    for _ in range(args.warmup):
+        one_step()
+    sess.sync(sptr)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+
+    launches0 = E.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            if small:
+                flush_l2(l2buf)
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev[k][0].record(stream)
+            one_step()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize()
+    sess.sync(sptr)
+    launches = E.kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    assert int(steps.item()) == moves_per_step, "walks are deterministic per step"
+
+    # end to end through the C-ABI with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        cap = n * stride  # >= total vertices: rows hold whole walks; PPR averages ~5
+        h_src = torch.from_numpy(spec.sources.view(np.int32)).pin_memory()
+        h_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        h_vert = torch.empty(cap, dtype=torch.int32).pin_memory()
+        h_stat = torch.empty(n, dtype=torch.uint8).pin_memory()
+        from paper_2107_11983_b200.host import QuerySpec
+        hspec = QuerySpec.from_list(spec.sources)
+        hspec_c_sources = h_src  # keep alive
+        hspec.sources = h_src.numpy().view(np.uint32)
+        for _ in range(1):
+            sess.run_host(hspec, h_off.data_ptr(), h_vert.data_ptr(), cap, h_stat.data_ptr(),
+                          qid_begin=lo, qid_end=hi)
+        e2e_s = []
+        for _ in range(args.steps):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m = sess.run_host(hspec, h_off.data_ptr(), h_vert.data_ptr(), cap, h_stat.data_ptr(),
+                              qid_begin=lo, qid_end=hi)
+            e2e_s.append(time.perf_counter() - t0)
+        total_vertices = int(h_off[n].item())
+        assert m.total_steps == moves_per_step
+        e2e = dict(seconds=float(sum(e2e_s)), h2d=n * 4, d2h=total_vertices * 4 + (n + 1) * 8 + n)
+        del hspec_c_sources
+
+    return dict(moves=moves_per_step, total_ms=total_ms, step_ms=step_ms, stats=stats,
+                launches=launches, clocks=clk.summary(), info=info, sampler=sampler.name,
+                flow=flow.name, preprocess_s=pre_s, setup_s=setup_s, e2e=e2e, n=n, dg=dg,
+                spec=spec, sess=sess)
+
+
+def cpu_baseline(key, cfg, dg, spec, threads=None):
+    """The unmodified reference (oracle/_ref) on a bounded sample — measurement
+    only; never on the product path."""
+    from oracle.oracle import PortOracle, RefOracle, ref_available
+    from paper_2107_11983_b200.host import ExecOptions, QuerySpec
+    threads = threads or os.cpu_count()
+    m = min(CPU_SAMPLE[key], spec.count)
+    sample = QuerySpec.from_list(spec.sources[:m])
+    hg = dg.download()
+    prog = program_of(cfg)
+    opts = ExecOptions(seed=1, threads=threads)
+    if ref_available():
+        rg = RefOracle().graph(hg)
+        del hg
+        res = rg.run(sample, prog, opts, interleaved=True, discard=True)
+        kind = "reference"
+    else:
+        res = PortOracle().run(hg, sample, prog, opts, threads=threads, discard=True)
+        kind = "port"
+    rate = res.metrics.total_steps / max(res.metrics.exec_seconds, 1e-9)
+    return dict(value=rate, unit="steps/s", cores=threads, kind=kind,
+                sample=f"first {m} of the config's queries ({res.metrics.total_steps} moves, "
+                       f"{res.metrics.exec_seconds:.2f} s exec, preprocess "
+                       f"{res.metrics.preprocess_seconds:.2f} s excluded as in engine.hpp:455,498), "
+                       f"run_interleaved k=64 k'=32, {threads} threads, no-op sink")
+
+
+def extras(args, rank, world, local_rank, dist):
+    """GPU-only numbers for the other configs (not bench lines; evidence)."""
+    out = {}
+    for key in ["c1", "c3", "c4", "c5"]:
+        if key == args.config:
+            continue
+        try:
+            a = argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 1, "no_e2e": True})
+            r = run_ours(a, CONFIGS[key], rank, world, local_rank, dist)
+            ms = r["total_ms"] / 3
+            b, _ = s_alg_bytes(CONFIGS[key], r["stats"], r["moves"])
+            peak, _ = measured_peak()
+            ach = r["moves"] * b / (ms * 1e-3) / 1e9
+            out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=r["moves"] / (ms * 1e-3),
+                            ms_per_step=ms, moves=r["moves"], achieved_gbs=ach,
+                            roofline_frac=ach / peak, bytes_per_move=b, E=r["info"]["E"])
+            del r
+            import torch
+            torch.cuda.empty_cache()
+        except Exception as e:  # evidence only; never fail the headline
+            out[key] = dict(error=f"{type(e).__name__}: {e}")
+    return out
+
+
+def reference_arm(args, cfg, rank, world):
+    """--impl reference: the reference's own CPU path, rank 0 only."""
+    if rank != 0:
+        return
+    from oracle.oracle import PortOracle, RefOracle, ref_available
+    from paper_2107_11983_b200 import engine as E
+    from paper_2107_11983_b200.host import ExecOptions, QuerySpec
+    threads = os.cpu_count()
+    # input preparation: the same seeded R-MAT CSR the GPU arm walks on
+    dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
+                            label_count=cfg["labels"], device=0)
+    V = dg.info()["V"]
+    spec, lo, hi = query_plan(cfg, V, 0, 1)
+    hg = dg.download()
+    del dg
+    m = min(CPU_SAMPLE[args.config], hi - lo)
+    sample = QuerySpec.from_list(spec.sources[:m])
+    prog = program_of(cfg)
+    opts = ExecOptions(seed=1, threads=threads)
+    kind = "reference" if ref_available() else "port"
+    if kind == "reference":
+        rg = RefOracle().graph(hg)
+        del hg
+        run = lambda: rg.run(sample, prog, opts, interleaved=True, discard=True)  # noqa: E731
+    else:
+        po = PortOracle()
+        run = lambda: po.run(hg, sample, prog, opts, threads=threads, discard=True)  # noqa: E731
+    for _ in range(args.warmup):
+        run()
+    moves = 0
+    secs = 0.0
+    for _ in range(args.steps):
+        r = run()
+        moves += r.metrics.total_steps
+        secs += r.metrics.exec_seconds
+    value = moves / secs
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic R-MAT",
+        "config": {"workload": cfg["workload"], "sample_queries": m}, "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": kind,
+                         "sample": f"first {m} queries per step, run_interleaved k=64 k'=32, "
+                                   f"no-op sink, preprocessing excluded (engine.hpp:455,498)"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        reference_arm(args, cfg, rank, world)
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        dist = tdist
+
+    r = run_ours(args, cfg, rank, world, local_rank, dist)
+    total_ms = r["total_ms"]
+    moves = r["moves"]
+    e2e_s = r["e2e"]["seconds"] if r["e2e"] else None
+    if dist:
+        t = torch.tensor([total_ms, e2e_s or 0.0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_max = float(t[0]), float(t[1])
+        mv = torch.tensor([moves], dtype=torch.int64, device="cuda")
+        dist.all_reduce(mv)
+        all_moves = int(mv.item())
+    else:
+        e2e_max = e2e_s
+        all_moves = moves
+    value = all_moves * args.steps / (total_ms * 1e-3)
+
+    peak, peak_kind = measured_peak()
+    b, b_desc = s_alg_bytes(cfg, r["stats"], moves)
+    mean_launch_s = total_ms / args.steps * 1e-3
+    achieved = moves * b / mean_launch_s / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(args.config)
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic R-MAT (seed 1) generated on device; paper graphs not available",
+        "config": {"workload": cfg["workload"], "queries_per_gpu": r["n"],
+                   "vertices": r["info"]["V"], "edges": r["info"]["E"],
+                   "sampler": r["sampler"], "flow": r["flow"],
+                   "parallelism": f"query shards x{world}, graph replicated",
+                   "l2": "flushed between steps (256 MiB write)" if cfg["scale"] <= 20
+                   else "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "bytes_per_move": b, "bytes_model": b_desc},
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "preprocess_seconds": r["preprocess_s"],
+    }
+    if r["e2e"]:
+        line["e2e"] = {"value": all_moves * args.steps / e2e_max, "unit": "steps/s",
+                       "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"],
+                       "api": "wf_session_run_host (pinned host buffers)"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config, cfg, r["dg"], r["spec"])
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {e}"}
+    if world == 1 and not args.no_extras:
+        del r
+        torch.cuda.empty_cache()
+        line["per_algorithm"] = extras(args, rank, world, local_rank, dist)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

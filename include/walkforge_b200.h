@@ -223,10 +223,20 @@ int wf_session_sync(wf_session* s, void* stream);
  * Queries run in chunks of `chunk_queries` (0 = auto); chunk k's walks are
  * compacted and copied to the host while chunk k+1 runs.  Pinned host memory
  * gives full copy bandwidth.  A FROM_LIST spec takes a HOST source list.
+ * Only queries [qid_begin, qid_end) run (qid_end 0 = all; a shard of a
+ * multi-GPU job); outputs are indexed relative to qid_begin.
  * WF_ERR_INVALID_ARG if the walks need more than vertices_capacity entries. */
-int wf_session_run_host(wf_session* s, const wf_query_spec* spec, uint64_t* offsets,
-                        uint32_t* vertices, uint64_t vertices_capacity, uint8_t* status,
-                        uint64_t chunk_queries, wf_run_metrics* metrics);
+int wf_session_run_host(wf_session* s, const wf_query_spec* spec, uint64_t qid_begin,
+                        uint64_t qid_end, uint64_t* offsets, uint32_t* vertices,
+                        uint64_t vertices_capacity, uint8_t* status, uint64_t chunk_queries,
+                        wf_run_metrics* metrics);
+
+/* Instrumentation (measurement only; no reference counterpart): when enabled,
+ * launches accumulate logical access counts used for the algorithmic sector
+ * figure of SURVEY §8 d — out[0] rejection trials, out[1] adjacency-search
+ * probes, out[2] edges scanned by per-step gathers.  Reading resets them. */
+int wf_session_set_stats(wf_session* s, int enable);
+int wf_session_stats(wf_session* s, uint64_t* out3);
 
 /* ---- walk sets: WalkSet (walker.hpp:47-55) -------------------------------- */
 int wf_walkset_info(const wf_walkset* w, uint64_t* n_queries, uint64_t* total_vertices,

@@ -163,13 +163,13 @@ class RefOracle:
 
     # -- graphs ------------------------------------------------------------------
     def graph(self, g: Graph) -> "RefGraph":
-        w64 = None if g.weights is None else g.weights.astype(np.float64)
-        lab = None if g.labels is None else g.labels.astype(np.uint32)
+        """Graph::from_csr over the device formats (f32 weights widened to f64,
+        u8 labels widened to u32 inside the reference's own vectors)."""
         h = C.c_void_p()
-        self._check(self.lib.wfref_graph_create(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
-                                                _ptr(w64, _f64p), _ptr(lab, _u32p),
-                                                C.c_uint32(g.vertex_count),
-                                                C.c_uint64(g.edge_count), C.byref(h)))
+        self._check(self.lib.wfref_graph_create_f32(
+            _ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p), _ptr(g.weights, _f32p),
+            _ptr(g.labels, _u8p), C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),
+            C.byref(h)))
         return RefGraph(self, h)
 
     def power_law(self, vertex_count, edge_count, seed, exponent=0.8, weighted=False,

@@ -146,6 +146,22 @@ int wfref_graph_create(const uint64_t* offsets, const uint32_t* neighbors, const
     });
 }
 
+// Same, from f32 weights and u8 labels (the device formats), widened while
+// filling the reference's vectors so no f64 copy exists outside them.
+int wfref_graph_create_f32(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
+                           const uint8_t* labels, uint32_t vertex_count, uint64_t edge_count,
+                           void** out) {
+    return guarded([&] {
+        std::vector<uint64_t> off(offsets, offsets + vertex_count + 1);
+        std::vector<VertexId> nbr(neighbors, neighbors + edge_count);
+        std::vector<double> w;
+        std::vector<uint32_t> l;
+        if (weights) w.assign(weights, weights + edge_count);
+        if (labels) l.assign(labels, labels + edge_count);
+        *out = new Graph(Graph::from_csr(std::move(off), std::move(nbr), std::move(w), std::move(l)));
+    });
+}
+
 int wfref_graph_build(uint32_t vertex_count, const uint32_t* edge_pairs, uint64_t n_edges,
                       const double* weights, const uint32_t* labels, void** out) {
     return guarded([&] {

@@ -203,7 +203,8 @@ EXPORTED_SYMBOLS = [
     "wf_graph_create", "wf_graph_create_device", "wf_graph_generate_rmat",
     "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_destroy",
     "wf_session_create", "wf_session_describe", "wf_session_destroy", "wf_session_run",
-    "wf_session_launch", "wf_session_sync", "wf_session_run_host",
+    "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_set_stats",
+    "wf_session_stats",
     "wf_walkset_info", "wf_walkset_copy", "wf_walkset_visit_counts", "wf_walkset_destroy",
     "wf_run", "wf_rng_probe", "wf_session_tables",
 ]

@@ -498,28 +498,57 @@ int wf_session_run(wf_session* sh, const wf_query_spec* spec, wf_walkset** out,
     });
 }
 
-int wf_session_run_host(wf_session* sh, const wf_query_spec* spec, uint64_t* offsets,
-                        uint32_t* vertices, uint64_t vertices_capacity, uint8_t* status,
-                        uint64_t chunk_queries, wf_run_metrics* metrics) {
+int wf_session_run_host(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin,
+                        uint64_t qid_end, uint64_t* offsets, uint32_t* vertices,
+                        uint64_t vertices_capacity, uint8_t* status, uint64_t chunk_queries,
+                        wf_run_metrics* metrics) {
     return guarded([&] {
         require(sh && spec && vertices, "null argument");
         Session& s = *sh->s;
         GraphStore& g = *s.g;
         DeviceGuard guard(g.device);
         uint64_t n = spec->mode == WF_QUERY_ONE_PER_VERTEX ? g.V : spec->count;
+        if (qid_end == 0) qid_end = n;
+        require(qid_begin <= qid_end && qid_end <= n, "query range out of bounds");
         if (spec->mode == WF_QUERY_FROM_SOURCE && spec->source >= g.V)
             config_error("query source " + std::to_string(spec->source) + " is not a vertex (V=" +
                          std::to_string(g.V) + ")");
         if (spec->mode == WF_QUERY_FROM_LIST) {
             require(spec->sources != nullptr || n == 0, "null source list");
             require(!is_device_pointer(spec->sources), "wf_session_run_host takes a host source list");
-            for (uint64_t i = 0; i < n; ++i)
+            for (uint64_t i = qid_begin; i < qid_end; ++i)
                 if (spec->sources[i] >= g.V)
                     config_error("query source " + std::to_string(spec->sources[i]) +
                                  " is not a vertex (V=" + std::to_string(g.V) + ")");
         }
-        run_to_host(s, *spec, spec->sources, n, offsets, vertices, vertices_capacity, status,
-                    chunk_queries, metrics);
+        run_to_host(s, *spec, spec->sources, qid_begin, qid_end, offsets, vertices,
+                    vertices_capacity, status, chunk_queries, metrics);
+    });
+}
+
+int wf_session_set_stats(wf_session* sh, int enable) {
+    return guarded([&] {
+        require(sh != nullptr, "null session");
+        Session& s = *sh->s;
+        DeviceGuard guard(s.g->device);
+        if (enable && !s.stats.get()) {
+            s.stats.allocate(3);
+            WF_CUDA(cudaMemset(s.stats.get(), 0, 24));
+        }
+        s.collect_stats = enable != 0;
+    });
+}
+
+int wf_session_stats(wf_session* sh, uint64_t* out3) {
+    return guarded([&] {
+        require(sh && out3, "null argument");
+        Session& s = *sh->s;
+        DeviceGuard guard(s.g->device);
+        out3[0] = out3[1] = out3[2] = 0;
+        if (!s.stats.get()) return;
+        WF_CUDA(cudaDeviceSynchronize());
+        WF_CUDA(cudaMemcpy(out3, s.stats.get(), 24, cudaMemcpyDeviceToHost));
+        WF_CUDA(cudaMemset(s.stats.get(), 0, 24));
     });
 }
 

@@ -81,6 +81,7 @@ struct WalkLaunch {
     double* scratch;  // gathered ALIAS: per-lane park area
     uint64_t scratch_stride;
     int use_label_index;
+    unsigned long long* stats;  // optional: [trials, search probes, scanned edges]
 };
 
 struct Walker {
@@ -91,6 +92,9 @@ struct Walker {
     uint32_t cur, prev;
     uint32_t cur_deg, prev_deg;
     uint32_t len;  // vertices on the path so far (moves + 1)
+    // lane-level logical access counters (survive refills); flushed to
+    // WalkLaunch::stats when requested — the instrumented S_alg of SURVEY §8 d
+    mutable uint32_t n_trials, n_probes, n_scanned;
 };
 
 // ---- graph helpers -------------------------------------------------------------
@@ -109,19 +113,23 @@ __device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t
 // Graph::has_edge (graph.cpp:182-188): std::binary_search on sorted lists,
 // linear scan otherwise.  Membership only, so any exact search is equivalent.
 __device__ __forceinline__ bool has_edge(const GraphView& g, uint64_t base, uint32_t deg,
-                                         uint32_t dst) {
+                                         uint32_t dst, uint32_t* probes = nullptr) {
     const uint32_t* ns = g.nbr + base;
+    uint32_t np = 0;
+    bool found = false;
     if (g.sorted) {
         uint32_t lo = 0, hi = deg;
         while (lo < hi) {
             uint32_t mid = (lo + hi) >> 1;
+            ++np;
             if (__ldg(ns + mid) < dst) lo = mid + 1; else hi = mid;
         }
-        return lo < deg && __ldg(ns + lo) == dst;
+        found = lo < deg && (++np, __ldg(ns + lo) == dst);
+    } else {
+        for (uint32_t i = 0; i < deg && !found; ++i, ++np) found = __ldg(ns + i) == dst;
     }
-    for (uint32_t i = 0; i < deg; ++i)
-        if (__ldg(ns + i) == dst) return true;
-    return false;
+    if (probes) *probes += np;
+    return found;
 }
 
 // cumulative_upper_index, sampler.hpp:48-60.
@@ -203,7 +211,7 @@ struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
         } else {
             uint32_t dst = __ldg(g.nbr + e);
             if (dst == q.prev) w = p.inv_a;
-            else if (has_edge(g, q.prev_base, q.prev_deg, dst)) w = 1.0;
+            else if (has_edge(g, q.prev_base, q.prev_deg, dst, &q.n_probes)) w = 1.0;
             else w = p.inv_b;
         }
         return p.weighted ? __dmul_rn(w, static_cast<double>(__ldg(g.weights + e))) : w;
@@ -259,7 +267,7 @@ __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunc
     if (dst == q.prev) return y < scaled(p.inv_a);
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
-    bool common = has_edge(L.g, q.prev_base, q.prev_deg, dst);
+    bool common = has_edge(L.g, q.prev_base, q.prev_deg, dst, &q.n_probes);
     return y < scaled(common ? 1.0 : p.inv_b);
 }
 
@@ -346,6 +354,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                     raise_device(L, WF_ERR_REJECTION_CAP);
                     return kFault;
                 }
+                ++q.n_trials;
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(L.prog.bound);
                 if (orej_accept<K>(L, q, base + x, y)) { pick = x; break; }
@@ -370,6 +379,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                     raise_device(L, WF_ERR_REJECTION_CAP);
                     return kFault;
                 }
+                ++q.n_trials;
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(ps);
                 if (y < P::weight_static(L.prog, L.g, base + x)) { pick = x; break; }
@@ -389,6 +399,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             }
         }
         double sum = 0.0, mx = 0.0;
+        q.n_scanned += d;
         for (uint32_t i = 0; i < d; ++i) {
             double w = P::weight(L.prog, L.g, q, base + i);
             sum += w;
@@ -419,6 +430,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                     raise_device(L, WF_ERR_REJECTION_CAP);
                     return kFault;
                 }
+                ++q.n_trials;
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(mx);
                 if (y < P::weight(L.prog, L.g, q, base + x)) { pick = x; break; }
@@ -489,6 +501,7 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
     q.cur_base = q.prev_base = 0;
     q.len = 0;
     q.rng.s = 0;
+    q.n_trials = q.n_probes = q.n_scanned = 0;
     bool active = false;
     bool drained = false;
     unsigned long long steps = 0;
@@ -550,6 +563,19 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
     // one atomic per warp for the step total
     for (int o = 16; o > 0; o >>= 1) steps += __shfl_xor_sync(kFull, steps, o);
     if (lane == 0 && steps) atomicAdd(L.steps_out, steps);
+    if (L.stats) {
+        unsigned long long t = q.n_trials, pr = q.n_probes, sc = q.n_scanned;
+        for (int o = 16; o > 0; o >>= 1) {
+            t += __shfl_xor_sync(kFull, t, o);
+            pr += __shfl_xor_sync(kFull, pr, o);
+            sc += __shfl_xor_sync(kFull, sc, o);
+        }
+        if (lane == 0) {
+            atomicAdd(L.stats, t);
+            atomicAdd(L.stats + 1, pr);
+            atomicAdd(L.stats + 2, sc);
+        }
+    }
 }
 
 }  // namespace wf

@@ -88,6 +88,8 @@ struct Session {
     DeviceBuffer<double> scratch;
     uint64_t scratch_stride = 0;
     int grid = 0;
+    bool collect_stats = false;
+    DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
 
     void build_tables(cudaStream_t st);
 };
@@ -134,8 +136,8 @@ struct WidenU64 {
 };
 
 // stream.cu: pipelined run + copy of the walk set into host buffers
-void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t n,
-                 uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
+void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
+                 uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics);
 
 // walk set copy-out (walk.cu)

@@ -53,12 +53,13 @@ struct Events {
 
 }  // namespace
 
-void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t n,
-                 uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
+void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
+                 uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics) {
     GraphStore& g = *s.g;
     DeviceGuard guard(g.device);
     const uint32_t stride = s.default_stride;
+    const uint64_t n = qe - qb;
     if (chunk == 0) chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (4ull * stride)));
     chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
     Streams st;
@@ -67,10 +68,13 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     Events evs;
     auto t0 = std::chrono::steady_clock::now();
 
+    // the shard's slice of the source list, addressed by absolute qid in the kernel
     DeviceBuffer<uint32_t> d_src;
+    const uint32_t* src_by_qid = nullptr;
     if (spec.mode == WF_QUERY_FROM_LIST && n) {
         d_src.allocate(n);
-        WF_CUDA(cudaMemcpyAsync(d_src.get(), host_sources, n * 4, cudaMemcpyHostToDevice, st.a));
+        WF_CUDA(cudaMemcpyAsync(d_src.get(), host_sources + qb, n * 4, cudaMemcpyHostToDevice, st.a));
+        src_by_qid = d_src.get() - qb;
     }
     DeviceBuffer<uint32_t> rows[2], lens[2], stage[2];
     DeviceBuffer<uint8_t> stat[2];
@@ -107,7 +111,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
         // buffer b (status / offsets / staging) is free once chunk k-2's copy drained
         if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(st.a, ev_copy[b], 0));
-        launch_walk(s, spec, d_src.get(), r0, r1, nullptr, rows[b].get(), stride, lens[b].get(),
+        launch_walk(s, spec, src_by_qid, qb + r0, qb + r1, nullptr, rows[b].get(), stride, lens[b].get(),
                     stat[b].get(), nullptr, ctr.get(), ctr.get() + 1, s.cursor.get(), st.a);
         cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(lens[b].get(), WidenU64{});
         WF_CUDA(cub::DeviceScan::InclusiveSum(scan_tmp.get(), scan_bytes, in, offs[b].get() + 1,
@@ -172,7 +176,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         for (uint64_t r = 0; r < n; ++r) {
             uint64_t len = offsets[r + 1] - offsets[r];
             if (len > stride) {
-                qids.push_back(r);
+                qids.push_back(qb + r);
                 mx = std::max<uint32_t>(mx, static_cast<uint32_t>(len));
             }
         }
@@ -182,12 +186,12 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         DeviceBuffer<uint8_t> sst(qids.size());
         DeviceBuffer<unsigned long long> c2(2);
         WF_CUDA(cudaMemset(c2.get(), 0, 16));
-        launch_walk(s, spec, d_src.get(), 0, qids.size(), dq.get(), p.get(), mx, l.get(), sst.get(),
+        launch_walk(s, spec, src_by_qid, 0, qids.size(), dq.get(), p.get(), mx, l.get(), sst.get(),
                     nullptr, c2.get(), c2.get() + 1, s.cursor.get(), nullptr);
         std::vector<uint32_t> hp(qids.size() * static_cast<uint64_t>(mx));
         WF_CUDA(cudaMemcpy(hp.data(), p.get(), hp.size() * 4, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < qids.size(); ++i) {
-            uint64_t r = qids[i];
+            uint64_t r = qids[i] - qb;
             std::copy(hp.begin() + i * mx, hp.begin() + i * mx + (offsets[r + 1] - offsets[r]),
                       vertices + offsets[r]);
         }

@@ -255,13 +255,15 @@ class Session:
             _vp(steps_ptr or None), _vp(overflow_ptr or None), _vp(stream or None)))
 
     def run_host(self, spec: QuerySpec, offsets_ptr: int, vertices_ptr: int, capacity: int,
-                 status_ptr: int, chunk: int = 0) -> RunMetrics:
+                 status_ptr: int, chunk: int = 0, qid_begin: int = 0,
+                 qid_end: int = 0) -> RunMetrics:
         """wf_session_run_host: run and stream the walk set into HOST buffers
         (pointers; pinned memory for full bandwidth)."""
         cs = spec.to_c()
         m = RunMetricsC()
         _check(load_library().wf_session_run_host(
-            self.h, C.byref(cs), _vp(offsets_ptr or None), _vp(vertices_ptr), C.c_uint64(capacity),
+            self.h, C.byref(cs), C.c_uint64(qid_begin), C.c_uint64(qid_end),
+            _vp(offsets_ptr or None), _vp(vertices_ptr), C.c_uint64(capacity),
             _vp(status_ptr or None), C.c_uint64(chunk), C.byref(m)))
         return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
 
@@ -284,6 +286,14 @@ class Session:
         if isinstance(p, host_mod.PprProgram):
             return self.opts.path_stride or 64
         return p.target_length
+
+    def set_stats(self, enable: bool) -> None:
+        _check(load_library().wf_session_set_stats(self.h, C.c_int(1 if enable else 0)))
+
+    def stats(self) -> dict:
+        out = np.zeros(3, np.uint64)
+        _check(load_library().wf_session_stats(self.h, _ptr(out, _u64p)))
+        return dict(trials=int(out[0]), probes=int(out[1]), scanned=int(out[2]))
 
     def sync(self, stream: int = 0) -> None:
         _check(load_library().wf_session_sync(self.h, _vp(stream or None)))
