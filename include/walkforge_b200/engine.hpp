@@ -1,0 +1,347 @@
+// Header-only C++ shim: the reference's engine API (proj/include/walkforge/
+// engine.hpp, interleave.hpp, algorithms.hpp, walker.hpp, graph.hpp, error.hpp)
+// with the same names and template signatures, executed by the B200 engine
+// through the C-ABI in walkforge_b200.h.
+//
+// A caller of the reference switches by including this header instead of
+// <walkforge/engine.hpp> + <walkforge/interleave.hpp> + <walkforge/algorithms.hpp>
+// (define WALKFORGE_B200_DROP_IN to alias namespace walkforge) and linking
+// libwalkforge_b200.so.  Differences, all checked at the boundary:
+//   * weights must be exactly representable in float32 (device storage), and
+//     labels < 256 — otherwise ConfigError;
+//   * programs are the five built-ins (the device functors); custom programs are
+//     written as device functors in csrc/engine.cuh (Program<K>);
+//   * ExecOptions::threads and prefetch are accepted and ignored (lanes replace
+//     worker threads); k / k' of run_interleaved are validated then ignored.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../walkforge_b200.h"
+
+namespace walkforge_b200 {
+
+// ---- errors: error.hpp:8-48 ---------------------------------------------------------
+struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ParseError : Error { using Error::Error; };
+struct FormatError : Error { using Error::Error; };
+struct ConfigError : Error { using Error::Error; };
+struct DistributionError : Error { using Error::Error; };
+struct ContractError : Error { using Error::Error; };
+struct RejectionCapError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };
+
+inline void check(int rc) {
+    if (rc == WF_OK) return;
+    std::string m = wf_last_error();
+    switch (rc) {
+        case WF_ERR_PARSE: throw ParseError(m);
+        case WF_ERR_FORMAT: throw FormatError(m);
+        case WF_ERR_CONFIG: throw ConfigError(m);
+        case WF_ERR_DISTRIBUTION: throw DistributionError(m);
+        case WF_ERR_CONTRACT: throw ContractError(m);
+        case WF_ERR_REJECTION_CAP: throw RejectionCapError(m);
+        case WF_ERR_IO: throw IoError(m);
+        default: throw DeviceError(m);
+    }
+}
+
+using VertexId = uint32_t;
+
+// ---- sampler.hpp:21 / program.hpp:17 / walker.hpp:12 ---------------------------------
+enum class SamplerKind : uint8_t { Naive, Its, Alias, Rej, ORej };
+enum class WalkerType : uint8_t { Unbiased, Static, Dynamic };
+enum class WalkStatus : uint8_t { Complete, DeadEnd };
+
+// ---- Graph (graph.hpp:17-107), resident in HBM ---------------------------------------
+class Graph {
+public:
+    Graph() = default;
+    static Graph from_csr(std::vector<uint64_t> offsets, std::vector<VertexId> neighbors,
+                          std::vector<double> weights = {}, std::vector<uint32_t> labels = {},
+                          int device = 0) {
+        if (offsets.size() < 2) throw ConfigError("graph must have at least one vertex");
+        std::vector<float> w32(weights.size());
+        for (size_t i = 0; i < weights.size(); ++i) {
+            w32[i] = static_cast<float>(weights[i]);
+            if (std::isfinite(weights[i]) && static_cast<double>(w32[i]) != weights[i])
+                throw ConfigError("edge weights must be exactly representable in float32");
+        }
+        if (!weights.empty() && weights.size() != neighbors.size())
+            throw ConfigError("weight array does not match edge count");
+        if (!labels.empty() && labels.size() != neighbors.size())
+            throw ConfigError("label array does not match edge count");
+        wf_graph* h = nullptr;
+        check(wf_graph_create(offsets.data(), neighbors.data(), weights.empty() ? nullptr : w32.data(),
+                              labels.empty() ? nullptr : labels.data(),
+                              static_cast<uint32_t>(offsets.size() - 1), neighbors.size(), device, &h));
+        Graph g;
+        g.h_ = std::shared_ptr<wf_graph>(h, wf_graph_destroy);
+        check(wf_graph_info_get(h, &g.info_));
+        return g;
+    }
+    uint32_t vertex_count() const { return info_.vertex_count; }
+    uint64_t edge_count() const { return info_.edge_count; }
+    bool has_weights() const { return info_.has_weights != 0; }
+    bool has_labels() const { return info_.has_labels != 0; }
+    double max_weight() const { return info_.max_weight; }
+    uint64_t max_degree() const { return info_.max_degree_lo; }
+    bool adjacency_sorted() const { return info_.adjacency_sorted != 0; }
+    bool has_edge(VertexId src, VertexId dst) const {
+        uint8_t out = 0;
+        check(wf_graph_has_edge(h_.get(), &src, &dst, 1, &out));
+        return out != 0;
+    }
+    wf_graph* handle() const { return h_.get(); }
+
+private:
+    std::shared_ptr<wf_graph> h_;
+    wf_graph_info info_{};
+};
+
+// ---- walker.hpp:47-84 ------------------------------------------------------------------
+struct WalkRecord {
+    uint64_t query_id = 0;
+    WalkStatus status = WalkStatus::Complete;
+    std::vector<VertexId> path;
+    bool operator==(const WalkRecord&) const = default;
+};
+using WalkSet = std::vector<WalkRecord>;
+
+struct QuerySpec {
+    enum class Mode : uint8_t { OnePerVertex, FromSource, FromFile };
+    static QuerySpec one_per_vertex() { return {}; }
+    static QuerySpec from_source(VertexId source, uint64_t count) {
+        QuerySpec s;
+        s.mode = Mode::FromSource;
+        s.source = source;
+        s.count = count;
+        return s;
+    }
+    static QuerySpec from_list(std::vector<VertexId> sources) {
+        QuerySpec s;
+        s.mode = Mode::FromFile;
+        s.sources = std::move(sources);
+        s.count = s.sources.size();
+        return s;
+    }
+    uint64_t total(const Graph& g) const {
+        return mode == Mode::OnePerVertex ? g.vertex_count() : (mode == Mode::FromSource ? count : sources.size());
+    }
+    wf_query_spec to_c() const {
+        wf_query_spec q{};
+        q.mode = mode == Mode::OnePerVertex ? WF_QUERY_ONE_PER_VERTEX
+                 : mode == Mode::FromSource ? WF_QUERY_FROM_SOURCE : WF_QUERY_FROM_LIST;
+        q.source = source;
+        q.count = mode == Mode::FromFile ? sources.size() : count;
+        q.sources = sources.empty() ? nullptr : sources.data();
+        return q;
+    }
+    Mode mode = Mode::OnePerVertex;
+    VertexId source = 0;
+    uint64_t count = 0;
+    std::vector<VertexId> sources;
+};
+
+// ---- engine.hpp:64-89 -------------------------------------------------------------------
+struct RunMetrics {
+    double preprocess_seconds = 0.0;
+    double exec_seconds = 0.0;
+    uint64_t total_steps = 0;
+    uint32_t max_in_flight = 0;
+};
+struct RunResult {
+    WalkSet walks;
+    RunMetrics metrics;
+};
+using BlockSink = std::function<void(uint32_t worker, WalkSet&& block)>;
+enum class PrefetchLevel : uint8_t { None, L1, L2, L3 };
+struct ExecOptions {
+    uint32_t threads = 1;
+    uint64_t seed = 0;
+    std::optional<SamplerKind> sampler;
+    bool use_static_tables = true;
+    PrefetchLevel prefetch = PrefetchLevel::L1;
+    uint32_t rej_trial_cap = 1u << 20;
+    BlockSink sink;
+};
+
+// ---- algorithms.hpp:20-193: parameters; the functors run on the device ----------------
+class PprProgram {
+public:
+    explicit PprProgram(double termination = 0.2) : stop_(termination) {
+        if (!(termination > 0.0 && termination <= 1.0))
+            throw ConfigError("termination probability must be in (0, 1], got " + std::to_string(termination));
+    }
+    WalkerType walker_type() const { return WalkerType::Unbiased; }
+    double termination() const { return stop_; }
+    wf_program_desc to_desc() const {
+        wf_program_desc d{};
+        d.kind = WF_PROGRAM_PPR;
+        d.termination = stop_;
+        return d;
+    }
+
+private:
+    double stop_;
+};
+
+class DeepWalkProgram {
+public:
+    DeepWalkProgram(const Graph& g, uint32_t target_length, bool weighted)
+        : length_(target_length), weighted_(weighted) {
+        if (target_length < 1) throw ConfigError("target length must be >= 1");
+        if (weighted && !g.has_weights()) throw ConfigError("weighted walks need a graph with edge weights");
+    }
+    WalkerType walker_type() const { return WalkerType::Static; }
+    uint32_t target_length() const { return length_; }
+    wf_program_desc to_desc() const {
+        wf_program_desc d{};
+        d.kind = WF_PROGRAM_DEEPWALK;
+        d.target_length = length_;
+        d.weighted = weighted_;
+        return d;
+    }
+
+private:
+    uint32_t length_;
+    bool weighted_;
+};
+
+struct Node2VecParams {
+    double a = 2.0;
+    double b = 0.5;
+    uint32_t target_length = 80;
+};
+
+class Node2VecProgram {
+public:
+    Node2VecProgram(const Graph& g, Node2VecParams params, bool weighted)
+        : params_(params), weighted_(weighted) {
+        if (!(std::isfinite(params.a) && params.a > 0.0)) throw ConfigError("return parameter a must be positive and finite");
+        if (!(std::isfinite(params.b) && params.b > 0.0)) throw ConfigError("in-out parameter b must be positive and finite");
+        if (params.target_length < 1) throw ConfigError("target length must be >= 1");
+        if (weighted && !g.has_weights()) throw ConfigError("weighted walks need a graph with edge weights");
+    }
+    WalkerType walker_type() const { return WalkerType::Dynamic; }
+    SamplerKind preferred_sampler() const { return SamplerKind::ORej; }
+    const Node2VecParams& params() const { return params_; }
+    wf_program_desc to_desc() const {
+        wf_program_desc d{};
+        d.kind = WF_PROGRAM_NODE2VEC;
+        d.a = params_.a;
+        d.b = params_.b;
+        d.target_length = params_.target_length;
+        d.weighted = weighted_;
+        return d;
+    }
+
+private:
+    Node2VecParams params_;
+    bool weighted_;
+};
+
+class MetaPathProgram {
+public:
+    MetaPathProgram(const Graph& g, std::vector<uint32_t> schema) : schema_(std::move(schema)) {
+        if (!g.has_labels()) throw ConfigError("meta-path walks need a graph with edge labels");
+        if (schema_.empty()) throw ConfigError("meta-path schema must be non-empty");
+    }
+    WalkerType walker_type() const { return WalkerType::Dynamic; }
+    const std::vector<uint32_t>& schema() const { return schema_; }
+    wf_program_desc to_desc() const {
+        wf_program_desc d{};
+        d.kind = WF_PROGRAM_METAPATH;
+        d.schema = schema_.data();
+        d.schema_len = static_cast<uint32_t>(schema_.size());
+        return d;
+    }
+
+private:
+    std::vector<uint32_t> schema_;
+};
+
+class UniformProgram {
+public:
+    explicit UniformProgram(uint32_t target_length) : length_(target_length) {
+        if (target_length < 1) throw ConfigError("target length must be >= 1");
+    }
+    WalkerType walker_type() const { return WalkerType::Unbiased; }
+    wf_program_desc to_desc() const {
+        wf_program_desc d{};
+        d.kind = WF_PROGRAM_UNIFORM;
+        d.target_length = length_;
+        return d;
+    }
+
+private:
+    uint32_t length_;
+};
+
+// ---- run_sequential / run_interleaved (engine.hpp:440-504, interleave.hpp:391-556) ---
+namespace detail {
+template <typename P>
+RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts) {
+    wf_program_desc d = prog.to_desc();
+    wf_exec_options o{};
+    o.seed = opts.seed;
+    o.sampler = opts.sampler ? static_cast<int32_t>(*opts.sampler) : WF_SAMPLER_DEFAULT;
+    o.use_static_tables = opts.use_static_tables ? 1 : 0;
+    o.rej_trial_cap = opts.rej_trial_cap;
+    o.threads = opts.threads;
+    wf_query_spec q = spec.to_c();
+    wf_walkset* ws = nullptr;
+    wf_run_metrics m{};
+    check(wf_run(g.handle(), &d, &q, &o, &ws, &m));
+    std::unique_ptr<wf_walkset, void (*)(wf_walkset*)> guard(ws, wf_walkset_destroy);
+    uint64_t n = 0, total = 0;
+    uint32_t maxlen = 0;
+    check(wf_walkset_info(ws, &n, &total, &maxlen));
+    std::vector<uint64_t> off(n + 1);
+    std::vector<uint32_t> verts(total);
+    std::vector<uint8_t> st(n);
+    check(wf_walkset_copy(ws, 0, n, off.data(), verts.data(), st.data()));
+    RunResult r;
+    r.metrics = {m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight};
+    WalkSet walks(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        walks[i].query_id = i;
+        walks[i].status = static_cast<WalkStatus>(st[i]);
+        walks[i].path.assign(verts.begin() + off[i], verts.begin() + off[i + 1]);
+    }
+    if (opts.sink) {
+        opts.sink(0, std::move(walks));  // one device worker: one block, qid order
+    } else {
+        r.walks = std::move(walks);
+    }
+    return r;
+}
+}  // namespace detail
+
+template <typename P>
+RunResult run_sequential(const Graph& g, const QuerySpec& spec, const P& prog,
+                         const ExecOptions& opts = {}) {
+    return detail::run(g, spec, prog, opts);
+}
+
+template <typename P>
+RunResult run_interleaved(const Graph& g, const QuerySpec& spec, const P& prog, uint32_t k,
+                          uint32_t k_prime, const ExecOptions& opts = {}) {
+    if (k == 0) throw ConfigError("task ring size must be >= 1");
+    if (k_prime == 0 || k_prime > k) throw ConfigError("search ring size must be in [1, k]");
+    return detail::run(g, spec, prog, opts);
+}
+
+}  // namespace walkforge_b200
+
+#ifdef WALKFORGE_B200_DROP_IN
+namespace walkforge = walkforge_b200;
+#endif

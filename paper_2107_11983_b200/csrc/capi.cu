@@ -358,6 +358,9 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         resolve_program(s, *prog, opts);
         s.error_word.allocate(1);
         WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
+        // random 32 B gathers: do not let L2 promote misses to 64/128 B fetches
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+        cudaGetLastError();
         s.cursor.allocate(1);
         h->counters.allocate(2);
         if (s.flow == kTables) s.build_tables(nullptr);

@@ -81,6 +81,7 @@ struct WalkLaunch {
     double* scratch;  // gathered ALIAS: per-lane park area
     uint64_t scratch_stride;
     int use_label_index;
+    int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     unsigned long long* stats;  // optional: [trials, search probes, scanned edges]
 };
 
@@ -99,14 +100,24 @@ struct Walker {
 
 // ---- graph helpers -------------------------------------------------------------
 
+// Random gathers (vertex words, buckets, neighbour ids, label records): cached
+// in L2 only (ld.global.cg).  L1 hit rates on these are ~2 %, and letting L1
+// allocate them made it request 2.8x the sectors the walk needs (ncu,
+// profiles/).  Search probes keep __ldg: their last probes share a line.
+template <typename T>
+__device__ __forceinline__ T ldr(const T* p) { return __ldcg(p); }
+__device__ __forceinline__ uint64_t ldr(const uint64_t* p) {
+    return static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
+}
+
 __device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t* vw, uint32_t v,
                                               uint64_t& base, uint32_t& deg) {
-    uint64_t w = __ldg(vw + v);
+    uint64_t w = ldr(vw + v);
     base = w >> kDegBits;
     deg = static_cast<uint32_t>(w & kDegEscape);
     if (deg == kDegEscape) {  // rare: very high degree
-        base = __ldg(g.offsets + v);
-        deg = static_cast<uint32_t>(__ldg(g.offsets + v + 1) - base);
+        base = ldr(g.offsets + v);
+        deg = static_cast<uint32_t>(ldr(g.offsets + v + 1) - base);
     }
 }
 
@@ -188,7 +199,7 @@ struct Program<WF_PROGRAM_DEEPWALK> {  // algorithms.hpp:41-67
     static constexpr bool prechecked = true;
     static constexpr bool has_max_weight = true;
     __device__ static double weight_static(const ProgParams& p, const GraphView& g, uint64_t e) {
-        return p.weighted ? static_cast<double>(__ldg(g.weights + e)) : 1.0;
+        return p.weighted ? static_cast<double>(ldr(g.weights + e)) : 1.0;
     }
     __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker&,
                                     uint64_t e) {
@@ -209,12 +220,12 @@ struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
         if (q.len == 1) {
             w = p.first;
         } else {
-            uint32_t dst = __ldg(g.nbr + e);
+            uint32_t dst = ldr(g.nbr + e);
             if (dst == q.prev) w = p.inv_a;
             else if (has_edge(g, q.prev_base, q.prev_deg, dst, &q.n_probes)) w = 1.0;
             else w = p.inv_b;
         }
-        return p.weighted ? __dmul_rn(w, static_cast<double>(__ldg(g.weights + e))) : w;
+        return p.weighted ? __dmul_rn(w, static_cast<double>(ldr(g.weights + e))) : w;
     }
     __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
         return 0.0;  // never called: dynamic programs have no static tables
@@ -260,10 +271,10 @@ __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunc
                                                                  const Walker& q, uint64_t e,
                                                                  double y) {
     const ProgParams& p = L.prog;
-    double ew = p.weighted ? static_cast<double>(__ldg(L.g.weights + e)) : 1.0;
+    double ew = p.weighted ? static_cast<double>(ldr(L.g.weights + e)) : 1.0;
     auto scaled = [&](double w) { return p.weighted ? __dmul_rn(w, ew) : w; };
     if (q.len == 1) return y < scaled(p.first);
-    uint32_t dst = __ldg(L.g.nbr + e);
+    uint32_t dst = ldr(L.g.nbr + e);
     if (dst == q.prev) return y < scaled(p.inv_a);
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
@@ -363,7 +374,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
     } else if constexpr (F == kTables) {
         if constexpr (S == WF_SAMPLER_ALIAS) {
             uint32_t x = q.rng.index(d);
-            uint4 b = __ldg(L.alias + base + x);
+            uint4 b = ldr(L.alias + base + x);
             uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
             dst = q.rng.bits53() < thr ? b.z : b.w;  // y < split <=> k < ceil(split 2^53)
             return kMoved;
@@ -394,7 +405,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 // (cumulative table over 0/1 weights), which is the j-th edge of
                 // the stably partitioned group.
                 double x = q.rng.real(static_cast<double>(d));
-                dst = __ldg(L.g.lab_nbr + base + static_cast<uint32_t>(x));
+                dst = ldr(L.g.lab_nbr + base + static_cast<uint32_t>(x));
                 return kMoved;
             }
         }
@@ -437,7 +448,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             }
         }
     }
-    dst = __ldg(L.g.nbr + base + pick);
+    dst = ldr(L.g.nbr + base + pick);
     return kMoved;
 }
 
@@ -447,8 +458,8 @@ __device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
     if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
         if (L.use_label_index) {
             const uint4* rec = L.g.lab_rec + 2 * static_cast<uint64_t>(q.cur);
-            uint4 r0 = __ldg(rec);
-            uint4 r1 = __ldg(rec + 1);
+            uint4 r0 = ldr(rec);
+            uint4 r1 = ldr(rec + 1);
             uint64_t base = (static_cast<uint64_t>(r0.y) << 32) | r0.x;
             uint32_t ends[kMaxIndexedLabels] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
             uint32_t l = __ldg(L.prog.schema + (q.len - 1));
@@ -473,14 +484,43 @@ __device__ __forceinline__ uint32_t source_at(const WalkLaunch& L, uint64_t qid)
     return __ldg(L.qsources + qid);
 }
 
-__device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int st) {
+// Path rows are written a full 32 B sector at a time: each lane stages its
+// next 8 vertices in shared memory ([slot][thread], conflict-free) and stores
+// them with two 16 B vector stores when the group fills or the walk ends.
+// Single 4 B stores to 32 B-strided rows made every step a partial-sector
+// write (ncu: 4x the algorithmic DRAM write bytes).  Used when rows are
+// 32 B-aligned (stride % 8 == 0); otherwise one 4 B store per vertex.
+struct PathStage {
+    uint32_t* s;  // kBlock * 8 words
+    __device__ __forceinline__ uint32_t& at(uint32_t slot) { return s[slot * kBlock + threadIdx.x]; }
+};
+
+__device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int st, PathStage ps) {
     L.lengths[q.row] = q.len;
     L.status[q.row] = static_cast<uint8_t>(st);
+    if (L.staged) {
+        const uint32_t g0 = q.len & ~7u;
+        const uint32_t end = min(q.len, L.stride);
+        uint32_t* row = L.paths + q.row * L.stride;
+        for (uint32_t p = g0; p < end; ++p) row[p] = ps.at(p & 7);
+    }
     if (q.len > L.stride) atomicAdd(L.overflow_out, 1ULL);
 }
 
-__device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint32_t v) {
-    if (q.len < L.stride) __stcs(L.paths + q.row * L.stride + q.len, v);
+__device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint32_t v, PathStage ps) {
+    const uint32_t p = q.len;
+    if (p < L.stride) {
+        if (L.staged) {
+            ps.at(p & 7) = v;
+            if ((p & 7) == 7) {
+                uint4* dst = reinterpret_cast<uint4*>(L.paths + q.row * L.stride + (p - 7));
+                dst[0] = make_uint4(ps.at(0), ps.at(1), ps.at(2), ps.at(3));
+                dst[1] = make_uint4(ps.at(4), ps.at(5), ps.at(6), ps.at(7));
+            }
+        } else {
+            L.paths[q.row * L.stride + p] = v;
+        }
+    }
     if (L.visit_counts) atomicAdd(L.visit_counts + v, 1u);
 }
 
@@ -494,6 +534,8 @@ template <int K, int S, int F>
 __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
     using P = Program<K>;
     const int lane = threadIdx.x & 31;
+    __shared__ uint32_t stage_words[8 * kBlock];
+    PathStage ps{stage_words};
     Walker q;
     q.row = 0;
     q.cur = q.prev = 0;
@@ -525,10 +567,10 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
                     q.cur = source_at(L, qid);
                     q.prev = 0xFFFFFFFFu;
                     q.len = 0;
-                    emit(L, q, q.cur);
+                    emit(L, q, q.cur, ps);
                     q.len = 1;
                     if (P::prechecked && P::finished(L.prog, q)) {
-                        finish(L, q, WF_WALK_COMPLETE);  // walk_already_finished, program.hpp:86-93
+                        finish(L, q, WF_WALK_COMPLETE, ps);  // walk_already_finished, program.hpp:86-93
                     } else {
                         load_current<K, S, F>(L, q);
                         active = true;
@@ -545,17 +587,17 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
                 q.prev_base = q.cur_base;
                 q.prev_deg = q.cur_deg;
                 q.cur = dst;
-                emit(L, q, dst);
+                emit(L, q, dst, ps);
                 q.len += 1;
                 steps += 1;
                 if (P::update(L.prog, q)) {
-                    finish(L, q, WF_WALK_COMPLETE);
+                    finish(L, q, WF_WALK_COMPLETE, ps);
                     active = false;
                 } else {
                     load_current<K, S, F>(L, q);
                 }
             } else {
-                finish(L, q, WF_WALK_DEAD_END);
+                finish(L, q, WF_WALK_DEAD_END, ps);
                 active = false;
             }
         }

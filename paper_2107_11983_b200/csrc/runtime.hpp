@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -64,8 +65,12 @@ struct GraphStore {
     void ensure_label_index(cudaStream_t st);
 };
 
+struct HostPipe;  // stream.cu: cached streams/buffers of the host-output pipeline
+void release_host_pipe(HostPipe* p);
+
 struct Session {
     GraphStore* g = nullptr;
+    std::unique_ptr<HostPipe, void (*)(HostPipe*)> pipe{nullptr, release_host_pipe};
     wf_program_desc desc{};
     std::vector<uint32_t> schema;
     DeviceBuffer<uint32_t> schema_dev;

@@ -3,6 +3,8 @@
 // double-buffered staging).  This is the end-to-end path: the reference hands
 // its walks back in host memory (RunResult::walks, engine.hpp:448-452) or
 // through a BlockSink per worker block (engine.hpp:76-79, output.cpp:133-200).
+// Streams, events and staging buffers are cached on the session (HostPipe) so
+// repeated calls pay no allocation or synchronising cudaMalloc/cudaFree.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -30,79 +32,95 @@ __global__ void k_compact_chunk(const uint32_t* __restrict__ rows, uint32_t stri
     }
 }
 
-struct Streams {
+}  // namespace
+
+struct HostPipe {
+    int device = 0;
     cudaStream_t a = nullptr, b = nullptr;
-    ~Streams() {
+    cudaEvent_t ev_comp[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+    uint64_t cap_rows = 0;     // chunk rows the buffers hold
+    uint32_t cap_stride = 0;
+    DeviceBuffer<uint32_t> rows[2], lens[2], stage[2];
+    DeviceBuffer<uint8_t> stat[2];
+    DeviceBuffer<uint64_t> offs[2];
+    DeviceBuffer<uint8_t> scan_tmp;
+    size_t scan_bytes = 0;
+    DeviceBuffer<uint32_t> src;
+    DeviceBuffer<unsigned long long> ctr;
+    uint64_t* h_tot = nullptr;  // pinned chunk totals
+
+    explicit HostPipe(int dev) : device(dev) {
+        WF_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        WF_CUDA(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            WF_CUDA(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
+            WF_CUDA(cudaEventCreateWithFlags(&ev_copy[i], cudaEventDisableTiming));
+        }
+        WF_CUDA(cudaMallocHost(&h_tot, 2 * sizeof(uint64_t)));
+        ctr.allocate(2);
+    }
+    ~HostPipe() {
+        DeviceGuard guard(device);
         if (a) cudaStreamDestroy(a);
         if (b) cudaStreamDestroy(b);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+            if (ev_copy[i]) cudaEventDestroy(ev_copy[i]);
+        }
+        if (h_tot) cudaFreeHost(h_tot);
+    }
+    void reserve(uint64_t chunk, uint32_t stride) {
+        if (chunk <= cap_rows && stride <= cap_stride) return;
+        cap_rows = std::max(cap_rows, chunk);
+        cap_stride = std::max(cap_stride, stride);
+        for (int i = 0; i < 2; ++i) {
+            rows[i].allocate(cap_rows * cap_stride);
+            stage[i].allocate(cap_rows * cap_stride);
+            lens[i].allocate(cap_rows);
+            stat[i].allocate(cap_rows);
+            offs[i].allocate(cap_rows + 1);
+            WF_CUDA(cudaMemset(offs[i].get(), 0, 8));
+        }
+        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(nullptr, WidenU64{});
+        scan_bytes = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, in, static_cast<uint64_t*>(nullptr),
+                                      static_cast<int64_t>(cap_rows), a);
+        scan_tmp.allocate(std::max<size_t>(scan_bytes, 1));
     }
 };
 
-struct Events {
-    std::vector<cudaEvent_t> ev;
-    cudaEvent_t make() {
-        cudaEvent_t e;
-        WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        ev.push_back(e);
-        return e;
-    }
-    ~Events() {
-        for (auto e : ev) cudaEventDestroy(e);
-    }
-};
-
-}  // namespace
+void release_host_pipe(HostPipe* p) { delete p; }
 
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics) {
     GraphStore& g = *s.g;
     DeviceGuard guard(g.device);
+    auto t0 = std::chrono::steady_clock::now();
     const uint32_t stride = s.default_stride;
     const uint64_t n = qe - qb;
-    if (chunk == 0) chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (4ull * stride)));
-    chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
-    Streams st;
-    WF_CUDA(cudaStreamCreateWithFlags(&st.a, cudaStreamNonBlocking));
-    WF_CUDA(cudaStreamCreateWithFlags(&st.b, cudaStreamNonBlocking));
-    Events evs;
-    auto t0 = std::chrono::steady_clock::now();
+    if (chunk == 0) {
+        // ~8 chunks for overlap, each at least 64 Ki queries, staging <= 256 MiB
+        chunk = std::max<uint64_t>(n / 8, 1ull << 16);
+        chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(1, (256ull << 20) / (4ull * stride)));
+    }
+    chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1)));
+    if (!s.pipe) s.pipe.reset(new HostPipe(g.device));
+    HostPipe& P = *s.pipe;
+    P.reserve(chunk, stride);
+    cudaStream_t A = P.a, B = P.b;
 
     // the shard's slice of the source list, addressed by absolute qid in the kernel
-    DeviceBuffer<uint32_t> d_src;
     const uint32_t* src_by_qid = nullptr;
     if (spec.mode == WF_QUERY_FROM_LIST && n) {
-        d_src.allocate(n);
-        WF_CUDA(cudaMemcpyAsync(d_src.get(), host_sources + qb, n * 4, cudaMemcpyHostToDevice, st.a));
-        src_by_qid = d_src.get() - qb;
+        if (P.src.size() < n) P.src.allocate(n);
+        WF_CUDA(cudaMemcpyAsync(P.src.get(), host_sources + qb, n * 4, cudaMemcpyHostToDevice, A));
+        src_by_qid = P.src.get() - qb;
     }
-    DeviceBuffer<uint32_t> rows[2], lens[2], stage[2];
-    DeviceBuffer<uint8_t> stat[2];
-    DeviceBuffer<uint64_t> offs[2];
-    size_t scan_bytes = 0;
-    {
-        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(nullptr, WidenU64{});
-        cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, in, static_cast<uint64_t*>(nullptr),
-                                      static_cast<int64_t>(chunk), st.a);
-    }
-    DeviceBuffer<uint8_t> scan_tmp(std::max<size_t>(scan_bytes, 1));
-    for (int b = 0; b < 2; ++b) {
-        rows[b].allocate(chunk * stride);
-        lens[b].allocate(chunk);
-        stat[b].allocate(chunk);
-        offs[b].allocate(chunk + 1);
-        stage[b].allocate(chunk * stride);
-        WF_CUDA(cudaMemsetAsync(offs[b].get(), 0, 8, st.a));
-    }
-    DeviceBuffer<unsigned long long> ctr(2);
-    WF_CUDA(cudaMemsetAsync(ctr.get(), 0, 16, st.a));
-    uint64_t* h_tot = nullptr;  // per-buffer chunk totals (pinned)
-    WF_CUDA(cudaMallocHost(&h_tot, 2 * sizeof(uint64_t)));
-    struct HostFree { uint64_t* p; ~HostFree() { if (p) cudaFreeHost(p); } } hf{h_tot};
+    WF_CUDA(cudaMemsetAsync(P.ctr.get(), 0, 16, A));
 
     const uint64_t nchunks = (n + chunk - 1) / chunk;
-    cudaEvent_t ev_comp[2] = {evs.make(), evs.make()};
-    cudaEvent_t ev_copy[2] = {evs.make(), evs.make()};
     bool copy_pending[2] = {false, false};
     std::vector<uint64_t> chunk_base(nchunks + 1, 0);
 
@@ -110,44 +128,46 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         const int b = static_cast<int>(k & 1);
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
         // buffer b (status / offsets / staging) is free once chunk k-2's copy drained
-        if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(st.a, ev_copy[b], 0));
-        launch_walk(s, spec, src_by_qid, qb + r0, qb + r1, nullptr, rows[b].get(), stride, lens[b].get(),
-                    stat[b].get(), nullptr, ctr.get(), ctr.get() + 1, s.cursor.get(), st.a);
-        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(lens[b].get(), WidenU64{});
-        WF_CUDA(cub::DeviceScan::InclusiveSum(scan_tmp.get(), scan_bytes, in, offs[b].get() + 1,
-                                              static_cast<int64_t>(nr), st.a));
+        if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(A, P.ev_copy[b], 0));
+        launch_walk(s, spec, src_by_qid, qb + r0, qb + r1, nullptr, P.rows[b].get(), stride,
+                    P.lens[b].get(), P.stat[b].get(), nullptr, P.ctr.get(), P.ctr.get() + 1,
+                    s.cursor.get(), A);
+        cub::TransformInputIterator<uint64_t, WidenU64, const uint32_t*> in(P.lens[b].get(), WidenU64{});
+        size_t sb = P.scan_bytes;
+        WF_CUDA(cub::DeviceScan::InclusiveSum(P.scan_tmp.get(), sb, in, P.offs[b].get() + 1,
+                                              static_cast<int64_t>(nr), A));
         count_launch();
         int blocks = static_cast<int>(std::min<uint64_t>((nr * 32 + 255) / 256, 65535));
-        k_compact_chunk<<<std::max(blocks, 1), 256, 0, st.a>>>(rows[b].get(), stride, lens[b].get(),
-                                                               offs[b].get(), nr, stage[b].get());
+        k_compact_chunk<<<std::max(blocks, 1), 256, 0, A>>>(P.rows[b].get(), stride, P.lens[b].get(),
+                                                            P.offs[b].get(), nr, P.stage[b].get());
         WF_LAUNCHED();
-        WF_CUDA(cudaMemcpyAsync(h_tot + b, offs[b].get() + nr, 8, cudaMemcpyDeviceToHost, st.a));
-        WF_CUDA(cudaEventRecord(ev_comp[b], st.a));
+        WF_CUDA(cudaMemcpyAsync(P.h_tot + b, P.offs[b].get() + nr, 8, cudaMemcpyDeviceToHost, A));
+        WF_CUDA(cudaEventRecord(P.ev_comp[b], A));
     };
 
     if (nchunks) enqueue_compute(0);
     for (uint64_t k = 0; k < nchunks; ++k) {
         const int b = static_cast<int>(k & 1);
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
-        WF_CUDA(cudaEventSynchronize(ev_comp[b]));
-        const uint64_t cnt = h_tot[b];
+        WF_CUDA(cudaEventSynchronize(P.ev_comp[b]));
+        const uint64_t cnt = P.h_tot[b];
         chunk_base[k + 1] = chunk_base[k] + cnt;
         if (chunk_base[k + 1] > capacity)
             raise(WF_ERR_INVALID_ARG, "vertices_capacity too small for the walk set");
         if (k + 1 < nchunks) enqueue_compute(k + 1);  // overlaps the copy below
-        WF_CUDA(cudaStreamWaitEvent(st.b, ev_comp[b], 0));
+        WF_CUDA(cudaStreamWaitEvent(B, P.ev_comp[b], 0));
         if (cnt)
-            WF_CUDA(cudaMemcpyAsync(vertices + chunk_base[k], stage[b].get(), cnt * 4,
-                                    cudaMemcpyDeviceToHost, st.b));
+            WF_CUDA(cudaMemcpyAsync(vertices + chunk_base[k], P.stage[b].get(), cnt * 4,
+                                    cudaMemcpyDeviceToHost, B));
         if (offsets)
-            WF_CUDA(cudaMemcpyAsync(offsets + r0, offs[b].get(), nr * 8, cudaMemcpyDeviceToHost, st.b));
+            WF_CUDA(cudaMemcpyAsync(offsets + r0, P.offs[b].get(), nr * 8, cudaMemcpyDeviceToHost, B));
         if (status)
-            WF_CUDA(cudaMemcpyAsync(status + r0, stat[b].get(), nr, cudaMemcpyDeviceToHost, st.b));
-        WF_CUDA(cudaEventRecord(ev_copy[b], st.b));
+            WF_CUDA(cudaMemcpyAsync(status + r0, P.stat[b].get(), nr, cudaMemcpyDeviceToHost, B));
+        WF_CUDA(cudaEventRecord(P.ev_copy[b], B));
         copy_pending[b] = true;
     }
-    WF_CUDA(cudaStreamSynchronize(st.b));
-    WF_CUDA(cudaStreamSynchronize(st.a));
+    WF_CUDA(cudaStreamSynchronize(B));
+    WF_CUDA(cudaStreamSynchronize(A));
     int err = 0;
     WF_CUDA(cudaMemcpy(&err, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
     if (err) {
@@ -159,7 +179,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     }
     // chunk-relative offsets -> absolute
     if (offsets) {
-        for (uint64_t k = 0; k < nchunks; ++k) {
+        for (uint64_t k = 1; k < nchunks; ++k) {
             const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk);
             const uint64_t base = chunk_base[k];
             for (uint64_t r = r0; r < r1; ++r) offsets[r] += base;
@@ -167,7 +187,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         offsets[n] = chunk_base[nchunks];
     }
     unsigned long long hc[2] = {0, 0};
-    WF_CUDA(cudaMemcpy(hc, ctr.get(), 16, cudaMemcpyDeviceToHost));
+    WF_CUDA(cudaMemcpy(hc, P.ctr.get(), 16, cudaMemcpyDeviceToHost));
     if (hc[1] > 0) {
         // walks longer than a row: re-run them whole and patch their paths
         if (!offsets) raise(WF_ERR_INVALID_ARG, "offsets are required to place overflowing walks");

@@ -1,0 +1,89 @@
+// Compiles against the header-only shim (include/walkforge_b200/engine.hpp)
+// exactly as a reference caller would (WALKFORGE_B200_DROP_IN: namespace
+// walkforge), runs the reference's own call pattern (test_engine.cpp:62-91,
+// acceptance.cpp:178-200) and prints FNV-1a digests of the walk sets for
+// tests/test_shim_gpu.py to compare with the golden fixtures.
+#define WALKFORGE_B200_DROP_IN
+#include "walkforge_b200/engine.hpp"
+
+#include <cstdio>
+#include <fstream>
+#include <map>
+#include <mutex>
+
+using namespace walkforge;
+
+static uint64_t fnv(const WalkSet& ws) {
+    uint64_t h = 1469598103934665603ULL;
+    auto mixin = [&](uint64_t x) {
+        for (int i = 0; i < 8; ++i) { h ^= (x >> (8 * i)) & 0xFF; h *= 1099511628211ULL; }
+    };
+    for (const auto& r : ws) {
+        mixin(r.query_id);
+        mixin(static_cast<uint64_t>(r.status));
+        mixin(r.path.size());
+        for (auto v : r.path) mixin(v);
+    }
+    return h;
+}
+
+int main(int argc, char** argv) {
+    if (argc < 2) return 2;
+    std::ifstream in(argv[1], std::ios::binary);
+    uint32_t V;
+    uint64_t E;
+    in.read(reinterpret_cast<char*>(&V), 4);
+    in.read(reinterpret_cast<char*>(&E), 8);
+    std::vector<uint64_t> off(V + 1);
+    std::vector<uint32_t> nbr(E);
+    std::vector<float> w32(E);
+    std::vector<uint32_t> lab(E);
+    in.read(reinterpret_cast<char*>(off.data()), off.size() * 8);
+    in.read(reinterpret_cast<char*>(nbr.data()), E * 4);
+    in.read(reinterpret_cast<char*>(w32.data()), E * 4);
+    in.read(reinterpret_cast<char*>(lab.data()), E * 4);
+    std::vector<double> w(w32.begin(), w32.end());
+    Graph g = Graph::from_csr(off, nbr, w, lab);
+
+    ExecOptions eo;
+    eo.seed = 7;
+    eo.sampler = SamplerKind::Alias;
+    RunResult a = run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 20, true), eo);
+    std::printf("deepwalk_alias %016llx %llu\n", (unsigned long long)fnv(a.walks),
+                (unsigned long long)a.metrics.total_steps);
+
+    ExecOptions n2v;
+    n2v.seed = 7;
+    n2v.sampler = SamplerKind::ORej;
+    RunResult b = run_interleaved(g, QuerySpec::one_per_vertex(),
+                                  Node2VecProgram(g, {.a = 2.0, .b = 0.5, .target_length = 20}, true),
+                                  64, 32, n2v);
+    std::printf("node2vec_orej %016llx %llu\n", (unsigned long long)fnv(b.walks),
+                (unsigned long long)b.metrics.total_steps);
+
+    // streaming sink mode, as the CLI drives it (walkforge.cpp:157-175)
+    ExecOptions mp;
+    mp.seed = 7;
+    mp.sampler = SamplerKind::Its;
+    std::map<uint32_t, WalkSet> blocks;
+    std::mutex mu;
+    mp.sink = [&](uint32_t worker, WalkSet&& block) {
+        std::lock_guard<std::mutex> lock(mu);
+        blocks[worker] = std::move(block);
+    };
+    RunResult c = run_sequential(g, QuerySpec::one_per_vertex(), MetaPathProgram(g, {0, 1, 2, 3}), mp);
+    WalkSet merged;
+    for (auto& [k, blk] : blocks) for (auto& r : blk) merged.push_back(std::move(r));
+    std::printf("metapath_its %016llx %llu sink_empty=%d\n", (unsigned long long)fnv(merged),
+                (unsigned long long)c.metrics.total_steps, (int)c.walks.empty());
+
+    try {
+        ExecOptions bad;
+        bad.sampler = SamplerKind::Naive;
+        run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 5, false), bad);
+        std::printf("naive_static no-error\n");
+    } catch (const ConfigError&) {
+        std::printf("naive_static ConfigError\n");
+    }
+    return 0;
+}

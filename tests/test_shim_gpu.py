@@ -1,0 +1,74 @@
+"""The header-only C++ shim compiled as a reference caller would use it
+(include/walkforge_b200/engine.hpp, WALKFORGE_B200_DROP_IN) reproduces the
+reference's golden walk sets."""
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_2107_11983_b200 import engine as E
+from tests import golden_util as gu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def fnv(ws):
+    h = 1469598103934665603
+    mask = (1 << 64) - 1
+
+    def mix(x):
+        nonlocal h
+        for i in range(8):
+            h ^= (x >> (8 * i)) & 0xFF
+            h = (h * 1099511628211) & mask
+    for q in range(len(ws)):
+        p = ws.path(q)
+        mix(q)
+        mix(int(ws.status[q]))
+        mix(len(p))
+        for v in p:
+            mix(int(v))
+    return h
+
+
+def build_shim(tmp):
+    exe = os.path.join(tmp, "shim_test")
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "shim_test.cpp"), "-o", exe,
+                           "-L", os.path.dirname(E.LIB_PATH), "-lwalkforge_b200",
+                           f"-Wl,-rpath,{os.path.dirname(E.LIB_PATH)}"])
+    return exe
+
+
+def test_shim_compiles_cpu_only():
+    """The shim is plain C++20 against the C header (no CUDA types leak)."""
+    with tempfile.TemporaryDirectory() as d:
+        assert os.path.exists(build_shim(d))
+
+
+@pytest.mark.gpu
+def test_shim_reproduces_golden_walks():
+    g = gu.graph("powerlaw")
+    with tempfile.TemporaryDirectory() as d:
+        exe = build_shim(d)
+        path = os.path.join(d, "g.bin")
+        with open(path, "wb") as f:
+            f.write(np.uint32(g.vertex_count).tobytes())
+            f.write(np.uint64(g.edge_count).tobytes())
+            f.write(g.offsets.tobytes())
+            f.write(g.neighbors.tobytes())
+            f.write(g.weights.tobytes())
+            f.write(g.labels.astype(np.uint32).tobytes())
+        out = subprocess.check_output([exe, path], text=True).splitlines()
+    res = {l.split()[0]: l.split()[1:] for l in out}
+    cases = {c["name"]: c for c in gu.cases()}
+    for key, case in [("deepwalk_alias", "pl_deepwalk_w_alias"),
+                      ("node2vec_orej", "pl_node2vec_w_orej"),
+                      ("metapath_its", "pl_metapath_its")]:
+        ws = gu.walks(cases[case])
+        assert res[key][0] == f"{fnv(ws):016x}", key
+        assert int(res[key][1]) == cases[case]["total_steps"]
+    assert res["metapath_its"][2] == "sink_empty=1"
+    assert res["naive_static"] == ["ConfigError"]

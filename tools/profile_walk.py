@@ -1,0 +1,54 @@
+"""Launch the walk kernel of one bench config a few times (for ncu / timing).
+
+    python tools/profile_walk.py --config c5 [--scale 24] [--launches 3]
+"""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--scale", type=int, default=0)
+    ap.add_argument("--launches", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+
+    from paper_2107_11983_b200 import engine as E
+    from paper_2107_11983_b200.host import ExecOptions
+    cfg = dict(bench.CONFIGS[args.config])
+    if args.scale:
+        cfg["scale"] = args.scale
+    dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
+                            label_count=cfg["labels"])
+    V = dg.info()["V"]
+    sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=bench.row_capacity(cfg)))
+    spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
+    n = hi - lo
+    stride = bench.row_capacity(cfg)
+    d_src = torch.from_numpy(spec.sources.view("int32")).cuda()
+    paths = torch.empty(n * stride, dtype=torch.int32, device="cuda")
+    lens = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = torch.empty(n, dtype=torch.uint8, device="cuda")
+    steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for i in range(args.launches):
+        steps.zero_()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), st.data_ptr(), 0,
+                    steps.data_ptr(), 0, 0, sources_dev_ptr=d_src.data_ptr())
+        sess.sync()
+        dt = time.perf_counter() - t
+        print(f"launch {i}: {steps.item()} moves {dt*1e3:.2f} ms {steps.item()/dt/1e9:.2f} G steps/s "
+              f"V={V} E={dg.info()['E']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
