@@ -363,7 +363,16 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         cudaGetLastError();
         s.cursor.allocate(1);
         h->counters.allocate(2);
+        // HBM budget for the decorated layouts (they trade capacity for one
+        // dependent random load per move); fall back to the compact forms.
+        size_t free_b = 0, total_b = 0;
+        WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t reserve = 8ull << 30;
+        const uint64_t E = s.g->E;
+        if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS)
+            s.alias_wide = 32 * E + reserve <= free_b;
         if (s.flow == kTables) s.build_tables(nullptr);
+        if (s.flow == kDirect && 16 * E + reserve <= free_b) s.build_adjacency(nullptr);
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) s.g->ensure_label_index(nullptr);
         s.grid = occupancy_grid(s);
         *out = h.release();
@@ -640,12 +649,14 @@ int wf_session_tables(const wf_session* sh, uint64_t* alias_thr, uint32_t* alias
         const GraphStore& g = *s.g;
         DeviceGuard guard(g.device);
         if (s.alias.get() && (alias_thr || alias_first_dst || alias_second_dst)) {
-            std::vector<uint4> b(g.E);
-            WF_CUDA(cudaMemcpy(b.data(), s.alias.get(), g.E * 16, cudaMemcpyDeviceToHost));
+            const uint64_t bs = s.alias_wide ? 2 : 1;
+            std::vector<uint4> b(g.E * bs);
+            WF_CUDA(cudaMemcpy(b.data(), s.alias.get(), g.E * 16 * bs, cudaMemcpyDeviceToHost));
             for (uint64_t i = 0; i < g.E; ++i) {
-                if (alias_thr) alias_thr[i] = (static_cast<uint64_t>(b[i].y) << 32) | b[i].x;
-                if (alias_first_dst) alias_first_dst[i] = b[i].z;
-                if (alias_second_dst) alias_second_dst[i] = b[i].w;
+                const uint4& x = b[i * bs];
+                if (alias_thr) alias_thr[i] = (static_cast<uint64_t>(x.y) << 32) | x.x;
+                if (alias_first_dst) alias_first_dst[i] = x.z;
+                if (alias_second_dst) alias_second_dst[i] = x.w;
             }
         }
         if (s.its.get() && its_cumulative)

@@ -82,6 +82,8 @@ struct WalkLaunch {
     uint64_t scratch_stride;
     int use_label_index;
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
+    int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
+    const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
     unsigned long long* stats;  // optional: [trials, search probes, scanned edges]
 };
 
@@ -96,6 +98,9 @@ struct Walker {
     // lane-level logical access counters (survive refills); flushed to
     // WalkLaunch::stats when requested — the instrumented S_alg of SURVEY §8 d
     mutable uint32_t n_trials, n_probes, n_scanned;
+    // vertex word of the destination when the sampler's load carried it
+    uint64_t nb_word;
+    bool have_nb;
 };
 
 // ---- graph helpers -------------------------------------------------------------
@@ -108,6 +113,16 @@ template <typename T>
 __device__ __forceinline__ T ldr(const T* p) { return __ldcg(p); }
 __device__ __forceinline__ uint64_t ldr(const uint64_t* p) {
     return static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
+}
+
+__device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint32_t v,
+                                            uint64_t& base, uint32_t& deg) {
+    base = w >> kDegBits;
+    deg = static_cast<uint32_t>(w & kDegEscape);
+    if (deg == kDegEscape) {  // rare: very high degree
+        base = ldr(g.offsets + v);
+        deg = static_cast<uint32_t>(ldr(g.offsets + v + 1) - base);
+    }
 }
 
 __device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t* vw, uint32_t v,
@@ -374,6 +389,21 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
     } else if constexpr (F == kTables) {
         if constexpr (S == WF_SAMPLER_ALIAS) {
             uint32_t x = q.rng.index(d);
+            if (L.alias_wide) {
+                // 32 B bucket = one sector: {thr, first_dst, second_dst} and the
+                // destinations' own vertex words, so the next step needs no
+                // dependent vertex-word load (one random sector per move).
+                const uint4* bp = L.alias + 2 * (base + x);
+                uint4 b = ldr(bp);
+                uint4 w = ldr(bp + 1);
+                uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
+                bool first = q.rng.bits53() < thr;  // y < split <=> k < ceil(split 2^53)
+                dst = first ? b.z : b.w;
+                q.nb_word = first ? (static_cast<uint64_t>(w.y) << 32) | w.x
+                                  : (static_cast<uint64_t>(w.w) << 32) | w.z;
+                q.have_nb = true;
+                return kMoved;
+            }
             uint4 b = ldr(L.alias + base + x);
             uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
             dst = q.rng.bits53() < thr ? b.z : b.w;  // y < split <=> k < ceil(split 2^53)
@@ -447,6 +477,14 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (y < P::weight(L.prog, L.g, q, base + x)) { pick = x; break; }
             }
         }
+    }
+    if (F == kDirect && L.adj) {
+        // decorated adjacency {dst, -, vertex word of dst}: one 16 B load
+        uint4 a = ldr(L.adj + base + pick);
+        dst = a.x;
+        q.nb_word = (static_cast<uint64_t>(a.w) << 32) | a.z;
+        q.have_nb = true;
+        return kMoved;
     }
     dst = ldr(L.g.nbr + base + pick);
     return kMoved;
@@ -544,6 +582,8 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
     q.len = 0;
     q.rng.s = 0;
     q.n_trials = q.n_probes = q.n_scanned = 0;
+    q.nb_word = 0;
+    q.have_nb = false;
     bool active = false;
     bool drained = false;
     unsigned long long steps = 0;
@@ -593,9 +633,12 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
                 if (P::update(L.prog, q)) {
                     finish(L, q, WF_WALK_COMPLETE, ps);
                     active = false;
+                } else if (q.have_nb) {
+                    unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
                 } else {
                     load_current<K, S, F>(L, q);
                 }
+                q.have_nb = false;
             } else {
                 finish(L, q, WF_WALK_DEAD_END, ps);
                 active = false;

@@ -95,8 +95,11 @@ struct Session {
     int grid = 0;
     bool collect_stats = false;
     DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
+    bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
+    DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
 
     void build_tables(cudaStream_t st);
+    void build_adjacency(cudaStream_t st);
 };
 
 struct WalkSetStore {

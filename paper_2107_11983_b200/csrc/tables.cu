@@ -53,7 +53,7 @@ __device__ __forceinline__ double unpark(const uint4* b) {
 
 template <typename WF>
 __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
-                               uint32_t V, WF wf, uint4* __restrict__ bucket,
+                               uint32_t V, WF wf, uint4* __restrict__ bucket, uint32_t bs,
                                uint8_t* __restrict__ exhausted, unsigned* any_exhausted) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
          v += (uint64_t)gridDim.x * blockDim.x) {
@@ -68,7 +68,7 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
             continue;
         }
         const uint32_t* dst = nbr + a0;
-        uint4* out = bucket + a0;
+        uint4* out = bucket + a0 * bs;  // bs = 2: wide 32 B buckets (second half decorated later)
         auto scaled = [&](uint32_t i) { return wf(a0 + i) * n / sum; };  // sampler.hpp:97
         auto next_large = [&](uint32_t from) {
             while (from < n && !(scaled(from) >= 1.0)) ++from;
@@ -92,30 +92,30 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
             } else if (consumed < demoted) {
                 c = next_large(c);
                 s = c;
-                sval = unpark(out + c);
+                sval = unpark(out + c * bs);
                 ++c;
                 ++consumed;
             } else {
                 break;
             }
-            store_bucket(out + s, sval, dst[s], dst[lcur]);
+            store_bucket(out + s * bs, sval, dst[s], dst[lcur]);
             lval -= 1.0 - sval;
             if (lval < 1.0) {
-                park(out + lcur, lval);
+                park(out + lcur * bs, lval);
                 ++demoted;
                 lcur = next_large(lcur + 1);
                 if (lcur < n) lval = scaled(lcur);
             }
         }
         // leftovers at probability exactly 1 (sampler.hpp:112-119)
-        for (uint32_t s = a; s < n; s = next_small(s + 1)) store_bucket(out + s, 1.0, dst[s], dst[s]);
+        for (uint32_t s = a; s < n; s = next_small(s + 1)) store_bucket(out + s * bs, 1.0, dst[s], dst[s]);
         while (consumed < demoted) {
             c = next_large(c);
-            store_bucket(out + c, 1.0, dst[c], dst[c]);
+            store_bucket(out + c * bs, 1.0, dst[c], dst[c]);
             ++c;
             ++consumed;
         }
-        for (uint32_t l = lcur; l < n; l = next_large(l + 1)) store_bucket(out + l, 1.0, dst[l], dst[l]);
+        for (uint32_t l = lcur; l < n; l = next_large(l + 1)) store_bucket(out + l * bs, 1.0, dst[l], dst[l]);
     }
 }
 
@@ -175,6 +175,30 @@ __global__ void k_sampling_view(const uint64_t* __restrict__ vword, const uint8_
     }
 }
 
+// Second half of each wide bucket: the sampling-view vertex words of its two
+// destinations, so a move lands with the next vertex's (base, degree) in hand.
+__global__ void k_decorate_alias(uint4* __restrict__ bucket, uint64_t E,
+                                 const uint64_t* __restrict__ sview) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 b = bucket[2 * e];
+        uint64_t w1 = sview[b.z], w2 = sview[b.w];
+        bucket[2 * e + 1] = make_uint4(static_cast<uint32_t>(w1), static_cast<uint32_t>(w1 >> 32),
+                                       static_cast<uint32_t>(w2), static_cast<uint32_t>(w2 >> 32));
+    }
+}
+
+// Decorated adjacency for Direct flows (NAIVE / O-REJ): {dst, 0, word(dst)}.
+__global__ void k_decorate_adj(const uint32_t* __restrict__ nbr, uint64_t E,
+                               const uint64_t* __restrict__ vword, uint4* __restrict__ adj) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t d = nbr[e];
+        uint64_t w = vword[d];
+        adj[e] = make_uint4(d, 0u, static_cast<uint32_t>(w), static_cast<uint32_t>(w >> 32));
+    }
+}
+
 template <typename WF>
 void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
     GraphStore& g = *s.g;
@@ -182,9 +206,10 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
     uint64_t blocks = (g.V + threads - 1) / threads;
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, static_cast<uint64_t>(sm_count(g.device)) * 64));
     if (s.kind == WF_SAMPLER_ALIAS) {
-        s.alias.allocate(std::max<uint64_t>(g.E, 1));
+        const uint32_t bs = s.alias_wide ? 2 : 1;
+        s.alias.allocate(std::max<uint64_t>(g.E, 1) * bs);
         k_static_alias<<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
-                                                   s.alias.get(), s.exhausted.get(), any);
+                                                   s.alias.get(), bs, s.exhausted.get(), any);
     } else if (s.kind == WF_SAMPLER_ITS) {
         s.its.allocate(std::max<uint64_t>(g.E, 1));
         k_static_its<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.its.get(),
@@ -223,7 +248,29 @@ void Session::build_tables(cudaStream_t st) {
         WF_LAUNCHED();
         WF_CUDA(cudaStreamSynchronize(st));
     }
+    if (kind == WF_SAMPLER_ALIAS && alias_wide && gs.E) {
+        const uint64_t* sv = any_exhausted ? sview.get() : gs.vword.get();
+        int blocks = std::max(1, std::min<int>(static_cast<int>((gs.E + 255) / 256), sm_count(gs.device) * 32));
+        k_decorate_alias<<<blocks, 256, 0, st>>>(alias.get(), gs.E, sv);
+        WF_LAUNCHED();
+        WF_CUDA(cudaStreamSynchronize(st));
+    }
     preprocess_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Session::build_adjacency(cudaStream_t st) {
+    GraphStore& gs = *g;
+    DeviceGuard guard(gs.device);
+    auto t0 = std::chrono::steady_clock::now();
+    adj.allocate(std::max<uint64_t>(gs.E, 1));
+    if (gs.E) {
+        int blocks = std::max(1, std::min<int>(static_cast<int>((gs.E + 255) / 256), sm_count(gs.device) * 32));
+        k_decorate_adj<<<blocks, 256, 0, st>>>(gs.nbr.get(), gs.E, gs.vword.get(), adj.get());
+        WF_LAUNCHED();
+    }
+    WF_CUDA(cudaStreamSynchronize(st));
+    preprocess_seconds +=
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
