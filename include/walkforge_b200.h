@@ -101,8 +101,13 @@ typedef struct wf_exec_options {
     uint32_t k;
     uint32_t k_prime;
     uint32_t path_stride;      /* device row capacity for unbounded walks (0 = auto) */
-    uint32_t reserved;
+    uint32_t layout_flags;     /* WF_LAYOUT_*: opt out of the decorated HBM layouts */
 } wf_exec_options;
+
+/* Decorated layouts trade HBM capacity for one fewer dependent random load per
+ * move; they are used automatically when memory allows unless opted out. */
+#define WF_LAYOUT_COMPACT_ALIAS 1u /* 16 B alias buckets (no destination vertex words) */
+#define WF_LAYOUT_NO_ADJ 2u        /* no decorated adjacency for NAIVE / O-REJ */
 
 typedef struct wf_query_spec {
     int32_t mode; /* wf_query_mode */

@@ -146,8 +146,12 @@ class ExecOptionsC(C.Structure):
         ("k", C.c_uint32),
         ("k_prime", C.c_uint32),
         ("path_stride", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("layout_flags", C.c_uint32),
     ]
+
+
+LAYOUT_COMPACT_ALIAS = 1
+LAYOUT_NO_ADJ = 2
 
 
 class QuerySpecC(C.Structure):

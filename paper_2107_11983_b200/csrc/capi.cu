@@ -369,10 +369,12 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
         const uint64_t reserve = 8ull << 30;
         const uint64_t E = s.g->E;
-        if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS)
+        const uint32_t lf = opts ? opts->layout_flags : 0;
+        if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS && !(lf & WF_LAYOUT_COMPACT_ALIAS))
             s.alias_wide = 32 * E + reserve <= free_b;
         if (s.flow == kTables) s.build_tables(nullptr);
-        if (s.flow == kDirect && 16 * E + reserve <= free_b) s.build_adjacency(nullptr);
+        if (s.flow == kDirect && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
+            s.build_adjacency(nullptr);
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) s.g->ensure_label_index(nullptr);
         s.grid = occupancy_grid(s);
         *out = h.release();

@@ -109,10 +109,34 @@ struct Walker {
 // in L2 only (ld.global.cg).  L1 hit rates on these are ~2 %, and letting L1
 // allocate them made it request 2.8x the sectors the walk needs (ncu,
 // profiles/).  Search probes keep __ldg: their last probes share a line.
-template <typename T>
-__device__ __forceinline__ T ldr(const T* p) { return __ldcg(p); }
+#define WF_LDR "ld.global.nc.L1::no_allocate"
+__device__ __forceinline__ uint32_t ldr(const uint32_t* p) {
+    uint32_t v;
+    asm(WF_LDR ".u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint64_t ldr(const uint64_t* p) {
-    return static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
+    uint64_t v;
+    asm(WF_LDR ".u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ldr(const float* p) {
+    float v;
+    asm(WF_LDR ".f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ldr(const uint4* p) {
+    uint4 v;
+    asm(WF_LDR ".v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+// One 256-bit load (sm_100: LDG.E.256): a whole 32 B sector in one request.
+// Two 16 B loads of the same sector cost 2x the L2 lookups and made the L2
+// fetch ~4 DRAM sectors per move (ncu, profiles/).
+__device__ __forceinline__ void ldr256(const uint4* p, uint4& a, uint4& b) {
+    asm(WF_LDR ".v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p));
 }
 
 __device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint32_t v,
@@ -393,9 +417,8 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 // 32 B bucket = one sector: {thr, first_dst, second_dst} and the
                 // destinations' own vertex words, so the next step needs no
                 // dependent vertex-word load (one random sector per move).
-                const uint4* bp = L.alias + 2 * (base + x);
-                uint4 b = ldr(bp);
-                uint4 w = ldr(bp + 1);
+                uint4 b, w;
+                ldr256(L.alias + 2 * (base + x), b, w);
                 uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
                 bool first = q.rng.bits53() < thr;  // y < split <=> k < ceil(split 2^53)
                 dst = first ? b.z : b.w;
@@ -496,8 +519,8 @@ __device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
     if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
         if (L.use_label_index) {
             const uint4* rec = L.g.lab_rec + 2 * static_cast<uint64_t>(q.cur);
-            uint4 r0 = ldr(rec);
-            uint4 r1 = ldr(rec + 1);
+            uint4 r0, r1;
+            ldr256(rec, r0, r1);
             uint64_t base = (static_cast<uint64_t>(r0.y) << 32) | r0.x;
             uint32_t ends[kMaxIndexedLabels] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
             uint32_t l = __ldg(L.prog.schema + (q.len - 1));

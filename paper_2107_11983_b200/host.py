@@ -154,6 +154,7 @@ class ExecOptions:
     k: int = 64
     k_prime: int = 32
     path_stride: int = 0
+    layout_flags: int = 0
 
     def to_c(self) -> ExecOptionsC:
         c = ExecOptionsC()
@@ -165,6 +166,7 @@ class ExecOptions:
         c.k = self.k
         c.k_prime = self.k_prime
         c.path_stride = self.path_stride
+        c.layout_flags = self.layout_flags
         return c
 
 

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--launches", type=int, default=3)
+    ap.add_argument("--layout", type=int, default=0)
     args = ap.parse_args()
     import torch
 
@@ -29,7 +30,7 @@ def main():
     dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
                             label_count=cfg["labels"])
     V = dg.info()["V"]
-    sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=bench.row_capacity(cfg)))
+    sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=bench.row_capacity(cfg), layout_flags=args.layout))
     spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
     n = hi - lo
     stride = bench.row_capacity(cfg)
