@@ -17,13 +17,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libwalkforge_b200.so")
+# experiment hooks (tools only): alternative defines build into another object dir / library
+EXTRA = os.environ.get("WF_BUILD_DEFINES", "").split()
+OBJ = os.environ.get("WF_BUILD_DIR", os.path.join(HERE, "_build"))
+LIB = os.environ.get("WF_LIB", os.path.join(HERE, "libwalkforge_b200.so"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
-                     f"-I{os.path.join(ROOT, 'include')}"]
+                     f"-I{os.path.join(ROOT, 'include')}"] + EXTRA
 
 
 def nvcc() -> str:

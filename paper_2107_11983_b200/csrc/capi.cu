@@ -375,7 +375,13 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         if (s.flow == kTables) s.build_tables(nullptr);
         if (s.flow == kDirect && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
             s.build_adjacency(nullptr);
-        if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) s.g->ensure_label_index(nullptr);
+        if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
+            s.g->ensure_label_index(nullptr);
+            WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (!(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
+                s.build_metapath_successors(nullptr);
+        }
+        if (s.desc.kind == WF_PROGRAM_NODE2VEC) s.g->ensure_search_index(nullptr);
         s.grid = occupancy_grid(s);
         *out = h.release();
     });

@@ -42,6 +42,10 @@ struct GraphView {
     const uint4* __restrict__ lab_rec;
     const uint32_t* __restrict__ lab_nbr;
     uint32_t label_count;
+    // adjacency search index (sorted graphs): sidx[(base >> 4) + v + k] =
+    // nbr[base + 16 k] for k < ceil(deg / 16); the ranges never overlap since
+    // ceil(d/16) <= floor((base+d)/16) - floor(base/16) + 1.
+    const uint32_t* __restrict__ sidx;
 };
 
 struct ProgParams {
@@ -84,6 +88,7 @@ struct WalkLaunch {
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
     const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
+    const uint4* __restrict__ mp_adj; // MetaPath: per partitioned edge {dst, 0, next-group word} or null
     unsigned long long* stats;  // optional: [trials, search probes, scanned edges]
 };
 
@@ -109,7 +114,9 @@ struct Walker {
 // in L2 only (ld.global.cg).  L1 hit rates on these are ~2 %, and letting L1
 // allocate them made it request 2.8x the sectors the walk needs (ncu,
 // profiles/).  Search probes keep __ldg: their last probes share a line.
-#define WF_LDR "ld.global.nc.L1::no_allocate"
+#ifndef WF_LDR
+#define WF_LDR "ld.global.cg"
+#endif
 __device__ __forceinline__ uint32_t ldr(const uint32_t* p) {
     uint32_t v;
     asm(WF_LDR ".u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -177,6 +184,44 @@ __device__ __forceinline__ bool has_edge(const GraphView& g, uint64_t base, uint
         found = lo < deg && (++np, __ldg(ns + lo) == dst);
     } else {
         for (uint32_t i = 0; i < deg && !found; ++i, ++np) found = __ldg(ns + i) == dst;
+    }
+    if (probes) *probes += np;
+    return found;
+}
+
+constexpr uint32_t kSidxBlock = 16;
+
+// Membership of dst in the sorted adjacency of v (base, deg) through the
+// search index: binary search over the block heads (E/16 + V words, mostly
+// L2-resident), then the block's 16 ids (64 B) read as 32 B sectors and
+// compared in registers.  Same answer as std::binary_search (graph.cpp:182-188)
+// with ~log2(deg/16) L2 probes + 2-3 sectors instead of ~log2(deg) DRAM probes.
+__device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t base, uint32_t deg,
+                                                 uint32_t v, uint32_t dst, uint32_t* probes) {
+    if (deg <= kSidxBlock || g.sidx == nullptr) return has_edge(g, base, deg, dst, probes);
+    const uint32_t* ix = g.sidx + (base >> 4) + v;
+    const uint32_t nblk = (deg + kSidxBlock - 1) / kSidxBlock;
+    uint32_t np = 0;
+    // largest k with ix[k] <= dst
+    uint32_t lo = 0, hi = nblk;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        ++np;
+        if (__ldg(ix + mid) <= dst) lo = mid + 1; else hi = mid;
+    }
+    bool found = false;
+    if (lo > 0) {
+        const uint64_t b0 = base + static_cast<uint64_t>(lo - 1) * kSidxBlock;
+        const uint64_t b1 = min(b0 + kSidxBlock, base + deg);
+        // aligned 32 B sectors covering [b0, b1)
+        for (uint64_t s = b0 & ~7ull; s < b1; s += 8) {
+            uint4 x, y;
+            ldr256(reinterpret_cast<const uint4*>(g.nbr + s), x, y);
+            ++np;
+            uint32_t e[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) found |= (s + i >= b0 && s + i < b1 && e[i] == dst);
+        }
     }
     if (probes) *probes += np;
     return found;
@@ -261,7 +306,7 @@ struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
         } else {
             uint32_t dst = ldr(g.nbr + e);
             if (dst == q.prev) w = p.inv_a;
-            else if (has_edge(g, q.prev_base, q.prev_deg, dst, &q.n_probes)) w = 1.0;
+            else if (has_edge_indexed(g, q.prev_base, q.prev_deg, q.prev, dst, &q.n_probes)) w = 1.0;
             else w = p.inv_b;
         }
         return p.weighted ? __dmul_rn(w, static_cast<double>(ldr(g.weights + e))) : w;
@@ -317,7 +362,7 @@ __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunc
     if (dst == q.prev) return y < scaled(p.inv_a);
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
-    bool common = has_edge(L.g, q.prev_base, q.prev_deg, dst, &q.n_probes);
+    bool common = has_edge_indexed(L.g, q.prev_base, q.prev_deg, q.prev, dst, &q.n_probes);
     return y < scaled(common ? 1.0 : p.inv_b);
 }
 
@@ -458,7 +503,20 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 // (cumulative table over 0/1 weights), which is the j-th edge of
                 // the stably partitioned group.
                 double x = q.rng.real(static_cast<double>(d));
-                dst = ldr(L.g.lab_nbr + base + static_cast<uint32_t>(x));
+                const uint32_t j = static_cast<uint32_t>(x);
+                if (L.mp_adj) {
+                    // {dst, -, group word of dst for the next schema label}: the
+                    // next move's label group arrives with this one load
+                    uint4 a = ldr(L.mp_adj + base + j);
+                    dst = a.x;
+                    const uint64_t w = (static_cast<uint64_t>(a.w) << 32) | a.z;
+                    if (w != ~0ull) {
+                        q.nb_word = w;
+                        q.have_nb = true;
+                    }
+                    return kMoved;
+                }
+                dst = ldr(L.g.lab_nbr + base + j);
                 return kMoved;
             }
         }

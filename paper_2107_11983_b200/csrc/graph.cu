@@ -352,6 +352,36 @@ void GraphStore::ensure_label_index(cudaStream_t st) {
     label_index_built = true;
 }
 
+namespace {
+__global__ void k_search_index(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                               uint32_t V, uint32_t* __restrict__ sidx) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < V; v += nwarps) {
+        uint64_t a = off[v], d = off[v + 1] - a;
+        if (d <= kSidxBlock) continue;
+        uint64_t nblk = (d + kSidxBlock - 1) / kSidxBlock;
+        uint32_t* ix = sidx + (a >> 4) + v;
+        for (uint64_t k = lane; k < nblk; k += 32) ix[k] = nbr[a + k * kSidxBlock];
+    }
+}
+}  // namespace
+
+// Block-head index for has_edge_indexed (Node2Vec's distance test); only for
+// sorted adjacency, where std::binary_search semantics apply.
+void GraphStore::ensure_search_index(cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (search_index_built || !sorted || E == 0) return;
+    DeviceGuard guard(device);
+    sidx.allocate((E >> 4) + V + 1);
+    k_search_index<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(offsets.get(), nbr.get(),
+                                                                              V, sidx.get());
+    WF_LAUNCHED();
+    WF_CUDA(cudaStreamSynchronize(st));
+    search_index_built = true;
+}
+
 static std::unique_ptr<GraphStore> alloc_graph(uint32_t V, uint64_t E, bool w, bool l, int device) {
     if (V == 0) config_error("graph must have at least one vertex");
     auto g = std::make_unique<GraphStore>();
@@ -359,7 +389,7 @@ static std::unique_ptr<GraphStore> alloc_graph(uint32_t V, uint64_t E, bool w, b
     g->V = V;
     g->E = E;
     g->offsets.allocate(static_cast<size_t>(V) + 1);
-    g->nbr.allocate(std::max<uint64_t>(E, 1));
+    g->nbr.allocate(E + kNbrPad);  // padded: search reads whole 32 B sectors
     if (w) g->weights.allocate(std::max<uint64_t>(E, 1));
     if (l) g->labels.allocate(std::max<uint64_t>(E, 1));
     return g;
@@ -505,7 +535,7 @@ GraphStore* graph_generate_rmat(const wf_rmat_params& p, int device) {
     }
     WF_CUDA(cudaMemcpyAsync(&g->E, g->offsets.get() + V, 8, cudaMemcpyDeviceToHost, st));
     WF_CUDA(cudaStreamSynchronize(st));
-    g->nbr.allocate(std::max<uint64_t>(g->E, 1));
+    g->nbr.allocate(g->E + kNbrPad);
     k_dedup<<<wblocks, 256, 0, st>>>(off0.get(), sorted_buf.get(), V, nullptr, g->offsets.get(),
                                      g->nbr.get(), 1);
     WF_LAUNCHED();

@@ -21,6 +21,8 @@
 
 namespace wf {
 
+constexpr uint64_t kNbrPad = 8;  // neighbour array slack: sector-wide reads at the end
+
 struct GraphStore {
     int device = 0;
     uint32_t V = 0;
@@ -40,6 +42,8 @@ struct GraphStore {
     bool label_index_built = false;
     DeviceBuffer<uint4> lab_rec;
     DeviceBuffer<uint32_t> lab_nbr;
+    bool search_index_built = false;
+    DeviceBuffer<uint32_t> sidx;  // adjacency search index (engine.cuh has_edge_indexed)
 
     GraphView view() const {
         GraphView g{};
@@ -54,6 +58,7 @@ struct GraphStore {
         g.lab_rec = lab_rec.get();
         g.lab_nbr = lab_nbr.get();
         g.label_count = label_count;
+        g.sidx = sidx.get();
         return g;
     }
     bool has_weights() const { return weights.get() != nullptr; }
@@ -63,6 +68,7 @@ struct GraphStore {
     // compute stats, build vertex words.  `labels_checked` = labels already u8.
     void finalize(cudaStream_t st);
     void ensure_label_index(cudaStream_t st);
+    void ensure_search_index(cudaStream_t st);
 };
 
 struct HostPipe;  // stream.cu: cached streams/buffers of the host-output pipeline
@@ -97,9 +103,13 @@ struct Session {
     DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
     bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
+    DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 
     void build_tables(cudaStream_t st);
     void build_adjacency(cudaStream_t st);
+    // MetaPath with a schema whose successor label is a function of the label
+    // (e.g. cyclic): returns false (no table) otherwise.
+    bool build_metapath_successors(cudaStream_t st);
 };
 
 struct WalkSetStore {

@@ -259,6 +259,68 @@ void Session::build_tables(cudaStream_t st) {
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+namespace {
+// Warp per vertex u over its label-partitioned edges: edge p of group l
+// (label l) gets {dst, 0, word} with word = (base_g << 24 | count) of dst's
+// group for label next[l]; ~0 when there is no successor label or the group
+// does not fit the packed word (the kernel then reads dst's label record).
+__global__ void k_metapath_successors(const uint4* __restrict__ rec, const uint32_t* __restrict__ lab_nbr,
+                                      uint32_t V, const int* __restrict__ next,
+                                      uint4* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t u = warp; u < V; u += nwarps) {
+        uint4 r0 = rec[2 * u], r1 = rec[2 * u + 1];
+        uint64_t base = (static_cast<uint64_t>(r0.y) << 32) | r0.x;
+        uint32_t ends[kMaxIndexedLabels] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        uint32_t deg = ends[kMaxIndexedLabels - 1];
+        for (uint32_t p = lane; p < deg; p += 32) {
+            int l = 0;
+            while (l < kMaxIndexedLabels - 1 && p >= ends[l]) ++l;
+            uint32_t d = lab_nbr[base + p];
+            uint64_t word = ~0ull;
+            int nl = next[l];
+            if (nl >= 0 && nl < kMaxIndexedLabels) {
+                uint4 s0 = rec[2 * (uint64_t)d], s1 = rec[2 * (uint64_t)d + 1];
+                uint64_t db = (static_cast<uint64_t>(s0.y) << 32) | s0.x;
+                uint32_t de[kMaxIndexedLabels] = {s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                uint32_t lo = nl == 0 ? 0 : de[nl - 1], hi = de[nl];
+                uint64_t gb = db + lo;
+                uint32_t cnt = hi - lo;
+                if (cnt < kDegEscape && gb < (1ull << 40)) word = (gb << kDegBits) | cnt;
+            }
+            out[base + p] = make_uint4(d, 0u, static_cast<uint32_t>(word), static_cast<uint32_t>(word >> 32));
+        }
+    }
+}
+}  // namespace
+
+bool Session::build_metapath_successors(cudaStream_t st) {
+    GraphStore& gs = *g;
+    if (!gs.label_index_built || schema.size() < 2) return false;
+    int next[kMaxIndexedLabels];
+    for (int i = 0; i < kMaxIndexedLabels; ++i) next[i] = -1;
+    for (size_t i = 0; i + 1 < schema.size(); ++i) {
+        uint32_t l = schema[i], n = schema[i + 1];
+        if (l >= static_cast<uint32_t>(kMaxIndexedLabels)) return false;
+        if (next[l] >= 0 && next[l] != static_cast<int>(n)) return false;  // not a function of l
+        next[l] = static_cast<int>(n);
+    }
+    DeviceGuard guard(gs.device);
+    auto t0 = std::chrono::steady_clock::now();
+    DeviceBuffer<int> dnext(kMaxIndexedLabels);
+    WF_CUDA(cudaMemcpy(dnext.get(), next, sizeof(next), cudaMemcpyHostToDevice));
+    mp_adj.allocate(std::max<uint64_t>(gs.E, 1));
+    int blocks = std::max(1, std::min<int>(static_cast<int>((gs.V * 32ull + 255) / 256), sm_count(gs.device) * 32));
+    k_metapath_successors<<<blocks, 256, 0, st>>>(gs.lab_rec.get(), gs.lab_nbr.get(), gs.V, dnext.get(),
+                                                  mp_adj.get());
+    WF_LAUNCHED();
+    WF_CUDA(cudaStreamSynchronize(st));
+    preprocess_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return true;
+}
+
 void Session::build_adjacency(cudaStream_t st) {
     GraphStore& gs = *g;
     DeviceGuard guard(gs.device);

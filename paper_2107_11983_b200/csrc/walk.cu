@@ -100,6 +100,7 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.staged = (stride % 8 == 0 && reinterpret_cast<uintptr_t>(paths) % 16 == 0) ? 1 : 0;
     L.alias_wide = s.alias_wide ? 1 : 0;
     L.adj = s.adj.get();
+    L.mp_adj = s.mp_adj.get();
     int grid = s.grid > 0 ? s.grid : occupancy_grid(s);
     uint64_t lanes_needed = (L.n_rows + 31) / 32 * 32;
     int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));

@@ -23,7 +23,8 @@ from .abi import (ExecOptionsC, GraphInfoC, ProgramDesc, QuerySpecC, RmatParamsC
                   raise_for)
 from .host import ExecOptions, Graph, QuerySpec, RunMetrics, RunResult, WalkSet
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwalkforge_b200.so")
+LIB_PATH = os.environ.get("WF_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                 "libwalkforge_b200.so")
 
 _u64p = C.POINTER(C.c_uint64)
 _u32p = C.POINTER(C.c_uint32)

@@ -31,6 +31,12 @@ __global__ void gather(const uint4* __restrict__ buf, uint64_t nslots, int iters
             acc += __ldcg(reinterpret_cast<const uint32_t*>(buf) + slot);
         } else if constexpr (G == 8) {
             acc += (uint32_t)__ldcg(reinterpret_cast<const unsigned long long*>(buf) + slot);
+        } else if constexpr (G == 33) {  // one 256-bit load of a 32 B sector
+            uint32_t a, b, c, d, e, f, g, h;
+            asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(d), "=r"(e), "=r"(f), "=r"(g), "=r"(h)
+                         : "l"(buf + slot * 2));
+            acc += a ^ h;
         } else {
             const uint4* p = buf + slot * (G / 16);
 #pragma unroll
@@ -59,7 +65,7 @@ __global__ void chase(const uint4* __restrict__ buf, uint64_t nslots, int iters,
 
 template <int G>
 double run(const uint4* buf, uint64_t bytes, int blocks, int iters, unsigned long long* sink) {
-    uint64_t nslots = G <= 4 ? bytes / 4 : (G == 8 ? bytes / 8 : bytes / G);
+    uint64_t nslots = G <= 4 ? bytes / 4 : (G == 8 ? bytes / 8 : (G == 33 ? bytes / 32 : bytes / G));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -76,6 +82,7 @@ double run(const uint4* buf, uint64_t bytes, int blocks, int iters, unsigned lon
 
 int main(int argc, char** argv) {
     uint64_t gib = argc > 1 ? strtoull(argv[1], nullptr, 10) : 32;
+    int only = argc > 2 ? atoi(argv[2]) : 0;  // 1: one pass per variant (for ncu)
     uint64_t bytes = gib << 30;
     uint4* buf = nullptr;
     if (cudaMalloc(&buf, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
@@ -95,6 +102,8 @@ int main(int argc, char** argv) {
         double r8 = run<8>(buf, bytes, blocks, iters, sink);
         double r16 = run<16>(buf, bytes, blocks, iters, sink);
         double r32 = run<32>(buf, bytes, blocks, iters, sink);
+        double r33 = run<33>(buf, bytes, blocks, iters, sink);
+        printf("  256-bit sector gathers/s: %.2fG (%.0f GB/s at 32B)\n", r33 / 1e9, r33 * 32 / 1e9);
         double r64 = run<64>(buf, bytes, blocks, iters, sink);
         double r128 = run<128>(buf, bytes, blocks, iters, sink);
         printf("  random gathers/s: 4B %.2fG (%.0f GB/s useful)  8B %.2fG  16B %.2fG  32B %.2fG (%.0f GB/s at 32B)"
