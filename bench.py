@@ -171,20 +171,49 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def s_alg_bytes(cfg, stats, moves):
-    """Algorithmic bytes per move (SURVEY §8 d, restated for our layout):
-    packed 8 B vertex word = 1 sector (never straddles), 16 B alias bucket = 1
-    sector, neighbour id = 1 sector, 32 B MetaPath label record = 1 sector,
-    path entry 4 B = 1/8 sector; O-REJ adds 1 sector per trial's neighbour load
-    and 1 per adjacency-search probe (instrumented counts)."""
+def s_alg_bytes(cfg, stats, moves, layout):
+    """Algorithmic 32 B sectors per move (SURVEY §8 d) for the layout the
+    session actually uses (abi.HAS_*), plus the random requests per move.
+
+    DeepWalk ALIAS: wide 32 B bucket (carries the destination's vertex word)
+    = 1 sector, else 16 B bucket + 8 B vertex word = 2.  PPR NAIVE: decorated
+    adjacency entry = 1, else neighbour + vertex word = 2.  MetaPath ITS:
+    successor-decorated partitioned edge = 1, else 32 B label record +
+    neighbour = 2.  Node2Vec O-REJ: one adjacency sector per trial + the
+    instrumented search probes (+1 vertex word without the decorated
+    adjacency).  Every move also writes 4 B of path = 1/8 sector."""
+    from paper_2107_11983_b200 import abi
     p = cfg["program"]
-    if p in ("deepwalk", "ppr", "metapath"):
-        return 2.125 * SECTOR, "vertex word + bucket/neighbour (+label record) + path, 2.125 sectors"
-    trials = stats["trials"] / max(moves, 1)
-    probes = stats["probes"] / max(moves, 1)
-    sectors = 1.0 + trials + probes + 0.125
-    return sectors * SECTOR, (f"vertex word + {trials:.3f} trial neighbour loads + {probes:.3f} "
-                              f"search probes + path = {sectors:.3f} sectors")
+    one = {"deepwalk": abi.HAS_WIDE_ALIAS, "ppr": abi.HAS_ADJ, "metapath": abi.HAS_MP_SUCC}
+    if p in one:
+        reads = 1.0 if layout & one[p] else 2.0
+        desc = {"deepwalk": "alias bucket", "ppr": "adjacency entry", "metapath": "partitioned edge"}[p]
+        text = (f"{desc}{' (decorated with the next vertex word)' if reads == 1 else ' + vertex word'}"
+                f" + 1/8 path = {reads + 0.125:.3f} sectors")
+    else:
+        trials = stats["trials"] / max(moves, 1)
+        probes = stats["probes"] / max(moves, 1)
+        base = 0.0 if layout & abi.HAS_ADJ else 1.0
+        reads = base + trials + probes
+        text = (f"{trials:.3f} trial adjacency sectors + {probes:.3f} search probe sectors"
+                f"{' + vertex word' if base else ''} + 1/8 path = {reads + 0.125:.3f} sectors")
+    return (reads + 0.125) * SECTOR, text, reads
+
+
+def random_access_block(moves_per_s, reads_per_move):
+    """Random HBM requests per second against the measured B200 ceiling for
+    random 32 B requests (tools/randbw.cu: every random sector miss fetches a
+    128 B line; profiles/random_access.json)."""
+    ceiling = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "random_access.json")) as f:
+            ceiling = float(json.load(f)["random_sector_requests_per_s"])
+    except Exception:
+        pass
+    req = moves_per_s * reads_per_move
+    return {"requests_per_move": reads_per_move, "requests_per_s": req,
+            "measured_ceiling_requests_per_s": ceiling,
+            "frac_of_ceiling": (req / ceiling) if ceiling else None}
 
 
 def flush_l2(buf):
@@ -208,6 +237,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     opts = ExecOptions(seed=1, path_stride=row_capacity(cfg))
     sess = E.Session(dg, prog, opts)
     sampler, flow, pre_s = sess.describe()
+    layout = sess.layout()
     spec, lo, hi = query_plan(cfg, V, rank, world)
     n = hi - lo
     stride = row_capacity(cfg)
@@ -297,7 +327,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
 
     return dict(moves=moves_per_step, total_ms=total_ms, step_ms=step_ms, stats=stats,
                 launches=launches, clocks=clk.summary(), info=info, sampler=sampler.name,
-                flow=flow.name, preprocess_s=pre_s, setup_s=setup_s, e2e=e2e, n=n, dg=dg,
+                flow=flow.name, preprocess_s=pre_s, setup_s=setup_s, e2e=e2e, n=n, dg=dg, layout=layout,
                 spec=spec, sess=sess)
 
 
@@ -338,12 +368,15 @@ def extras(args, rank, world, local_rank, dist):
             a = argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 1, "no_e2e": True})
             r = run_ours(a, CONFIGS[key], rank, world, local_rank, dist)
             ms = r["total_ms"] / 3
-            b, _ = s_alg_bytes(CONFIGS[key], r["stats"], r["moves"])
+            b, bdesc, reads = s_alg_bytes(CONFIGS[key], r["stats"], r["moves"], r["layout"])
             peak, _ = measured_peak()
             ach = r["moves"] * b / (ms * 1e-3) / 1e9
-            out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=r["moves"] / (ms * 1e-3),
+            rate = r["moves"] / (ms * 1e-3)
+            out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=rate,
                             ms_per_step=ms, moves=r["moves"], achieved_gbs=ach,
-                            roofline_frac=ach / peak, bytes_per_move=b, E=r["info"]["E"])
+                            roofline_frac=ach / peak, bytes_per_move=b, bytes_model=bdesc,
+                            random_access=random_access_block(rate, reads),
+                            E=r["info"]["E"])
             del r
             import torch
             torch.cuda.empty_cache()
@@ -449,7 +482,7 @@ def main():
     value = all_moves * args.steps / (total_ms * 1e-3)
 
     peak, peak_kind = measured_peak()
-    b, b_desc = s_alg_bytes(cfg, r["stats"], moves)
+    b, b_desc, reads = s_alg_bytes(cfg, r["stats"], moves, r["layout"])
     mean_launch_s = total_ms / args.steps * 1e-3
     achieved = moves * b / mean_launch_s / 1e9
     traffic = None
@@ -473,6 +506,7 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "bytes_per_move": b, "bytes_model": b_desc},
+        "random_access": random_access_block(moves * args.steps / (total_ms * 1e-3), reads),
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "preprocess_seconds": r["preprocess_s"],

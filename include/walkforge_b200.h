@@ -192,6 +192,13 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
 /* Resolved sampler and flow (0 Direct, 1 Tables, 2 Gathered). */
 int wf_session_describe(const wf_session* s, int32_t* sampler, int32_t* flow,
                         double* preprocess_seconds);
+/* Which HBM layouts the session uses (bitmask of WF_LAYOUT_HAS_*). */
+#define WF_LAYOUT_HAS_WIDE_ALIAS 1u   /* 32 B alias buckets with destination vertex words */
+#define WF_LAYOUT_HAS_ADJ 2u          /* decorated adjacency (NAIVE / O-REJ) */
+#define WF_LAYOUT_HAS_MP_SUCC 4u      /* MetaPath successor-decorated partitioned edges */
+#define WF_LAYOUT_HAS_LABEL_INDEX 8u  /* MetaPath label-partitioned CSR */
+#define WF_LAYOUT_HAS_SEARCH_INDEX 16u /* adjacency search index (Node2Vec) */
+int wf_session_layout(const wf_session* s, uint32_t* flags);
 void wf_session_destroy(wf_session* s);
 
 /* Runs every query of `spec` (run_sequential / run_interleaved,

@@ -153,6 +153,12 @@ class ExecOptionsC(C.Structure):
 LAYOUT_COMPACT_ALIAS = 1
 LAYOUT_NO_ADJ = 2
 
+HAS_WIDE_ALIAS = 1
+HAS_ADJ = 2
+HAS_MP_SUCC = 4
+HAS_LABEL_INDEX = 8
+HAS_SEARCH_INDEX = 16
+
 
 class QuerySpecC(C.Structure):
     _fields_ = [
@@ -208,7 +214,7 @@ EXPORTED_SYMBOLS = [
     "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_destroy",
     "wf_session_create", "wf_session_describe", "wf_session_destroy", "wf_session_run",
     "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_set_stats",
-    "wf_session_stats",
+    "wf_session_stats", "wf_session_layout",
     "wf_walkset_info", "wf_walkset_copy", "wf_walkset_visit_counts", "wf_walkset_destroy",
     "wf_run", "wf_rng_probe", "wf_session_tables",
 ]

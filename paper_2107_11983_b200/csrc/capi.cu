@@ -397,6 +397,20 @@ int wf_session_describe(const wf_session* s, int32_t* sampler, int32_t* flow,
     });
 }
 
+int wf_session_layout(const wf_session* sh, uint32_t* flags) {
+    return guarded([&] {
+        require(sh && flags, "null argument");
+        const Session& s = *sh->s;
+        uint32_t f = 0;
+        if (s.alias_wide) f |= WF_LAYOUT_HAS_WIDE_ALIAS;
+        if (s.adj.get()) f |= WF_LAYOUT_HAS_ADJ;
+        if (s.mp_adj.get()) f |= WF_LAYOUT_HAS_MP_SUCC;
+        if (s.desc.kind == WF_PROGRAM_METAPATH && s.g->label_index_built) f |= WF_LAYOUT_HAS_LABEL_INDEX;
+        if (s.desc.kind == WF_PROGRAM_NODE2VEC && s.g->search_index_built) f |= WF_LAYOUT_HAS_SEARCH_INDEX;
+        *flags = f;
+    });
+}
+
 void wf_session_destroy(wf_session* s) {
     if (s) {
         DeviceGuard guard(s->s->g->device);

@@ -145,6 +145,16 @@ __device__ __forceinline__ void ldr256(const uint4* p, uint4& a, uint4& b) {
         : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
         : "l"(p));
 }
+// A random 16 B entry read as its aligned 32 B sector with one 256-bit load:
+// measured (tools/randbw.cu) random 16 B requests sustain 20.9 G/s while 4 B,
+// 8 B and 256-bit requests sustain 36.6 G/s — every random miss costs a 128 B
+// line either way, so the wider load is free.
+__device__ __forceinline__ uint4 ldr16(const uint4* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    uint4 lo, hi;
+    ldr256(reinterpret_cast<const uint4*>(a & ~static_cast<uintptr_t>(31)), lo, hi);
+    return (a & 16) ? hi : lo;
+}
 
 __device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint32_t v,
                                             uint64_t& base, uint32_t& deg) {
@@ -346,19 +356,18 @@ struct Program<WF_PROGRAM_METAPATH> {  // algorithms.hpp:141-173
 // the adjacency search.  Same accept decisions, same draws — bit-exact.
 template <int K>
 __device__ __forceinline__ bool orej_accept(const WalkLaunch& L, const Walker& q, uint64_t e,
-                                            double y) {
+                                            double y, uint32_t /*dst*/) {
     return y < Program<K>::weight(L.prog, L.g, q, e);
 }
 
 template <>
 __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunch& L,
                                                                  const Walker& q, uint64_t e,
-                                                                 double y) {
+                                                                 double y, uint32_t dst) {
     const ProgParams& p = L.prog;
     double ew = p.weighted ? static_cast<double>(ldr(L.g.weights + e)) : 1.0;
     auto scaled = [&](double w) { return p.weighted ? __dmul_rn(w, ew) : w; };
     if (q.len == 1) return y < scaled(p.first);
-    uint32_t dst = ldr(L.g.nbr + e);
     if (dst == q.prev) return y < scaled(p.inv_a);
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
@@ -452,7 +461,25 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 ++q.n_trials;
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(L.prog.bound);
-                if (orej_accept<K>(L, q, base + x, y)) { pick = x; break; }
+                // one sector per trial: the candidate's id (and, with the
+                // decorated adjacency, its vertex word for the next step)
+                uint32_t dx;
+                uint64_t wx = 0;
+                if (L.adj) {
+                    uint4 a = ldr16(L.adj + base + x);
+                    dx = a.x;
+                    wx = (static_cast<uint64_t>(a.w) << 32) | a.z;
+                } else {
+                    dx = ldr(L.g.nbr + base + x);
+                }
+                if (orej_accept<K>(L, q, base + x, y, dx)) {
+                    dst = dx;
+                    if (L.adj) {
+                        q.nb_word = wx;
+                        q.have_nb = true;
+                    }
+                    return kMoved;
+                }
             }
         }
     } else if constexpr (F == kTables) {
@@ -472,7 +499,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 q.have_nb = true;
                 return kMoved;
             }
-            uint4 b = ldr(L.alias + base + x);
+            uint4 b = ldr16(L.alias + base + x);
             uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
             dst = q.rng.bits53() < thr ? b.z : b.w;  // y < split <=> k < ceil(split 2^53)
             return kMoved;
@@ -507,7 +534,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (L.mp_adj) {
                     // {dst, -, group word of dst for the next schema label}: the
                     // next move's label group arrives with this one load
-                    uint4 a = ldr(L.mp_adj + base + j);
+                    uint4 a = ldr16(L.mp_adj + base + j);
                     dst = a.x;
                     const uint64_t w = (static_cast<uint64_t>(a.w) << 32) | a.z;
                     if (w != ~0ull) {
@@ -561,7 +588,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
     }
     if (F == kDirect && L.adj) {
         // decorated adjacency {dst, -, vertex word of dst}: one 16 B load
-        uint4 a = ldr(L.adj + base + pick);
+        uint4 a = ldr16(L.adj + base + pick);
         dst = a.x;
         q.nb_word = (static_cast<uint64_t>(a.w) << 32) | a.z;
         q.have_nb = true;

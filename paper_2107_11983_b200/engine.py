@@ -288,6 +288,11 @@ class Session:
             return self.opts.path_stride or 64
         return p.target_length
 
+    def layout(self) -> int:
+        f = C.c_uint32()
+        _check(load_library().wf_session_layout(self.h, C.byref(f)))
+        return f.value
+
     def set_stats(self, enable: bool) -> None:
         _check(load_library().wf_session_set_stats(self.h, C.c_int(1 if enable else 0)))
 
