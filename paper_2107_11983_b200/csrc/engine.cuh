@@ -693,6 +693,7 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
     q.nb_word = 0;
     q.have_nb = false;
     bool active = false;
+    bool fresh = false;
     bool drained = false;
     unsigned long long steps = 0;
     for (;;) {
@@ -722,12 +723,18 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
                     } else {
                         load_current<K, S, F>(L, q);
                         active = true;
+                        fresh = true;
                     }
                 }
             }
         }
         if (!__any_sync(kFull, active)) break;
-        if (active) {
+        // A lane refilled this iteration sits one iteration out: its source's
+        // vertex word is still in flight, and consuming it now would stall the
+        // whole warp on that load while the other lanes could move.
+        const bool ready = active && !fresh;
+        fresh = false;
+        if (ready) {
             uint32_t dst = 0;
             int r = move<K, S, F>(L, q, dst);
             if (r == kMoved) {
