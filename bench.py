@@ -393,18 +393,28 @@ def reference_arm(args, cfg, rank, world):
     from paper_2107_11983_b200 import engine as E
     from paper_2107_11983_b200.host import ExecOptions, QuerySpec
     threads = os.cpu_count()
-    # input preparation: the same seeded R-MAT CSR the GPU arm walks on
-    dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
-                            label_count=cfg["labels"], device=0)
-    V = dg.info()["V"]
+    # input preparation: the same seeded R-MAT CSR the GPU arm walks on, built
+    # on the CPU by the oracle's C restatement of the generator (bit-identical
+    # to the device build, tests/test_rmat_cpu.py) so no engine code runs on
+    # this arm; s26 (2.1 B edges) is built on the device and downloaded.
+    if cfg["scale"] <= 24:
+        hg = PortOracle().rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
+                               label_count=cfg["labels"])
+        graph_source = "CPU R-MAT (oracle/wf_oracle.c)"
+    else:
+        dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
+                                label_count=cfg["labels"], device=0)
+        hg = dg.download()
+        del dg
+        graph_source = "device R-MAT, downloaded"
+    V = hg.vertex_count
     spec, lo, hi = query_plan(cfg, V, 0, 1)
-    hg = dg.download()
-    del dg
     m = min(CPU_SAMPLE[args.config], hi - lo)
     sample = QuerySpec.from_list(spec.sources[:m])
     prog = program_of(cfg)
     opts = ExecOptions(seed=1, threads=threads)
     kind = "reference" if ref_available() else "port"
+    E_count = hg.edge_count
     if kind == "reference":
         rg = RefOracle().graph(hg)
         del hg
@@ -425,7 +435,9 @@ def reference_arm(args, cfg, rank, world):
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic R-MAT",
-        "config": {"workload": cfg["workload"], "sample_queries": m}, "impl": "reference",
+        "config": {"workload": cfg["workload"], "sample_queries": m, "graph": graph_source,
+                   "edges": int(E_count)},
+        "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": kind,
                          "sample": f"first {m} queries per step, run_interleaved k=64 k'=32, "
                                    f"no-op sink, preprocessing excluded (engine.hpp:455,498)"},

@@ -49,8 +49,33 @@ class _WfoResult(C.Structure):
                 ("preprocess_seconds", C.c_double)]
 
 
+class _WfoCsr(C.Structure):
+    _fields_ = [("vertex_count", C.c_uint32), ("edge_count", C.c_uint64), ("offsets", _u64p),
+                ("neighbors", _u32p), ("weights", _f32p), ("labels", _u8p)]
+
+
 class PortOracle:
     """The C restatement (wf_oracle.c)."""
+
+    def rmat(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, weighted=False,
+             label_count=0, threads=0) -> Graph:
+        """CPU R-MAT CSR (same definition as the device generator)."""
+        g = _WfoCsr()
+        rc = self.lib.wfo_rmat_csr(C.c_uint32(scale), C.c_uint32(edge_factor), C.c_double(a),
+                                   C.c_double(b), C.c_double(c), C.c_uint64(seed),
+                                   C.c_int(int(weighted)), C.c_uint32(label_count),
+                                   C.c_int(threads), C.byref(g))
+        raise_for(rc, "bad R-MAT parameters")
+        try:
+            V, E = g.vertex_count, g.edge_count
+            off = np.ctypeslib.as_array(g.offsets, shape=(V + 1,)).copy()
+            nbr = np.ctypeslib.as_array(g.neighbors, shape=(E,)).copy() if E else np.zeros(0, np.uint32)
+            w = np.ctypeslib.as_array(g.weights, shape=(E,)).copy() if weighted and E else None
+            lab = (np.ctypeslib.as_array(g.labels, shape=(E,)).copy()
+                   if label_count and E else None)
+        finally:
+            self.lib.wfo_rmat_free(C.byref(g))
+        return Graph(off, nbr, w, lab)
 
     def __init__(self, path: str = PORT_LIB):
         if not os.path.exists(path):

@@ -15,6 +15,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
+#include <unistd.h>
 
 /* ---- RNG: include/walkforge/rng.hpp ---------------------------------------- */
 
@@ -836,4 +837,217 @@ int wfo_static_tables(const wfo_graph* g, const wf_program_desc* prog, int sampl
     if (rej_p_star && t.rej_p_star) memcpy(rej_p_star, t.rej_p_star, g->vertex_count * sizeof(double));
     wfo_tables_free(&t);
     return WF_OK;
+}
+
+/* ---- synthetic R-MAT CSR, multithreaded --------------------- */
+
+#define WFO_RMAT_SALT 0x524D4154454447ULL
+#define WFO_WEIGHT_SALT 0x57464757454947ULL /* graph.cpp:26 */
+#define WFO_LABEL_SALT 0x5746474C41424CULL  /* graph.cpp:27 */
+
+typedef struct {
+    uint64_t premix;
+    uint32_t scale, t1, t2, t3;
+} wfo_rmat_gen;
+
+static inline void wfo_rmat_edge(const wfo_rmat_gen* g, uint64_t i, uint32_t* s, uint32_t* d) {
+    wfo_rng r;
+    r.state = wfo_mix(g->premix ^ wfo_mix(i ^ WFO_SALT));
+    uint32_t ss = 0, dd = 0;
+    for (uint32_t lvl = 0; lvl < g->scale; lvl += 2) {
+        uint64_t x = wfo_next(&r);
+        for (int h = 0; h < 2; ++h) {
+            uint32_t l = lvl + h;
+            if (l >= g->scale) break;
+            uint32_t u = h == 0 ? (uint32_t)(x >> 32) : (uint32_t)x;
+            uint32_t bit = 1u << (g->scale - 1 - l);
+            if (u >= g->t1) {
+                if (u < g->t2) dd |= bit;
+                else if (u < g->t3) ss |= bit;
+                else { ss |= bit; dd |= bit; }
+            }
+        }
+    }
+    *s = ss;
+    *d = dd;
+}
+
+typedef struct {
+    const wfo_rmat_gen* gen;
+    uint64_t lo, hi;
+    uint32_t* deg;           /* pass 0 */
+    uint64_t* cursor;        /* pass 1 */
+    uint32_t* raw;           /* pass 1 */
+    /* pass 2/3: vertex range */
+    uint32_t vlo, vhi;
+    const uint64_t* off0;
+    uint32_t* ndeg;
+    const uint64_t* off1;
+    uint32_t* out;
+    int pass;
+    /* attributes */
+    uint64_t elo, ehi, wmix, lmix;
+    float* w;
+    uint8_t* lab;
+    uint32_t label_count;
+} wfo_rmat_job;
+
+static int wfo_cmp_u32(const void* a, const void* b) {
+    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return x < y ? -1 : (x > y);
+}
+
+static void* wfo_rmat_worker(void* arg) {
+    wfo_rmat_job* j = arg;
+    if (j->pass == 0 || j->pass == 1) {
+        for (uint64_t i = j->lo; i < j->hi; ++i) {
+            uint32_t s, d;
+            wfo_rmat_edge(j->gen, i, &s, &d);
+            if (s == d) continue;
+            if (j->pass == 0) {
+                __atomic_fetch_add(&j->deg[s], 1u, __ATOMIC_RELAXED);
+                __atomic_fetch_add(&j->deg[d], 1u, __ATOMIC_RELAXED);
+            } else {
+                j->raw[__atomic_fetch_add(&j->cursor[s], 1ull, __ATOMIC_RELAXED)] = d;
+                j->raw[__atomic_fetch_add(&j->cursor[d], 1ull, __ATOMIC_RELAXED)] = s;
+            }
+        }
+    } else if (j->pass == 2) { /* sort + count distinct */
+        for (uint32_t v = j->vlo; v < j->vhi; ++v) {
+            uint64_t a = j->off0[v], n = j->off0[v + 1] - a;
+            if (n > 1) qsort(j->raw + a, n, sizeof(uint32_t), wfo_cmp_u32);
+            uint32_t c = 0;
+            for (uint64_t e = 0; e < n; ++e) c += (e == 0 || j->raw[a + e] != j->raw[a + e - 1]);
+            j->ndeg[v] = c;
+        }
+    } else if (j->pass == 3) { /* compact */
+        for (uint32_t v = j->vlo; v < j->vhi; ++v) {
+            uint64_t a = j->off0[v], n = j->off0[v + 1] - a, w = j->off1[v];
+            for (uint64_t e = 0; e < n; ++e)
+                if (e == 0 || j->raw[a + e] != j->raw[a + e - 1]) j->out[w++] = j->raw[a + e];
+        }
+    } else { /* attributes: synthetic_weight / synthetic_label, graph.cpp:279-287 */
+        for (uint64_t e = j->elo; e < j->ehi; ++e) {
+            if (j->w) {
+                wfo_rng r;
+                r.state = wfo_mix(j->wmix ^ wfo_mix(e ^ WFO_SALT));
+                j->w[e] = (float)(1.0 + wfo_real(&r, 4.0));
+            }
+            if (j->lab) {
+                wfo_rng r;
+                r.state = wfo_mix(j->lmix ^ wfo_mix(e ^ WFO_SALT));
+                j->lab[e] = (uint8_t)wfo_index(&r, j->label_count);
+            }
+        }
+    }
+    return NULL;
+}
+
+static void wfo_run_jobs(wfo_rmat_job* jobs, int n) {
+    pthread_t* th = calloc(n, sizeof(pthread_t));
+    for (int i = 0; i < n; ++i) pthread_create(&th[i], NULL, wfo_rmat_worker, &jobs[i]);
+    for (int i = 0; i < n; ++i) pthread_join(th[i], NULL);
+    free(th);
+}
+
+static uint32_t wfo_thr32(double x) {
+    double t = floor(x * 4294967296.0);
+    return t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+int wfo_rmat_csr(uint32_t scale, uint32_t edge_factor, double a, double b, double c, uint64_t seed,
+                 int weighted, uint32_t label_count, int threads, wfo_csr* out) {
+    memset(out, 0, sizeof(*out));
+    if (scale < 1 || scale > 31 || edge_factor < 1) return WF_ERR_CONFIG;
+    if (threads <= 0) threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (threads < 1) threads = 1;
+    wfo_rmat_gen gen = {wfo_mix((seed ^ WFO_RMAT_SALT) + WFO_GAMMA), scale, wfo_thr32(a),
+                        wfo_thr32(a + b), wfo_thr32(a + b + c)};
+    const uint32_t V = 1u << scale;
+    const uint64_t n = (uint64_t)edge_factor << scale;
+    uint32_t* deg = calloc(V, sizeof(uint32_t));
+    wfo_rmat_job* jobs = calloc(threads, sizeof(wfo_rmat_job));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].gen = &gen;
+        jobs[t].lo = n * t / threads;
+        jobs[t].hi = n * (t + 1) / threads;
+        jobs[t].deg = deg;
+        jobs[t].pass = 0;
+    }
+    wfo_run_jobs(jobs, threads);
+    uint64_t* off0 = malloc((V + 1ull) * sizeof(uint64_t));
+    off0[0] = 0;
+    for (uint32_t v = 0; v < V; ++v) off0[v + 1] = off0[v] + deg[v];
+    free(deg);
+    uint64_t E0 = off0[V];
+    uint32_t* raw = malloc((E0 ? E0 : 1) * sizeof(uint32_t));
+    uint64_t* cursor = malloc(V * sizeof(uint64_t));
+    memcpy(cursor, off0, V * sizeof(uint64_t));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].cursor = cursor;
+        jobs[t].raw = raw;
+        jobs[t].pass = 1;
+    }
+    wfo_run_jobs(jobs, threads);
+    free(cursor);
+    uint32_t* ndeg = malloc(V * sizeof(uint32_t));
+    /* vertex ranges balanced by edges: R-MAT hubs sit at low ids */
+    uint32_t* cut = malloc((threads + 1) * sizeof(uint32_t));
+    cut[0] = 0;
+    for (int t = 1, v = 0; t <= threads; ++t) {
+        uint64_t target = E0 * (uint64_t)t / threads;
+        while ((uint32_t)v < V && off0[v] < target) ++v;
+        cut[t] = t == threads ? V : (uint32_t)v;
+    }
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].vlo = cut[t];
+        jobs[t].vhi = cut[t + 1];
+        jobs[t].off0 = off0;
+        jobs[t].ndeg = ndeg;
+        jobs[t].pass = 2;
+    }
+    wfo_run_jobs(jobs, threads);
+    uint64_t* off1 = malloc((V + 1ull) * sizeof(uint64_t));
+    off1[0] = 0;
+    for (uint32_t v = 0; v < V; ++v) off1[v + 1] = off1[v] + ndeg[v];
+    free(ndeg);
+    uint64_t E = off1[V];
+    uint32_t* nbr = malloc((E + 8) * sizeof(uint32_t));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].off1 = off1;
+        jobs[t].out = nbr;
+        jobs[t].pass = 3;
+    }
+    wfo_run_jobs(jobs, threads);
+    free(raw);
+    free(off0);
+    free(cut);
+    float* w = weighted ? malloc((E ? E : 1) * sizeof(float)) : NULL;
+    uint8_t* lab = label_count ? malloc(E ? E : 1) : NULL;
+    if (w || lab) {
+        for (int t = 0; t < threads; ++t) {
+            jobs[t].elo = E * t / threads;
+            jobs[t].ehi = E * (t + 1) / threads;
+            jobs[t].wmix = wfo_mix((seed ^ WFO_WEIGHT_SALT) + WFO_GAMMA);
+            jobs[t].lmix = wfo_mix((seed ^ WFO_LABEL_SALT) + WFO_GAMMA);
+            jobs[t].w = w;
+            jobs[t].lab = lab;
+            jobs[t].label_count = label_count;
+            jobs[t].pass = 4;
+        }
+        wfo_run_jobs(jobs, threads);
+    }
+    free(jobs);
+    out->vertex_count = V;
+    out->edge_count = E;
+    out->offsets = off1;
+    out->neighbors = nbr;
+    out->weights = w;
+    out->labels = lab;
+    return WF_OK;
+}
+
+void wfo_rmat_free(wfo_csr* g) {
+    free(g->offsets); free(g->neighbors); free(g->weights); free(g->labels);
+    memset(g, 0, sizeof(*g));
 }

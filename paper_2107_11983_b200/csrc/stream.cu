@@ -32,6 +32,12 @@ __global__ void k_compact_chunk(const uint32_t* __restrict__ rows, uint32_t stri
     }
 }
 
+__global__ void k_add_base(uint64_t* __restrict__ offs, uint64_t n, uint64_t base) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        offs[i] += base;
+}
+
 }  // namespace
 
 struct HostPipe {
@@ -102,7 +108,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     const uint64_t n = qe - qb;
     if (chunk == 0) {
         // ~8 chunks for overlap, each at least 64 Ki queries, staging <= 256 MiB
-        chunk = std::max<uint64_t>(n / 8, 1ull << 16);
+        chunk = std::max<uint64_t>(n / 8, 1ull << 18);
         chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(1, (256ull << 20) / (4ull * stride)));
     }
     chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1)));
@@ -159,8 +165,14 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         if (cnt)
             WF_CUDA(cudaMemcpyAsync(vertices + chunk_base[k], P.stage[b].get(), cnt * 4,
                                     cudaMemcpyDeviceToHost, B));
-        if (offsets)
+        if (offsets) {
+            if (chunk_base[k]) {  // chunk-relative -> absolute, on the copy stream
+                int blocks = static_cast<int>(std::min<uint64_t>((nr + 255) / 256, 4096));
+                k_add_base<<<std::max(blocks, 1), 256, 0, B>>>(P.offs[b].get(), nr, chunk_base[k]);
+                WF_LAUNCHED();
+            }
             WF_CUDA(cudaMemcpyAsync(offsets + r0, P.offs[b].get(), nr * 8, cudaMemcpyDeviceToHost, B));
+        }
         if (status)
             WF_CUDA(cudaMemcpyAsync(status + r0, P.stat[b].get(), nr, cudaMemcpyDeviceToHost, B));
         WF_CUDA(cudaEventRecord(P.ev_copy[b], B));
@@ -177,15 +189,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
                              " trials; asserted bound does not match the weights"
                        : std::string("device-side contract violation"));
     }
-    // chunk-relative offsets -> absolute
-    if (offsets) {
-        for (uint64_t k = 1; k < nchunks; ++k) {
-            const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk);
-            const uint64_t base = chunk_base[k];
-            for (uint64_t r = r0; r < r1; ++r) offsets[r] += base;
-        }
-        offsets[n] = chunk_base[nchunks];
-    }
+    if (offsets) offsets[n] = chunk_base[nchunks];
     unsigned long long hc[2] = {0, 0};
     WF_CUDA(cudaMemcpy(hc, P.ctr.get(), 16, cudaMemcpyDeviceToHost));
     if (hc[1] > 0) {

@@ -16,7 +16,7 @@ from paper_2107_11983_b200 import engine as E
 from paper_2107_11983_b200.host import (DeepWalkProgram, ExecOptions, MetaPathProgram,
                                         Node2VecProgram, PprProgram, QuerySpec, UniformProgram)
 from tests import golden_util as gu
-from tests.rmat_ref import rmat_csr
+from oracle.rmat_ref import rmat_csr
 
 pytestmark = pytest.mark.gpu
 

@@ -39,16 +39,22 @@ def main():
     lens = torch.empty(n, dtype=torch.int32, device="cuda")
     st = torch.empty(n, dtype=torch.uint8, device="cuda")
     steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
     for i in range(args.launches):
         steps.zero_()
         torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t = time.perf_counter()
+        e0.record(stream)
         sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), st.data_ptr(), 0,
-                    steps.data_ptr(), 0, 0, sources_dev_ptr=d_src.data_ptr())
-        sess.sync()
+                    steps.data_ptr(), 0, stream.cuda_stream, sources_dev_ptr=d_src.data_ptr())
+        e1.record(stream)
+        sess.sync(stream.cuda_stream)
         dt = time.perf_counter() - t
-        print(f"launch {i}: {steps.item()} moves {dt*1e3:.2f} ms {steps.item()/dt/1e9:.2f} G steps/s "
-              f"V={V} E={dg.info()['E']}", flush=True)
+        ms = e0.elapsed_time(e1)
+        print(f"launch {i}: {steps.item()} moves {ms:.3f} ms (events; wall {dt*1e3:.2f}) "
+              f"{steps.item()/ms/1e6:.2f} G steps/s V={V} E={dg.info()['E']} layout={sess.layout()}",
+              flush=True)
 
 
 if __name__ == "__main__":
