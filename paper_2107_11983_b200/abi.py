@@ -152,6 +152,8 @@ class ExecOptionsC(C.Structure):
 
 LAYOUT_COMPACT_ALIAS = 1
 LAYOUT_NO_ADJ = 2
+LAYOUT_MP_SUCC = 4
+LAYOUT_FORCE_ADJ = 8
 
 HAS_WIDE_ALIAS = 1
 HAS_ADJ = 2

@@ -373,12 +373,22 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS && !(lf & WF_LAYOUT_COMPACT_ALIAS))
             s.alias_wide = 32 * E + reserve <= free_b;
         if (s.flow == kTables) s.build_tables(nullptr);
-        if (s.flow == kDirect && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
+        // The decorated adjacency saves the dependent vertex-word load but is 4x
+        // the neighbour array: when the compact graph (neighbours + vertex
+        // words) is near L2 size, its L2 hits win (C2: 12.8 vs 11.3 G moves/s).
+        int l2 = 0;
+        WF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.g->device));
+        const uint64_t compact = 4 * E + 8ull * s.g->V;
+        const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
+        if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
             s.build_adjacency(nullptr);
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
             s.g->ensure_label_index(nullptr);
             WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            if (!(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
+            // opt-in: one random 16 B read per move instead of record + neighbour,
+            // but over a 4x larger array; measured slower on R-MAT s22 (the
+            // 32 B label records of hot vertices hit in L2), profiles/.
+            if ((lf & WF_LAYOUT_MP_SUCC) && 16 * E + reserve <= free_b)
                 s.build_metapath_successors(nullptr);
         }
         if (s.desc.kind == WF_PROGRAM_NODE2VEC) s.g->ensure_search_index(nullptr);

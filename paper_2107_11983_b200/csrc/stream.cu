@@ -135,6 +135,8 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
         // buffer b (status / offsets / staging) is free once chunk k-2's copy drained
         if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(A, P.ev_copy[b], 0));
+        // offs[b][0] = 0 (the previous user of this buffer rebased it in place)
+        WF_CUDA(cudaMemsetAsync(P.offs[b].get(), 0, 8, A));
         launch_walk(s, spec, src_by_qid, qb + r0, qb + r1, nullptr, P.rows[b].get(), stride,
                     P.lens[b].get(), P.stat[b].get(), nullptr, P.ctr.get(), P.ctr.get() + 1,
                     s.cursor.get(), A);

@@ -207,7 +207,7 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, static_cast<uint64_t>(sm_count(g.device)) * 64));
     if (s.kind == WF_SAMPLER_ALIAS) {
         const uint32_t bs = s.alias_wide ? 2 : 1;
-        s.alias.allocate(std::max<uint64_t>(g.E, 1) * bs);
+        s.alias.allocate((g.E + 2) * bs);  // +2: 32 B reads of the last 16 B entry stay in bounds
         k_static_alias<<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
                                                    s.alias.get(), bs, s.exhausted.get(), any);
     } else if (s.kind == WF_SAMPLER_ITS) {
@@ -311,7 +311,7 @@ bool Session::build_metapath_successors(cudaStream_t st) {
     auto t0 = std::chrono::steady_clock::now();
     DeviceBuffer<int> dnext(kMaxIndexedLabels);
     WF_CUDA(cudaMemcpy(dnext.get(), next, sizeof(next), cudaMemcpyHostToDevice));
-    mp_adj.allocate(std::max<uint64_t>(gs.E, 1));
+    mp_adj.allocate(gs.E + 2);
     int blocks = std::max(1, std::min<int>(static_cast<int>((gs.V * 32ull + 255) / 256), sm_count(gs.device) * 32));
     k_metapath_successors<<<blocks, 256, 0, st>>>(gs.lab_rec.get(), gs.lab_nbr.get(), gs.V, dnext.get(),
                                                   mp_adj.get());
@@ -325,7 +325,7 @@ void Session::build_adjacency(cudaStream_t st) {
     GraphStore& gs = *g;
     DeviceGuard guard(gs.device);
     auto t0 = std::chrono::steady_clock::now();
-    adj.allocate(std::max<uint64_t>(gs.E, 1));
+    adj.allocate(gs.E + 2);
     if (gs.E) {
         int blocks = std::max(1, std::min<int>(static_cast<int>((gs.E + 255) / 256), sm_count(gs.device) * 32));
         k_decorate_adj<<<blocks, 256, 0, st>>>(gs.nbr.get(), gs.E, gs.vword.get(), adj.get());

@@ -1,0 +1,140 @@
+"""Full BASELINE-size configurations (SURVEY §8 d: C1-C4) on the GPU.
+
+* sampled parity: a few hundred query ids of each full-size run are replayed by
+  the unmodified reference (oracle/_ref run_qids: its own ResolvedRun +
+  StepDriver) on the same CSR and must match bit for bit;
+* size-independent properties over the WHOLE run: every consecutive pair is an
+  edge, fixed-length walks have their length unless dead-ended at a vertex with
+  no usable edge, MetaPath edges carry the schema label, PPR's mean length is
+  the geometric 1/0.2, total steps = sum of path lengths - n, visit counts sum
+  to the number of path vertices, and repeated runs are identical.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import PortOracle, RefOracle, ref_available
+from paper_2107_11983_b200 import engine as E
+from paper_2107_11983_b200.host import (DeepWalkProgram, ExecOptions, MetaPathProgram,
+                                        Node2VecProgram, PprProgram, QuerySpec)
+
+pytestmark = pytest.mark.gpu
+
+
+def _edges_ok(g, ws):
+    """Every consecutive pair (u, v) of every path is an edge of g."""
+    lens = ws.lengths().astype(np.int64)
+    starts = ws.offsets[:-1].astype(np.int64)
+    idx = np.arange(ws.vertices.size, dtype=np.int64)
+    row = np.repeat(np.arange(lens.size), lens)
+    is_last = idx == (starts[row] + lens[row] - 1)
+    u = ws.vertices[:-1][~is_last[:-1]].astype(np.int64)
+    v = ws.vertices[1:][~is_last[:-1]].astype(np.int64)
+    lo = g.offsets[u].astype(np.int64)
+    hi = g.offsets[u + 1].astype(np.int64)
+    # binary search v in neighbors[lo:hi] (sorted adjacency), vectorised
+    L, H = lo.copy(), hi.copy()
+    for _ in range(40):
+        active = L < H
+        if not active.any():
+            break
+        mid = (L + H) // 2
+        less = g.neighbors[np.minimum(mid, g.edge_count - 1)] < v
+        L = np.where(active & less, mid + 1, L)
+        H = np.where(active & ~less, mid, H)
+    found = (L < hi) & (g.neighbors[np.minimum(L, g.edge_count - 1)] == v)
+    return bool(found.all()), u, v, L
+
+
+def _sample_parity(hg, spec, prog, opts, got, k=300, seed=0):
+    n = len(got)
+    qids = np.unique(np.random.default_rng(seed).integers(0, n, k)).astype(np.uint64)
+    if ref_available():
+        want = RefOracle().graph(hg).run_qids(spec, prog, opts, qids)
+    else:
+        want = PortOracle().run(hg, spec, prog, opts, qids=qids, threads=8)
+    for i, q in enumerate(qids):
+        assert got.status[q] == want.walks.status[i], int(q)
+        assert np.array_equal(got.path(int(q)), want.walks.path(i)), int(q)
+
+
+@pytest.fixture(scope="module")
+def s22():
+    dg = E.DeviceGraph.rmat(22, 16, seed=1, weighted=True, label_count=5)
+    return dg, dg.download()
+
+
+def test_c1_deepwalk_s16_full_run_matches_reference():
+    dg = E.DeviceGraph.rmat(16, 16, seed=1, weighted=True)
+    hg = dg.download()
+    prog, opts = DeepWalkProgram(80, True), ExecOptions(seed=1)
+    got = E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, opts)
+    if ref_available():
+        want = RefOracle().graph(hg).run(QuerySpec.one_per_vertex(), prog, opts)
+    else:
+        want = PortOracle().run(hg, QuerySpec.one_per_vertex(), prog, opts, threads=8)
+    assert got.walks.equals(want.walks)
+    assert got.metrics.total_steps == want.metrics.total_steps
+
+
+def test_c2_ppr_s20_full_size():
+    dg = E.DeviceGraph.rmat(20, 16, seed=1)
+    hg = dg.download()
+    src = np.random.default_rng(1).integers(0, hg.vertex_count, 1 << 20, dtype=np.uint32)
+    spec, prog, opts = QuerySpec.from_list(src), PprProgram(0.2), ExecOptions(seed=1)
+    sess = E.Session(dg, prog, opts)
+    ws = sess.run(spec)
+    got = ws.to_host()
+    ok, *_ = _edges_ok(hg, got)
+    assert ok
+    counts = ws.visit_counts()
+    assert int(counts.sum()) == got.vertices.size
+    assert np.array_equal(counts, np.bincount(got.vertices, minlength=hg.vertex_count))
+    # geometric lengths over walks whose source has edges
+    deg = np.diff(hg.offsets)[src]
+    moves = got.lengths()[deg > 0] - 1
+    assert abs(moves.mean() - 5.0) < 0.05
+    assert ws.metrics.total_steps == got.vertices.size - got.status.size
+    _sample_parity(hg, spec, prog, opts, got, k=2000)
+    # whole run against the reference (cheap at this size)
+    if ref_available():
+        want = RefOracle().graph(hg).run(spec, prog, opts)
+        assert got.equals(want.walks)
+
+
+def test_c3_node2vec_s22_full_size(s22):
+    dg, hg = s22
+    spec, prog, opts = QuerySpec.one_per_vertex(), Node2VecProgram(2.0, 0.5, 80, False), ExecOptions(seed=1)
+    got = E.run_sequential(dg, spec, prog, opts).walks
+    ok, *_ = _edges_ok(hg, got)
+    assert ok
+    deg = np.diff(hg.offsets)
+    # symmetric graph: only isolated sources dead-end; everything else has 80 vertices
+    assert np.all(got.lengths()[deg > 0] == 80)
+    assert np.all(got.lengths()[deg == 0] == 1)
+    _sample_parity(hg, spec, prog, opts, got, k=200)
+    again = E.run_sequential(dg, spec, prog, opts).walks
+    assert again.equals(got)
+
+
+def test_c4_metapath_s22_full_size(s22):
+    dg, hg = s22
+    schema = [i % 5 for i in range(79)]
+    spec, prog, opts = QuerySpec.one_per_vertex(), MetaPathProgram(schema), ExecOptions(seed=1)
+    got = E.run_sequential(dg, spec, prog, opts).walks
+    ok, u, v, pos = _edges_ok(hg, got)
+    assert ok
+    # the traversed edge carries the schema label of its position
+    lens = got.lengths().astype(np.int64)
+    row = np.repeat(np.arange(lens.size), lens)
+    in_row = np.arange(got.vertices.size, dtype=np.int64) - got.offsets[:-1].astype(np.int64)[row]
+    step = in_row[in_row < lens[row] - 1]
+    assert np.all(hg.labels[pos] == np.asarray(schema, np.uint8)[step])
+    # complete walks have 80 vertices; a dead end has no edge with the next label
+    done = got.status == 0
+    assert np.all(lens[done] == 80)
+    dead = np.flatnonzero(~done)[:2000]
+    for q in dead:
+        last = int(got.path(int(q))[-1])
+        want_label = schema[lens[q] - 1]
+        assert not np.any(hg.labels[hg.offsets[last]:hg.offsets[last + 1]] == want_label)
+    _sample_parity(hg, spec, prog, opts, got, k=300)

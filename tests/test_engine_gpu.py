@@ -295,3 +295,71 @@ def test_has_edge_matches_reference(rmat12):
     got = dg.has_edge(src, dst)
     want = np.array([d in set(hg.neighbors_of(int(s)).tolist()) for s, d in zip(src, dst)])
     assert np.array_equal(got, want)
+
+
+LAYOUT_CASES = [
+    ("deepwalk_compact_alias", lambda: DeepWalkProgram(40, True), abi.LAYOUT_COMPACT_ALIAS, 0),
+    ("deepwalk_wide_alias", lambda: DeepWalkProgram(40, True), 0, abi.HAS_WIDE_ALIAS),
+    ("ppr_adj", lambda: PprProgram(0.2), abi.LAYOUT_FORCE_ADJ, abi.HAS_ADJ),
+    ("ppr_no_adj", lambda: PprProgram(0.2), abi.LAYOUT_NO_ADJ, 0),
+    ("node2vec_adj", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_FORCE_ADJ,
+     abi.HAS_ADJ | abi.HAS_SEARCH_INDEX),
+    ("node2vec_w_adj", lambda: Node2VecProgram(0.5, 3.0, 30, True), abi.LAYOUT_FORCE_ADJ,
+     abi.HAS_ADJ | abi.HAS_SEARCH_INDEX),
+    ("node2vec_no_adj", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_NO_ADJ,
+     abi.HAS_SEARCH_INDEX),
+    ("metapath_succ", lambda: MetaPathProgram([i % 5 for i in range(40)]), abi.LAYOUT_MP_SUCC,
+     abi.HAS_MP_SUCC | abi.HAS_LABEL_INDEX),
+    ("metapath_succ_irregular", lambda: MetaPathProgram([0, 1, 0, 2, 3, 1, 4]), abi.LAYOUT_MP_SUCC,
+     abi.HAS_LABEL_INDEX),  # successor of 0 is not unique: falls back to records
+    ("metapath_records", lambda: MetaPathProgram([i % 5 for i in range(40)]), 0,
+     abi.HAS_LABEL_INDEX),
+]
+
+
+@pytest.mark.parametrize("name,mk,flags,expect", LAYOUT_CASES, ids=[c[0] for c in LAYOUT_CASES])
+def test_every_hbm_layout_is_bit_exact(rmat12, name, mk, flags, expect):
+    """Each decorated / compact layout (abi.LAYOUT_*) gives the reference's walks."""
+    dg, hg = rmat12
+    prog = mk()
+    spec = QuerySpec.one_per_vertex()
+    if name.startswith("ppr"):
+        spec = QuerySpec.from_list(np.random.default_rng(8).integers(0, hg.vertex_count, 20000))
+    opts = ExecOptions(seed=23, layout_flags=flags)
+    sess = E.Session(dg, prog, opts)
+    assert sess.layout() & expect == expect
+    if not expect & abi.HAS_WIDE_ALIAS and name.startswith("deepwalk"):
+        assert not sess.layout() & abi.HAS_WIDE_ALIAS
+    _compare_with_reference(dg, hg, spec, prog, opts)
+
+
+@pytest.mark.parametrize("prog,chunk", [(PprProgram(0.1), 1000), (DeepWalkProgram(24, True), 777),
+                                        (Node2VecProgram(2.0, 0.5, 16, False), 0),
+                                        (MetaPathProgram([i % 5 for i in range(12)]), 513)])
+def test_run_host_streaming_equals_run(rmat12, prog, chunk):
+    """wf_session_run_host (chunked compute/copy pipeline into host buffers),
+    called repeatedly on one session and on qid sub-ranges, equals the walk set
+    of run_sequential — including PPR walks that outgrow their row (stride 8)."""
+    dg, hg = rmat12
+    src = np.random.default_rng(3).integers(0, hg.vertex_count, 9000).astype(np.uint32)
+    spec = QuerySpec.from_list(src)
+    opts = ExecOptions(seed=17, path_stride=8)
+    whole = E.run_sequential(dg, spec, prog, opts).walks
+    sess = E.Session(dg, prog, opts)
+    for rep in range(3):
+        res = sess.run_to_numpy(spec, chunk=chunk)
+        assert res.walks.equals(whole), rep
+        assert res.metrics.total_steps == int(whole.lengths().sum()) - len(whole)
+    # a shard [lo, hi) through the raw call
+    lo, hi = 2500, 7100
+    n = hi - lo
+    off = np.zeros(n + 1, np.uint64)
+    cap = int(whole.offsets[hi] - whole.offsets[lo]) + 16
+    verts = np.zeros(cap, np.uint32)
+    st = np.zeros(n, np.uint8)
+    sess.run_host(spec, off.ctypes.data, verts.ctypes.data, cap, st.ctypes.data, chunk=chunk,
+                  qid_begin=lo, qid_end=hi)
+    base = whole.offsets[lo]
+    assert np.array_equal(off, whole.offsets[lo:hi + 1] - base)
+    assert np.array_equal(verts[:int(off[-1])], whole.vertices[int(base):int(whole.offsets[hi])])
+    assert np.array_equal(st, whole.status[lo:hi])
