@@ -20,15 +20,18 @@ namespace {
 __global__ void k_compact_chunk(const uint32_t* __restrict__ rows, uint32_t stride,
                                 const uint32_t* __restrict__ lengths,
                                 const uint64_t* __restrict__ offs, uint64_t nrows,
-                                uint32_t* __restrict__ out) {
+                                uint32_t* __restrict__ out, uint64_t cap) {
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t r = warp; r < nrows; r += nwarps) {
         uint32_t len = min(lengths[r], stride);
         const uint32_t* src = rows + r * stride;
-        uint32_t* dst = out + offs[r];
-        for (uint32_t j = lane; j < len; j += 32) dst[j] = src[j];
+        const uint64_t o = offs[r];
+        // rows that outgrew `stride` leave gaps (patched on the host), so the
+        // true chunk total may exceed the staging buffer: never write past it
+        for (uint32_t j = lane; j < len; j += 32)
+            if (o + j < cap) out[o + j] = src[j];
     }
 }
 
@@ -147,7 +150,8 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         count_launch();
         int blocks = static_cast<int>(std::min<uint64_t>((nr * 32 + 255) / 256, 65535));
         k_compact_chunk<<<std::max(blocks, 1), 256, 0, A>>>(P.rows[b].get(), stride, P.lens[b].get(),
-                                                            P.offs[b].get(), nr, P.stage[b].get());
+                                                            P.offs[b].get(), nr, P.stage[b].get(),
+                                                            P.stage[b].size());
         WF_LAUNCHED();
         WF_CUDA(cudaMemcpyAsync(P.h_tot + b, P.offs[b].get() + nr, 8, cudaMemcpyDeviceToHost, A));
         WF_CUDA(cudaEventRecord(P.ev_comp[b], A));
@@ -158,10 +162,26 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         const int b = static_cast<int>(k & 1);
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
         WF_CUDA(cudaEventSynchronize(P.ev_comp[b]));
-        const uint64_t cnt = P.h_tot[b];
+        uint64_t cnt = P.h_tot[b];
         chunk_base[k + 1] = chunk_base[k] + cnt;
         if (chunk_base[k + 1] > capacity)
             raise(WF_ERR_INVALID_ARG, "vertices_capacity too small for the walk set");
+        if (cnt > P.stage[b].size()) {
+            // rare (walks outgrew their rows): stage this chunk in a larger buffer
+            WF_CUDA(cudaStreamSynchronize(B));
+            DeviceBuffer<uint32_t> big(cnt);
+            int blocks = static_cast<int>(std::min<uint64_t>((nr * 32 + 255) / 256, 65535));
+            k_compact_chunk<<<std::max(blocks, 1), 256, 0, A>>>(P.rows[b].get(), stride,
+                                                                P.lens[b].get(), P.offs[b].get(), nr,
+                                                                big.get(), cnt);
+            WF_LAUNCHED();
+            WF_CUDA(cudaStreamSynchronize(A));
+            WF_CUDA(cudaMemcpy(vertices + chunk_base[k], big.get(), cnt * 4, cudaMemcpyDeviceToHost));
+            P.stage[b].allocate(cnt);  // grown for the next user (nothing pending on it)
+            WF_CUDA(cudaMemsetAsync(P.stage[b].get(), 0, 4, A));
+            WF_CUDA(cudaStreamSynchronize(A));
+            cnt = 0;  // already copied
+        }
         if (k + 1 < nchunks) enqueue_compute(k + 1);  // overlaps the copy below
         WF_CUDA(cudaStreamWaitEvent(B, P.ev_comp[b], 0));
         if (cnt)

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--layout", type=int, default=0)
+    ap.add_argument("--queries", type=int, default=0, help="override the batch size (random-source configs)")
     args = ap.parse_args()
     import torch
 
@@ -31,6 +32,8 @@ def main():
                             label_count=cfg["labels"])
     V = dg.info()["V"]
     sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=bench.row_capacity(cfg), layout_flags=args.layout))
+    if args.queries and cfg["queries"] == "random":
+        cfg["n_queries"] = args.queries
     spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
     n = hi - lo
     stride = bench.row_capacity(cfg)
