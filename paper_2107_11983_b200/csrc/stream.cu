@@ -111,7 +111,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     const uint64_t n = qe - qb;
     if (chunk == 0) {
         // ~8 chunks for overlap, each at least 64 Ki queries, staging <= 256 MiB
-        chunk = std::max<uint64_t>(n / 8, 1ull << 18);
+        chunk = std::max<uint64_t>(n / 8, 1ull << 19);  // tools/e2e_sweep.py
         chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(1, (256ull << 20) / (4ull * stride)));
     }
     chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1)));
