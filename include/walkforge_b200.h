@@ -264,6 +264,28 @@ int wf_walkset_copy(const wf_walkset* w, uint64_t qid_begin, uint64_t qid_end, u
 int wf_walkset_visit_counts(const wf_walkset* w, uint32_t* counts);
 void wf_walkset_destroy(wf_walkset* w);
 
+/* ---- walk record encoding: OutputFormat (output.hpp:17-27, output.cpp:26-47) -
+ * Text   "<qid>\t<complete|dead_end>\t<v0> <v1> ...\n"   (append_text_record)
+ * Binary u64 qid | u8 status | u32 length | u32 path[length] (append_binary_record)
+ * Encoded on the device; bytes are identical to the reference's writers. */
+typedef enum wf_output_format { WF_OUTPUT_TEXT = 0, WF_OUTPUT_BINARY = 1 } wf_output_format;
+
+/* Encodes n records (query ids qid_base..qid_base+n-1) from ragged arrays
+ * (offsets u64[n+1] relative, vertices, status; host or device pointers) into
+ * `out` (host or device, `capacity` bytes).  *bytes = encoded size; with
+ * out == NULL only the size is computed.  WF_ERR_INVALID_ARG if it does not fit. */
+int wf_encode_walks(const uint64_t* offsets, const uint32_t* vertices, const uint8_t* status,
+                    uint64_t n, uint64_t qid_base, int format, char* out, uint64_t capacity,
+                    uint64_t* bytes);
+
+/* Writes queries [qid_begin, qid_end) of a walk set to a file in qid order
+ * (DoubleBufferedWriter + OrderedBlockSink, output.cpp:49-200): blocks are
+ * encoded on the device and written by a host thread while the next block is
+ * encoded (double-buffered pinned memory).  qid_end 0 = all.  WF_ERR_IO on
+ * file errors. */
+int wf_walkset_write(const wf_walkset* w, const char* path, int format, uint64_t qid_begin,
+                     uint64_t qid_end, uint64_t* bytes_written);
+
 /* ---- convenience: run_sequential in one call -------------------------------- */
 int wf_run(const wf_graph* g, const wf_program_desc* prog, const wf_query_spec* spec,
            const wf_exec_options* opts, wf_walkset** out, wf_run_metrics* metrics);

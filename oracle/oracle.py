@@ -326,6 +326,28 @@ class RefGraph:
                                                C.c_int(int(discard)), C.byref(h), C.byref(m)))
         return self._collect(h, m, None)
 
+    def run_encoded(self, spec: QuerySpec, prog, opts: ExecOptions, fmt: int,
+                    path: Optional[str] = None) -> bytes:
+        """run_sequential, then the reference's own record writers: the encoded
+        bytes (append_text_record / append_binary_record), and with `path` the
+        file written by DoubleBufferedWriter."""
+        lib = self.ref.lib
+        desc, cspec, copts = prog.to_c(), spec.to_c(), opts.to_c()
+        h = C.c_void_p()
+        m = RunMetricsC()
+        self.ref._check(lib.wfref_run(self.h, C.byref(desc), C.byref(cspec), C.byref(copts),
+                                      C.c_int(0), C.c_int(0), C.byref(h), C.byref(m)))
+        try:
+            n = C.c_uint64()
+            self.ref._check(lib.wfref_encode(h, C.c_int(fmt), None, C.c_uint64(0), C.byref(n)))
+            buf = C.create_string_buffer(max(n.value, 1))
+            self.ref._check(lib.wfref_encode(h, C.c_int(fmt), buf, C.c_uint64(n.value), C.byref(n)))
+            if path is not None:
+                self.ref._check(lib.wfref_write_file(h, path.encode(), C.c_int(fmt)))
+            return buf.raw[:n.value]
+        finally:
+            lib.wfref_result_destroy(h)
+
     def run_qids(self, spec: QuerySpec, prog, opts: ExecOptions, qids) -> RunResult:
         desc = prog.to_c()
         cspec = spec.to_c()

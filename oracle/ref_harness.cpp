@@ -25,6 +25,7 @@
 #include "walkforge/algorithms.hpp"
 #include "walkforge/engine.hpp"
 #include "walkforge/interleave.hpp"
+#include "walkforge/output.hpp"
 #include "walkforge/synthetic.hpp"
 
 #include "../include/walkforge_b200.h"
@@ -341,6 +342,34 @@ int wfref_result_copy(const void* rp, uint64_t* qids, uint64_t* offsets, uint32_
 }
 
 void wfref_result_destroy(void* r) { delete static_cast<RefResult*>(r); }
+
+// Record encoding through the reference's own writers (output.cpp:26-47).
+// out == NULL: size only.
+int wfref_encode(const void* rp, int format, char* out, uint64_t capacity, uint64_t* written) {
+    return guarded([&] {
+        const RefResult& r = *static_cast<const RefResult*>(rp);
+        std::string buf;
+        for (const WalkRecord& w : r.walks) {
+            if (format == 0) append_text_record(buf, w);
+            else append_binary_record(buf, w);
+        }
+        *written = buf.size();
+        if (out) {
+            if (buf.size() > capacity) throw ConfigError("buffer too small");
+            std::memcpy(out, buf.data(), buf.size());
+        }
+    });
+}
+
+// A whole walk set through DoubleBufferedWriter (output.cpp:49-131).
+int wfref_write_file(const void* rp, const char* path, int format) {
+    return guarded([&] {
+        const RefResult& r = *static_cast<const RefResult*>(rp);
+        DoubleBufferedWriter writer(path, format == 0 ? OutputFormat::Text : OutputFormat::Binary);
+        writer.write_all(r.walks);
+        writer.finish();
+    });
+}
 
 // ---- static tables ----------------------------------------------------------
 

@@ -218,5 +218,5 @@ EXPORTED_SYMBOLS = [
     "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_set_stats",
     "wf_session_stats", "wf_session_layout",
     "wf_walkset_info", "wf_walkset_copy", "wf_walkset_visit_counts", "wf_walkset_destroy",
-    "wf_run", "wf_rng_probe", "wf_session_tables",
+    "wf_run", "wf_rng_probe", "wf_session_tables", "wf_encode_walks", "wf_walkset_write",
 ]

@@ -636,6 +636,24 @@ int wf_walkset_visit_counts(const wf_walkset* wh, uint32_t* counts) {
     });
 }
 
+int wf_encode_walks(const uint64_t* offsets, const uint32_t* vertices, const uint8_t* status,
+                    uint64_t n, uint64_t qid_base, int format, char* out, uint64_t capacity,
+                    uint64_t* bytes) {
+    return guarded([&] {
+        require(offsets && (vertices || n == 0) && (status || n == 0) && bytes, "null argument");
+        *bytes = encode_walks(offsets, vertices, status, n, qid_base, format, out, capacity);
+    });
+}
+
+int wf_walkset_write(const wf_walkset* w, const char* path, int format, uint64_t qid_begin,
+                     uint64_t qid_end, uint64_t* bytes_written) {
+    return guarded([&] {
+        require(w && path, "null argument");
+        uint64_t b = write_walkset(*w->w, path, format, qid_begin, qid_end);
+        if (bytes_written) *bytes_written = b;
+    });
+}
+
 void wf_walkset_destroy(wf_walkset* w) {
     if (w) {
         DeviceGuard guard(w->w->device);

@@ -158,6 +158,11 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics);
 
+// output.cu: record encoding (text / binary, byte-identical to output.cpp)
+uint64_t encode_walks(const uint64_t* offsets, const uint32_t* vertices, const uint8_t* status,
+                      uint64_t n, uint64_t qid_base, int fmt, char* out, uint64_t capacity);
+uint64_t write_walkset(const WalkSetStore& w, const char* path, int fmt, uint64_t qb, uint64_t qe);
+
 // walk set copy-out (walk.cu)
 void walkset_visit_counts(const WalkSetStore& w, uint32_t* counts_dev, cudaStream_t st);
 void walkset_copy(const WalkSetStore& w, uint64_t qb, uint64_t qe, uint64_t* offsets,

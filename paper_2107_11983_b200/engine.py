@@ -197,6 +197,14 @@ class DeviceWalkSet:
                                               _vp(offsets_ptr or None), _vp(vertices_ptr or None),
                                               _vp(status_ptr or None)))
 
+    def write(self, path: str, fmt: int = 0, qid_begin: int = 0, qid_end: int = 0) -> int:
+        """wf_walkset_write: the walk set as text (0) or binary (1) records."""
+        n = C.c_uint64()
+        _check(load_library().wf_walkset_write(self.h, path.encode(), C.c_int(fmt),
+                                               C.c_uint64(qid_begin), C.c_uint64(qid_end),
+                                               C.byref(n)))
+        return n.value
+
     def visit_counts(self) -> np.ndarray:
         out = np.zeros(self.V, np.uint32)
         _check(load_library().wf_walkset_visit_counts(self.h, _ptr(out, _u32p)))
@@ -350,6 +358,23 @@ def run_interleaved(g, spec: QuerySpec, prog, k: int, k_prime: int,
     if k_prime == 0 or k_prime > k:
         raise abi.ConfigError("search ring size must be in [1, k]")
     return run_sequential(g, spec, prog, o)
+
+
+def encode_walks(ws: WalkSet, fmt: int = 0, qid_base: int = 0) -> bytes:
+    """wf_encode_walks over a host WalkSet: the reference's record bytes."""
+    lib = load_library()
+    off = np.ascontiguousarray(ws.offsets, dtype=np.uint64)
+    verts = np.ascontiguousarray(ws.vertices, dtype=np.uint32)
+    st = np.ascontiguousarray(ws.status, dtype=np.uint8)
+    n = C.c_uint64()
+    _check(lib.wf_encode_walks(_ptr(off, _u64p), _ptr(verts, _u32p), _ptr(st, _u8p),
+                               C.c_uint64(len(ws)), C.c_uint64(qid_base), C.c_int(fmt), None,
+                               C.c_uint64(0), C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    _check(lib.wf_encode_walks(_ptr(off, _u64p), _ptr(verts, _u32p), _ptr(st, _u8p),
+                               C.c_uint64(len(ws)), C.c_uint64(qid_base), C.c_int(fmt), buf,
+                               C.c_uint64(n.value), C.byref(n)))
+    return buf.raw[:n.value]
 
 
 def rng_probe(seed: int, streams, draws: int) -> np.ndarray:
