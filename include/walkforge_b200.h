@@ -185,6 +185,31 @@ int wf_graph_has_edge(const wf_graph* g, const uint32_t* src, const uint32_t* ds
                       uint8_t* out);
 void wf_graph_destroy(wf_graph* g);
 
+/* ---- graph ingest (graph.cpp:190-453) -------------------------------------- */
+/* WFG1 binary files, Graph::read_binary / write_binary: magic "WFG1", u64 V,
+ * u64 E, u8 flags, u64 offsets[V+1], u32 neighbors[E], f64 weights[E]?, u32
+ * labels[E]?.  Reading applies the reference's FormatError checks; weights
+ * must be float32-exact and labels < 256 (device storage, ConfigError). */
+int wf_graph_read_wfg1(const char* path, int device, wf_graph** out);
+int wf_graph_write_wfg1(const wf_graph* g, const char* path);
+
+/* Text edge lists, load_edge_list (graph.cpp:307-453): `src dst [weight
+ * [label]]` per line, '#' comments; ids remapped to dense ids in ascending
+ * numeric order; CSR assembled on the device (stable sort by (src, dst), input
+ * order breaking ties); random attributes keyed on the final edge index. */
+typedef enum wf_attr_mode { WF_ATTR_NONE = 0, WF_ATTR_FROM_FILE = 1, WF_ATTR_RANDOM = 2 } wf_attr_mode;
+typedef struct wf_edge_list_options {
+    int32_t undirected; /* Directedness::Undirected: emit both directions */
+    int32_t weights;    /* wf_attr_mode */
+    int32_t labels;     /* wf_attr_mode */
+    uint32_t label_count;
+    uint64_t seed;
+} wf_edge_list_options;
+int wf_graph_load_edge_list(const char* path, const wf_edge_list_options* opts, int device,
+                            wf_graph** out);
+/* LoadedGraph::original_ids: u64[V] (identity for graphs not loaded from text). */
+int wf_graph_original_ids(const wf_graph* g, uint64_t* out);
+
 /* ---- sessions: ResolvedRun (engine.hpp:275-294) ------------------------------
  * Resolves the sampler (program default or override), checks the
  * program/sampler pairing (resolve_flow, engine.hpp:255-272), and builds the

@@ -206,6 +206,30 @@ class RefOracle:
                                                    C.c_uint32(label_count), C.byref(h)))
         return RefGraph(self, h)
 
+    def load_edge_list(self, path, undirected=False, weights=0, labels=0, label_count=5,
+                       seed=0):
+        """load_edge_list through the reference; returns (RefGraph, original_ids)."""
+        h = C.c_void_p()
+        n = C.c_uint64()
+        self._check(self.lib.wfref_load_edge_list(path.encode(), C.c_int(int(undirected)),
+                                                  C.c_int(weights), C.c_int(labels),
+                                                  C.c_uint32(label_count), C.c_uint64(seed),
+                                                  C.byref(h), C.byref(n), None, C.c_uint64(0)))
+        self.lib.wfref_graph_destroy(h)
+        ids = np.zeros(n.value, np.uint64)
+        h = C.c_void_p()
+        self._check(self.lib.wfref_load_edge_list(path.encode(), C.c_int(int(undirected)),
+                                                  C.c_int(weights), C.c_int(labels),
+                                                  C.c_uint32(label_count), C.c_uint64(seed),
+                                                  C.byref(h), C.byref(n), _ptr(ids, _u64p),
+                                                  C.c_uint64(ids.size)))
+        return RefGraph(self, h), ids
+
+    def read_binary(self, path) -> "RefGraph":
+        h = C.c_void_p()
+        self._check(self.lib.wfref_graph_read_binary(path.encode(), C.byref(h)))
+        return RefGraph(self, h)
+
     def ring(self, n, seed=0, weighted=False, label_count=0) -> "RefGraph":
         h = C.c_void_p()
         self._check(self.lib.wfref_graph_ring(C.c_uint32(n), C.c_uint64(seed),
@@ -294,6 +318,9 @@ class RefGraph:
         self.ref.lib.wfref_graph_export(self.h, _ptr(off, _u64p), _ptr(nbr, _u32p),
                                         _ptr(w, _f64p), _ptr(lab, _u32p))
         return off, nbr, w, lab
+
+    def write_binary(self, path) -> None:
+        self.ref._check(self.ref.lib.wfref_graph_write_binary(self.h, path.encode()))
 
     def has_edge(self, u, v) -> bool:
         return bool(self.ref.lib.wfref_has_edge(self.h, C.c_uint32(u), C.c_uint32(v)))

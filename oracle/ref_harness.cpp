@@ -198,6 +198,33 @@ int wfref_graph_ring(uint32_t n, uint64_t seed, int weighted, uint32_t label_cou
 
 void wfref_graph_destroy(void* g) { delete static_cast<Graph*>(g); }
 
+// load_edge_list (graph.cpp:307-453).  weights/labels: 0 none, 1 file, 2 random.
+int wfref_load_edge_list(const char* path, int undirected, int weights, int labels,
+                         uint32_t label_count, uint64_t seed, void** out, uint64_t* n_ids,
+                         uint64_t* ids, uint64_t ids_cap) {
+    return guarded([&] {
+        EdgeListOptions o;
+        o.directedness = undirected ? Directedness::Undirected : Directedness::Directed;
+        o.weights = static_cast<WeightMode>(weights);
+        o.labels = static_cast<LabelMode>(labels);
+        o.label_count = label_count;
+        o.seed = seed;
+        LoadedGraph lg = load_edge_list(path, o);
+        *n_ids = lg.original_ids.size();
+        if (ids)
+            for (size_t i = 0; i < lg.original_ids.size() && i < ids_cap; ++i) ids[i] = lg.original_ids[i];
+        *out = new Graph(std::move(lg.graph));
+    });
+}
+
+int wfref_graph_write_binary(const void* g, const char* path) {
+    return guarded([&] { static_cast<const Graph*>(g)->write_binary(path); });
+}
+
+int wfref_graph_read_binary(const char* path, void** out) {
+    return guarded([&] { *out = new Graph(Graph::read_binary(path)); });
+}
+
 int wfref_graph_info(const void* gp, uint32_t* v, uint64_t* e, int* has_w, int* has_l,
                      uint64_t* max_degree, double* max_weight, int* sorted) {
     const Graph& g = *static_cast<const Graph*>(gp);

@@ -196,6 +196,16 @@ class GraphInfoC(C.Structure):
     ]
 
 
+class EdgeListOptionsC(C.Structure):
+    _fields_ = [
+        ("undirected", C.c_int32),
+        ("weights", C.c_int32),
+        ("labels", C.c_int32),
+        ("label_count", C.c_uint32),
+        ("seed", C.c_uint64),
+    ]
+
+
 class RmatParamsC(C.Structure):
     _fields_ = [
         ("scale", C.c_uint32),
@@ -214,6 +224,7 @@ EXPORTED_SYMBOLS = [
     "wf_abi_version", "wf_last_error", "wf_kernel_launches",
     "wf_graph_create", "wf_graph_create_device", "wf_graph_generate_rmat",
     "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_destroy",
+    "wf_graph_read_wfg1", "wf_graph_write_wfg1", "wf_graph_load_edge_list", "wf_graph_original_ids",
     "wf_session_create", "wf_session_describe", "wf_session_destroy", "wf_session_run",
     "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_set_stats",
     "wf_session_stats", "wf_session_layout",

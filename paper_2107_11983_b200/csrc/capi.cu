@@ -339,6 +339,45 @@ int wf_graph_has_edge(const wf_graph* g, const uint32_t* src, const uint32_t* ds
     });
 }
 
+int wf_graph_read_wfg1(const char* path, int device, wf_graph** out) {
+    return guarded([&] {
+        require(path && out, "null argument");
+        auto h = std::make_unique<wf_graph>();
+        h->g.reset(graph_read_wfg1(path, device < 0 ? current_device() : device));
+        *out = h.release();
+    });
+}
+
+int wf_graph_write_wfg1(const wf_graph* g, const char* path) {
+    return guarded([&] {
+        require(g && path, "null argument");
+        graph_write_wfg1(*g->g, path);
+    });
+}
+
+int wf_graph_load_edge_list(const char* path, const wf_edge_list_options* opts, int device,
+                            wf_graph** out) {
+    return guarded([&] {
+        require(path && out, "null argument");
+        wf_edge_list_options o{};
+        if (opts) o = *opts;
+        std::vector<uint64_t> ids;
+        auto h = std::make_unique<wf_graph>();
+        h->g.reset(graph_load_edge_list(path, o, device < 0 ? current_device() : device, &ids));
+        h->g->original_ids = std::move(ids);
+        *out = h.release();
+    });
+}
+
+int wf_graph_original_ids(const wf_graph* g, uint64_t* out) {
+    return guarded([&] {
+        require(g && out, "null argument");
+        const GraphStore& s = *g->g;
+        if (s.original_ids.size() == s.V) std::copy(s.original_ids.begin(), s.original_ids.end(), out);
+        else for (uint32_t v = 0; v < s.V; ++v) out[v] = v;
+    });
+}
+
 void wf_graph_destroy(wf_graph* g) {
     if (g) {
         DeviceGuard guard(g->g->device);

@@ -37,6 +37,7 @@ struct GraphStore {
     double max_weight = 0.0;
     uint32_t label_count = 0;
     std::vector<uint8_t> label_present;  // 256 flags (MetaPath constructor check)
+    std::vector<uint64_t> original_ids;  // edge-list ingest: dense id -> input id
 
     std::mutex mu;
     bool label_index_built = false;
@@ -147,6 +148,12 @@ GraphStore* graph_from_device(const uint64_t* offsets, const uint32_t* neighbors
 GraphStore* graph_generate_rmat(const wf_rmat_params& p, int device);
 void graph_has_edge(const GraphStore& g, const uint32_t* src, const uint32_t* dst, uint64_t n,
                     uint8_t* out);
+
+// graph_io.cu
+GraphStore* graph_read_wfg1(const char* path, int device);
+void graph_write_wfg1(const GraphStore& g, const char* path);
+GraphStore* graph_load_edge_list(const char* path, const wf_edge_list_options& o, int device,
+                                 std::vector<uint64_t>* original_ids);
 
 // u32 -> u64 widening for scans over lengths / degrees
 struct WidenU64 {

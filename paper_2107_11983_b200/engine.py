@@ -107,6 +107,34 @@ class DeviceGraph:
         _check(lib.wf_graph_generate_rmat(C.byref(p), C.c_int(device), C.byref(h)))
         return cls(h)
 
+    @classmethod
+    def read_wfg1(cls, path: str, device: int = 0) -> "DeviceGraph":
+        """Graph::read_binary (graph.cpp:215-277)."""
+        h = _vp()
+        _check(load_library().wf_graph_read_wfg1(path.encode(), C.c_int(device), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_edge_list(cls, path: str, undirected: bool = False, weights: int = 0,
+                       labels: int = 0, label_count: int = 5, seed: int = 0,
+                       device: int = 0) -> "DeviceGraph":
+        """load_edge_list (graph.cpp:307-453); weights/labels: 0 none, 1 from
+        file, 2 random (EdgeListOptions, graph.hpp:80-87)."""
+        o = abi.EdgeListOptionsC(1 if undirected else 0, weights, labels, label_count, seed)
+        h = _vp()
+        _check(load_library().wf_graph_load_edge_list(path.encode(), C.byref(o), C.c_int(device),
+                                                      C.byref(h)))
+        return cls(h)
+
+    def write_wfg1(self, path: str) -> None:
+        """Graph::write_binary (graph.cpp:190-213)."""
+        _check(load_library().wf_graph_write_wfg1(self.h, path.encode()))
+
+    def original_ids(self) -> np.ndarray:
+        out = np.zeros(self.vertex_count, np.uint64)
+        _check(load_library().wf_graph_original_ids(self.h, _ptr(out, _u64p)))
+        return out
+
     def __del__(self):
         try:
             if self.h:
