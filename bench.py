@@ -268,7 +268,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), stat.data_ptr(),
                     counts.data_ptr() if counts is not None else 0, steps.data_ptr(),
                     over.data_ptr(), sptr, sources_dev_ptr=d_src.data_ptr())
-        if counts is not None and world > 1:
+        if counts is not None and dist is not None:
             dist.all_reduce(counts)  # NCCL: the one collective of the path
 
     # logical access counts for S_alg (one instrumented pass, untimed)
@@ -488,7 +488,7 @@ def main():
 
     import torch
     dist = None
-    if world > 1:
+    if world > 1 or "RANK" in os.environ:  # any torchrun launch, even N=1
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))

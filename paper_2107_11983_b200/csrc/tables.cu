@@ -208,6 +208,9 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
     if (s.kind == WF_SAMPLER_ALIAS) {
         const uint32_t bs = s.alias_wide ? 2 : 1;
         s.alias.allocate((g.E + 2) * bs);  // +2: 32 B reads of the last 16 B entry stay in bounds
+        // buckets of exhausted vertices are never built; zero them so the
+        // decoration pass reads valid vertex ids there
+        WF_CUDA(cudaMemsetAsync(s.alias.get(), 0, s.alias.bytes(), st));
         k_static_alias<<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
                                                    s.alias.get(), bs, s.exhausted.get(), any);
     } else if (s.kind == WF_SAMPLER_ITS) {
