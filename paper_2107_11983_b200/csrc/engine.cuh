@@ -42,10 +42,13 @@ struct GraphView {
     const uint4* __restrict__ lab_rec;
     const uint32_t* __restrict__ lab_nbr;
     uint32_t label_count;
-    // adjacency search index (sorted graphs): sidx[(base >> 4) + v + k] =
-    // nbr[base + 16 k] for k < ceil(deg / 16); the ranges never overlap since
-    // ceil(d/16) <= floor((base+d)/16) - floor(base/16) + 1.
-    const uint32_t* __restrict__ sidx;
+    // adjacency search index (sorted graphs), a sector-wide B-tree over each
+    // neighbour list: level l (stride s_l = 16 * 8^l) holds
+    // sidx[l][(base >> log2 s_l) + v + k] = nbr[base + s_l k], k < ceil(deg/s_l);
+    // per-vertex ranges never overlap since ceil(d/s) <= floor((base+d)/s) -
+    // floor(base/s) + 1.
+    const uint32_t* sidx[9];
+    int sidx_levels;
 };
 
 struct ProgParams {
@@ -201,30 +204,68 @@ __device__ __forceinline__ bool has_edge(const GraphView& g, uint64_t base, uint
 
 constexpr uint32_t kSidxBlock = 16;
 
+constexpr int kSidxMaxLevels = 9;  // strides 2^4 .. 2^28: top level <= 8 heads for deg < 2^31
+
+__host__ __device__ __forceinline__ int sidx_shift(int l) { return 4 + 3 * l; }
+
+// The 16 words of the two aligned 32 B sectors starting at a's sector of
+// index i (index levels are hot: L1-allocating read-only loads).
+__device__ __forceinline__ void load_two_sectors(const uint32_t* a, uint64_t i, uint32_t w[16]) {
+    const uint4* p = reinterpret_cast<const uint4*>(a + (i & ~7ull));
+    uint4 x0, x1, y0, y1;
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(x0.x), "=r"(x0.y), "=r"(x0.z), "=r"(x0.w), "=r"(x1.x), "=r"(x1.y), "=r"(x1.z), "=r"(x1.w)
+        : "l"(p));
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(y0.x), "=r"(y0.y), "=r"(y0.z), "=r"(y0.w), "=r"(y1.x), "=r"(y1.y), "=r"(y1.z), "=r"(y1.w)
+        : "l"(p + 2));
+    w[0] = x0.x; w[1] = x0.y; w[2] = x0.z; w[3] = x0.w; w[4] = x1.x; w[5] = x1.y; w[6] = x1.z; w[7] = x1.w;
+    w[8] = y0.x; w[9] = y0.y; w[10] = y0.z; w[11] = y0.w; w[12] = y1.x; w[13] = y1.y; w[14] = y1.z; w[15] = y1.w;
+}
+
 // Membership of dst in the sorted adjacency of v (base, deg) through the
-// search index: binary search over the block heads (E/16 + V words, mostly
-// L2-resident), then the block's 16 ids (64 B) read as 32 B sectors and
-// compared in registers.  Same answer as std::binary_search (graph.cpp:182-188)
-// with ~log2(deg/16) L2 probes + 2-3 sectors instead of ~log2(deg) DRAM probes.
+// sector B-tree: from the top level down, each level reads the <= 8 heads of
+// the current group (two sectors, one round trip) and picks the last head
+// <= dst; the chosen 16-id block is then read as 32 B sectors and compared in
+// registers.  Same answer as std::binary_search (graph.cpp:182-188) in
+// ~log8(deg/16) + 1 dependent rounds instead of ~log2(deg).
 __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t base, uint32_t deg,
                                                  uint32_t v, uint32_t dst, uint32_t* probes) {
-    if (deg <= kSidxBlock || g.sidx == nullptr) return has_edge(g, base, deg, dst, probes);
-    const uint32_t* ix = g.sidx + (base >> 4) + v;
-    const uint32_t nblk = (deg + kSidxBlock - 1) / kSidxBlock;
-    uint32_t np = 0;
-    // largest k with ix[k] <= dst
-    uint32_t lo = 0, hi = nblk;
-    while (lo < hi) {
-        uint32_t mid = (lo + hi) >> 1;
-        ++np;
-        if (__ldg(ix + mid) <= dst) lo = mid + 1; else hi = mid;
+    if (deg <= kSidxBlock || g.sidx_levels == 0) return has_edge(g, base, deg, dst, probes);
+    int l = 0;
+    while (((static_cast<uint64_t>(deg) + (1ull << sidx_shift(l)) - 1) >> sidx_shift(l)) > 8) {
+        if (++l >= g.sidx_levels) return has_edge(g, base, deg, dst, probes);
     }
+    uint32_t np = 0;
+    uint64_t group = 0;  // first head index of the current group at level l
+    uint64_t k = 0;
+    for (; l >= 0; --l) {
+        const int sh = sidx_shift(l);
+        const uint64_t n = (static_cast<uint64_t>(deg) + (1ull << sh) - 1) >> sh;
+        const uint64_t cnt = (n - group) < 8 ? (n - group) : 8;
+        const uint64_t i0 = (base >> sh) + v + group;
+        uint32_t w[16];
+        load_two_sectors(g.sidx[l], i0, w);
+        np += 2;
+        const uint32_t off = static_cast<uint32_t>(i0 & 7);
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j) c += (j >= off && j < off + cnt && w[j] <= dst) ? 1u : 0u;
+        if (c == 0) {  // only at the top: dst below the smallest neighbour
+            if (probes) *probes += np;
+            return false;
+        }
+        k = group + c - 1;
+        group = k * 8;
+    }
+    // block k: neighbours [b0, b1)
+    const uint64_t b0 = base + k * kSidxBlock;
+    const uint64_t b1 = min(b0 + kSidxBlock, base + deg);
     bool found = false;
-    if (lo > 0) {
-        const uint64_t b0 = base + static_cast<uint64_t>(lo - 1) * kSidxBlock;
-        const uint64_t b1 = min(b0 + kSidxBlock, base + deg);
-        // aligned 32 B sectors covering [b0, b1)
-        for (uint64_t s = b0 & ~7ull; s < b1; s += 8) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const uint64_t s = (b0 & ~7ull) + 8ull * t;
+        if (s < b1) {
             uint4 x, y;
             ldr256(reinterpret_cast<const uint4*>(g.nbr + s), x, y);
             ++np;

@@ -354,31 +354,45 @@ void GraphStore::ensure_label_index(cudaStream_t st) {
 
 namespace {
 __global__ void k_search_index(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
-                               uint32_t V, uint32_t* __restrict__ sidx) {
+                               uint32_t V, int shift, uint32_t* __restrict__ level) {
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t v = warp; v < V; v += nwarps) {
         uint64_t a = off[v], d = off[v + 1] - a;
         if (d <= kSidxBlock) continue;
-        uint64_t nblk = (d + kSidxBlock - 1) / kSidxBlock;
-        uint32_t* ix = sidx + (a >> 4) + v;
-        for (uint64_t k = lane; k < nblk; k += 32) ix[k] = nbr[a + k * kSidxBlock];
+        uint64_t n = (d + (1ull << shift) - 1) >> shift;
+        uint32_t* ix = level + (a >> shift) + v;
+        for (uint64_t k = lane; k < n; k += 32) ix[k] = nbr[a + (k << shift)];
     }
 }
 }  // namespace
 
-// Block-head index for has_edge_indexed (Node2Vec's distance test); only for
-// sorted adjacency, where std::binary_search semantics apply.
+// Sector B-tree over every adjacency list for has_edge_indexed (Node2Vec's
+// distance test); only for sorted adjacency, where std::binary_search
+// semantics apply.  Level l has stride 16 * 8^l; levels are added until the
+// largest list has <= 8 heads at the top.
 void GraphStore::ensure_search_index(cudaStream_t st) {
     std::lock_guard<std::mutex> lock(mu);
     if (search_index_built || !sorted || E == 0) return;
     DeviceGuard guard(device);
-    sidx.allocate((E >> 4) + V + 1);
-    k_search_index<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(offsets.get(), nbr.get(),
-                                                                              V, sidx.get());
-    WF_LAUNCHED();
+    int levels = 0;
+    if (max_degree > kSidxBlock) {
+        while (levels < kSidxMaxLevels) {
+            const int sh = sidx_shift(levels);
+            ++levels;
+            if (((static_cast<uint64_t>(max_degree) + (1ull << sh) - 1) >> sh) <= 8) break;
+        }
+    }
+    for (int l = 0; l < levels; ++l) {
+        const int sh = sidx_shift(l);
+        sidx[l].allocate((E >> sh) + V + 16);  // +16: two-sector reads at the end
+        k_search_index<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(
+            offsets.get(), nbr.get(), V, sh, sidx[l].get());
+        WF_LAUNCHED();
+    }
     WF_CUDA(cudaStreamSynchronize(st));
+    sidx_levels = levels;
     search_index_built = true;
 }
 

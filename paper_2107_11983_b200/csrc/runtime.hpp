@@ -44,7 +44,8 @@ struct GraphStore {
     DeviceBuffer<uint4> lab_rec;
     DeviceBuffer<uint32_t> lab_nbr;
     bool search_index_built = false;
-    DeviceBuffer<uint32_t> sidx;  // adjacency search index (engine.cuh has_edge_indexed)
+    int sidx_levels = 0;
+    DeviceBuffer<uint32_t> sidx[kSidxMaxLevels];  // sector B-tree levels (has_edge_indexed)
 
     GraphView view() const {
         GraphView g{};
@@ -59,7 +60,8 @@ struct GraphStore {
         g.lab_rec = lab_rec.get();
         g.lab_nbr = lab_nbr.get();
         g.label_count = label_count;
-        g.sidx = sidx.get();
+        g.sidx_levels = sidx_levels;
+        for (int l = 0; l < kSidxMaxLevels; ++l) g.sidx[l] = sidx[l].get();
         return g;
     }
     bool has_weights() const { return weights.get() != nullptr; }
