@@ -44,9 +44,8 @@ struct GraphView {
     uint32_t label_count;
     // adjacency search index (sorted graphs), a sector-wide B-tree over each
     // neighbour list: level l (stride s_l = 16 * 8^l) holds
-    // sidx[l][(base >> log2 s_l) + v + k] = nbr[base + s_l k], k < ceil(deg/s_l);
-    // per-vertex ranges never overlap since ceil(d/s) <= floor((base+d)/s) -
-    // floor(base/s) + 1.
+    // sidx[l][sidx_base(base, v, log2 s_l) + k] = nbr[base + s_l k], k < ceil(deg/s_l),
+    // in sector-aligned groups of 8 heads.
     const uint32_t* sidx[9];
     int sidx_levels;
 };
@@ -208,19 +207,12 @@ constexpr int kSidxMaxLevels = 9;  // strides 2^4 .. 2^28: top level <= 8 heads 
 
 __host__ __device__ __forceinline__ int sidx_shift(int l) { return 4 + 3 * l; }
 
-// The 16 words of the two aligned 32 B sectors starting at a's sector of
-// index i (index levels are hot: L1-allocating read-only loads).
-__device__ __forceinline__ void load_two_sectors(const uint32_t* a, uint64_t i, uint32_t w[16]) {
-    const uint4* p = reinterpret_cast<const uint4*>(a + (i & ~7ull));
-    uint4 x0, x1, y0, y1;
-    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(x0.x), "=r"(x0.y), "=r"(x0.z), "=r"(x0.w), "=r"(x1.x), "=r"(x1.y), "=r"(x1.z), "=r"(x1.w)
-        : "l"(p));
-    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(y0.x), "=r"(y0.y), "=r"(y0.z), "=r"(y0.w), "=r"(y1.x), "=r"(y1.y), "=r"(y1.z), "=r"(y1.w)
-        : "l"(p + 2));
-    w[0] = x0.x; w[1] = x0.y; w[2] = x0.z; w[3] = x0.w; w[4] = x1.x; w[5] = x1.y; w[6] = x1.z; w[7] = x1.w;
-    w[8] = y0.x; w[9] = y0.y; w[10] = y0.z; w[11] = y0.w; w[12] = y1.x; w[13] = y1.y; w[14] = y1.z; w[15] = y1.w;
+// Start of v's heads at a level with stride 2^sh, in 8-word sectors so every
+// group of 8 heads is one aligned 32 B sector: v owns
+// ceil(deg / 2^(sh+3)) <= floor((base+deg) / 2^(sh+3)) - floor(base / 2^(sh+3)) + 1
+// sectors, so consecutive vertices never overlap.
+__host__ __device__ __forceinline__ uint64_t sidx_base(uint64_t base, uint64_t v, int sh) {
+    return 8 * ((base >> (sh + 3)) + v);
 }
 
 // Membership of dst in the sorted adjacency of v (base, deg) through the
@@ -242,15 +234,18 @@ __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t ba
     for (; l >= 0; --l) {
         const int sh = sidx_shift(l);
         const uint64_t n = (static_cast<uint64_t>(deg) + (1ull << sh) - 1) >> sh;
-        const uint64_t cnt = (n - group) < 8 ? (n - group) : 8;
-        const uint64_t i0 = (base >> sh) + v + group;
-        uint32_t w[16];
-        load_two_sectors(g.sidx[l], i0, w);
-        np += 2;
-        const uint32_t off = static_cast<uint32_t>(i0 & 7);
+        const uint32_t cnt = static_cast<uint32_t>((n - group) < 8 ? (n - group) : 8);
+        // groups are sector-aligned: one 256-bit load per level
+        const uint4* p = reinterpret_cast<const uint4*>(g.sidx[l] + sidx_base(base, v, sh) + group);
+        uint4 x, y;
+        asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w), "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w)
+            : "l"(p));
+        ++np;
+        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
         uint32_t c = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < 16; ++j) c += (j >= off && j < off + cnt && w[j] <= dst) ? 1u : 0u;
+        for (uint32_t j = 0; j < 8; ++j) c += (j < cnt && w[j] <= dst) ? 1u : 0u;
         if (c == 0) {  // only at the top: dst below the smallest neighbour
             if (probes) *probes += np;
             return false;
@@ -717,8 +712,17 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
 // 531-538), so PPR's geometric terminations never idle a lane while queries
 // remain.  Every walker draws only from its own (seed, qid) stream, so the
 // output is independent of scheduling, exactly as in the reference.
+// Full occupancy (8 x 256 threads per SM, <= 32 registers) for the flows whose
+// state fits it: every resident walker is one more request in flight.  The
+// gathered flows (per-step scans, on-the-fly Vose) keep their registers.
 template <int K, int S, int F>
-__global__ void __launch_bounds__(kBlock) walk_kernel(const WalkLaunch L) {
+constexpr int walk_min_blocks() {
+    // Node2Vec's O-REJ step (adjacency search) needs ~40 registers without spills
+    return F == kGathered ? 1 : (K == WF_PROGRAM_NODE2VEC ? 6 : 8);
+}
+
+template <int K, int S, int F>
+__global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kernel(const WalkLaunch L) {
     using P = Program<K>;
     const int lane = threadIdx.x & 31;
     __shared__ uint32_t stage_words[8 * kBlock];

@@ -362,7 +362,7 @@ __global__ void k_search_index(const uint64_t* __restrict__ off, const uint32_t*
         uint64_t a = off[v], d = off[v + 1] - a;
         if (d <= kSidxBlock) continue;
         uint64_t n = (d + (1ull << shift) - 1) >> shift;
-        uint32_t* ix = level + (a >> shift) + v;
+        uint32_t* ix = level + sidx_base(a, v, shift);
         for (uint64_t k = lane; k < n; k += 32) ix[k] = nbr[a + (k << shift)];
     }
 }
@@ -386,7 +386,7 @@ void GraphStore::ensure_search_index(cudaStream_t st) {
     }
     for (int l = 0; l < levels; ++l) {
         const int sh = sidx_shift(l);
-        sidx[l].allocate((E >> sh) + V + 16);  // +16: two-sector reads at the end
+        sidx[l].allocate(sidx_base(E, V, sh) + 8);  // sector-aligned groups, see sidx_base
         k_search_index<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(
             offsets.get(), nbr.get(), V, sh, sidx[l].get());
         WF_LAUNCHED();
