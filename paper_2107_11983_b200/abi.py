@@ -154,12 +154,14 @@ LAYOUT_COMPACT_ALIAS = 1
 LAYOUT_NO_ADJ = 2
 LAYOUT_MP_SUCC = 4
 LAYOUT_FORCE_ADJ = 8
+LAYOUT_SEARCH_TREE = 16
 
 HAS_WIDE_ALIAS = 1
 HAS_ADJ = 2
 HAS_MP_SUCC = 4
 HAS_LABEL_INDEX = 8
 HAS_SEARCH_INDEX = 16
+HAS_EDGE_HASH = 32
 
 
 class QuerySpecC(C.Structure):

@@ -72,6 +72,14 @@ def build(verbose: bool = False, jobs: int = 4) -> str:
         cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt",
                                                                "-lpthread", "-ldl"]
         subprocess.check_call(cmd)
+    # the reference CLI's front-end (cli/walkforge.cpp) over the C-ABI
+    cli_src = os.path.join(HERE, "cli", "walkforge.cpp")
+    cli = os.path.join(os.path.dirname(LIB), "walkforge_b200")
+    if os.path.exists(cli_src) and (not os.path.exists(cli) or os.path.getmtime(cli) < max(
+            os.path.getmtime(cli_src), os.path.getmtime(LIB))):
+        subprocess.check_call(["g++", "-std=c++20", "-O2", f"-I{os.path.join(ROOT, 'include')}",
+                               cli_src, "-o", cli, f"-L{os.path.dirname(LIB)}",
+                               f"-l:{os.path.basename(LIB)}", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

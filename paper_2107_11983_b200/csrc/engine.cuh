@@ -48,6 +48,10 @@ struct GraphView {
     // in sector-aligned groups of 8 heads.
     const uint32_t* sidx[9];
     int sidx_levels;
+    // edge hash set (Node2Vec's distance test): open addressing over 32 B
+    // buckets of four u64 keys (src << 32 | dst), load factor <= 1/2
+    const unsigned long long* ehash;
+    uint64_t ehash_buckets;
 };
 
 struct ProgParams {
@@ -207,12 +211,13 @@ constexpr int kSidxMaxLevels = 9;  // strides 2^4 .. 2^28: top level <= 8 heads 
 
 __host__ __device__ __forceinline__ int sidx_shift(int l) { return 4 + 3 * l; }
 
-// Start of v's heads at a level with stride 2^sh, in 8-word sectors so every
-// group of 8 heads is one aligned 32 B sector: v owns
-// ceil(deg / 2^(sh+3)) <= floor((base+deg) / 2^(sh+3)) - floor(base / 2^(sh+3)) + 1
-// sectors, so consecutive vertices never overlap.
+// Start of v's heads at a level with stride 2^sh: v owns ceil(deg / 2^sh) <=
+// floor((base+deg) / 2^sh) - floor(base / 2^sh) + 1 words, so consecutive
+// vertices never overlap and each level stays ~E/2^sh + V words (the
+// sector-aligned variant padded every vertex to 8 words and fell out of L2:
+// 10.2 vs 12.2 G steps/s on C3).
 __host__ __device__ __forceinline__ uint64_t sidx_base(uint64_t base, uint64_t v, int sh) {
-    return 8 * ((base >> (sh + 3)) + v);
+    return (base >> sh) + v;
 }
 
 // Membership of dst in the sorted adjacency of v (base, deg) through the
@@ -235,17 +240,26 @@ __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t ba
         const int sh = sidx_shift(l);
         const uint64_t n = (static_cast<uint64_t>(deg) + (1ull << sh) - 1) >> sh;
         const uint32_t cnt = static_cast<uint32_t>((n - group) < 8 ? (n - group) : 8);
-        // groups are sector-aligned: one 256-bit load per level
-        const uint4* p = reinterpret_cast<const uint4*>(g.sidx[l] + sidx_base(base, v, sh) + group);
-        uint4 x, y;
-        asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-            : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w), "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w)
-            : "l"(p));
-        ++np;
-        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+        // the group's <= 8 heads span at most two sectors of the compact level
+        const uint64_t i0 = sidx_base(base, v, sh) + group;
+        const uint32_t off = static_cast<uint32_t>(i0 & 7);
+        const uint4* p = reinterpret_cast<const uint4*>(g.sidx[l] + (i0 & ~7ull));
         uint32_t c = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) c += (j < cnt && w[j] <= dst) ? 1u : 0u;
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && off + cnt <= 8) break;
+            uint4 x, y;
+            asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w), "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w)
+                : "l"(p + 2 * h));
+            ++np;
+            const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const uint32_t idx = 8 * h + j;
+                c += (idx >= off && idx < off + cnt && w[j] <= dst) ? 1u : 0u;
+            }
+        }
         if (c == 0) {  // only at the top: dst below the smallest neighbour
             if (probes) *probes += np;
             return false;
@@ -271,6 +285,50 @@ __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t ba
     }
     if (probes) *probes += np;
     return found;
+}
+
+constexpr unsigned long long kHashEmpty = ~0ull;  // (2^32-1, 2^32-1) is never an edge
+
+__host__ __device__ __forceinline__ uint64_t ehash_bucket(uint64_t key, uint64_t nb) {
+    const uint64_t h = splitmix_mix(key ^ 0x6A09E667F3BCC909ULL);
+#ifdef __CUDA_ARCH__
+    return __umul64hi(h, nb);
+#else
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(h) * nb) >> 64);
+#endif
+}
+
+// Graph::has_edge (graph.cpp:182-188) as an exact hash-set lookup: one 32 B
+// bucket (a single 256-bit load) answers almost every query — a random
+// sector instead of a binary search's chain of dependent probes.  Same
+// membership answer for sorted and unsorted adjacency alike.
+__device__ __forceinline__ bool has_edge_hashed(const GraphView& g, uint32_t u, uint32_t v,
+                                                uint32_t* probes) {
+    const unsigned long long key = (static_cast<unsigned long long>(u) << 32) | v;
+    uint64_t b = ehash_bucket(key, g.ehash_buckets);
+    uint32_t np = 0;
+    bool found = false;
+    for (;;) {
+        uint4 x, y;
+        ldr256(reinterpret_cast<const uint4*>(g.ehash + 4 * b), x, y);
+        ++np;
+        const unsigned long long k0 = (static_cast<unsigned long long>(x.y) << 32) | x.x;
+        const unsigned long long k1 = (static_cast<unsigned long long>(x.w) << 32) | x.z;
+        const unsigned long long k2 = (static_cast<unsigned long long>(y.y) << 32) | y.x;
+        const unsigned long long k3 = (static_cast<unsigned long long>(y.w) << 32) | y.z;
+        if (k0 == key || k1 == key || k2 == key || k3 == key) { found = true; break; }
+        if (k0 == kHashEmpty || k1 == kHashEmpty || k2 == kHashEmpty || k3 == kHashEmpty) break;
+        b = b + 1 == g.ehash_buckets ? 0 : b + 1;
+    }
+    if (probes) *probes += np;
+    return found;
+}
+
+// Node2Vec's "is dst a neighbour of prev" (algorithms.hpp:116-118).
+__device__ __forceinline__ bool prev_has_edge(const GraphView& g, uint32_t prev, uint64_t prev_base,
+                                              uint32_t prev_deg, uint32_t dst, uint32_t* probes) {
+    if (g.ehash) return has_edge_hashed(g, prev, dst, probes);
+    return has_edge_indexed(g, prev_base, prev_deg, prev, dst, probes);
 }
 
 // cumulative_upper_index, sampler.hpp:48-60.
@@ -352,7 +410,7 @@ struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
         } else {
             uint32_t dst = ldr(g.nbr + e);
             if (dst == q.prev) w = p.inv_a;
-            else if (has_edge_indexed(g, q.prev_base, q.prev_deg, q.prev, dst, &q.n_probes)) w = 1.0;
+            else if (prev_has_edge(g, q.prev, q.prev_base, q.prev_deg, dst, &q.n_probes)) w = 1.0;
             else w = p.inv_b;
         }
         return p.weighted ? __dmul_rn(w, static_cast<double>(ldr(g.weights + e))) : w;
@@ -407,7 +465,7 @@ __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunc
     if (dst == q.prev) return y < scaled(p.inv_a);
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
-    bool common = has_edge_indexed(L.g, q.prev_base, q.prev_deg, q.prev, dst, &q.n_probes);
+    bool common = prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, &q.n_probes);
     return y < scaled(common ? 1.0 : p.inv_b);
 }
 

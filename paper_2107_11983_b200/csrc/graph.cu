@@ -386,7 +386,7 @@ void GraphStore::ensure_search_index(cudaStream_t st) {
     }
     for (int l = 0; l < levels; ++l) {
         const int sh = sidx_shift(l);
-        sidx[l].allocate(sidx_base(E, V, sh) + 8);  // sector-aligned groups, see sidx_base
+        sidx[l].allocate(sidx_base(E, V, sh) + 16);  // +16: two-sector reads at the end
         k_search_index<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(
             offsets.get(), nbr.get(), V, sh, sidx[l].get());
         WF_LAUNCHED();
@@ -394,6 +394,48 @@ void GraphStore::ensure_search_index(cudaStream_t st) {
     WF_CUDA(cudaStreamSynchronize(st));
     sidx_levels = levels;
     search_index_built = true;
+}
+
+namespace {
+// Warp per vertex: insert every (v, nbr) key with atomicCAS into the first
+// empty slot of its bucket chain (open addressing, 4 slots per 32 B bucket).
+__global__ void k_edge_hash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                            uint32_t V, unsigned long long* __restrict__ table, uint64_t nb) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < V; v += nwarps) {
+        const uint64_t a = off[v], b = off[v + 1];
+        for (uint64_t e = a + lane; e < b; e += 32) {
+            const unsigned long long key = (static_cast<unsigned long long>(v) << 32) | nbr[e];
+            uint64_t bk = ehash_bucket(key, nb);
+            for (bool done = false; !done;) {
+                for (int s = 0; s < 4 && !done; ++s) {
+                    unsigned long long old = atomicCAS(table + 4 * bk + s, kHashEmpty, key);
+                    done = old == kHashEmpty || old == key;  // duplicates (multigraphs) stored once
+                }
+                bk = bk + 1 == nb ? 0 : bk + 1;
+            }
+        }
+    }
+}
+}  // namespace
+
+// Exact edge set for Node2Vec's distance test (has_edge_hashed), 2 slots per
+// edge (load factor 1/2): one random 32 B bucket per membership query.
+void GraphStore::ensure_edge_hash(cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (edge_hash_built || E == 0) return;
+    DeviceGuard guard(device);
+    const uint64_t nb = std::max<uint64_t>(1, (2 * E + 3) / 4);
+    ehash.allocate(4 * nb);
+    WF_CUDA(cudaMemsetAsync(ehash.get(), 0xFF, ehash.bytes(), st));
+    k_edge_hash<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(offsets.get(), nbr.get(), V,
+                                                                           ehash.get(), nb);
+    WF_LAUNCHED();
+    WF_CUDA(cudaStreamSynchronize(st));
+    ehash_buckets = nb;
+    edge_hash_built = true;
 }
 
 static std::unique_ptr<GraphStore> alloc_graph(uint32_t V, uint64_t E, bool w, bool l, int device) {

@@ -46,6 +46,9 @@ struct GraphStore {
     bool search_index_built = false;
     int sidx_levels = 0;
     DeviceBuffer<uint32_t> sidx[kSidxMaxLevels];  // sector B-tree levels (has_edge_indexed)
+    bool edge_hash_built = false;
+    uint64_t ehash_buckets = 0;
+    DeviceBuffer<unsigned long long> ehash;  // edge hash set (has_edge_hashed)
 
     GraphView view() const {
         GraphView g{};
@@ -62,6 +65,8 @@ struct GraphStore {
         g.label_count = label_count;
         g.sidx_levels = sidx_levels;
         for (int l = 0; l < kSidxMaxLevels; ++l) g.sidx[l] = sidx[l].get();
+        g.ehash = ehash.get();
+        g.ehash_buckets = ehash_buckets;
         return g;
     }
     bool has_weights() const { return weights.get() != nullptr; }
@@ -72,6 +77,7 @@ struct GraphStore {
     void finalize(cudaStream_t st);
     void ensure_label_index(cudaStream_t st);
     void ensure_search_index(cudaStream_t st);
+    void ensure_edge_hash(cudaStream_t st);
 };
 
 struct HostPipe;  // stream.cu: cached streams/buffers of the host-output pipeline

@@ -303,11 +303,15 @@ LAYOUT_CASES = [
     ("ppr_adj", lambda: PprProgram(0.2), abi.LAYOUT_FORCE_ADJ, abi.HAS_ADJ),
     ("ppr_no_adj", lambda: PprProgram(0.2), abi.LAYOUT_NO_ADJ, 0),
     ("node2vec_adj", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_FORCE_ADJ,
-     abi.HAS_ADJ | abi.HAS_SEARCH_INDEX),
+     abi.HAS_ADJ | abi.HAS_EDGE_HASH),
     ("node2vec_w_adj", lambda: Node2VecProgram(0.5, 3.0, 30, True), abi.LAYOUT_FORCE_ADJ,
-     abi.HAS_ADJ | abi.HAS_SEARCH_INDEX),
+     abi.HAS_ADJ | abi.HAS_EDGE_HASH),
     ("node2vec_no_adj", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_NO_ADJ,
-     abi.HAS_SEARCH_INDEX),
+     abi.HAS_EDGE_HASH),
+    ("node2vec_search_tree", lambda: Node2VecProgram(2.0, 0.5, 40, False),
+     abi.LAYOUT_SEARCH_TREE | abi.LAYOUT_FORCE_ADJ, abi.HAS_ADJ | abi.HAS_SEARCH_INDEX),
+    ("node2vec_w_search_tree", lambda: Node2VecProgram(0.5, 3.0, 30, True),
+     abi.LAYOUT_SEARCH_TREE, abi.HAS_SEARCH_INDEX),
     ("metapath_succ", lambda: MetaPathProgram([i % 5 for i in range(40)]), abi.LAYOUT_MP_SUCC,
      abi.HAS_MP_SUCC | abi.HAS_LABEL_INDEX),
     ("metapath_succ_irregular", lambda: MetaPathProgram([0, 1, 0, 2, 3, 1, 4]), abi.LAYOUT_MP_SUCC,
