@@ -434,8 +434,12 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
             // distance test: exact edge hash set (one random bucket per query)
             // unless opted out or HBM is short; then the sector B-tree
             WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            if (!(lf & WF_LAYOUT_SEARCH_TREE) && 16 * E + reserve <= free_b) s.g->ensure_edge_hash(nullptr);
-            else s.g->ensure_search_index(nullptr);
+            if (!(lf & WF_LAYOUT_SEARCH_TREE) && (s.g->edge_hash_built || 16 * E + reserve <= free_b)) {
+                s.g->ensure_edge_hash(nullptr);
+                s.use_edge_hash = true;
+            } else {
+                s.g->ensure_search_index(nullptr);
+            }
         }
         s.grid = occupancy_grid(s);
         *out = h.release();
@@ -461,9 +465,9 @@ int wf_session_layout(const wf_session* sh, uint32_t* flags) {
         if (s.adj.get()) f |= WF_LAYOUT_HAS_ADJ;
         if (s.mp_adj.get()) f |= WF_LAYOUT_HAS_MP_SUCC;
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.g->label_index_built) f |= WF_LAYOUT_HAS_LABEL_INDEX;
-        if (s.desc.kind == WF_PROGRAM_NODE2VEC && s.g->search_index_built && !s.g->edge_hash_built)
+        if (s.desc.kind == WF_PROGRAM_NODE2VEC && !s.use_edge_hash && s.g->search_index_built)
             f |= WF_LAYOUT_HAS_SEARCH_INDEX;
-        if (s.desc.kind == WF_PROGRAM_NODE2VEC && s.g->edge_hash_built) f |= WF_LAYOUT_HAS_EDGE_HASH;
+        if (s.desc.kind == WF_PROGRAM_NODE2VEC && s.use_edge_hash) f |= WF_LAYOUT_HAS_EDGE_HASH;
         *flags = f;
     });
 }

@@ -73,6 +73,7 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
     WalkLaunch L{};
     L.g = g.view();
+    if (!s.use_edge_hash) L.g.ehash = nullptr;  // per-session choice (B-tree opt-in)
     L.sview = s.any_exhausted ? s.sview.get() : g.vword.get();
     L.alias = s.alias.get();
     L.its = s.its.get();
