@@ -76,7 +76,6 @@ struct WalkLaunch {
     const uint32_t* __restrict__ qsources;
     uint64_t qid_begin;
     const uint64_t* __restrict__ qid_map;  // optional: cursor position -> qid
-    int map_rows_by_qid;  // 0: output row = cursor position (overflow re-runs); 1: qid - qid_begin (scheduling)
     uint64_t n_rows;
     uint64_t seed_mixed;
     uint32_t trial_cap;
@@ -771,52 +770,16 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
 // 531-538), so PPR's geometric terminations never idle a lane while queries
 // remain.  Every walker draws only from its own (seed, qid) stream, so the
 // output is independent of scheduling, exactly as in the reference.
-// PPR + NAIVE scheduling: a walk's length (absent dead ends) is a function of
-// its RNG stream alone — move i consumes draw 2i (index) and draw 2i+1 (the
-// stop coin, algorithms.hpp:31) — so walks predicted to outlive `horizon`
-// moves are put first in the cursor order.  The longest walks then start in
-// the first wave instead of trailing the kernel; results are unchanged (each
-// walk depends only on (seed, qid) and lands in its own row).
-static __global__ void k_ppr_schedule(uint64_t seed_mixed, uint64_t stop_thr, uint64_t qid_begin, uint64_t n,
-                               int horizon, uint64_t* __restrict__ order,
-                               unsigned long long* __restrict__ counters) {
-    const int lane = threadIdx.x & 31;
-    for (uint64_t r0 = blockIdx.x * (uint64_t)blockDim.x; r0 < n; r0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = r0 + threadIdx.x;
-        const uint64_t qid = qid_begin + r;
-        bool longw = false;
-        if (r < n) {
-            Rng g{stream_state(seed_mixed, qid)};
-            longw = true;
-            for (int i = 0; i < horizon; ++i) {
-                g.s += kGamma;  // the move's index draw
-                if (g.bits53() < stop_thr) { longw = false; break; }
-            }
-        }
-        const unsigned lm = __ballot_sync(kFull, r < n && longw);
-        const unsigned sm = __ballot_sync(kFull, r < n && !longw);
-        unsigned long long lb = 0, sb = 0;
-        if (lane == 0) {
-            if (lm) lb = atomicAdd(counters, static_cast<unsigned long long>(__popc(lm)));
-            if (sm) sb = atomicAdd(counters + 1, static_cast<unsigned long long>(__popc(sm)));
-        }
-        lb = __shfl_sync(kFull, lb, 0);
-        sb = __shfl_sync(kFull, sb, 0);
-        const unsigned below = (1u << lane) - 1;
-        if (r < n) {
-            if (longw) order[lb + __popc(lm & below)] = qid;
-            else order[n - 1 - (sb + __popc(sm & below))] = qid;
-        }
-    }
-}
-
 // Full occupancy (8 x 256 threads per SM, <= 32 registers) for the flows whose
 // state fits it: every resident walker is one more request in flight.  The
 // gathered flows (per-step scans, on-the-fly Vose) keep their registers.
 template <int K, int S, int F>
 constexpr int walk_min_blocks() {
-    // Node2Vec's O-REJ step (adjacency search) needs ~40 registers without spills
-    return F == kGathered ? 1 : (K == WF_PROGRAM_NODE2VEC ? 6 : 8);
+    // Node2Vec's O-REJ step (adjacency search) needs ~40 registers without
+    // spills; MetaPath's label-index ITS path is the C4 hot loop (its generic
+    // gathered fallback shares the kernel).
+    if (F == kGathered) return (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) ? 6 : 1;
+    return K == WF_PROGRAM_NODE2VEC ? 6 : 8;
 }
 
 template <int K, int S, int F>
@@ -854,7 +817,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     drained = true;
                 } else {
                     uint64_t qid = L.qid_map ? __ldg(L.qid_map + row) : L.qid_begin + row;
-                    q.row = L.map_rows_by_qid ? qid - L.qid_begin : row;
+                    q.row = row;
                     q.rng.s = stream_state(L.seed_mixed, qid);
                     q.cur = source_at(L, qid);
                     q.prev = 0xFFFFFFFFu;

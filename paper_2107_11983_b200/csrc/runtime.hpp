@@ -112,8 +112,6 @@ struct Session {
     DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
     bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
     bool use_edge_hash = false;  // Node2Vec distance test through the graph's edge hash set
-    DeviceBuffer<uint64_t> order;                 // PPR long-walks-first cursor order
-    DeviceBuffer<unsigned long long> order_ctr;   // [long, short] append counters
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
     DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 

@@ -117,20 +117,6 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
         L.scratch = s.scratch.get();
         L.scratch_stride = per_lane;
     }
-    if (qid_map == nullptr && s.desc.kind == WF_PROGRAM_PPR && s.kind == WF_SAMPLER_NAIVE &&
-        L.n_rows >= (1ull << 16)) {
-        // long walks first (k_ppr_schedule): the geometric tail starts in wave one
-        if (s.order.size() < L.n_rows) s.order.allocate(L.n_rows);
-        if (!s.order_ctr.get()) s.order_ctr.allocate(2);
-        WF_CUDA(cudaMemsetAsync(s.order_ctr.get(), 0, 16, st));
-        const int horizon = 16;  // P(move count > 16) = 0.8^16 ~ 2.8 % at stop 0.2
-        const int blocks = static_cast<int>(std::min<uint64_t>((L.n_rows + 255) / 256, 148ull * 16));
-        k_ppr_schedule<<<blocks, 256, 0, st>>>(L.seed_mixed, s.params.stop_thr, qid_begin, L.n_rows,
-                                               horizon, s.order.get(), s.order_ctr.get());
-        WF_LAUNCHED();
-        L.qid_map = s.order.get();
-        L.map_rows_by_qid = 1;
-    }
     WF_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
     fn<<<grid, kBlock, 0, st>>>(L);
     WF_LAUNCHED();
