@@ -726,7 +726,7 @@ __device__ __forceinline__ uint32_t source_at(const WalkLaunch& L, uint64_t qid)
 
 // Path rows are written a full 32 B sector at a time: each lane stages its
 // next 8 vertices in shared memory ([slot][thread], conflict-free) and stores
-// them with two 16 B vector stores when the group fills or the walk ends.
+// them with one 256-bit store when the group fills or the walk ends.
 // Single 4 B stores to 32 B-strided rows made every step a partial-sector
 // write (ncu: 4x the algorithmic DRAM write bytes).  Used when rows are
 // 32 B-aligned (stride % 8 == 0); otherwise one 4 B store per vertex.
@@ -735,14 +735,30 @@ struct PathStage {
     __device__ __forceinline__ uint32_t& at(uint32_t slot) { return s[slot * kBlock + threadIdx.x]; }
 };
 
+// One 256-bit store (st.global.v8, sm_100) of a lane's staged 8-word group.
+__device__ __forceinline__ void store_group(uint32_t* dst, PathStage ps) {
+    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(ps.at(0)),
+                 "r"(ps.at(1)), "r"(ps.at(2)), "r"(ps.at(3)), "r"(ps.at(4)), "r"(ps.at(5)), "r"(ps.at(6)),
+                 "r"(ps.at(7))
+                 : "memory");
+}
+
 __device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int st, PathStage ps) {
+#ifdef WF_DIAG_FINISH_TIME
+    // diagnostic builds only (tools/profile_walk.py --diag-times): the walk's
+    // completion time in 32 ns units replaces its length
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    L.lengths[q.row] = static_cast<uint32_t>(t >> 5);
+#else
     L.lengths[q.row] = q.len;
+#endif
     L.status[q.row] = static_cast<uint8_t>(st);
     if (L.staged) {
+        // the open group as one whole-sector store (words past the length are
+        // unspecified row padding, as the rest of the row)
         const uint32_t g0 = q.len & ~7u;
-        const uint32_t end = min(q.len, L.stride);
-        uint32_t* row = L.paths + q.row * L.stride;
-        for (uint32_t p = g0; p < end; ++p) row[p] = ps.at(p & 7);
+        if (g0 < min(q.len, L.stride)) store_group(L.paths + q.row * L.stride + g0, ps);
     }
     if (q.len > L.stride) atomicAdd(L.overflow_out, 1ULL);
 }
@@ -752,15 +768,13 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
     if (p < L.stride) {
         if (L.staged) {
             ps.at(p & 7) = v;
-            if ((p & 7) == 7) {
-                uint4* dst = reinterpret_cast<uint4*>(L.paths + q.row * L.stride + (p - 7));
-                dst[0] = make_uint4(ps.at(0), ps.at(1), ps.at(2), ps.at(3));
-                dst[1] = make_uint4(ps.at(4), ps.at(5), ps.at(6), ps.at(7));
-            }
+            if ((p & 7) == 7) store_group(L.paths + q.row * L.stride + (p - 7), ps);
         } else {
             L.paths[q.row * L.stride + p] = v;
         }
     }
+    // In-kernel: these atomics overlap the walk's load latency.  Counting the
+    // rows in a pass after the kernel measured slower (C2: 0.29 vs 0.25 ms).
     if (L.visit_counts) atomicAdd(L.visit_counts + v, 1u);
 }
 
@@ -775,12 +789,23 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
 // gathered flows (per-step scans, on-the-fly Vose) keep their registers.
 template <int K, int S, int F>
 constexpr int walk_min_blocks() {
-    // Node2Vec's O-REJ step (adjacency search) needs ~40 registers without
-    // spills; MetaPath's label-index ITS path is the C4 hot loop (its generic
+    // Node2Vec's O-REJ step (edge hash probe) needs ~48 registers without
+    // spills (5 blocks: 23.9 vs 22.9 G steps/s at 6 with 76 B of spills, C3);
+    // MetaPath's label-index ITS path is the C4 hot loop (its generic
     // gathered fallback shares the kernel).
     if (F == kGathered) return (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) ? 6 : 1;
-    return K == WF_PROGRAM_NODE2VEC ? 6 : 8;
+#ifndef WF_N2V_BLOCKS
+#define WF_N2V_BLOCKS 5
+#endif
+    return K == WF_PROGRAM_NODE2VEC ? WF_N2V_BLOCKS : 8;
 }
+
+// Rows a warp claims from the global cursor per atomic.  One atomic per refill
+// put every warp's refill on one L2 address (~every other iteration for PPR).
+#ifndef WF_CLAIM
+#define WF_CLAIM 32
+#endif
+constexpr uint32_t kClaim = WF_CLAIM;
 
 template <int K, int S, int F>
 __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kernel(const WalkLaunch L) {
@@ -801,21 +826,55 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     bool active = false;
     bool fresh = false;
     bool drained = false;
+    // warp-uniform claim state, kept in shared memory (registers are the
+    // occupancy limit of the O-REJ kernels): next unstarted row of the warp's
+    // claimed block and the rows left in it
+    __shared__ unsigned long long claim_next[kBlock / 32];
+    __shared__ uint32_t claim_left[kBlock / 32];
+    const int wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        claim_next[wid] = 0;
+        claim_left[wid] = 0;
+    }
+    __syncwarp();
     unsigned long long steps = 0;
     for (;;) {
-        // refill lanes without a live walker
+        // refill lanes without a live walker from the warp's claimed block of rows
         for (;;) {
             unsigned need = __ballot_sync(kFull, !active && !drained);
             if (need == 0) break;
-            int leader = __ffs(need) - 1;
-            unsigned long long first = 0;
-            if (lane == leader) first = atomicAdd(L.cursor, static_cast<unsigned long long>(__popc(need)));
-            first = __shfl_sync(kFull, first, leader);
-            if (!active && !drained) {
-                uint64_t row = first + __popc(need & ((1u << lane) - 1));
-                if (row >= L.n_rows) {
-                    drained = true;
-                } else {
+            uint64_t wnext = claim_next[wid];
+            uint32_t wleft = claim_left[wid];
+            if (wleft == 0) {
+                // guided claim: up to kClaim rows while the queue is long,
+                // shrinking to the lanes in need near its end (balance)
+                const uint64_t est = wnext < L.n_rows ? L.n_rows - wnext : 0;
+                const uint64_t share = est / (2ull * gridDim.x * (kBlock / 32));
+                const uint32_t want = max(static_cast<uint32_t>(__popc(need)),
+                                          share < kClaim ? static_cast<uint32_t>(share) : kClaim);
+                unsigned long long first = 0;
+                if (lane == 0) first = atomicAdd(L.cursor, static_cast<unsigned long long>(want));
+                first = __shfl_sync(kFull, first, 0);
+                wnext = first;
+                const uint64_t rest = first >= L.n_rows ? 0 : L.n_rows - first;
+                wleft = rest < want ? static_cast<uint32_t>(rest) : want;
+                if (wleft == 0) {  // queue drained: every idle lane is done
+                    drained = drained || !active;
+                    continue;
+                }
+            }
+            const uint32_t rank = __popc(need & ((1u << lane) - 1));
+            const uint32_t take = min(static_cast<uint32_t>(__popc(need)), wleft);
+            const uint64_t my = wnext + rank;
+            __syncwarp();
+            if (lane == 0) {
+                claim_next[wid] = wnext + take;
+                claim_left[wid] = wleft - take;
+            }
+            __syncwarp();
+            if (!active && !drained && rank < take) {
+                uint64_t row = my;
+                {
                     uint64_t qid = L.qid_map ? __ldg(L.qid_map + row) : L.qid_begin + row;
                     q.row = row;
                     q.rng.s = stream_state(L.seed_mixed, qid);

@@ -98,7 +98,7 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.error_word = s.error_word.get();
     L.use_label_index = g.label_index_built ? 1 : 0;
     L.stats = s.collect_stats ? s.stats.get() : nullptr;
-    L.staged = (stride % 8 == 0 && reinterpret_cast<uintptr_t>(paths) % 16 == 0) ? 1 : 0;
+    L.staged = (stride % 8 == 0 && reinterpret_cast<uintptr_t>(paths) % 32 == 0) ? 1 : 0;
     L.alias_wide = s.alias_wide ? 1 : 0;
     L.adj = s.adj.get();
     L.mp_adj = s.mp_adj.get();

@@ -20,6 +20,10 @@ def main():
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--layout", type=int, default=0)
     ap.add_argument("--queries", type=int, default=0, help="override the batch size (random-source configs)")
+    ap.add_argument("--counts", action="store_true", help="PPR: also accumulate visit counts")
+    ap.add_argument("--diag-times", action="store_true",
+                    help="library built with -DWF_DIAG_FINISH_TIME: print walk completion-time percentiles")
+    ap.add_argument("--flush", action="store_true", help="write 256 MiB between launches (cold L2, as bench.py)")
     args = ap.parse_args()
     import torch
 
@@ -42,15 +46,19 @@ def main():
     lens = torch.empty(n, dtype=torch.int32, device="cuda")
     st = torch.empty(n, dtype=torch.uint8, device="cuda")
     steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    counts = torch.zeros(V, dtype=torch.int32, device="cuda") if args.counts else None
     stream = torch.cuda.current_stream()
+    l2buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
     for i in range(args.launches):
         steps.zero_()
+        if l2buf is not None:
+            bench.flush_l2(l2buf)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t = time.perf_counter()
         e0.record(stream)
-        sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), st.data_ptr(), 0,
-                    steps.data_ptr(), 0, stream.cuda_stream, sources_dev_ptr=d_src.data_ptr())
+        sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), st.data_ptr(),
+                    counts.data_ptr() if counts is not None else 0, steps.data_ptr(), 0, stream.cuda_stream, sources_dev_ptr=d_src.data_ptr())
         e1.record(stream)
         sess.sync(stream.cuda_stream)
         dt = time.perf_counter() - t
@@ -58,6 +66,12 @@ def main():
         print(f"launch {i}: {steps.item()} moves {ms:.3f} ms (events; wall {dt*1e3:.2f}) "
               f"{steps.item()/ms/1e6:.2f} G steps/s V={V} E={dg.info()['E']} layout={sess.layout()}",
               flush=True)
+        if args.diag_times:
+            import numpy as np
+            t = lens.cpu().numpy().view(np.uint32).astype(np.int64)
+            t = (t - t.min()) * 32e-3  # us
+            qs = [50, 90, 99, 99.9, 99.99, 100]
+            print("  finish us: " + " ".join(f"p{q}={np.percentile(t, q):.1f}" for q in qs), flush=True)
 
 
 if __name__ == "__main__":
