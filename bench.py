@@ -261,13 +261,22 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     small = cfg["scale"] <= 20  # working set near L2 size: flush between steps
     l2buf = torch.zeros((256 << 20) // 4, dtype=torch.float32, device=dev) if small else None
 
-    def one_step():
+    def device_step():
+        s = torch.cuda.current_stream()
         steps.zero_()
         if counts is not None:
             counts.zero_()
         sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), stat.data_ptr(),
                     counts.data_ptr() if counts is not None else 0, steps.data_ptr(),
-                    over.data_ptr(), sptr, sources_dev_ptr=d_src.data_ptr())
+                    over.data_ptr(), s.cuda_stream, sources_dev_ptr=d_src.data_ptr())
+
+    graph = None
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            device_step()
         if counts is not None and dist is not None:
             dist.all_reduce(counts)  # NCCL: the one collective of the path
 
@@ -278,6 +287,19 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     stats = sess.stats()
     moves_per_step = int(steps.item())
     sess.set_stats(False)
+    # The step's device work (counter resets + the walk kernel) is captured
+    # once as a CUDA graph and replayed: a 0.2 ms kernel otherwise waits
+    # ~20 us per step for the host to submit it.  Every replay runs the whole
+    # walk kernel; wf_session_launch is capturable (no host sync, no allocation
+    # once warm).
+    launches_c0 = E.kernel_launches()
+    if not args.no_graph:
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            device_step()
+        torch.cuda.synchronize()
+    kernels_per_step = E.kernel_launches() - launches_c0 if graph is not None else None
     for _ in range(args.warmup):
         one_step()
     sess.sync(sptr)
@@ -300,6 +322,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             torch.cuda.synchronize()
     sess.sync(sptr)
     launches = E.kernel_launches() - launches0
+    if kernels_per_step is not None:  # replays do not pass the host-side counter
+        launches = kernels_per_step * args.steps
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(step_ms))
     assert int(steps.item()) == moves_per_step, "walks are deterministic per step"
@@ -473,6 +497,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch each step from the host instead of a CUDA graph replay")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -530,7 +555,9 @@ def main():
                    "sampler": r["sampler"], "flow": r["flow"],
                    "parallelism": f"query shards x{world}, graph replicated",
                    "l2": "flushed between steps (256 MiB write)" if cfg["scale"] <= 20
-                   else "inputs larger than L2"},
+                   else "inputs larger than L2",
+                   "launch": "host launch per step" if args.no_graph
+                   else "CUDA graph replay per step (counter resets + walk kernel)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",

@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -227,10 +228,7 @@ void check_device_error(Session& s) {
     WF_CUDA(cudaMemcpy(&h, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
     if (h != 0) {
         WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
-        if (h == WF_ERR_REJECTION_CAP)
-            raise(h, "rejection sampling exceeded " + std::to_string(s.trial_cap) +
-                         " trials; asserted bound does not match the weights");
-        raise(h, "device-side contract violation");
+        raise_device_error(s, h);
     }
 }
 
@@ -421,6 +419,10 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
         if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
             s.build_adjacency(nullptr);
+        if (const char* e = getenv("WF_ADJ_FROM")) {  // experiment
+            if (s.flow == kDirect && !s.adj.get()) s.build_adjacency(nullptr);
+            s.adj_from = static_cast<uint32_t>(atoi(e));
+        }
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
             s.g->ensure_label_index(nullptr);
             WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -611,10 +613,7 @@ int wf_session_run_host(wf_session* sh, const wf_query_spec* spec, uint64_t qid_
         if (spec->mode == WF_QUERY_FROM_LIST) {
             require(spec->sources != nullptr || n == 0, "null source list");
             require(!is_device_pointer(spec->sources), "wf_session_run_host takes a host source list");
-            for (uint64_t i = qid_begin; i < qid_end; ++i)
-                if (spec->sources[i] >= g.V)
-                    config_error("query source " + std::to_string(spec->sources[i]) +
-                                 " is not a vertex (V=" + std::to_string(g.V) + ")");
+            // sources are range-checked by the walk kernel (ConfigError after the run)
         }
         run_to_host(s, *spec, spec->sources, qid_begin, qid_end, offsets, vertices,
                     vertices_capacity, status, chunk_queries, metrics);

@@ -52,6 +52,9 @@ struct GraphView {
     // buckets of four u64 keys (src << 32 | dst), load factor <= 1/2
     const unsigned long long* ehash;
     uint64_t ehash_buckets;
+    // instrumented runs only: [trials, search probes, scanned edges] (the
+    // S_alg access counts of SURVEY 8d), else null
+    unsigned long long* stats;
 };
 
 struct ProgParams {
@@ -77,6 +80,8 @@ struct WalkLaunch {
     uint64_t qid_begin;
     const uint64_t* __restrict__ qid_map;  // optional: cursor position -> qid
     uint64_t n_rows;
+    uint32_t static_blocks;  // kClaim-row blocks dealt to each warp before the cursor
+    uint64_t dyn_base;       // = warps * static_blocks * kClaim: first cursor-claimed row
     uint64_t seed_mixed;
     uint32_t trial_cap;
     uint32_t stride;
@@ -94,8 +99,8 @@ struct WalkLaunch {
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
     const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
+    uint32_t adj_from;                // NAIVE: moves from path length >= adj_from use `adj`
     const uint4* __restrict__ mp_adj; // MetaPath: per partitioned edge {dst, 0, next-group word} or null
-    unsigned long long* stats;  // optional: [trials, search probes, scanned edges]
 };
 
 struct Walker {
@@ -106,9 +111,6 @@ struct Walker {
     uint32_t cur, prev;
     uint32_t cur_deg, prev_deg;
     uint32_t len;  // vertices on the path so far (moves + 1)
-    // lane-level logical access counters (survive refills); flushed to
-    // WalkLaunch::stats when requested — the instrumented S_alg of SURVEY §8 d
-    mutable uint32_t n_trials, n_probes, n_scanned;
     // vertex word of the destination when the sampler's load carried it
     uint64_t nb_word;
     bool have_nb;
@@ -186,7 +188,7 @@ __device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t
 // Graph::has_edge (graph.cpp:182-188): std::binary_search on sorted lists,
 // linear scan otherwise.  Membership only, so any exact search is equivalent.
 __device__ __forceinline__ bool has_edge(const GraphView& g, uint64_t base, uint32_t deg,
-                                         uint32_t dst, uint32_t* probes = nullptr) {
+                                         uint32_t dst, unsigned long long* probes = nullptr) {
     const uint32_t* ns = g.nbr + base;
     uint32_t np = 0;
     bool found = false;
@@ -201,7 +203,7 @@ __device__ __forceinline__ bool has_edge(const GraphView& g, uint64_t base, uint
     } else {
         for (uint32_t i = 0; i < deg && !found; ++i, ++np) found = __ldg(ns + i) == dst;
     }
-    if (probes) *probes += np;
+    if (probes) atomicAdd(probes, static_cast<unsigned long long>(np));
     return found;
 }
 
@@ -227,7 +229,7 @@ __host__ __device__ __forceinline__ uint64_t sidx_base(uint64_t base, uint64_t v
 // registers.  Same answer as std::binary_search (graph.cpp:182-188) in
 // ~log8(deg/16) + 1 dependent rounds instead of ~log2(deg).
 __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t base, uint32_t deg,
-                                                 uint32_t v, uint32_t dst, uint32_t* probes) {
+                                                 uint32_t v, uint32_t dst, unsigned long long* probes) {
     if (deg <= kSidxBlock || g.sidx_levels == 0) return has_edge(g, base, deg, dst, probes);
     int l = 0;
     while (((static_cast<uint64_t>(deg) + (1ull << sidx_shift(l)) - 1) >> sidx_shift(l)) > 8) {
@@ -261,7 +263,7 @@ __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t ba
             }
         }
         if (c == 0) {  // only at the top: dst below the smallest neighbour
-            if (probes) *probes += np;
+            if (probes) atomicAdd(probes, static_cast<unsigned long long>(np));
             return false;
         }
         k = group + c - 1;
@@ -283,7 +285,7 @@ __device__ __forceinline__ bool has_edge_indexed(const GraphView& g, uint64_t ba
             for (int i = 0; i < 8; ++i) found |= (s + i >= b0 && s + i < b1 && e[i] == dst);
         }
     }
-    if (probes) *probes += np;
+    if (probes) atomicAdd(probes, static_cast<unsigned long long>(np));
     return found;
 }
 
@@ -303,7 +305,7 @@ __host__ __device__ __forceinline__ uint64_t ehash_bucket(uint64_t key, uint64_t
 // sector instead of a binary search's chain of dependent probes.  Same
 // membership answer for sorted and unsorted adjacency alike.
 __device__ __forceinline__ bool has_edge_hashed(const GraphView& g, uint32_t u, uint32_t v,
-                                                uint32_t* probes) {
+                                                unsigned long long* probes) {
     const unsigned long long key = (static_cast<unsigned long long>(u) << 32) | v;
     uint64_t b = ehash_bucket(key, g.ehash_buckets);
     uint32_t np = 0;
@@ -320,13 +322,13 @@ __device__ __forceinline__ bool has_edge_hashed(const GraphView& g, uint32_t u, 
         if (k0 == kHashEmpty || k1 == kHashEmpty || k2 == kHashEmpty || k3 == kHashEmpty) break;
         b = b + 1 == g.ehash_buckets ? 0 : b + 1;
     }
-    if (probes) *probes += np;
+    if (probes) atomicAdd(probes, static_cast<unsigned long long>(np));
     return found;
 }
 
 // Node2Vec's "is dst a neighbour of prev" (algorithms.hpp:116-118).
 __device__ __forceinline__ bool prev_has_edge(const GraphView& g, uint32_t prev, uint64_t prev_base,
-                                              uint32_t prev_deg, uint32_t dst, uint32_t* probes) {
+                                              uint32_t prev_deg, uint32_t dst, unsigned long long* probes) {
     if (g.ehash) return has_edge_hashed(g, prev, dst, probes);
     return has_edge_indexed(g, prev_base, prev_deg, prev, dst, probes);
 }
@@ -410,7 +412,7 @@ struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
         } else {
             uint32_t dst = ldr(g.nbr + e);
             if (dst == q.prev) w = p.inv_a;
-            else if (prev_has_edge(g, q.prev, q.prev_base, q.prev_deg, dst, &q.n_probes)) w = 1.0;
+            else if (prev_has_edge(g, q.prev, q.prev_base, q.prev_deg, dst, g.stats ? g.stats + 1 : nullptr)) w = 1.0;
             else w = p.inv_b;
         }
         return p.weighted ? __dmul_rn(w, static_cast<double>(ldr(g.weights + e))) : w;
@@ -465,7 +467,7 @@ __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunc
     if (dst == q.prev) return y < scaled(p.inv_a);
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
-    bool common = prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, &q.n_probes);
+    bool common = prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, L.g.stats ? L.g.stats + 1 : nullptr);
     return y < scaled(common ? 1.0 : p.inv_b);
 }
 
@@ -552,7 +554,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                     raise_device(L, WF_ERR_REJECTION_CAP);
                     return kFault;
                 }
-                ++q.n_trials;
+                if (L.g.stats) atomicAdd(L.g.stats, 1ull);
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(L.prog.bound);
                 // one sector per trial: the candidate's id (and, with the
@@ -609,7 +611,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                     raise_device(L, WF_ERR_REJECTION_CAP);
                     return kFault;
                 }
-                ++q.n_trials;
+                if (L.g.stats) atomicAdd(L.g.stats, 1ull);
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(ps);
                 if (y < P::weight_static(L.prog, L.g, base + x)) { pick = x; break; }
@@ -642,7 +644,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             }
         }
         double sum = 0.0, mx = 0.0;
-        q.n_scanned += d;
+        if (L.g.stats) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
         for (uint32_t i = 0; i < d; ++i) {
             double w = P::weight(L.prog, L.g, q, base + i);
             sum += w;
@@ -673,14 +675,14 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                     raise_device(L, WF_ERR_REJECTION_CAP);
                     return kFault;
                 }
-                ++q.n_trials;
+                if (L.g.stats) atomicAdd(L.g.stats, 1ull);
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(mx);
                 if (y < P::weight(L.prog, L.g, q, base + x)) { pick = x; break; }
             }
         }
     }
-    if (F == kDirect && L.adj) {
+    if (F == kDirect && L.adj && q.len >= L.adj_from) {
         // decorated adjacency {dst, -, vertex word of dst}: one 16 B load
         uint4 a = ldr16(L.adj + base + pick);
         dst = a.x;
@@ -805,6 +807,9 @@ constexpr int walk_min_blocks() {
 #ifndef WF_CLAIM
 #define WF_CLAIM 32
 #endif
+#ifndef WF_STAGE_CLAIM
+#define WF_STAGE_CLAIM 0
+#endif
 constexpr uint32_t kClaim = WF_CLAIM;
 
 template <int K, int S, int F>
@@ -820,7 +825,6 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     q.cur_base = q.prev_base = 0;
     q.len = 0;
     q.rng.s = 0;
-    q.n_trials = q.n_probes = q.n_scanned = 0;
     q.nb_word = 0;
     q.have_nb = false;
     bool active = false;
@@ -831,10 +835,27 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     // claimed block and the rows left in it
     __shared__ unsigned long long claim_next[kBlock / 32];
     __shared__ uint32_t claim_left[kBlock / 32];
+#if WF_STAGE_CLAIM
+    // claim-time staging: the sources of the claimed rows and their vertex
+    // words, loaded by the whole warp at once, so a refilled lane can move in
+    // the same iteration (no source -> word load chain per walk)
+    constexpr bool kStage = !(K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered);
+    __shared__ unsigned long long claim_first[kBlock / 32];
+    __shared__ uint32_t claim_src[kBlock / 32][kClaim];
+    __shared__ unsigned long long claim_word[kBlock / 32][kClaim];
+#else
+    constexpr bool kStage = false;
+#endif
     const int wid = threadIdx.x >> 5;
+    // A static prefix of the rows is dealt to the warps in kClaim-row blocks,
+    // round robin (block k of warp w = k * warps + w), without the cursor
+    // atomic whose round trip was the refill's top stall (ncu, C2); the rest
+    // is claimed through the cursor for balance.
+    __shared__ uint32_t claim_k[kBlock / 32];
     if (lane == 0) {
         claim_next[wid] = 0;
         claim_left[wid] = 0;
+        claim_k[wid] = 0;
     }
     __syncwarp();
     unsigned long long steps = 0;
@@ -846,26 +867,50 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
             uint64_t wnext = claim_next[wid];
             uint32_t wleft = claim_left[wid];
             if (wleft == 0) {
+                const uint32_t nwarps = gridDim.x * (kBlock / 32);
+                const uint32_t k = claim_k[wid];
+                if (k < L.static_blocks) {
+                    wnext = (static_cast<uint64_t>(k) * nwarps + blockIdx.x * (kBlock / 32) + wid) * kClaim;
+                    wleft = kClaim;
+                    __syncwarp();
+                    if (lane == 0) claim_k[wid] = k + 1;
+                } else {
                 // guided claim: up to kClaim rows while the queue is long,
                 // shrinking to the lanes in need near its end (balance)
-                const uint64_t est = wnext < L.n_rows ? L.n_rows - wnext : 0;
-                const uint64_t share = est / (2ull * gridDim.x * (kBlock / 32));
+                const uint64_t at = wnext > L.dyn_base ? wnext : L.dyn_base;
+                const uint64_t est = at < L.n_rows ? L.n_rows - at : 0;
+                const uint64_t share = est / (2ull * nwarps);
                 const uint32_t want = max(static_cast<uint32_t>(__popc(need)),
                                           share < kClaim ? static_cast<uint32_t>(share) : kClaim);
                 unsigned long long first = 0;
                 if (lane == 0) first = atomicAdd(L.cursor, static_cast<unsigned long long>(want));
-                first = __shfl_sync(kFull, first, 0);
+                first = __shfl_sync(kFull, first, 0) + L.dyn_base;
                 wnext = first;
                 const uint64_t rest = first >= L.n_rows ? 0 : L.n_rows - first;
                 wleft = rest < want ? static_cast<uint32_t>(rest) : want;
+                }
                 if (wleft == 0) {  // queue drained: every idle lane is done
                     drained = drained || !active;
                     continue;
                 }
+#if WF_STAGE_CLAIM
+                if constexpr (kStage) {
+                    uint32_t src = 0;
+                    unsigned long long word = 0;
+                    if (static_cast<uint32_t>(lane) < wleft) {
+                        const uint64_t qid = L.qid_map ? __ldg(L.qid_map + wnext + lane) : L.qid_begin + wnext + lane;
+                        src = source_at(L, qid);
+                        if (src < L.g.V) word = ldr(L.sview + src);
+                    }
+                    claim_src[wid][lane] = src;
+                    claim_word[wid][lane] = word;
+                    if (lane == 0) claim_first[wid] = wnext;
+                    __syncwarp();
+                }
+#endif
             }
             const uint32_t rank = __popc(need & ((1u << lane) - 1));
             const uint32_t take = min(static_cast<uint32_t>(__popc(need)), wleft);
-            const uint64_t my = wnext + rank;
             __syncwarp();
             if (lane == 0) {
                 claim_next[wid] = wnext + take;
@@ -873,22 +918,41 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
             }
             __syncwarp();
             if (!active && !drained && rank < take) {
-                uint64_t row = my;
+                const uint64_t row = wnext + rank;
+                const uint64_t qid = L.qid_map ? __ldg(L.qid_map + row) : L.qid_begin + row;
+                q.row = row;
+                q.rng.s = stream_state(L.seed_mixed, qid);
+#if WF_STAGE_CLAIM
+                const uint32_t slot = kStage ? static_cast<uint32_t>(row - claim_first[wid]) : 0;
+                q.cur = kStage ? claim_src[wid][slot] : source_at(L, qid);
+#else
+                q.cur = source_at(L, qid);
+#endif
+                q.prev = 0xFFFFFFFFu;
+                q.len = 0;
+                if (q.cur >= L.g.V) {
+                    // QuerySpec validation (walker.cpp:8-109) on the device: the
+                    // run reports ConfigError (its rows are not results)
+                    raise_device(L, WF_ERR_CONFIG);
+                    q.cur = 0;
+                }
                 {
-                    uint64_t qid = L.qid_map ? __ldg(L.qid_map + row) : L.qid_begin + row;
-                    q.row = row;
-                    q.rng.s = stream_state(L.seed_mixed, qid);
-                    q.cur = source_at(L, qid);
-                    q.prev = 0xFFFFFFFFu;
-                    q.len = 0;
                     emit(L, q, q.cur, ps);
                     q.len = 1;
                     if (P::prechecked && P::finished(L.prog, q)) {
                         finish(L, q, WF_WALK_COMPLETE, ps);  // walk_already_finished, program.hpp:86-93
                     } else {
-                        load_current<K, S, F>(L, q);
-                        active = true;
-                        fresh = true;
+#if WF_STAGE_CLAIM
+                        if constexpr (kStage) {
+                            unpack_word(L.g, claim_word[wid][slot], q.cur, q.cur_base, q.cur_deg);
+                            active = true;
+                        } else
+#endif
+                        {
+                            load_current<K, S, F>(L, q);
+                            active = true;
+                            fresh = true;
+                        }
                     }
                 }
             }
@@ -928,19 +992,6 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     // one atomic per warp for the step total
     for (int o = 16; o > 0; o >>= 1) steps += __shfl_xor_sync(kFull, steps, o);
     if (lane == 0 && steps) atomicAdd(L.steps_out, steps);
-    if (L.stats) {
-        unsigned long long t = q.n_trials, pr = q.n_probes, sc = q.n_scanned;
-        for (int o = 16; o > 0; o >>= 1) {
-            t += __shfl_xor_sync(kFull, t, o);
-            pr += __shfl_xor_sync(kFull, pr, o);
-            sc += __shfl_xor_sync(kFull, sc, o);
-        }
-        if (lane == 0) {
-            atomicAdd(L.stats, t);
-            atomicAdd(L.stats + 1, pr);
-            atomicAdd(L.stats + 2, sc);
-        }
-    }
 }
 
 }  // namespace wf

@@ -113,6 +113,7 @@ struct Session {
     bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
     bool use_edge_hash = false;  // Node2Vec distance test through the graph's edge hash set
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
+    uint32_t adj_from = 0;       // NAIVE moves from this path length on read `adj`
     DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 
     void build_tables(cudaStream_t st);
@@ -168,6 +169,9 @@ GraphStore* graph_load_edge_list(const char* path, const wf_edge_list_options& o
 struct WidenU64 {
     __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
 };
+
+// stream.cu: the exception of a device-side error word (error.hpp classes)
+[[noreturn]] void raise_device_error(const Session& s, int code);
 
 // stream.cu: pipelined run + copy of the walk set into host buffers
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,

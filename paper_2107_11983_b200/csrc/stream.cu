@@ -46,6 +46,8 @@ __global__ void k_add_base(uint64_t* __restrict__ offs, uint64_t n, uint64_t bas
 struct HostPipe {
     int device = 0;
     cudaStream_t a = nullptr, b = nullptr;
+    cudaStream_t c = nullptr;            // host -> device source copies, per chunk
+    std::vector<cudaEvent_t> ev_src;     // chunk k's sources resident
     cudaEvent_t ev_comp[2] = {nullptr, nullptr};
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
     uint64_t cap_rows = 0;     // chunk rows the buffers hold
@@ -62,6 +64,7 @@ struct HostPipe {
     explicit HostPipe(int dev) : device(dev) {
         WF_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
         WF_CUDA(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        WF_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
             WF_CUDA(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
             WF_CUDA(cudaEventCreateWithFlags(&ev_copy[i], cudaEventDisableTiming));
@@ -73,11 +76,20 @@ struct HostPipe {
         DeviceGuard guard(device);
         if (a) cudaStreamDestroy(a);
         if (b) cudaStreamDestroy(b);
+        if (c) cudaStreamDestroy(c);
+        for (cudaEvent_t e : ev_src) cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
             if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
             if (ev_copy[i]) cudaEventDestroy(ev_copy[i]);
         }
         if (h_tot) cudaFreeHost(h_tot);
+    }
+    void reserve_src_events(uint64_t nchunks) {
+        while (ev_src.size() < nchunks) {
+            cudaEvent_t e;
+            WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev_src.push_back(e);
+        }
     }
     void reserve(uint64_t chunk, uint32_t stride) {
         if (chunk <= cap_rows && stride <= cap_stride) return;
@@ -101,6 +113,14 @@ struct HostPipe {
 
 void release_host_pipe(HostPipe* p) { delete p; }
 
+void raise_device_error(const Session& s, int code) {
+    if (code == WF_ERR_REJECTION_CAP)
+        raise(code, "rejection sampling exceeded " + std::to_string(s.trial_cap) +
+                        " trials; asserted bound does not match the weights");
+    if (code == WF_ERR_CONFIG) raise(code, "query source is not a vertex");
+    raise(code, "device-side contract violation");
+}
+
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics) {
@@ -120,22 +140,32 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     P.reserve(chunk, stride);
     cudaStream_t A = P.a, B = P.b;
 
-    // the shard's slice of the source list, addressed by absolute qid in the kernel
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    // the shard's slice of the source list, addressed by absolute qid in the
+    // kernel; copied chunk by chunk on stream C so chunk k+1's sources move
+    // while chunk k computes
     const uint32_t* src_by_qid = nullptr;
-    if (spec.mode == WF_QUERY_FROM_LIST && n) {
+    const bool list = spec.mode == WF_QUERY_FROM_LIST && n;
+    if (list) {
         if (P.src.size() < n) P.src.allocate(n);
-        WF_CUDA(cudaMemcpyAsync(P.src.get(), host_sources + qb, n * 4, cudaMemcpyHostToDevice, A));
         src_by_qid = P.src.get() - qb;
+        P.reserve_src_events(nchunks);
+        for (uint64_t k = 0; k < nchunks; ++k) {
+            const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk);
+            WF_CUDA(cudaMemcpyAsync(P.src.get() + r0, host_sources + qb + r0, (r1 - r0) * 4,
+                                    cudaMemcpyHostToDevice, P.c));
+            WF_CUDA(cudaEventRecord(P.ev_src[k], P.c));
+        }
     }
     WF_CUDA(cudaMemsetAsync(P.ctr.get(), 0, 16, A));
 
-    const uint64_t nchunks = (n + chunk - 1) / chunk;
     bool copy_pending[2] = {false, false};
     std::vector<uint64_t> chunk_base(nchunks + 1, 0);
 
     auto enqueue_compute = [&](uint64_t k) {
         const int b = static_cast<int>(k & 1);
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
+        if (list) WF_CUDA(cudaStreamWaitEvent(A, P.ev_src[k], 0));
         // buffer b (status / offsets / staging) is free once chunk k-2's copy drained
         if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(A, P.ev_copy[b], 0));
         // offs[b][0] = 0 (the previous user of this buffer rebased it in place)
@@ -161,6 +191,9 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     for (uint64_t k = 0; k < nchunks; ++k) {
         const int b = static_cast<int>(k & 1);
         const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
+        // chunk k+1's walk is queued behind chunk k's before the host waits for
+        // chunk k's vertex count, so the compute stream never idles on the host
+        if (k + 1 < nchunks) enqueue_compute(k + 1);
         WF_CUDA(cudaEventSynchronize(P.ev_comp[b]));
         uint64_t cnt = P.h_tot[b];
         chunk_base[k + 1] = chunk_base[k] + cnt;
@@ -182,7 +215,6 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             WF_CUDA(cudaStreamSynchronize(A));
             cnt = 0;  // already copied
         }
-        if (k + 1 < nchunks) enqueue_compute(k + 1);  // overlaps the copy below
         WF_CUDA(cudaStreamWaitEvent(B, P.ev_comp[b], 0));
         if (cnt)
             WF_CUDA(cudaMemcpyAsync(vertices + chunk_base[k], P.stage[b].get(), cnt * 4,
@@ -206,10 +238,14 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     WF_CUDA(cudaMemcpy(&err, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
     if (err) {
         WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
-        raise(err, err == WF_ERR_REJECTION_CAP
-                       ? "rejection sampling exceeded " + std::to_string(s.trial_cap) +
-                             " trials; asserted bound does not match the weights"
-                       : std::string("device-side contract violation"));
+        if (err == WF_ERR_CONFIG && spec.mode == WF_QUERY_FROM_LIST) {
+            // the kernel flagged a source outside [0, V): name it as the host check would
+            for (uint64_t i = qb; i < qe; ++i)
+                if (host_sources[i] >= g.V)
+                    config_error("query source " + std::to_string(host_sources[i]) +
+                                 " is not a vertex (V=" + std::to_string(g.V) + ")");
+        }
+        raise_device_error(s, err);
     }
     if (offsets) offsets[n] = chunk_base[nchunks];
     unsigned long long hc[2] = {0, 0};

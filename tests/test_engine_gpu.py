@@ -259,6 +259,7 @@ def test_session_launch_chunks_equal_whole_run(rmat12):
 
 
 def test_errors_surface_as_reference_classes(rmat12):
+    import torch
     dg, hg = rmat12
     with pytest.raises(abi.ConfigError):
         E.Session(dg, MetaPathProgram([0, 1]), ExecOptions(sampler=abi.Sampler.OREJ))
@@ -266,6 +267,28 @@ def test_errors_surface_as_reference_classes(rmat12):
         E.Session(dg, DeepWalkProgram(5, True), ExecOptions(sampler=abi.Sampler.NAIVE))
     with pytest.raises(abi.ConfigError):
         E.run_sequential(dg, QuerySpec.from_source(hg.vertex_count + 3, 4), PprProgram(0.2))
+    # a source list with a non-vertex: the host list through run_host (checked by
+    # the walk kernel, named on the host) and a device list through launch
+    bad = np.arange(64, dtype=np.uint32)
+    bad[37] = hg.vertex_count + 9
+    sess = E.Session(dg, PprProgram(0.2), ExecOptions(seed=1, path_stride=64))
+    off = np.zeros(65, np.uint64)
+    verts = np.zeros(64 * 64, np.uint32)
+    st = np.zeros(64, np.uint8)
+    with pytest.raises(abi.ConfigError, match=str(hg.vertex_count + 9)):
+        sess.run_host(QuerySpec.from_list(bad), off.ctypes.data, verts.ctypes.data, verts.size,
+                      st.ctypes.data)
+    d_src = torch.from_numpy(bad.view(np.int32)).cuda()
+    paths = torch.empty(64 * 64, dtype=torch.int32, device="cuda")
+    lens = torch.empty(64, dtype=torch.int32, device="cuda")
+    stat = torch.empty(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(abi.ConfigError):
+        sess.launch(QuerySpec.from_list(bad), 0, 64, paths.data_ptr(), 64, lens.data_ptr(),
+                    stat.data_ptr(), 0, 0, 0, 0, sources_dev_ptr=d_src.data_ptr())
+        sess.sync(0)
+    # the session is usable again after the error
+    good = QuerySpec.from_list(np.arange(64, dtype=np.uint32))
+    sess.run_host(good, off.ctypes.data, verts.ctypes.data, verts.size, st.ctypes.data)
     # a trial cap the bound cannot meet: RejectionCapError raised after the sync
     with pytest.raises(abi.RejectionCapError):
         E.run_sequential(dg, QuerySpec.one_per_vertex(), Node2VecProgram(0.01, 0.5, 10, False),

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--counts", action="store_true", help="PPR: also accumulate visit counts")
     ap.add_argument("--diag-times", action="store_true",
                     help="library built with -DWF_DIAG_FINISH_TIME: print walk completion-time percentiles")
+    ap.add_argument("--graph", action="store_true", help="replay the launch as a captured CUDA graph")
     ap.add_argument("--flush", action="store_true", help="write 256 MiB between launches (cold L2, as bench.py)")
     args = ap.parse_args()
     import torch
@@ -49,6 +50,20 @@ def main():
     counts = torch.zeros(V, dtype=torch.int32, device="cuda") if args.counts else None
     stream = torch.cuda.current_stream()
     l2buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
+    def launch():
+        s = torch.cuda.current_stream()
+        sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), st.data_ptr(),
+                    counts.data_ptr() if counts is not None else 0, steps.data_ptr(), 0, s.cuda_stream,
+                    sources_dev_ptr=d_src.data_ptr())
+
+    graph = None
+    if args.graph:
+        launch()  # warm (no allocation inside the capture)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            launch()
+        torch.cuda.synchronize()
     for i in range(args.launches):
         steps.zero_()
         if l2buf is not None:
@@ -57,8 +72,10 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t = time.perf_counter()
         e0.record(stream)
-        sess.launch(spec, lo, hi, paths.data_ptr(), stride, lens.data_ptr(), st.data_ptr(),
-                    counts.data_ptr() if counts is not None else 0, steps.data_ptr(), 0, stream.cuda_stream, sources_dev_ptr=d_src.data_ptr())
+        if graph is not None:
+            graph.replay()
+        else:
+            launch()
         e1.record(stream)
         sess.sync(stream.cuda_stream)
         dt = time.perf_counter() - t
