@@ -280,6 +280,12 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         if counts is not None and dist is not None:
             dist.all_reduce(counts)  # NCCL: the one collective of the path
 
+    # launch tuner (wf_session_tune, the device analogue of the reference's
+    # tune_ring_sizes): picks blocks/SM for launches of this size; untimed
+    tuned = None
+    if not args.no_tune:
+        tuned = sess.tune(spec, lo, hi, sources_dev_ptr=d_src.data_ptr())[0]
+
     # logical access counts for S_alg (one instrumented pass, untimed)
     sess.set_stats(True)
     one_step()
@@ -360,7 +366,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     return dict(moves=moves_per_step, total_ms=total_ms, step_ms=step_ms, stats=stats,
                 launches=launches, clocks=clk.summary(), info=info, sampler=sampler.name,
                 flow=flow.name, preprocess_s=pre_s, setup_s=setup_s, e2e=e2e, n=n, dg=dg, layout=layout,
-                spec=spec, sess=sess)
+                spec=spec, sess=sess, tuned=tuned)
 
 
 def cpu_baseline(key, cfg, dg, spec, threads=None):
@@ -413,7 +419,7 @@ def extras(args, rank, world, local_rank, dist):
             peak, _ = measured_peak()
             ach = r["moves"] * b / (ms * 1e-3) / 1e9
             rate = r["moves"] / (ms * 1e-3)
-            out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=rate,
+            out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=rate, blocks_per_sm=r["tuned"],
                             ms_per_step=ms, moves=r["moves"], achieved_gbs=ach,
                             roofline_frac=ach / peak, bytes_per_move=b, bytes_model=bdesc,
                             random_access=random_access_block(rate, reads),
@@ -497,6 +503,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tune", action="store_true", help="skip the launch tuner (occupancy grid)")
     ap.add_argument("--no-graph", action="store_true", help="launch each step from the host instead of a CUDA graph replay")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -557,7 +564,8 @@ def main():
                    "l2": "flushed between steps (256 MiB write)" if cfg["scale"] <= 20
                    else "inputs larger than L2",
                    "launch": "host launch per step" if args.no_graph
-                   else "CUDA graph replay per step (counter resets + walk kernel)"},
+                   else "CUDA graph replay per step (counter resets + walk kernel)",
+                   "blocks_per_sm": r["tuned"] if r["tuned"] is not None else "occupancy max (untuned)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",

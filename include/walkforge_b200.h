@@ -279,6 +279,18 @@ int wf_session_run_host(wf_session* s, const wf_query_spec* spec, uint64_t qid_b
 int wf_session_set_stats(wf_session* s, int enable);
 int wf_session_stats(wf_session* s, uint64_t* out3);
 
+/* Launch tuner: the device analogue of tune_ring_sizes (tune.cpp:46-111).  The
+ * reference sweeps the interleave ring sizes (k, k') for its CPU; on the device
+ * the knob is the number of resident walkers — blocks per SM — which trades
+ * memory-level parallelism against per-move latency (Little's law: more lanes
+ * in flight than the memory system can serve only lengthen every walk's chain).
+ * Times whole launches of queries [qid_begin, qid_end) (host or device source
+ * list; results discarded) at each candidate and keeps the fastest for launches
+ * of that size (same power-of-two bucket of rows) on this session.  Walk
+ * results never depend on it.  Out: the chosen blocks/SM and its time. */
+int wf_session_tune(wf_session* s, const wf_query_spec* spec, uint64_t qid_begin, uint64_t qid_end,
+                    int32_t* blocks_per_sm, double* best_ms);
+
 /* ---- walk sets: WalkSet (walker.hpp:47-55) -------------------------------- */
 int wf_walkset_info(const wf_walkset* w, uint64_t* n_queries, uint64_t* total_vertices,
                     uint32_t* max_length);

@@ -303,6 +303,16 @@ int cmd_tune(const Args& a) {
     std::printf("device lanes in flight %u (rings replaced by the persistent walker queue)\n", m.max_in_flight);
     std::printf("probe uniform length 10: %.1f steps/s\n",
                 m.exec_seconds > 0 ? static_cast<double>(m.total_steps) / m.exec_seconds : 0.0);
+    // the device knob the rings become: resident walkers (blocks/SM), timed
+    // over whole launches of the probe (wf_session_tune)
+    wf_session* s = nullptr;
+    check(wf_session_create(g.get(), &d, &o, &s));
+    int32_t blocks = 0;
+    double ms = 0.0;
+    const int rc = wf_session_tune(s, &q, 0, 0, &blocks, &ms);
+    wf_session_destroy(s);
+    check(rc);
+    std::printf("launch tuner: %d blocks/SM (%.3f ms per launch of the probe)\n", blocks, ms);
     std::printf("recommended: k=64 k'=32 (accepted and ignored on the device)\n");
     return 0;
 }

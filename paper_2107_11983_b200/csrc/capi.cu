@@ -419,10 +419,6 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
         if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
             s.build_adjacency(nullptr);
-        if (const char* e = getenv("WF_ADJ_FROM")) {  // experiment
-            if (s.flow == kDirect && !s.adj.get()) s.build_adjacency(nullptr);
-            s.adj_from = static_cast<uint32_t>(atoi(e));
-        }
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
             s.g->ensure_label_index(nullptr);
             WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -643,6 +639,69 @@ int wf_session_stats(wf_session* sh, uint64_t* out3) {
         WF_CUDA(cudaDeviceSynchronize());
         WF_CUDA(cudaMemcpy(out3, s.stats.get(), 24, cudaMemcpyDeviceToHost));
         WF_CUDA(cudaMemset(s.stats.get(), 0, 24));
+    });
+}
+
+// Launch tuner (tune.cpp:46-111's role): candidate blocks/SM from the occupancy
+// maximum down to a quarter, each timed over whole launches of the range.
+int wf_session_tune(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin, uint64_t qid_end,
+                    int32_t* blocks_per_sm, double* best_ms) {
+    return guarded([&] {
+        require(sh && spec, "null argument");
+        Session& s = *sh->s;
+        GraphStore& g = *s.g;
+        DeviceGuard guard(g.device);
+        ResolvedSpec rs;
+        resolve_spec(g, spec, rs);
+        if (qid_end == 0) qid_end = rs.n;
+        require(qid_begin < qid_end && qid_end <= rs.n, "query range out of bounds");
+        const uint64_t n = qid_end - qid_begin;
+        const uint32_t stride = s.default_stride;
+        size_t free_b = 0, total_b = 0;
+        WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t need = n * (stride * 4ull + 5) + (s.desc.kind == WF_PROGRAM_PPR ? g.V * 4ull : 0);
+        if (need > free_b / 2) raise(WF_ERR_INVALID_ARG, "tune range needs more scratch than half the free HBM; tune a smaller range");
+        DeviceBuffer<uint32_t> paths(n * stride), lens(n), counts;
+        DeviceBuffer<uint8_t> stat(n);
+        if (s.desc.kind == WF_PROGRAM_PPR) counts.allocate(g.V);
+        DeviceBuffer<unsigned long long> ctr(2);
+        const int bucket = row_bucket(n);
+        s.tuned_blocks.erase(bucket);
+        const int max_per_sm = std::max(1, s.grid / sm_count(g.device));
+        std::vector<int> cands;
+        for (int c : {max_per_sm, max_per_sm * 3 / 4, max_per_sm / 2, max_per_sm * 3 / 8, max_per_sm / 4})
+            if (c >= 1 && std::find(cands.begin(), cands.end(), c) == cands.end()) cands.push_back(c);
+        cudaEvent_t e0, e1;
+        WF_CUDA(cudaEventCreate(&e0));
+        WF_CUDA(cudaEventCreate(&e1));
+        double best = 1e300;
+        int pick = max_per_sm;
+        for (int c : cands) {
+            s.tuned_blocks[bucket] = c;
+            float mn = 1e30f;
+            for (int rep = 0; rep < 4; ++rep) {  // first launch warms, then best of 3
+                if (counts.get()) WF_CUDA(cudaMemsetAsync(counts.get(), 0, g.V * 4ull, nullptr));
+                WF_CUDA(cudaEventRecord(e0, nullptr));
+                launch_walk(s, rs.spec, rs.dev_sources, qid_begin, qid_end, nullptr, paths.get(), stride,
+                            lens.get(), stat.get(), counts.get(), ctr.get(), ctr.get() + 1,
+                            s.cursor.get(), nullptr);
+                WF_CUDA(cudaEventRecord(e1, nullptr));
+                WF_CUDA(cudaEventSynchronize(e1));
+                float ms = 0.f;
+                WF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (rep > 0) mn = std::min(mn, ms);
+            }
+            if (mn < best) {
+                best = mn;
+                pick = c;
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        check_device_error(s);
+        s.tuned_blocks[bucket] = pick;
+        if (blocks_per_sm) *blocks_per_sm = pick;
+        if (best_ms) *best_ms = best;
     });
 }
 

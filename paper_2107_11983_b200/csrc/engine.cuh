@@ -99,7 +99,6 @@ struct WalkLaunch {
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
     const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
-    uint32_t adj_from;                // NAIVE: moves from path length >= adj_from use `adj`
     const uint4* __restrict__ mp_adj; // MetaPath: per partitioned edge {dst, 0, next-group word} or null
 };
 
@@ -174,9 +173,13 @@ __device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint
     }
 }
 
+#ifndef WF_LDR_WORD
+#define WF_LDR_WORD WF_LDR
+#endif
 __device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t* vw, uint32_t v,
                                               uint64_t& base, uint32_t& deg) {
-    uint64_t w = ldr(vw + v);
+    uint64_t w;
+    asm(WF_LDR_WORD ".u64 %0, [%1];" : "=l"(w) : "l"(vw + v));
     base = w >> kDegBits;
     deg = static_cast<uint32_t>(w & kDegEscape);
     if (deg == kDegEscape) {  // rare: very high degree
@@ -682,7 +685,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             }
         }
     }
-    if (F == kDirect && L.adj && q.len >= L.adj_from) {
+    if (F == kDirect && L.adj) {
         // decorated adjacency {dst, -, vertex word of dst}: one 16 B load
         uint4 a = ldr16(L.adj + base + pick);
         dst = a.x;

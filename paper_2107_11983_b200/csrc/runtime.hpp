@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -107,13 +108,13 @@ struct Session {
     DeviceBuffer<unsigned long long> cursor;
     DeviceBuffer<double> scratch;
     uint64_t scratch_stride = 0;
-    int grid = 0;
+    int grid = 0;                       // occupancy grid (max blocks/SM x SMs)
+    std::map<int, int> tuned_blocks;    // wf_session_tune: log2 row bucket -> blocks/SM
     bool collect_stats = false;
     DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
     bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
     bool use_edge_hash = false;  // Node2Vec distance test through the graph's edge hash set
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
-    uint32_t adj_from = 0;       // NAIVE moves from this path length on read `adj`
     DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 
     void build_tables(cudaStream_t st);
@@ -148,6 +149,7 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
                  unsigned long long* steps_out, unsigned long long* overflow_out,
                  unsigned long long* cursor, cudaStream_t st);
 int occupancy_grid(const Session& s);
+int row_bucket(uint64_t n_rows);  // tuner key: ceil(log2(rows))
 
 // graph.cu
 GraphStore* graph_from_host(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,

@@ -56,6 +56,12 @@ KernelFn select_kernel(int prog, int sampler, int flow) {
 
 }  // namespace
 
+int row_bucket(uint64_t n_rows) {
+    int b = 0;
+    while ((1ull << b) < n_rows && b < 63) ++b;
+    return b;
+}
+
 int occupancy_grid(const Session& s) {
     KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
     int per_sm = 0;
@@ -102,9 +108,12 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.staged = (stride % 8 == 0 && reinterpret_cast<uintptr_t>(paths) % 32 == 0) ? 1 : 0;
     L.alias_wide = s.alias_wide ? 1 : 0;
     L.adj = s.adj.get();
-    L.adj_from = s.adj_from;
     L.mp_adj = s.mp_adj.get();
     int grid = s.grid > 0 ? s.grid : occupancy_grid(s);
+    if (!s.tuned_blocks.empty()) {  // wf_session_tune's pick for launches of this size
+        auto it = s.tuned_blocks.find(row_bucket(L.n_rows));
+        if (it != s.tuned_blocks.end()) grid = it->second * sm_count(g.device);
+    }
     uint64_t lanes_needed = (L.n_rows + 31) / 32 * 32;
     int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));
     grid = std::max(1, std::min(grid, grid_needed));

@@ -329,6 +329,20 @@ class Session:
         _check(load_library().wf_session_layout(self.h, C.byref(f)))
         return f.value
 
+    def tune(self, spec: QuerySpec, qid_begin: int = 0, qid_end: int = 0,
+             sources_dev_ptr: int = 0) -> tuple:
+        """wf_session_tune: time whole launches of the range at each candidate
+        blocks/SM and keep the fastest for launches of that size.  Returns
+        (blocks_per_sm, best_ms)."""
+        cs = spec.to_c()
+        if sources_dev_ptr:
+            cs.sources = C.cast(_vp(sources_dev_ptr), _u32p)
+        b = C.c_int32()
+        ms = C.c_double()
+        _check(load_library().wf_session_tune(self.h, C.byref(cs), C.c_uint64(qid_begin),
+                                              C.c_uint64(qid_end), C.byref(b), C.byref(ms)))
+        return b.value, ms.value
+
     def set_stats(self, enable: bool) -> None:
         _check(load_library().wf_session_set_stats(self.h, C.c_int(1 if enable else 0)))
 

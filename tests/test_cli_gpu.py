@@ -77,3 +77,16 @@ def test_cli_convert_and_run_match_reference(i):
         assert open(walks, "rb").read() == open(want_path, "rb").read()
         want = rg.run(spec, prog, opts)
         assert int(metrics["total_steps"]) == want.metrics.total_steps
+
+
+@pytest.mark.gpu
+def test_cli_tune_reports_launch_choice():
+    with tempfile.TemporaryDirectory() as d:
+        el = os.path.join(d, "g.txt")
+        _edge_list(el)
+        wfg = os.path.join(d, "g.wfg")
+        r = subprocess.run([CLI, "convert", el, wfg], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([CLI, "tune", wfg], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        assert "launch tuner:" in r.stdout and "blocks/SM" in r.stdout

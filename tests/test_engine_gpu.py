@@ -390,3 +390,37 @@ def test_run_host_streaming_equals_run(rmat12, prog, chunk):
     assert np.array_equal(off, whole.offsets[lo:hi + 1] - base)
     assert np.array_equal(verts[:int(off[-1])], whole.vertices[int(base):int(whole.offsets[hi])])
     assert np.array_equal(st, whole.status[lo:hi])
+
+
+def test_launch_tuner_keeps_results(rmat12):
+    """wf_session_tune only changes the grid: walks are identical before and after."""
+    import torch
+    dg, hg = rmat12
+    rng = np.random.default_rng(5)
+    src = rng.integers(0, hg.vertex_count, 20000, dtype=np.uint32)
+    spec = QuerySpec.from_list(src)
+    sess = E.Session(dg, PprProgram(0.2), ExecOptions(seed=3, path_stride=64))
+    n = src.size
+
+    def run():
+        d_src = torch.from_numpy(src.view(np.int32)).cuda()
+        paths = torch.zeros(n * 64, dtype=torch.int32, device="cuda")
+        lens = torch.zeros(n, dtype=torch.int32, device="cuda")
+        st = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        counts = torch.zeros(hg.vertex_count, dtype=torch.int32, device="cuda")
+        sess.launch(spec, 0, n, paths.data_ptr(), 64, lens.data_ptr(), st.data_ptr(), counts.data_ptr(),
+                    sources_dev_ptr=d_src.data_ptr())
+        sess.sync(0)
+        L = lens.cpu().numpy()
+        P = paths.cpu().numpy().reshape(n, 64)
+        rows = [P[i, :min(L[i], 64)].copy() for i in range(n)]
+        return L, rows, st.cpu().numpy(), counts.cpu().numpy()
+
+    before = run()
+    blocks, ms = sess.tune(spec)
+    assert 1 <= blocks <= 8 and ms > 0
+    after = run()
+    assert np.array_equal(before[0], after[0])
+    assert all(np.array_equal(a, b) for a, b in zip(before[1], after[1]))
+    assert np.array_equal(before[2], after[2])
+    assert np.array_equal(before[3], after[3])
