@@ -8,6 +8,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <vector>
 
@@ -127,6 +129,14 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     GraphStore& g = *s.g;
     DeviceGuard guard(g.device);
     auto t0 = std::chrono::steady_clock::now();
+    // WF_TRACE_HOST=1: host-side timeline of the pipeline on stderr (diagnostics)
+    static const bool trace_on = getenv("WF_TRACE_HOST") != nullptr;
+    auto trace = [&](const char* what, long long k) {
+        if (trace_on)
+            std::fprintf(stderr, "[run_host %8.1f us] %s %lld\n",
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(),
+                         what, k);
+    };
     const uint32_t stride = s.default_stride;
     const uint64_t n = qe - qb;
     if (chunk == 0) {
@@ -140,7 +150,12 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     P.reserve(chunk, stride);
     cudaStream_t A = P.a, B = P.b;
 
-    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    // Chunk boundaries.  (A geometric ramp of small first chunks, to start the
+    // first device->host copy earlier, measured slower on C2: each PPR launch
+    // pays its own tail of long walks.)
+    std::vector<uint64_t> bounds{0};
+    while (bounds.back() < n) bounds.push_back(std::min(n, bounds.back() + chunk));
+    const uint64_t nchunks = bounds.size() - 1;
     // the shard's slice of the source list, addressed by absolute qid in the
     // kernel; copied chunk by chunk on stream C so chunk k+1's sources move
     // while chunk k computes
@@ -151,7 +166,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         src_by_qid = P.src.get() - qb;
         P.reserve_src_events(nchunks);
         for (uint64_t k = 0; k < nchunks; ++k) {
-            const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk);
+            const uint64_t r0 = bounds[k], r1 = bounds[k + 1];
             WF_CUDA(cudaMemcpyAsync(P.src.get() + r0, host_sources + qb + r0, (r1 - r0) * 4,
                                     cudaMemcpyHostToDevice, P.c));
             WF_CUDA(cudaEventRecord(P.ev_src[k], P.c));
@@ -164,7 +179,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
 
     auto enqueue_compute = [&](uint64_t k) {
         const int b = static_cast<int>(k & 1);
-        const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
+        const uint64_t r0 = bounds[k], r1 = bounds[k + 1], nr = r1 - r0;
         if (list) WF_CUDA(cudaStreamWaitEvent(A, P.ev_src[k], 0));
         // buffer b (status / offsets / staging) is free once chunk k-2's copy drained
         if (copy_pending[b]) WF_CUDA(cudaStreamWaitEvent(A, P.ev_copy[b], 0));
@@ -190,11 +205,13 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     if (nchunks) enqueue_compute(0);
     for (uint64_t k = 0; k < nchunks; ++k) {
         const int b = static_cast<int>(k & 1);
-        const uint64_t r0 = k * chunk, r1 = std::min(n, r0 + chunk), nr = r1 - r0;
+        const uint64_t r0 = bounds[k], r1 = bounds[k + 1], nr = r1 - r0;
         // chunk k+1's walk is queued behind chunk k's before the host waits for
         // chunk k's vertex count, so the compute stream never idles on the host
         if (k + 1 < nchunks) enqueue_compute(k + 1);
+        trace("queued compute", static_cast<long long>(k + 1));
         WF_CUDA(cudaEventSynchronize(P.ev_comp[b]));
+        trace("chunk computed", static_cast<long long>(k));
         uint64_t cnt = P.h_tot[b];
         chunk_base[k + 1] = chunk_base[k] + cnt;
         if (chunk_base[k + 1] > capacity)
@@ -231,8 +248,10 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             WF_CUDA(cudaMemcpyAsync(status + r0, P.stat[b].get(), nr, cudaMemcpyDeviceToHost, B));
         WF_CUDA(cudaEventRecord(P.ev_copy[b], B));
         copy_pending[b] = true;
+        trace("copies queued", static_cast<long long>(k));
     }
     WF_CUDA(cudaStreamSynchronize(B));
+    trace("copies done", -1);
     WF_CUDA(cudaStreamSynchronize(A));
     int err = 0;
     WF_CUDA(cudaMemcpy(&err, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
@@ -278,6 +297,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
                       vertices + offsets[r]);
         }
     }
+    trace("done", -1);
     if (metrics) {
         metrics->preprocess_seconds = s.preprocess_seconds;
         metrics->exec_seconds =

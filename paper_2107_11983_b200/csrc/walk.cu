@@ -110,9 +110,20 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.adj = s.adj.get();
     L.mp_adj = s.mp_adj.get();
     int grid = s.grid > 0 ? s.grid : occupancy_grid(s);
-    if (!s.tuned_blocks.empty()) {  // wf_session_tune's pick for launches of this size
-        auto it = s.tuned_blocks.find(row_bucket(L.n_rows));
-        if (it != s.tuned_blocks.end()) grid = it->second * sm_count(g.device);
+    if (!s.tuned_blocks.empty()) {
+        // wf_session_tune's pick for the nearest tuned launch size (row buckets
+        // are powers of two: a chunked run of a tuned batch lands one or two
+        // buckets below it)
+        const int b = row_bucket(L.n_rows);
+        int best = -1, dist = 1 << 30;
+        for (const auto& kv : s.tuned_blocks) {
+            const int d = kv.first > b ? kv.first - b : b - kv.first;
+            if (d < dist) {
+                dist = d;
+                best = kv.second;
+            }
+        }
+        if (best > 0 && dist <= 3) grid = best * sm_count(g.device);
     }
     uint64_t lanes_needed = (L.n_rows + 31) / 32 * 32;
     int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));

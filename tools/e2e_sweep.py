@@ -12,20 +12,27 @@ import bench  # noqa: E402
 from paper_2107_11983_b200 import engine as E  # noqa: E402
 from paper_2107_11983_b200.host import ExecOptions, QuerySpec  # noqa: E402
 
-cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "c2"]
 dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"], label_count=cfg["labels"])
 V = dg.info()["V"]
 spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
 n = hi - lo
 stride = bench.row_capacity(cfg)
 sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=stride))
+if "--tune" in sys.argv:
+    d_src = torch.from_numpy(spec.sources.view(np.int32)).cuda()
+    print("tuned blocks/SM, ms:", sess.tune(spec, lo, hi, sources_dev_ptr=d_src.data_ptr()))
 h_src = torch.from_numpy(spec.sources.view(np.int32)).pin_memory()
 hspec = QuerySpec.from_list(h_src.numpy().view(np.uint32))
 cap = n * stride
 h_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
 h_vert = torch.empty(cap, dtype=torch.int32).pin_memory()
 h_stat = torch.empty(n, dtype=torch.uint8).pin_memory()
-for chunk in [0, 1 << 16, 1 << 17, 1 << 18, 1 << 19, 1 << 20, 1 << 21]:
+chunks = [0, 1 << 17, 1 << 18, 3 << 17, 1 << 19, 3 << 18, 1 << 20, 1 << 21]
+for a in sys.argv:
+    if a.startswith("--chunks="):
+        chunks = [int(x) for x in a.split("=", 1)[1].split(",")]
+for chunk in chunks:
     if chunk > n:
         continue
     ts = []
