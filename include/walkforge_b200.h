@@ -108,9 +108,10 @@ typedef struct wf_exec_options {
  * move; they are used automatically when memory allows unless opted out. */
 #define WF_LAYOUT_COMPACT_ALIAS 1u /* 16 B alias buckets (no destination vertex words) */
 #define WF_LAYOUT_NO_ADJ 2u        /* no decorated adjacency for NAIVE / O-REJ */
-#define WF_LAYOUT_MP_SUCC 4u       /* opt in: MetaPath successor-decorated edges (cyclic schemas) */
+#define WF_LAYOUT_MP_SUCC 4u       /* MetaPath successor-decorated edges (cyclic schemas; default when HBM allows) */
 #define WF_LAYOUT_FORCE_ADJ 8u     /* decorated adjacency even when the compact graph fits L2 */
 #define WF_LAYOUT_SEARCH_TREE 16u  /* Node2Vec: sector B-tree instead of the edge hash set */
+#define WF_LAYOUT_NO_MP_SUCC 32u   /* MetaPath: label records + partitioned neighbours only */
 
 typedef struct wf_query_spec {
     int32_t mode; /* wf_query_mode */

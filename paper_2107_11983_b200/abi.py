@@ -155,6 +155,7 @@ LAYOUT_NO_ADJ = 2
 LAYOUT_MP_SUCC = 4
 LAYOUT_FORCE_ADJ = 8
 LAYOUT_SEARCH_TREE = 16
+LAYOUT_NO_MP_SUCC = 32
 
 HAS_WIDE_ALIAS = 1
 HAS_ADJ = 2

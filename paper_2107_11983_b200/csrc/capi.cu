@@ -422,10 +422,11 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
             s.g->ensure_label_index(nullptr);
             WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            // opt-in: one random 16 B read per move instead of record + neighbour,
-            // but over a 4x larger array; measured slower on R-MAT s22 (the
-            // 32 B label records of hot vertices hit in L2), profiles/.
-            if ((lf & WF_LAYOUT_MP_SUCC) && 16 * E + reserve <= free_b)
+            // one random 16 B read per move (the partitioned edge carrying the
+            // next schema label's group of its destination) instead of label
+            // record + neighbour: C4 2.07 -> 1.87 ms since the warp-claimed
+            // refill (it measured slower while the cursor atomic bound C4)
+            if (!(lf & WF_LAYOUT_NO_MP_SUCC) && 16 * E + reserve <= free_b)
                 s.build_metapath_successors(nullptr);
         }
         if (s.desc.kind == WF_PROGRAM_NODE2VEC) {

@@ -339,8 +339,10 @@ LAYOUT_CASES = [
      abi.HAS_MP_SUCC | abi.HAS_LABEL_INDEX),
     ("metapath_succ_irregular", lambda: MetaPathProgram([0, 1, 0, 2, 3, 1, 4]), abi.LAYOUT_MP_SUCC,
      abi.HAS_LABEL_INDEX),  # successor of 0 is not unique: falls back to records
-    ("metapath_records", lambda: MetaPathProgram([i % 5 for i in range(40)]), 0,
+    ("metapath_records", lambda: MetaPathProgram([i % 5 for i in range(40)]), abi.LAYOUT_NO_MP_SUCC,
      abi.HAS_LABEL_INDEX),
+    ("metapath_default_succ", lambda: MetaPathProgram([i % 5 for i in range(40)]), 0,
+     abi.HAS_MP_SUCC | abi.HAS_LABEL_INDEX),
 ]
 
 

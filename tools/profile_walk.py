@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--counts", action="store_true", help="PPR: also accumulate visit counts")
     ap.add_argument("--diag-times", action="store_true",
                     help="library built with -DWF_DIAG_FINISH_TIME: print walk completion-time percentiles")
+    ap.add_argument("--tune", action="store_true", help="run the launch tuner first (wf_session_tune)")
     ap.add_argument("--graph", action="store_true", help="replay the launch as a captured CUDA graph")
     ap.add_argument("--flush", action="store_true", help="write 256 MiB between launches (cold L2, as bench.py)")
     args = ap.parse_args()
@@ -56,6 +57,8 @@ def main():
                     counts.data_ptr() if counts is not None else 0, steps.data_ptr(), 0, s.cuda_stream,
                     sources_dev_ptr=d_src.data_ptr())
 
+    if args.tune:
+        print("tuned blocks/SM, ms:", sess.tune(spec, lo, hi, sources_dev_ptr=d_src.data_ptr()), flush=True)
     graph = None
     if args.graph:
         launch()  # warm (no allocation inside the capture)
