@@ -439,6 +439,10 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
             } else {
                 s.g->ensure_search_index(nullptr);
             }
+            if (!(lf & WF_LAYOUT_NO_EDGE_FILTER)) {
+                s.g->ensure_edge_filter(nullptr);
+                s.use_edge_filter = true;
+            }
         }
         s.grid = occupancy_grid(s);
         *out = h.release();
@@ -463,6 +467,7 @@ int wf_session_layout(const wf_session* sh, uint32_t* flags) {
         if (s.alias_wide) f |= WF_LAYOUT_HAS_WIDE_ALIAS;
         if (s.adj.get()) f |= WF_LAYOUT_HAS_ADJ;
         if (s.mp_adj.get()) f |= WF_LAYOUT_HAS_MP_SUCC;
+        if (s.use_edge_filter) f |= WF_LAYOUT_HAS_EDGE_FILTER;
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.g->label_index_built) f |= WF_LAYOUT_HAS_LABEL_INDEX;
         if (s.desc.kind == WF_PROGRAM_NODE2VEC && !s.use_edge_hash && s.g->search_index_built)
             f |= WF_LAYOUT_HAS_SEARCH_INDEX;

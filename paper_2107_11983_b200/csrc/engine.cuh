@@ -52,6 +52,11 @@ struct GraphView {
     // buckets of four u64 keys (src << 32 | dst), load factor <= 1/2
     const unsigned long long* ehash;
     uint64_t ehash_buckets;
+    // edge pre-filter (Node2Vec): blocked Bloom filter of unordered vertex
+    // pairs, one 32 B sector per pair with kFilterBits bits set; "absent" is
+    // exact (no false negatives), "maybe" falls through to the exact test
+    const uint4* efilter;
+    uint64_t efilter_sectors;  // power of two
     // instrumented runs only: [trials, search probes, scanned edges] (the
     // S_alg access counts of SURVEY 8d), else null
     unsigned long long* stats;
@@ -303,6 +308,33 @@ __host__ __device__ __forceinline__ uint64_t ehash_bucket(uint64_t key, uint64_t
 #endif
 }
 
+constexpr int kFilterBits = 4;  // bits per pair in its 256-bit sector
+
+// The pair's sector and its kFilterBits bit positions (8 bits each) from one
+// 64-bit mix of the unordered pair.
+__host__ __device__ __forceinline__ uint64_t efilter_hash(uint32_t u, uint32_t v) {
+    const uint32_t a = u < v ? u : v, b = u < v ? v : u;
+    return splitmix_mix(((static_cast<uint64_t>(a) << 32) | b) ^ 0xBB67AE8584CAA73BULL);
+}
+
+// false: no edge between u and v in either direction (exact); true: maybe.
+__device__ __forceinline__ bool efilter_maybe(const GraphView& g, uint32_t u, uint32_t v) {
+    const uint64_t h = efilter_hash(u, v);
+    uint4 lo, hi;
+    ldr256(g.efilter + 2 * (h & (g.efilter_sectors - 1)), lo, hi);
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    bool maybe = true;
+#pragma unroll
+    for (int i = 0; i < kFilterBits; ++i) {
+        const uint32_t bit = static_cast<uint32_t>(h >> (32 + 8 * i)) & 255u;
+        uint32_t word = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) word = (bit >> 5) == static_cast<uint32_t>(k) ? w[k] : word;
+        maybe = maybe && ((word >> (bit & 31)) & 1u);
+    }
+    return maybe;
+}
+
 // Graph::has_edge (graph.cpp:182-188) as an exact hash-set lookup: one 32 B
 // bucket (a single 256-bit load) answers almost every query — a random
 // sector instead of a binary search's chain of dependent probes.  Same
@@ -332,6 +364,10 @@ __device__ __forceinline__ bool has_edge_hashed(const GraphView& g, uint32_t u, 
 // Node2Vec's "is dst a neighbour of prev" (algorithms.hpp:116-118).
 __device__ __forceinline__ bool prev_has_edge(const GraphView& g, uint32_t prev, uint64_t prev_base,
                                               uint32_t prev_deg, uint32_t dst, unsigned long long* probes) {
+    if (g.efilter) {
+        if (probes) atomicAdd(probes, 1ull);  // the filter's sector is a request too
+        if (!efilter_maybe(g, prev, dst)) return false;
+    }
     if (g.ehash) return has_edge_hashed(g, prev, dst, probes);
     return has_edge_indexed(g, prev_base, prev_deg, prev, dst, probes);
 }
@@ -471,6 +507,9 @@ __device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunc
     if (y < scaled(p.lo_w)) return true;
     if (!(y < scaled(p.hi_w))) return false;
     bool common = prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, L.g.stats ? L.g.stats + 1 : nullptr);
+#ifdef WF_DIAG_COMMON
+    if (common && L.g.stats) atomicAdd(L.g.stats + 2, 1ull);  // diagnostics: distance tests answered "edge"
+#endif
     return y < scaled(common ? 1.0 : p.inv_b);
 }
 

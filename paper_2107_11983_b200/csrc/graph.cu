@@ -421,6 +421,50 @@ __global__ void k_edge_hash(const uint64_t* __restrict__ off, const uint32_t* __
 }
 }  // namespace
 
+namespace {
+// Warp per vertex: set each edge's kFilterBits bits in its pair's sector.
+__global__ void k_edge_filter(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                              uint32_t V, uint32_t* __restrict__ words, uint64_t sectors) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < V; v += nwarps) {
+        const uint64_t a = off[v], b = off[v + 1];
+        for (uint64_t e = a + lane; e < b; e += 32) {
+            const uint64_t h = efilter_hash(static_cast<uint32_t>(v), nbr[e]);
+            uint32_t* sec = words + 8 * (h & (sectors - 1));
+            for (int i = 0; i < kFilterBits; ++i) {
+                const uint32_t bit = static_cast<uint32_t>(h >> (32 + 8 * i)) & 255u;
+                atomicOr(sec + (bit >> 5), 1u << (bit & 31));
+            }
+        }
+    }
+}
+}  // namespace
+
+// Pre-filter for Node2Vec's distance test: ~8 bits per stored pair (a
+// power-of-two number of 32 B sectors, at most 64 MiB so it can stay in L2).
+// Only ~5 % of the distance tests on R-MAT find an edge, so most are answered
+// by one L2-resident sector instead of a DRAM bucket of the exact set.
+void GraphStore::ensure_edge_filter(cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (edge_filter_built || E == 0) return;
+    DeviceGuard guard(device);
+    uint64_t sectors = 1;
+#ifndef WF_FILTER_MAX_LOG2
+#define WF_FILTER_MAX_LOG2 21
+#endif
+    while (sectors * 256 < 8 * E && sectors < (1ull << WF_FILTER_MAX_LOG2)) sectors <<= 1;
+    efilter.allocate(2 * sectors);
+    WF_CUDA(cudaMemsetAsync(efilter.get(), 0, efilter.bytes(), st));
+    k_edge_filter<<<blocks_for((uint64_t)V * 32, 256, device), 256, 0, st>>>(
+        offsets.get(), nbr.get(), V, reinterpret_cast<uint32_t*>(efilter.get()), sectors);
+    WF_LAUNCHED();
+    WF_CUDA(cudaStreamSynchronize(st));
+    efilter_sectors = sectors;
+    edge_filter_built = true;
+}
+
 // Exact edge set for Node2Vec's distance test (has_edge_hashed), 2 slots per
 // edge (load factor 1/2): one random 32 B bucket per membership query.
 void GraphStore::ensure_edge_hash(cudaStream_t st) {

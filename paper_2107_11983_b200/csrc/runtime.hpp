@@ -50,6 +50,9 @@ struct GraphStore {
     bool edge_hash_built = false;
     uint64_t ehash_buckets = 0;
     DeviceBuffer<unsigned long long> ehash;  // edge hash set (has_edge_hashed)
+    bool edge_filter_built = false;
+    uint64_t efilter_sectors = 0;
+    DeviceBuffer<uint4> efilter;  // blocked Bloom filter of vertex pairs (efilter_maybe)
 
     GraphView view() const {
         GraphView g{};
@@ -68,6 +71,8 @@ struct GraphStore {
         for (int l = 0; l < kSidxMaxLevels; ++l) g.sidx[l] = sidx[l].get();
         g.ehash = ehash.get();
         g.ehash_buckets = ehash_buckets;
+        g.efilter = efilter.get();
+        g.efilter_sectors = efilter_sectors;
         return g;
     }
     bool has_weights() const { return weights.get() != nullptr; }
@@ -79,6 +84,7 @@ struct GraphStore {
     void ensure_label_index(cudaStream_t st);
     void ensure_search_index(cudaStream_t st);
     void ensure_edge_hash(cudaStream_t st);
+    void ensure_edge_filter(cudaStream_t st);
 };
 
 struct HostPipe;  // stream.cu: cached streams/buffers of the host-output pipeline
@@ -114,6 +120,7 @@ struct Session {
     DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
     bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
     bool use_edge_hash = false;  // Node2Vec distance test through the graph's edge hash set
+    bool use_edge_filter = false;  // ... behind the graph's pair pre-filter
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
     DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 

@@ -81,6 +81,7 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     WalkLaunch L{};
     L.g = g.view();
     if (!s.use_edge_hash) L.g.ehash = nullptr;  // per-session choice (B-tree opt-in)
+    if (!s.use_edge_filter) L.g.efilter = nullptr;
     L.sview = s.any_exhausted ? s.sview.get() : g.vword.get();
     L.alias = s.alias.get();
     L.its = s.its.get();

@@ -330,7 +330,11 @@ LAYOUT_CASES = [
     ("node2vec_w_adj", lambda: Node2VecProgram(0.5, 3.0, 30, True), abi.LAYOUT_FORCE_ADJ,
      abi.HAS_ADJ | abi.HAS_EDGE_HASH),
     ("node2vec_no_adj", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_NO_ADJ,
+     abi.HAS_EDGE_HASH | abi.HAS_EDGE_FILTER),
+    ("node2vec_no_filter", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_NO_EDGE_FILTER,
      abi.HAS_EDGE_HASH),
+    ("node2vec_w_no_filter_tree", lambda: Node2VecProgram(0.5, 3.0, 30, True),
+     abi.LAYOUT_NO_EDGE_FILTER | abi.LAYOUT_SEARCH_TREE, abi.HAS_SEARCH_INDEX),
     ("node2vec_search_tree", lambda: Node2VecProgram(2.0, 0.5, 40, False),
      abi.LAYOUT_SEARCH_TREE | abi.LAYOUT_FORCE_ADJ, abi.HAS_ADJ | abi.HAS_SEARCH_INDEX),
     ("node2vec_w_search_tree", lambda: Node2VecProgram(0.5, 3.0, 30, True),
