@@ -366,15 +366,17 @@ def test_every_hbm_layout_is_bit_exact(rmat12, name, mk, flags, expect):
     _compare_with_reference(dg, hg, spec, prog, opts)
 
 
-@pytest.mark.parametrize("prog,chunk", [(PprProgram(0.1), 1000), (DeepWalkProgram(24, True), 777),
-                                        (Node2VecProgram(2.0, 0.5, 16, False), 0),
-                                        (MetaPathProgram([i % 5 for i in range(12)]), 513)])
-def test_run_host_streaming_equals_run(rmat12, prog, chunk):
+@pytest.mark.parametrize("prog,chunk,nsrc", [(PprProgram(0.1), 1000, 9000),
+                                             (PprProgram(0.2), 1 << 14, 1 << 18),
+                                             (DeepWalkProgram(24, True), 777, 9000),
+                                             (Node2VecProgram(2.0, 0.5, 16, False), 0, 9000),
+                                             (MetaPathProgram([i % 5 for i in range(12)]), 513, 9000)])
+def test_run_host_streaming_equals_run(rmat12, prog, chunk, nsrc):
     """wf_session_run_host (chunked compute/copy pipeline into host buffers),
     called repeatedly on one session and on qid sub-ranges, equals the walk set
     of run_sequential — including PPR walks that outgrow their row (stride 8)."""
     dg, hg = rmat12
-    src = np.random.default_rng(3).integers(0, hg.vertex_count, 9000).astype(np.uint32)
+    src = np.random.default_rng(3).integers(0, hg.vertex_count, nsrc).astype(np.uint32)
     spec = QuerySpec.from_list(src)
     opts = ExecOptions(seed=17, path_stride=8)
     whole = E.run_sequential(dg, spec, prog, opts).walks
@@ -384,7 +386,7 @@ def test_run_host_streaming_equals_run(rmat12, prog, chunk):
         assert res.walks.equals(whole), rep
         assert res.metrics.total_steps == int(whole.lengths().sum()) - len(whole)
     # a shard [lo, hi) through the raw call
-    lo, hi = 2500, 7100
+    lo, hi = 2500, min(nsrc, 7100 + nsrc // 2)
     n = hi - lo
     off = np.zeros(n + 1, np.uint64)
     cap = int(whole.offsets[hi] - whole.offsets[lo]) + 16
