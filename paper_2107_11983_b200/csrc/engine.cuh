@@ -178,13 +178,9 @@ __device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint
     }
 }
 
-#ifndef WF_LDR_WORD
-#define WF_LDR_WORD WF_LDR
-#endif
 __device__ __forceinline__ void decode_vertex(const GraphView& g, const uint64_t* vw, uint32_t v,
                                               uint64_t& base, uint32_t& deg) {
-    uint64_t w;
-    asm(WF_LDR_WORD ".u64 %0, [%1];" : "=l"(w) : "l"(vw + v));
+    uint64_t w = ldr(vw + v);  // (L1-allocating ld.ca / ld.nc measured no different, C2)
     base = w >> kDegBits;
     deg = static_cast<uint32_t>(w & kDegEscape);
     if (deg == kDegEscape) {  // rare: very high degree
@@ -822,15 +818,17 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
     if (L.visit_counts) atomicAdd(L.visit_counts + v, 1u);
 }
 
-// The persistent step kernel.  One walker per lane; lanes whose walk ended pull
-// the next query id from a global cursor with one atomic per warp (the GPU
-// analogue of the interleaved executor's admit/refill, interleave.hpp:436-464,
-// 531-538), so PPR's geometric terminations never idle a lane while queries
-// remain.  Every walker draws only from its own (seed, qid) stream, so the
-// output is independent of scheduling, exactly as in the reference.
-// Full occupancy (8 x 256 threads per SM, <= 32 registers) for the flows whose
-// state fits it: every resident walker is one more request in flight.  The
+// The persistent step kernel.  One walker per lane; lanes whose walk ended take
+// the next row from their warp's claimed block of rows (the GPU analogue of the
+// interleaved executor's admit/refill, interleave.hpp:436-464, 531-538), so
+// PPR's geometric terminations never idle a lane while queries remain.  Every
+// walker draws only from its own (seed, qid) stream, so the output is
+// independent of scheduling, exactly as in the reference.
+//
+// Register bound: 8 x 256 threads per SM (<= 32 registers) for the flows whose
+// state fits it; the launch tuner (wf_session_tune) may run fewer blocks.  The
 // gathered flows (per-step scans, on-the-fly Vose) keep their registers.
+// Build knobs (experiments only): WF_N2V_BLOCKS, WF_CLAIM.
 template <int K, int S, int F>
 constexpr int walk_min_blocks() {
     // Node2Vec's O-REJ step (edge hash probe) needs ~48 registers without
@@ -845,7 +843,8 @@ constexpr int walk_min_blocks() {
 }
 
 // Rows a warp claims from the global cursor per atomic.  One atomic per refill
-// put every warp's refill on one L2 address (~every other iteration for PPR).
+// put every warp's refill on one L2 address (~every other iteration for PPR):
+// C4 15.9 -> 31.7 G steps/s, C5 33.5 -> 40.5 G with 32-row claims.
 #ifndef WF_CLAIM
 #define WF_CLAIM 32
 #endif
