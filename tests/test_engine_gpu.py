@@ -432,3 +432,27 @@ def test_launch_tuner_keeps_results(rmat12):
     assert all(np.array_equal(a, b) for a, b in zip(before[1], after[1]))
     assert np.array_equal(before[2], after[2])
     assert np.array_equal(before[3], after[3])
+
+
+def test_degree_escape_vertex_matches_reference():
+    """A vertex of degree >= 2^24 - 1 does not fit the packed vertex word and is
+    read through the offsets (kDegEscape): walks through it stay bit-exact."""
+    from paper_2107_11983_b200.host import Graph
+    D = (1 << 24) + 37
+    V = D + 1
+    offsets = np.empty(V + 1, np.uint64)
+    offsets[0] = 0
+    offsets[1:] = D + np.arange(0, V, dtype=np.uint64)
+    nbr = np.empty(2 * D, np.uint32)
+    nbr[:D] = np.arange(1, V, dtype=np.uint32)
+    nbr[D:] = 0
+    w = np.random.default_rng(1).uniform(1.0, 5.0, 2 * D).astype(np.float32)
+    hg = Graph(offsets, nbr, w)
+    dg = E.DeviceGraph.from_host(hg)
+    src = np.where(np.arange(512) % 2 == 0, 0, np.random.default_rng(2).integers(1, V, 512)).astype(np.uint32)
+    spec = QuerySpec.from_list(src)
+    for prog, sampler in [(PprProgram(0.2), None), (DeepWalkProgram(12, True), None),
+                          (DeepWalkProgram(12, True), abi.Sampler.ITS),
+                          (Node2VecProgram(2.0, 0.5, 12, False), None), (UniformProgram(12), None)]:
+        opts = ExecOptions(seed=31, sampler=sampler)
+        _compare_with_reference(dg, hg, spec, prog, opts)
