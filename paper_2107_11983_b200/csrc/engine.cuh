@@ -758,6 +758,34 @@ __device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
     decode_vertex(L.g, L.sview, q.cur, q.cur_base, q.cur_deg);
 }
 
+// What load_current would read for a walk starting at `src`, packed as a
+// vertex word (base << 24 | deg) for claim-time staging; kNoWord when it does
+// not pack (a label group of >= 2^24 - 1 edges): that lane loads it itself.
+constexpr unsigned long long kNoWord = ~0ull;
+template <int K, int S, int F>
+__device__ __forceinline__ unsigned long long start_word(const WalkLaunch& L, uint32_t src) {
+    if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
+        if (L.use_label_index) {
+            uint4 r0, r1;
+            ldr256(L.g.lab_rec + 2 * static_cast<uint64_t>(src), r0, r1);
+            const uint64_t base = (static_cast<uint64_t>(r0.y) << 32) | r0.x;
+            const uint32_t ends[kMaxIndexedLabels] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            const uint32_t l = __ldg(L.prog.schema);
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxIndexedLabels; ++i) {
+                if (static_cast<uint32_t>(i) == l) hi = ends[i];
+                if (static_cast<uint32_t>(i) + 1 == l) lo = ends[i];
+            }
+            if (l >= static_cast<uint32_t>(kMaxIndexedLabels)) lo = hi = 0;
+            const uint64_t gb = base + lo;
+            const uint32_t cnt = hi - lo;
+            return cnt < kDegEscape && gb < (1ull << 40) ? (gb << kDegBits) | cnt : kNoWord;
+        }
+    }
+    return ldr(L.sview + src);
+}
+
 __device__ __forceinline__ uint32_t source_at(const WalkLaunch& L, uint64_t qid) {  // walker.hpp:70-77
     if (L.qmode == WF_QUERY_ONE_PER_VERTEX) return static_cast<uint32_t>(qid);
     if (L.qmode == WF_QUERY_FROM_SOURCE) return L.qsource;
@@ -877,9 +905,8 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     // words are loaded by the whole warp at once (one coalesced load + one
     // gather per 32 rows) into shared memory, so a refilled lane moves in the
     // same iteration instead of sitting one out on its own source -> word load
-    // chain (C1 -5 %, C5 -1.6 %; and no register spills).  MetaPath's
-    // label-index flow loads a label record instead and keeps the sit-out.
-    constexpr bool kStage = !(K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered);
+    // chain (C1 -5 %, C5 -1.6 %; and no register spills).  For MetaPath's
+    // label index the staged word is the source's first label group.
     __shared__ unsigned long long claim_first[kBlock / 32];
     __shared__ uint32_t claim_src[kBlock / 32][kClaim];
     __shared__ unsigned long long claim_word[kBlock / 32][kClaim];
@@ -930,13 +957,13 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     drained = drained || !active;
                     continue;
                 }
-                if constexpr (kStage) {
+                {
                     uint32_t src = 0;
                     unsigned long long word = 0;
                     if (static_cast<uint32_t>(lane) < wleft) {
                         const uint64_t qid = L.qid_map ? __ldg(L.qid_map + wnext + lane) : L.qid_begin + wnext + lane;
                         src = source_at(L, qid);
-                        if (src < L.g.V) word = ldr(L.sview + src);
+                        if (src < L.g.V) word = start_word<K, S, F>(L, src);
                     }
                     claim_src[wid][lane] = src;
                     claim_word[wid][lane] = word;
@@ -957,8 +984,8 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                 const uint64_t qid = L.qid_map ? __ldg(L.qid_map + row) : L.qid_begin + row;
                 q.row = row;
                 q.rng.s = stream_state(L.seed_mixed, qid);
-                const uint32_t slot = kStage ? static_cast<uint32_t>(row - claim_first[wid]) : 0;
-                q.cur = kStage ? claim_src[wid][slot] : source_at(L, qid);
+                const uint32_t slot = static_cast<uint32_t>(row - claim_first[wid]);
+                q.cur = claim_src[wid][slot];
                 q.prev = 0xFFFFFFFFu;
                 q.len = 0;
                 if (q.cur >= L.g.V) {
@@ -973,12 +1000,12 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     if (P::prechecked && P::finished(L.prog, q)) {
                         finish(L, q, WF_WALK_COMPLETE, ps);  // walk_already_finished, program.hpp:86-93
                     } else {
-                        if constexpr (kStage) {
-                            unpack_word(L.g, claim_word[wid][slot], q.cur, q.cur_base, q.cur_deg);
-                            active = true;
+                        const unsigned long long w = claim_word[wid][slot];
+                        active = true;
+                        if (w != kNoWord) {
+                            unpack_word(L.g, w, q.cur, q.cur_base, q.cur_deg);
                         } else {
                             load_current<K, S, F>(L, q);
-                            active = true;
                             fresh = true;
                         }
                     }
@@ -986,9 +1013,9 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
             }
         }
         if (!__any_sync(kFull, active)) break;
-        // A lane refilled without staging (MetaPath label index) sits one
-        // iteration out: its label record is still in flight, and consuming it
-        // now would stall the whole warp on that load.
+        // A lane whose start could not be staged (a label group too large for
+        // a packed word) sits one iteration out: its load is still in flight,
+        // and consuming it now would stall the whole warp on that load.
         const bool ready = active && !fresh;
         fresh = false;
         if (ready) {
