@@ -456,3 +456,34 @@ def test_degree_escape_vertex_matches_reference():
                           (Node2VecProgram(2.0, 0.5, 12, False), None), (UniformProgram(12), None)]:
         opts = ExecOptions(seed=31, sampler=sampler)
         _compare_with_reference(dg, hg, spec, prog, opts)
+
+
+@pytest.mark.parametrize("prog,chunk,stride", [(PprProgram(0.2), 1 << 14, 64), (PprProgram(0.1), 5000, 8),
+                                               (DeepWalkProgram(24, True), 7777, 0),
+                                               (MetaPathProgram([i % 5 for i in range(12)]), 0, 0)])
+def test_run_host_pinned_equals_run(rmat12, prog, chunk, stride):
+    """Pinned host buffers (the bench's e2e path): the same bytes as the walk
+    set of run_sequential, including walks that outgrow their row, and a
+    too-small capacity is an error, not an overrun."""
+    import torch
+    dg, hg = rmat12
+    src = np.random.default_rng(9).integers(0, hg.vertex_count, 1 << 17).astype(np.uint32)
+    spec = QuerySpec.from_list(src)
+    opts = ExecOptions(seed=41, path_stride=stride)
+    whole = E.run_sequential(dg, spec, prog, opts).walks
+    n = src.size
+    total = int(whole.offsets[-1])
+    sess = E.Session(dg, prog, opts)
+    h_off = torch.zeros(n + 1, dtype=torch.int64).pin_memory()
+    h_vert = torch.zeros(total + 64, dtype=torch.int32).pin_memory()
+    h_stat = torch.zeros(n, dtype=torch.uint8).pin_memory()
+    for rep in range(2):
+        h_vert.fill_(-1)
+        m = sess.run_host(spec, h_off.data_ptr(), h_vert.data_ptr(), total + 64, h_stat.data_ptr(), chunk=chunk)
+        assert np.array_equal(h_off.numpy().view(np.uint64), whole.offsets), rep
+        assert np.array_equal(h_vert.numpy()[:total].view(np.uint32), whole.vertices), rep
+        assert np.array_equal(h_stat.numpy(), whole.status), rep
+        assert m.total_steps == total - n
+    # too small a capacity is an error, not an overrun
+    with pytest.raises(abi.InvalidArgument):
+        sess.run_host(spec, h_off.data_ptr(), h_vert.data_ptr(), total - 1, h_stat.data_ptr(), chunk=chunk)
