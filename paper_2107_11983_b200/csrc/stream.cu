@@ -214,8 +214,13 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         trace("chunk computed", static_cast<long long>(k));
         uint64_t cnt = P.h_tot[b];
         chunk_base[k + 1] = chunk_base[k] + cnt;
-        if (chunk_base[k + 1] > capacity)
+        if (chunk_base[k + 1] > capacity) {
+            // drain what is in flight into the caller's buffers before unwinding
+            cudaStreamSynchronize(A);
+            cudaStreamSynchronize(B);
+            cudaStreamSynchronize(P.c);
             raise(WF_ERR_INVALID_ARG, "vertices_capacity too small for the walk set");
+        }
         if (cnt > P.stage[b].size()) {
             // rare (walks outgrew their rows): stage this chunk in a larger buffer
             WF_CUDA(cudaStreamSynchronize(B));
