@@ -569,7 +569,14 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "bytes_per_move": b, "bytes_model": b_desc},
+                     "bytes_per_move": b, "bytes_model": b_desc,
+                     # BASELINE's own definition: HBM bandwidth / measured DRAM
+                     # bytes per step (ncu, cold cache, includes the 128 B line
+                     # fetched for every 32 B random request)
+                     "measured_sectors": None if not traffic else {
+                         "bytes_per_move": traffic / moves,
+                         "ceiling_steps_per_s": peak / (traffic / moves) * 1e9,
+                         "frac": value / world / (peak / (traffic / moves) * 1e9)}},
         "random_access": random_access_block(moves * args.steps / (total_ms * 1e-3), reads),
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
