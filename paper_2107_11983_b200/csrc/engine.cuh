@@ -118,6 +118,11 @@ struct Walker {
     // vertex word of the destination when the sampler's load carried it
     uint64_t nb_word;
     bool have_nb;
+    // nb_word holds the current vertex's raw word, not yet unpacked into
+    // cur_base / cur_deg: the next move unpacks it after taking its first
+    // draw, so the RNG arithmetic overlaps the word's load instead of waiting
+    // behind the unpack's escape branch
+    bool pend;
 };
 
 // ---- graph helpers -------------------------------------------------------------
@@ -572,12 +577,23 @@ __device__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double*
     second_out = x;
 }
 
+// Deferred unpack of the current vertex word (Walker::pend): on for every
+// program but Node2Vec, whose O-REJ kernel measured 3 % slower with it.
+template <int K>
+constexpr bool kDeferWord = K != WF_PROGRAM_NODE2VEC;
+
 // One move: StepDriver::step (engine.hpp:342-426).  Draw order per sampler is
 // the reference contract (engine.hpp:330-333): NAIVE x; ITS x_real; ALIAS x
 // then y; REJ / O-REJ (x, y) per trial; dead ends consume no draws.
 template <int K, int S, int F>
 __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& dst) {
     using P = Program<K>;
+    if constexpr (kDeferWord<K>) {
+        if (q.pend) {
+            unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
+            q.pend = false;
+        }
+    }
     const uint32_t d = q.cur_deg;
     const uint64_t base = q.cur_base;
     if (d == 0) return kDead;
@@ -758,6 +774,14 @@ __device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
     decode_vertex(L.g, L.sview, q.cur, q.cur_base, q.cur_deg);
 }
 
+// True when load_current is a plain vertex-word read (everything but
+// MetaPath's label-index flow), which can then be deferred (Walker::pend).
+template <int K, int S, int F>
+__device__ __forceinline__ bool plain_word(const WalkLaunch& L) {
+    if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) return !L.use_label_index;
+    return true;
+}
+
 // What load_current would read for a walk starting at `src`, packed as a
 // vertex word (base << 24 | deg) for claim-time staging; kNoWord when it does
 // not pack (a label group of >= 2^24 - 1 edges): that lane loads it itself.
@@ -831,8 +855,8 @@ __device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int
     if (q.len > L.stride) atomicAdd(L.overflow_out, 1ULL);
 }
 
-__device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint32_t v, PathStage ps) {
-    const uint32_t p = q.len;
+__device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint32_t p, uint32_t v,
+                                     PathStage ps) {
     if (p < L.stride) {
         if (L.staged) {
             ps.at(p & 7) = v;
@@ -863,11 +887,14 @@ constexpr int walk_min_blocks() {
     // spills (5 blocks: 23.9 vs 22.9 G steps/s at 6 with 76 B of spills, C3);
     // MetaPath's label-index ITS path is the C4 hot loop (its generic
     // gathered fallback shares the kernel).
-    if (F == kGathered) return (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) ? 6 : 1;
+#ifndef WF_MIN_BLOCKS
+#define WF_MIN_BLOCKS 4
+#endif
+    if (F == kGathered) return (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) ? WF_MIN_BLOCKS : 1;
 #ifndef WF_N2V_BLOCKS
 #define WF_N2V_BLOCKS 5
 #endif
-    return K == WF_PROGRAM_NODE2VEC ? WF_N2V_BLOCKS : 8;
+    return K == WF_PROGRAM_NODE2VEC ? WF_N2V_BLOCKS : WF_MIN_BLOCKS;
 }
 
 // Rows a warp claims from the global cursor per atomic.  One atomic per refill
@@ -893,6 +920,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     q.rng.s = 0;
     q.nb_word = 0;
     q.have_nb = false;
+    q.pend = false;
     bool active = false;
     bool fresh = false;
     bool drained = false;
@@ -995,7 +1023,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     q.cur = 0;
                 }
                 {
-                    emit(L, q, q.cur, ps);
+                    emit(L, q, 0, q.cur, ps);
                     q.len = 1;
                     if (P::prechecked && P::finished(L.prog, q)) {
                         finish(L, q, WF_WALK_COMPLETE, ps);  // walk_already_finished, program.hpp:86-93
@@ -1003,7 +1031,12 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                         const unsigned long long w = claim_word[wid][slot];
                         active = true;
                         if (w != kNoWord) {
-                            unpack_word(L.g, w, q.cur, q.cur_base, q.cur_deg);
+                            if constexpr (kDeferWord<K>) {
+                                q.nb_word = w;
+                                q.pend = true;
+                            } else {
+                                unpack_word(L.g, w, q.cur, q.cur_base, q.cur_deg);
+                            }
                         } else {
                             load_current<K, S, F>(L, q);
                             fresh = true;
@@ -1026,14 +1059,30 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                 q.prev_base = q.cur_base;
                 q.prev_deg = q.cur_deg;
                 q.cur = dst;
-                emit(L, q, dst, ps);
+                const uint32_t p = q.len;
                 q.len += 1;
                 steps += 1;
-                if (P::update(L.prog, q)) {
+                // update (PPR's stop coin) before the path store: its draw
+                // overlaps the neighbour load the store waits for (Node2Vec,
+                // with kDeferWord off, keeps its original order)
+                bool done;
+                if constexpr (K == WF_PROGRAM_NODE2VEC) {
+                    emit(L, q, p, dst, ps);
+                    done = P::update(L.prog, q);
+                } else {
+                    done = P::update(L.prog, q);
+                    emit(L, q, p, dst, ps);
+                }
+                if (done) {
                     finish(L, q, WF_WALK_COMPLETE, ps);
                     active = false;
                 } else if (q.have_nb) {
-                    unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
+                    // unpacked by the next move (kDeferWord)
+                    if constexpr (kDeferWord<K>) q.pend = true;
+                    else unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
+                } else if (kDeferWord<K> && plain_word<K, S, F>(L)) {
+                    q.nb_word = ldr(L.sview + q.cur);
+                    q.pend = true;
                 } else {
                     load_current<K, S, F>(L, q);
                 }

@@ -36,6 +36,8 @@ struct Rng {
         s += kGamma;
         return splitmix_mix(s);
     }
+    // The next draw without taking it (same value next() will return).
+    __device__ __forceinline__ uint64_t peek() const { return splitmix_mix(s + kGamma); }
     // uniform_index, rng.hpp:34-38: (r * n) >> 64.
     __device__ __forceinline__ uint32_t index(uint32_t n) {
         return static_cast<uint32_t>(__umul64hi(next(), static_cast<uint64_t>(n)));
