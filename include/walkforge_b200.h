@@ -12,6 +12,12 @@
  * Error model: every function returns a wf_status.  Status codes map 1:1 onto
  * the reference exception classes (proj/include/walkforge/error.hpp:8-48); the
  * message of the last failure on the calling thread is wf_last_error().
+ *
+ * Threading (the reference's model, SPEC "graph read-only shared, no locks on
+ * the hot path"): a wf_graph may be shared by sessions on any threads (its lazily
+ * built indexes are built under a lock); a wf_session and a wf_walkset must be
+ * used by one thread at a time (they own streams, staging buffers and the claim
+ * cursor of their launches).
  */
 #ifndef WALKFORGE_B200_H
 #define WALKFORGE_B200_H
