@@ -88,10 +88,19 @@ def main():
               flush=True)
         if args.diag_times:
             import numpy as np
-            t = lens.cpu().numpy().view(np.uint32).astype(np.int64)
-            t = (t - t.min()) * 32e-3  # us
+            raw = lens.cpu().numpy().view(np.uint32).astype(np.int64)
+            t = raw >> 8
+            t = ((t - t.min()) % (1 << 24)) * 32e-3  # us
+            ln = raw & 255
             qs = [50, 90, 99, 99.9, 99.99, 100]
             print("  finish us: " + " ".join(f"p{q}={np.percentile(t, q):.1f}" for q in qs), flush=True)
+            last = np.argsort(t)[-8:]
+            print("  last walks (finish us, length): " + " ".join(f"({t[i]:.0f},{ln[i]})" for i in last))
+            for lo, hi in [(1, 8), (8, 16), (16, 32), (32, 64), (64, 256)]:
+                sel = (ln >= lo) & (ln < hi)
+                if sel.any():
+                    print(f"  length [{lo},{hi}): n={sel.sum()} mean finish {t[sel].mean():.1f} us, "
+                          f"max {t[sel].max():.1f} us")
 
 
 if __name__ == "__main__":
