@@ -838,10 +838,11 @@ __device__ __forceinline__ void store_group(uint32_t* dst, PathStage ps) {
 __device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int st, PathStage ps) {
 #ifdef WF_DIAG_FINISH_TIME
     // diagnostic builds only (tools/profile_walk.py --diag-times): the walk's
-    // completion time in 32 ns units replaces its length
+    // completion time in 32 ns units (low 24 bits) and min(length, 255)
+    // replace its length
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    L.lengths[q.row] = static_cast<uint32_t>(t >> 5);
+    L.lengths[q.row] = (static_cast<uint32_t>(t >> 5) << 8) | min(q.len, 255u);
 #else
     L.lengths[q.row] = q.len;
 #endif
