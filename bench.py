@@ -360,7 +360,24 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             e2e_s.append(time.perf_counter() - t0)
         total_vertices = int(h_off[n].item())
         assert m.total_steps == moves_per_step
-        e2e = dict(seconds=float(sum(e2e_s)), h2d=n * 4, d2h=total_vertices * 4 + (n + 1) * 8 + n)
+        e2e_off = dict(seconds=float(sum(e2e_s)), h2d=n * 4, d2h=total_vertices * 4 + (n + 1) * 8 + n,
+                       api="wf_session_run_host (offsets u64 + status u8, pinned host buffers)")
+        # the records form (length | status << 31 per query, walker.hpp:47-55's
+        # WalkRecord without the implicit qid): 4 B per query instead of 9
+        h_rec = torch.empty(n, dtype=torch.int32).pin_memory()
+        sess.run_host_records(hspec, h_rec.data_ptr(), h_vert.data_ptr(), cap, qid_begin=lo, qid_end=hi)
+        e2e_s = []
+        for _ in range(args.steps):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m = sess.run_host_records(hspec, h_rec.data_ptr(), h_vert.data_ptr(), cap, qid_begin=lo, qid_end=hi)
+            e2e_s.append(time.perf_counter() - t0)
+        assert m.total_steps == moves_per_step
+        assert int((h_rec.numpy().view(np.uint32) & 0x7FFFFFFF).astype(np.int64).sum()) == total_vertices
+        e2e = dict(seconds=float(sum(e2e_s)), h2d=n * 4, d2h=total_vertices * 4 + n * 4,
+                   api="wf_session_run_host_records (pinned host buffers)", offsets_api=e2e_off)
         del hspec_c_sources
 
     return dict(moves=moves_per_step, total_ms=total_ms, step_ms=step_ms, stats=stats,
@@ -530,15 +547,16 @@ def main():
     total_ms = r["total_ms"]
     moves = r["moves"]
     e2e_s = r["e2e"]["seconds"] if r["e2e"] else None
+    e2e_off_s = r["e2e"]["offsets_api"]["seconds"] if r["e2e"] else None
     if dist:
-        t = torch.tensor([total_ms, e2e_s or 0.0], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, e2e_s or 0.0, e2e_off_s or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_max = float(t[0]), float(t[1])
+        total_ms, e2e_max, e2e_off_max = float(t[0]), float(t[1]), float(t[2])
         mv = torch.tensor([moves], dtype=torch.int64, device="cuda")
         dist.all_reduce(mv)
         all_moves = int(mv.item())
     else:
-        e2e_max = e2e_s
+        e2e_max, e2e_off_max = e2e_s, e2e_off_s
         all_moves = moves
     value = all_moves * args.steps / (total_ms * 1e-3)
 
@@ -583,9 +601,13 @@ def main():
         "preprocess_seconds": r["preprocess_s"],
     }
     if r["e2e"]:
+        eo = r["e2e"]["offsets_api"]
         line["e2e"] = {"value": all_moves * args.steps / e2e_max, "unit": "steps/s",
                        "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"],
-                       "api": "wf_session_run_host (pinned host buffers)"}
+                       "api": r["e2e"]["api"],
+                       "offsets_api": {"value": all_moves * args.steps / e2e_off_max,
+                                       "h2d_bytes_per_step": eo["h2d"], "d2h_bytes_per_step": eo["d2h"],
+                                       "api": eo["api"]}}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config, cfg, r["dg"], r["spec"])

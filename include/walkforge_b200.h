@@ -281,6 +281,18 @@ int wf_session_run_host(wf_session* s, const wf_query_spec* spec, uint64_t qid_b
                         uint64_t vertices_capacity, uint8_t* status, uint64_t chunk_queries,
                         wf_run_metrics* metrics);
 
+/* The same, with the walk set as records in query order — the shape of the
+ * reference's WalkRecord{qid, status, path} (walker.hpp:47-55) without the
+ * implicit qid:
+ *   records  u32[n]   path length | status << 31  (status 1 = dead end)
+ *   vertices u32[...] the paths back to back
+ * 4 B per query instead of 9 (offsets + status): the lighter form to stream
+ * over PCIe. */
+int wf_session_run_host_records(wf_session* s, const wf_query_spec* spec, uint64_t qid_begin,
+                                uint64_t qid_end, uint32_t* records, uint32_t* vertices,
+                                uint64_t vertices_capacity, uint64_t chunk_queries,
+                                wf_run_metrics* metrics);
+
 /* Instrumentation (measurement only; no reference counterpart): when enabled,
  * launches accumulate logical access counts used for the algorithmic sector
  * figure of SURVEY §8 d — out[0] rejection trials, out[1] adjacency-search

@@ -597,28 +597,47 @@ int wf_session_run(wf_session* sh, const wf_query_spec* spec, wf_walkset** out,
     });
 }
 
+namespace {
+void run_host_checked(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin, uint64_t qid_end,
+                      uint64_t* offsets, uint32_t* vertices, uint64_t vertices_capacity, uint8_t* status,
+                      uint64_t chunk_queries, wf_run_metrics* metrics, uint32_t* records) {
+    require(sh && spec && vertices, "null argument");
+    Session& s = *sh->s;
+    GraphStore& g = *s.g;
+    DeviceGuard guard(g.device);
+    uint64_t n = spec->mode == WF_QUERY_ONE_PER_VERTEX ? g.V : spec->count;
+    if (qid_end == 0) qid_end = n;
+    require(qid_begin <= qid_end && qid_end <= n, "query range out of bounds");
+    if (spec->mode == WF_QUERY_FROM_SOURCE && spec->source >= g.V)
+        config_error("query source " + std::to_string(spec->source) + " is not a vertex (V=" +
+                     std::to_string(g.V) + ")");
+    if (spec->mode == WF_QUERY_FROM_LIST) {
+        require(spec->sources != nullptr || n == 0, "null source list");
+        require(!is_device_pointer(spec->sources), "wf_session_run_host takes a host source list");
+        // sources are range-checked by the walk kernel (ConfigError after the run)
+    }
+    run_to_host(s, *spec, spec->sources, qid_begin, qid_end, offsets, vertices, vertices_capacity, status,
+                chunk_queries, metrics, records);
+}
+}  // namespace
+
+int wf_session_run_host_records(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin,
+                                uint64_t qid_end, uint32_t* records, uint32_t* vertices,
+                                uint64_t vertices_capacity, uint64_t chunk_queries, wf_run_metrics* metrics) {
+    return guarded([&] {
+        require(records != nullptr, "null argument");
+        run_host_checked(sh, spec, qid_begin, qid_end, nullptr, vertices, vertices_capacity, nullptr,
+                         chunk_queries, metrics, records);
+    });
+}
+
 int wf_session_run_host(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin,
                         uint64_t qid_end, uint64_t* offsets, uint32_t* vertices,
                         uint64_t vertices_capacity, uint8_t* status, uint64_t chunk_queries,
                         wf_run_metrics* metrics) {
     return guarded([&] {
-        require(sh && spec && vertices, "null argument");
-        Session& s = *sh->s;
-        GraphStore& g = *s.g;
-        DeviceGuard guard(g.device);
-        uint64_t n = spec->mode == WF_QUERY_ONE_PER_VERTEX ? g.V : spec->count;
-        if (qid_end == 0) qid_end = n;
-        require(qid_begin <= qid_end && qid_end <= n, "query range out of bounds");
-        if (spec->mode == WF_QUERY_FROM_SOURCE && spec->source >= g.V)
-            config_error("query source " + std::to_string(spec->source) + " is not a vertex (V=" +
-                         std::to_string(g.V) + ")");
-        if (spec->mode == WF_QUERY_FROM_LIST) {
-            require(spec->sources != nullptr || n == 0, "null source list");
-            require(!is_device_pointer(spec->sources), "wf_session_run_host takes a host source list");
-            // sources are range-checked by the walk kernel (ConfigError after the run)
-        }
-        run_to_host(s, *spec, spec->sources, qid_begin, qid_end, offsets, vertices,
-                    vertices_capacity, status, chunk_queries, metrics);
+        run_host_checked(sh, spec, qid_begin, qid_end, offsets, vertices, vertices_capacity, status,
+                         chunk_queries, metrics, nullptr);
     });
 }
 

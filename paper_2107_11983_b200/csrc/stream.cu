@@ -37,6 +37,14 @@ __global__ void k_compact_chunk(const uint32_t* __restrict__ rows, uint32_t stri
     }
 }
 
+// Packed record headers: length | status << 31 (wf_session_run_host_records).
+__global__ void k_pack_records(const uint32_t* __restrict__ lens, const uint8_t* __restrict__ stat, uint64_t n,
+                               uint32_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = lens[i] | (static_cast<uint32_t>(stat[i]) << 31);
+}
+
 __global__ void k_add_base(uint64_t* __restrict__ offs, uint64_t n, uint64_t base) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -56,6 +64,7 @@ struct HostPipe {
     uint32_t cap_stride = 0;
     DeviceBuffer<uint32_t> rows[2], lens[2], stage[2];
     DeviceBuffer<uint8_t> stat[2];
+    DeviceBuffer<uint32_t> packed[2];  // record headers (records mode)
     DeviceBuffer<uint64_t> offs[2];
     DeviceBuffer<uint8_t> scan_tmp;
     size_t scan_bytes = 0;
@@ -102,6 +111,7 @@ struct HostPipe {
             stage[i].allocate(cap_rows * cap_stride);
             lens[i].allocate(cap_rows);
             stat[i].allocate(cap_rows);
+            packed[i].allocate(cap_rows);
             offs[i].allocate(cap_rows + 1);
             WF_CUDA(cudaMemset(offs[i].get(), 0, 8));
         }
@@ -125,7 +135,7 @@ void raise_device_error(const Session& s, int code) {
 
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
-                 uint64_t chunk, wf_run_metrics* metrics) {
+                 uint64_t chunk, wf_run_metrics* metrics, uint32_t* records) {
     GraphStore& g = *s.g;
     DeviceGuard guard(g.device);
     auto t0 = std::chrono::steady_clock::now();
@@ -198,6 +208,11 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
                                                             P.offs[b].get(), nr, P.stage[b].get(),
                                                             P.stage[b].size());
         WF_LAUNCHED();
+        if (records) {
+            k_pack_records<<<std::max(1, static_cast<int>(std::min<uint64_t>((nr + 255) / 256, 4096))), 256, 0, A>>>(
+                P.lens[b].get(), P.stat[b].get(), nr, P.packed[b].get());
+            WF_LAUNCHED();
+        }
         WF_CUDA(cudaMemcpyAsync(P.h_tot + b, P.offs[b].get() + nr, 8, cudaMemcpyDeviceToHost, A));
         WF_CUDA(cudaEventRecord(P.ev_comp[b], A));
     };
@@ -251,6 +266,8 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         }
         if (status)
             WF_CUDA(cudaMemcpyAsync(status + r0, P.stat[b].get(), nr, cudaMemcpyDeviceToHost, B));
+        if (records)
+            WF_CUDA(cudaMemcpyAsync(records + r0, P.packed[b].get(), nr * 4, cudaMemcpyDeviceToHost, B));
         WF_CUDA(cudaEventRecord(P.ev_copy[b], B));
         copy_pending[b] = true;
         trace("copies queued", static_cast<long long>(k));
@@ -274,6 +291,13 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     if (offsets) offsets[n] = chunk_base[nchunks];
     unsigned long long hc[2] = {0, 0};
     WF_CUDA(cudaMemcpy(hc, P.ctr.get(), 16, cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> rec_offs;  // records mode: offsets rebuilt on the host when needed
+    if (hc[1] > 0 && !offsets && records) {
+        rec_offs.resize(n + 1);
+        rec_offs[0] = 0;
+        for (uint64_t r = 0; r < n; ++r) rec_offs[r + 1] = rec_offs[r] + (records[r] & 0x7FFFFFFFu);
+        offsets = rec_offs.data();
+    }
     if (hc[1] > 0) {
         // walks longer than a row: re-run them whole and patch their paths
         if (!offsets) raise(WF_ERR_INVALID_ARG, "offsets are required to place overflowing walks");

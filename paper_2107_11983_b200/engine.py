@@ -304,6 +304,17 @@ class Session:
             _vp(status_ptr or None), C.c_uint64(chunk), C.byref(m)))
         return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
 
+    def run_host_records(self, spec: QuerySpec, records_ptr: int, vertices_ptr: int, capacity: int,
+                         chunk: int = 0, qid_begin: int = 0, qid_end: int = 0) -> RunMetrics:
+        """wf_session_run_host_records: records u32[n] (length | status << 31)
+        and the paths back to back, into HOST buffers (pinned for full bandwidth)."""
+        cs = spec.to_c()
+        m = RunMetricsC()
+        _check(load_library().wf_session_run_host_records(
+            self.h, C.byref(cs), C.c_uint64(qid_begin), C.c_uint64(qid_end), _vp(records_ptr),
+            _vp(vertices_ptr), C.c_uint64(capacity), C.c_uint64(chunk), C.byref(m)))
+        return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
+
     def run_to_numpy(self, spec: QuerySpec, chunk: int = 0) -> RunResult:
         """Convenience over run_host with numpy (pageable) buffers."""
         n = self.graph.vertex_count if spec.mode == abi.QueryMode.ONE_PER_VERTEX else spec.count

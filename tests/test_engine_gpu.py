@@ -487,3 +487,28 @@ def test_run_host_pinned_equals_run(rmat12, prog, chunk, stride):
     # too small a capacity is an error, not an overrun
     with pytest.raises(abi.InvalidArgument):
         sess.run_host(spec, h_off.data_ptr(), h_vert.data_ptr(), total - 1, h_stat.data_ptr(), chunk=chunk)
+
+
+@pytest.mark.parametrize("prog,chunk,stride", [(PprProgram(0.2), 1 << 14, 64), (PprProgram(0.1), 5000, 8),
+                                               (Node2VecProgram(2.0, 0.5, 16, False), 0, 0)])
+def test_run_host_records_equals_run(rmat12, prog, chunk, stride):
+    """wf_session_run_host_records: length | status << 31 per query and the
+    paths back to back — the same walk set, including walks that outgrow their row."""
+    import torch
+    dg, hg = rmat12
+    src = np.random.default_rng(12).integers(0, hg.vertex_count, 1 << 17).astype(np.uint32)
+    spec = QuerySpec.from_list(src)
+    opts = ExecOptions(seed=43, path_stride=stride)
+    whole = E.run_sequential(dg, spec, prog, opts).walks
+    n = src.size
+    total = int(whole.offsets[-1])
+    sess = E.Session(dg, prog, opts)
+    h_rec = torch.zeros(n, dtype=torch.int32).pin_memory()
+    h_vert = torch.zeros(total + 64, dtype=torch.int32).pin_memory()
+    for rep in range(2):
+        m = sess.run_host_records(spec, h_rec.data_ptr(), h_vert.data_ptr(), total + 64, chunk=chunk)
+        rec = h_rec.numpy().view(np.uint32)
+        assert np.array_equal(rec & 0x7FFFFFFF, np.diff(whole.offsets).astype(np.uint32)), rep
+        assert np.array_equal((rec >> 31).astype(np.uint8), whole.status), rep
+        assert np.array_equal(h_vert.numpy()[:total].view(np.uint32), whole.vertices), rep
+        assert m.total_steps == total - n
