@@ -15,8 +15,11 @@
 //     worker threads); k / k' of run_interleaved are validated then ignored.
 #pragma once
 
+#include <cctype>
+#include <charconv>
 #include <cmath>
 #include <cstdint>
+#include <fstream>
 #include <functional>
 #include <memory>
 #include <optional>
@@ -132,6 +135,42 @@ struct QuerySpec {
         s.sources = std::move(sources);
         s.count = s.sources.size();
         return s;
+    }
+    // QuerySpec::from_file (walker.cpp:22-78): `vertex [count]` per line, '#'
+    // starts a comment, blank lines skipped; same messages and error classes.
+    static QuerySpec from_file(const std::string& path) {
+        std::ifstream in(path);
+        if (!in) throw Error("cannot open query file '" + path + "'");
+        std::vector<VertexId> out;
+        std::string line;
+        uint64_t line_no = 0;
+        while (std::getline(in, line)) {
+            ++line_no;
+            std::string_view view(line);
+            if (auto h = view.find('#'); h != std::string_view::npos) view = view.substr(0, h);
+            uint64_t fields[2] = {0, 1};
+            int nf = 0;
+            size_t pos = 0;
+            while (pos < view.size()) {
+                while (pos < view.size() && std::isspace(static_cast<unsigned char>(view[pos]))) ++pos;
+                const size_t start = pos;
+                while (pos < view.size() && !std::isspace(static_cast<unsigned char>(view[pos]))) ++pos;
+                if (pos == start) continue;
+                if (nf >= 2) throw ParseError(path + ":" + std::to_string(line_no) + ": too many columns");
+                const char* b = view.data() + start;
+                const char* e = view.data() + pos;
+                auto [ptr, ec] = std::from_chars(b, e, fields[nf]);
+                if (ec != std::errc() || ptr != e)
+                    throw ParseError(path + ":" + std::to_string(line_no) + ": expected `vertex [count]`");
+                ++nf;
+            }
+            if (nf == 0) continue;
+            if (fields[0] > UINT32_MAX)
+                throw ParseError(path + ":" + std::to_string(line_no) + ": vertex id out of range");
+            for (uint64_t i = 0; i < fields[1]; ++i) out.push_back(static_cast<VertexId>(fields[0]));
+        }
+        if (out.empty()) throw ParseError(path + ": no queries");
+        return from_list(std::move(out));
     }
     uint64_t total(const Graph& g) const {
         return mode == Mode::OnePerVertex ? g.vertex_count() : (mode == Mode::FromSource ? count : sources.size());

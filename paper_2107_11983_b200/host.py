@@ -122,6 +122,38 @@ class QuerySpec:
         return cls(QueryMode.FROM_SOURCE, source=source, count=count)
 
     @classmethod
+    def from_file(cls, path: str) -> "QuerySpec":
+        """QuerySpec::from_file (walker.cpp:22-78): `vertex [count]` per line,
+        '#' comments, blank lines skipped; the reference's messages and classes."""
+        from .abi import ParseError, WalkforgeError
+        try:
+            f = open(path, "r", encoding="utf-8", errors="surrogateescape")
+        except OSError:
+            raise WalkforgeError(f"cannot open query file '{path}'") from None
+        out = []
+        with f:
+            for line_no, line in enumerate(f, 1):
+                line = line.rstrip("\n").split("#", 1)[0]
+                tok = line.split()
+                if not tok:
+                    continue
+                if len(tok) > 2:
+                    raise ParseError(f"{path}:{line_no}: too many columns")
+                vals = []
+                for t in tok:
+                    # std::from_chars on uint64: decimal digits only, no sign, no overflow
+                    if not t.isascii() or not t.isdigit() or int(t) >= 1 << 64:
+                        raise ParseError(f"{path}:{line_no}: expected `vertex [count]`")
+                    vals.append(int(t))
+                v, c = vals[0], (vals[1] if len(vals) == 2 else 1)
+                if v > 0xFFFFFFFF:
+                    raise ParseError(f"{path}:{line_no}: vertex id out of range")
+                out.extend([v] * c)
+        if not out:
+            raise ParseError(f"{path}: no queries")
+        return cls.from_list(np.asarray(out, dtype=np.uint32))
+
+    @classmethod
     def from_list(cls, sources) -> "QuerySpec":
         s = np.ascontiguousarray(sources, dtype=np.uint32)
         return cls(QueryMode.FROM_LIST, count=s.size, sources=s)

@@ -85,5 +85,20 @@ int main(int argc, char** argv) {
     } catch (const ConfigError&) {
         std::printf("naive_static ConfigError\n");
     }
+
+    // QuerySpec::from_file (walker.cpp:22-78) — the reference CLI test's file
+    {
+        const std::string qf = std::string(argv[1]) + ".queries.txt";
+        { std::ofstream(qf) << "# sources\n3 2\n7\n"; }
+        QuerySpec q = QuerySpec::from_file(qf);
+        std::printf("query_file %zu %u %u %u\n", q.sources.size(), q.sources[0], q.sources[1], q.sources[2]);
+        { std::ofstream(qf) << "1 2 3\n"; }
+        try {
+            QuerySpec::from_file(qf);
+        } catch (const ParseError& e) {
+            std::printf("query_file_error ParseError %s\n", e.what() + qf.size());
+        }
+        std::remove(qf.c_str());
+    }
     return 0;
 }
