@@ -23,6 +23,7 @@
 #include <functional>
 #include <memory>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -103,12 +104,117 @@ public:
         check(wf_graph_has_edge(h_.get(), &src, &dst, 1, &out));
         return out != 0;
     }
+    double avg_degree() const { return static_cast<double>(edge_count()) / vertex_count(); }
+
+    // Host-side CSR accessors (graph.hpp:27-71).  The CSR lives in HBM; the
+    // first accessor call downloads one host copy (wf_graph_download), shared
+    // by copies of this Graph.
+    uint64_t edge_begin(VertexId v) const { return host().offsets[v]; }
+    uint32_t degree(VertexId v) const {
+        check_vertex(v);
+        const HostCsr& c = host();
+        return static_cast<uint32_t>(c.offsets[v + 1] - c.offsets[v]);
+    }
+    std::span<const VertexId> neighbors(VertexId v) const {
+        check_vertex(v);
+        const HostCsr& c = host();
+        return {c.neighbors.data() + c.offsets[v], c.neighbors.data() + c.offsets[v + 1]};
+    }
+    VertexId neighbor(uint64_t edge) const { return host().neighbors[edge]; }
+    double weight(uint64_t edge) const {
+        check_edge(edge);
+        if (!has_weights()) throw ConfigError("graph has no edge weights");
+        return host().weights[edge];
+    }
+    uint32_t label(uint64_t edge) const {
+        check_edge(edge);
+        if (!has_labels()) throw ConfigError("graph has no edge labels");
+        return host().labels[edge];
+    }
+    const uint64_t* offsets_data() const { return host().offsets.data(); }
+    const VertexId* neighbors_data() const { return host().neighbors.data(); }
+    const double* weights_data() const { return has_weights() ? host().weights.data() : nullptr; }
+    const uint32_t* labels_data() const { return has_labels() ? host().labels.data() : nullptr; }
+
+    // WFG1 files (graph.cpp:190-277), byte-identical to the reference's.
+    void write_binary(const std::string& path) const { check(wf_graph_write_wfg1(h_.get(), path.c_str())); }
+    static Graph read_binary(const std::string& path, int device = 0) {
+        wf_graph* h = nullptr;
+        check(wf_graph_read_wfg1(path.c_str(), device, &h));
+        return adopt(h);
+    }
+    static Graph adopt(wf_graph* h) {
+        Graph g;
+        g.h_ = std::shared_ptr<wf_graph>(h, wf_graph_destroy);
+        check(wf_graph_info_get(h, &g.info_));
+        return g;
+    }
     wf_graph* handle() const { return h_.get(); }
 
 private:
+    struct HostCsr {
+        std::vector<uint64_t> offsets;
+        std::vector<VertexId> neighbors;
+        std::vector<double> weights;  // widened exactly from the device's f32
+        std::vector<uint32_t> labels;
+    };
+    const HostCsr& host() const {
+        if (!csr_) {
+            auto c = std::make_shared<HostCsr>();
+            c->offsets.resize(vertex_count() + 1ull);
+            c->neighbors.resize(edge_count());
+            std::vector<float> w(has_weights() ? edge_count() : 0);
+            std::vector<uint8_t> l(has_labels() ? edge_count() : 0);
+            check(wf_graph_download(h_.get(), c->offsets.data(), c->neighbors.data(),
+                                    w.empty() ? nullptr : w.data(), l.empty() ? nullptr : l.data()));
+            c->weights.assign(w.begin(), w.end());
+            c->labels.assign(l.begin(), l.end());
+            csr_ = std::move(c);
+        }
+        return *csr_;
+    }
+    void check_vertex(VertexId v) const {  // graph.hpp:87-91
+        if (v >= vertex_count())
+            throw ConfigError("vertex id " + std::to_string(v) + " out of range (V=" +
+                              std::to_string(vertex_count()) + ")");
+    }
+    void check_edge(uint64_t e) const {  // graph.hpp:93-96
+        if (e >= edge_count()) throw ConfigError("edge index " + std::to_string(e) + " out of range");
+    }
     std::shared_ptr<wf_graph> h_;
     wf_graph_info info_{};
+    mutable std::shared_ptr<const HostCsr> csr_;
 };
+
+// ---- load_edge_list (graph.hpp:119-139, graph.cpp:307-453) --------------------------------
+enum class Directedness : uint8_t { Directed, Undirected };
+enum class WeightMode : uint8_t { None, FromFile, Random };
+enum class LabelMode : uint8_t { None, FromFile, Random };
+struct EdgeListOptions {
+    Directedness directedness = Directedness::Directed;
+    WeightMode weights = WeightMode::None;
+    LabelMode labels = LabelMode::None;
+    uint32_t label_count = 5;
+    uint64_t seed = 0;
+};
+struct LoadedGraph {
+    Graph graph;
+    std::vector<uint64_t> original_ids;
+};
+inline LoadedGraph load_edge_list(const std::string& path, const EdgeListOptions& o = {}, int device = 0) {
+    wf_edge_list_options c{};
+    c.undirected = o.directedness == Directedness::Undirected ? 1 : 0;
+    c.weights = static_cast<int32_t>(o.weights);  // None / FromFile / Random map 1:1 (wf_attr_mode)
+    c.labels = static_cast<int32_t>(o.labels);
+    c.label_count = o.label_count;
+    c.seed = o.seed;
+    wf_graph* h = nullptr;
+    check(wf_graph_load_edge_list(path.c_str(), &c, device, &h));
+    LoadedGraph lg{Graph::adopt(h), {}};
+    lg.original_ids.resize(lg.graph.vertex_count());
+    check(wf_graph_original_ids(h, lg.original_ids.data()));
+    return lg;
+}
 
 // ---- walker.hpp:47-84 ------------------------------------------------------------------
 struct WalkRecord {

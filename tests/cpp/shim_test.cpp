@@ -86,6 +86,26 @@ int main(int argc, char** argv) {
         std::printf("naive_static ConfigError\n");
     }
 
+    // Graph accessors (graph.hpp:27-71) against the CSR this program uploaded,
+    // and the WFG1 round trip (graph.cpp:190-277)
+    {
+        bool ok = g.degree(5) == g.neighbors(5).size() && g.edge_begin(5) + g.degree(5) == g.edge_begin(6) &&
+                  g.neighbor(g.edge_begin(5)) == g.neighbors(5)[0] && g.weights_data() != nullptr;
+        const std::string wf = std::string(argv[1]) + ".wfg";
+        g.write_binary(wf);
+        Graph h = Graph::read_binary(wf);
+        ok = ok && h.vertex_count() == g.vertex_count() && h.edge_count() == g.edge_count();
+        for (uint64_t e = 0; ok && e < g.edge_count(); e += 7)
+            ok = h.neighbor(e) == g.neighbor(e) && h.weight(e) == g.weight(e) && h.label(e) == g.label(e);
+        std::remove(wf.c_str());
+        try {
+            g.degree(g.vertex_count());
+            ok = false;
+        } catch (const ConfigError&) {
+        }
+        std::printf("graph_accessors %s\n", ok ? "ok" : "mismatch");
+    }
+
     // QuerySpec::from_file (walker.cpp:22-78) — the reference CLI test's file
     {
         const std::string qf = std::string(argv[1]) + ".queries.txt";
