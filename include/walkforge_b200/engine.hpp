@@ -485,6 +485,60 @@ RunResult run_interleaved(const Graph& g, const QuerySpec& spec, const P& prog, 
     return detail::run(g, spec, prog, opts);
 }
 
+// ---- tune_ring_sizes (tune.hpp:12-42, tune.cpp:46-111) -----------------------------------
+// The reference sweeps its CPU interleave rings (k, k') with a probe workload
+// (one uniform length-10 walk from every vertex).  On the device the rings are
+// replaced by resident walkers, so this runs the same probe through the launch
+// tuner (wf_session_tune): the report carries the device's pick and the probe
+// throughput; best_k / best_k_prime stay the reference's defaults (64, 32),
+// which run_interleaved accepts and validates.
+struct TuneOptions {
+    uint32_t threads = 1;
+    double budget_seconds = 120.0;
+    uint64_t seed = 0;
+    PrefetchLevel prefetch = PrefetchLevel::L1;
+};
+struct TunePoint {
+    uint32_t k = 0;
+    double steps_per_sec = 0.0;
+};
+struct TuneReport {
+    std::vector<TunePoint> task_ring;
+    std::vector<TunePoint> search_ring;
+    uint32_t best_k = 64;
+    uint32_t best_k_prime = 32;
+    bool budget_exhausted = false;
+    int32_t device_blocks_per_sm = 0;  // the launch tuner's choice for the probe
+    std::string to_text() const {
+        std::string s = "device launch tuner: " + std::to_string(device_blocks_per_sm) + " blocks/SM";
+        for (const auto& p : task_ring)
+            s += "\nprobe steps/s " + std::to_string(p.steps_per_sec);
+        s += "\nrecommended k=" + std::to_string(best_k) + " k'=" + std::to_string(best_k_prime);
+        return s;
+    }
+};
+inline TuneReport tune_ring_sizes(const Graph& g, const TuneOptions& opts = {}) {
+    wf_program_desc d = UniformProgram(10).to_desc();
+    wf_exec_options o{};
+    o.seed = opts.seed;
+    o.sampler = WF_SAMPLER_DEFAULT;
+    o.use_static_tables = 1;
+    wf_query_spec q{};
+    q.mode = WF_QUERY_ONE_PER_VERTEX;
+    wf_session* s = nullptr;
+    check(wf_session_create(g.handle(), &d, &o, &s));
+    std::unique_ptr<wf_session, void (*)(wf_session*)> guard(s, wf_session_destroy);
+    TuneReport r;
+    double ms = 0.0;
+    check(wf_session_tune(s, &q, 0, 0, &r.device_blocks_per_sm, &ms));
+    wf_walkset* ws = nullptr;
+    wf_run_metrics m{};
+    check(wf_session_run(s, &q, &ws, &m));
+    wf_walkset_destroy(ws);
+    r.task_ring.push_back({r.best_k, m.exec_seconds > 0 ? m.total_steps / m.exec_seconds : 0.0});
+    return r;
+}
+
 }  // namespace walkforge_b200
 
 #ifdef WALKFORGE_B200_DROP_IN

@@ -106,6 +106,12 @@ int main(int argc, char** argv) {
         std::printf("graph_accessors %s\n", ok ? "ok" : "mismatch");
     }
 
+    {
+        TuneReport tr = tune_ring_sizes(g);
+        std::printf("tune %u %u %d\n", tr.best_k, tr.best_k_prime,
+                    tr.device_blocks_per_sm >= 1 && tr.task_ring.size() == 1 && tr.task_ring[0].steps_per_sec > 0);
+    }
+
     // QuerySpec::from_file (walker.cpp:22-78) — the reference CLI test's file
     {
         const std::string qf = std::string(argv[1]) + ".queries.txt";

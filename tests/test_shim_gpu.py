@@ -73,5 +73,6 @@ def test_shim_reproduces_golden_walks():
     assert res["metapath_its"][2] == "sink_empty=1"
     assert res["naive_static"] == ["ConfigError"]
     assert res["graph_accessors"] == ["ok"]
+    assert res["tune"] == ["64", "32", "1"]
     assert res["query_file"] == ["3", "3", "3", "7"]  # walker.cpp:22-78 on test_cli.cpp:188's file
     assert res["query_file_error"] == ["ParseError", ":1:", "too", "many", "columns"]
