@@ -5,6 +5,7 @@
 // tests/test_shim_gpu.py to compare with the golden fixtures.
 #define WALKFORGE_B200_DROP_IN
 #include "walkforge_b200/engine.hpp"
+#include "walkforge_b200/output.hpp"
 
 #include <cstdio>
 #include <fstream>
@@ -104,6 +105,30 @@ int main(int argc, char** argv) {
         } catch (const ConfigError&) {
         }
         std::printf("graph_accessors %s\n", ok ? "ok" : "mismatch");
+    }
+
+    // output.hpp: the reference CLI's writer pattern (BlockSink -> ordered
+    // sink -> double-buffered writer), text and binary, from the DeepWalk run
+    for (int fmt = 0; fmt < 2; ++fmt) {
+        const std::string of = std::string(argv[1]) + (fmt ? ".walks.bin" : ".walks.txt");
+        DoubleBufferedWriter w(of, fmt ? OutputFormat::Binary : OutputFormat::Text, kMinOutputBuffer);
+        OrderedBlockSink sink(w, 2);
+        ExecOptions wo = eo;
+        wo.sink = [&](uint32_t, WalkSet&& ws) {
+            // split into two worker blocks pushed out of order
+            WalkSet first(ws.begin(), ws.begin() + ws.size() / 2), second(ws.begin() + ws.size() / 2, ws.end());
+            sink.push(1, std::move(second));
+            sink.push(0, std::move(first));
+        };
+        run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 20, true), wo);
+        sink.finish();
+        w.finish();
+        std::printf("written_%s %s\n", fmt ? "bin" : "txt", of.c_str());
+    }
+    try {
+        DoubleBufferedWriter bad("/nonexistent_dir/x.txt", OutputFormat::Text);
+    } catch (const IoError&) {
+        std::printf("writer_open IoError\n");
     }
 
     {

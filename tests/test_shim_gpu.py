@@ -62,7 +62,13 @@ def test_shim_reproduces_golden_walks():
             f.write(g.weights.tobytes())
             f.write(g.labels.astype(np.uint32).tobytes())
         out = subprocess.check_output([exe, path], text=True).splitlines()
-    res = {l.split()[0]: l.split()[1:] for l in out}
+        res = {l.split()[0]: l.split()[1:] for l in out}
+        # output.hpp's writer + ordered sink: the reference's record bytes
+        # (wf_encode_walks is pinned byte-identical to output.cpp elsewhere)
+        dw = gu.walks({c["name"]: c for c in gu.cases()}["pl_deepwalk_w_alias"])
+        for key, fmt in [("written_txt", 0), ("written_bin", 1)]:
+            with open(res[key][0], "rb") as f:
+                assert f.read() == E.encode_walks(dw, fmt), key
     cases = {c["name"]: c for c in gu.cases()}
     for key, case in [("deepwalk_alias", "pl_deepwalk_w_alias"),
                       ("node2vec_orej", "pl_node2vec_w_orej"),
@@ -74,5 +80,6 @@ def test_shim_reproduces_golden_walks():
     assert res["naive_static"] == ["ConfigError"]
     assert res["graph_accessors"] == ["ok"]
     assert res["tune"] == ["64", "32", "1"]
+    assert res["writer_open"] == ["IoError"]
     assert res["query_file"] == ["3", "3", "3", "7"]  # walker.cpp:22-78 on test_cli.cpp:188's file
     assert res["query_file_error"] == ["ParseError", ":1:", "too", "many", "columns"]
