@@ -171,7 +171,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def s_alg_bytes(cfg, stats, moves, layout):
+def s_alg_bytes(cfg, stats, moves, layout, walks=0):
     """Algorithmic 32 B sectors per move (SURVEY §8 d) for the layout the
     session actually uses (abi.HAS_*), plus the random requests per move.
 
@@ -181,7 +181,9 @@ def s_alg_bytes(cfg, stats, moves, layout):
     successor-decorated partitioned edge = 1, else 32 B label record +
     neighbour = 2.  Node2Vec O-REJ: one adjacency sector per trial + the
     instrumented search probes (+1 vertex word without the decorated
-    adjacency).  Every move also writes 4 B of path = 1/8 sector."""
+    adjacency).  Every move also writes 4 B of path = 1/8 sector.  PPR's
+    visit counts add one 4 B read-modify-write (one sector request) per
+    emitted vertex: (moves + walks) / moves per move."""
     from paper_2107_11983_b200 import abi
     p = cfg["program"]
     one = {"deepwalk": abi.HAS_WIDE_ALIAS, "ppr": abi.HAS_ADJ, "metapath": abi.HAS_MP_SUCC}
@@ -195,6 +197,10 @@ def s_alg_bytes(cfg, stats, moves, layout):
             desc = {"deepwalk": "16 B alias bucket + 8 B vertex word",
                     "ppr": "4 B neighbour + 8 B vertex word",
                     "metapath": "32 B label record + 4 B partitioned neighbour"}[p]
+        if p == "ppr" and walks:
+            cnt = (moves + walks) / max(moves, 1)
+            text = f"{desc} + {cnt:.3f} visit-count sectors + 1/8 path = {reads + cnt + 0.125:.3f} sectors"
+            return (reads + cnt + 0.125) * SECTOR, text, reads + cnt
         text = f"{desc} + 1/8 path = {reads + 0.125:.3f} sectors"
     else:
         trials = stats["trials"] / max(moves, 1)
@@ -561,7 +567,7 @@ def main():
     value = all_moves * args.steps / (total_ms * 1e-3)
 
     peak, peak_kind = measured_peak()
-    b, b_desc, reads = s_alg_bytes(cfg, r["stats"], moves, r["layout"])
+    b, b_desc, reads = s_alg_bytes(cfg, r["stats"], moves, r["layout"], walks=r["n"])
     mean_launch_s = total_ms / args.steps * 1e-3
     achieved = moves * b / mean_launch_s / 1e9
     traffic = None
