@@ -512,3 +512,24 @@ def test_run_host_records_equals_run(rmat12, prog, chunk, stride):
         assert np.array_equal((rec >> 31).astype(np.uint8), whole.status), rep
         assert np.array_equal(h_vert.numpy()[:total].view(np.uint32), whole.vertices), rep
         assert m.total_steps == total - n
+
+
+def test_degenerate_inputs_match_reference():
+    """Edgeless graphs, a single vertex, and empty query sets."""
+    from paper_2107_11983_b200.host import Graph
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefOracle()
+    for V in [1, 4]:
+        hg = Graph(np.zeros(V + 1, np.uint64), np.zeros(0, np.uint32))
+        dg = E.DeviceGraph.from_host(hg)
+        rg = ref.graph(hg)
+        for prog in [PprProgram(0.2), DeepWalkProgram(9, False), UniformProgram(5),
+                     Node2VecProgram(2.0, 0.5, 7, False)]:
+            for spec in [QuerySpec.one_per_vertex(), QuerySpec.from_source(V - 1, 6),
+                         QuerySpec.from_source(0, 0)]:
+                opts = ExecOptions(seed=2)
+                got = E.run_sequential(dg, spec, prog, opts)
+                want = rg.run(spec, prog, opts)
+                assert got.walks.equals(want.walks), (V, prog, spec.mode)
+                assert got.metrics.total_steps == want.metrics.total_steps == 0
