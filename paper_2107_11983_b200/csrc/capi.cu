@@ -694,8 +694,10 @@ int wf_session_tune(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begi
         s.tuned_blocks.erase(bucket);
         const int max_per_sm = std::max(1, s.grid / sm_count(g.device));
         std::vector<int> cands;
-        for (int c : {max_per_sm, max_per_sm * 3 / 4, max_per_sm / 2, max_per_sm * 3 / 8, max_per_sm / 4})
-            if (c >= 1 && std::find(cands.begin(), cands.end(), c) == cands.end()) cands.push_back(c);
+        // every count from the occupancy maximum down to a quarter of it (at
+        // least 2 candidates below the maximum)
+        const int lowest = std::max(1, std::min(max_per_sm / 4, max_per_sm - 2));
+        for (int c = max_per_sm; c >= lowest; --c) cands.push_back(c);
         cudaEvent_t e0, e1;
         WF_CUDA(cudaEventCreate(&e0));
         WF_CUDA(cudaEventCreate(&e1));
