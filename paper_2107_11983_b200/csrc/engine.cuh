@@ -20,7 +20,10 @@ namespace wf {
 
 constexpr uint32_t kDegBits = 24;
 constexpr uint32_t kDegEscape = (1u << kDegBits) - 1;  // degree >= this: read offsets
-constexpr int kBlock = 256;
+#ifndef WF_BLOCK
+#define WF_BLOCK 256
+#endif
+constexpr int kBlock = WF_BLOCK;  // walk kernel threads per block
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kMaxIndexedLabels = 6;  // 32 B label record: u64 base + 6 u32 group ends
 
@@ -881,7 +884,8 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
 // Register bound: 8 x 256 threads per SM (<= 32 registers) for the flows whose
 // state fits it; the launch tuner (wf_session_tune) may run fewer blocks.  The
 // gathered flows (per-step scans, on-the-fly Vose) keep their registers.
-// Build knobs (experiments only): WF_N2V_BLOCKS, WF_CLAIM.
+// Build knobs (experiments only): WF_BLOCK, WF_MIN_BLOCKS, WF_N2V_BLOCKS,
+// WF_CLAIM (128-thread blocks measured the same as 256).
 template <int K, int S, int F>
 constexpr int walk_min_blocks() {
     // Node2Vec's O-REJ step (edge hash probe) needs ~48 registers without
