@@ -108,6 +108,23 @@ struct WalkLaunch {
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
     const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
     const uint4* __restrict__ mp_adj; // MetaPath: per partitioned edge {dst, 0, next-group word} or null
+    // Host streaming (run_to_host; all null otherwise).  Rows are grouped in
+    // tiles of 2^tile_shift and chunks of 2^chunk_tiles_shift tiles.  Finished
+    // rows report to their tile's word (rows << 40 | vertices); the report
+    // that completes a tile adds it to its chunk's word (tiles << 40 |
+    // vertices), and the one that completes a chunk publishes the chunk's
+    // vertex total + 1 to host-mapped chunk_flag[chunk].
+    unsigned long long* tile_word;
+    unsigned long long* chunk_word;
+    unsigned long long* chunk_flag;
+    uint32_t tile_shift;
+    uint32_t chunk_tiles_shift;
+    // FROM_LIST sources arriving while the kernel runs: src_ready counts the
+    // resident 2^src_shift-row blocks of the source list (written by the copy
+    // stream behind each block's copy); null = all resident at launch
+    const unsigned int* src_ready;
+    uint32_t src_shift;
+    uint64_t src_row0;  // rows of the list before this launch's first row
 };
 
 struct Walker {
@@ -813,9 +830,17 @@ __device__ __forceinline__ unsigned long long start_word(const WalkLaunch& L, ui
     return ldr(L.sview + src);
 }
 
+template <bool ST>
 __device__ __forceinline__ uint32_t source_at(const WalkLaunch& L, uint64_t qid) {  // walker.hpp:70-77
     if (L.qmode == WF_QUERY_ONE_PER_VERTEX) return static_cast<uint32_t>(qid);
     if (L.qmode == WF_QUERY_FROM_SOURCE) return L.qsource;
+    if constexpr (ST) {
+        // L2 only, ordered after wait_sources: the list lands while the
+        // kernel runs
+        uint32_t v;
+        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(L.qsources + qid) : "memory");
+        return v;
+    }
     return __ldg(L.qsources + qid);
 }
 
@@ -857,6 +882,62 @@ __device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int
         if (g0 < min(q.len, L.stride)) store_group(L.paths + q.row * L.stride + g0, ps);
     }
     if (q.len > L.stride) atomicAdd(L.overflow_out, 1ULL);
+}
+
+// Host streaming: `rows` finished rows of tile `tile` carrying `verts`
+// vertices (one call per tile per warp iteration).  Callers have fenced their
+// row / length / status stores, so a published chunk is complete in memory
+// for the compaction kernel the host queues on seeing its flag.
+constexpr int kCountShift = 40;
+constexpr unsigned long long kSumMask = (1ull << kCountShift) - 1;
+static __device__ __noinline__ void stream_report(unsigned long long* tile_word, unsigned long long* chunk_word,
+                                           unsigned long long* chunk_flag, uint64_t n_rows,
+                                           uint32_t shifts, uint32_t tile, uint32_t rows, uint32_t verts) {
+    const uint32_t tile_shift = shifts & 0xFF, chunk_tiles_shift = shifts >> 8;
+    const unsigned long long add = (static_cast<unsigned long long>(rows) << kCountShift) | verts;
+    const unsigned long long now = atomicAdd(tile_word + tile, add) + add;
+    const uint64_t t0 = static_cast<uint64_t>(tile) << tile_shift;
+    const uint64_t tile_rows = min(static_cast<uint64_t>(1) << tile_shift, n_rows - t0);
+    if ((now >> kCountShift) != tile_rows) return;
+    // this report completed the tile: add it to its chunk
+    __threadfence();
+    const uint32_t chunk = tile >> chunk_tiles_shift;
+    const uint64_t ntiles = (n_rows + (1ull << tile_shift) - 1) >> tile_shift;
+    const uint64_t c0 = static_cast<uint64_t>(chunk) << chunk_tiles_shift;
+    const uint64_t chunk_tiles = min(static_cast<uint64_t>(1) << chunk_tiles_shift, ntiles - c0);
+    const unsigned long long cadd = (1ull << kCountShift) | (now & kSumMask);
+    const unsigned long long cnow = atomicAdd(chunk_word + chunk, cadd) + cadd;
+    if ((cnow >> kCountShift) != chunk_tiles) return;
+    // ... and the chunk: publish its vertex total to the host
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(chunk_flag + chunk), "l"((cnow & kSumMask) + 1)
+                 : "memory");
+}
+__device__ __forceinline__ void stream_report(const WalkLaunch& L, uint32_t tile, uint32_t rows, uint32_t verts) {
+    stream_report(L.tile_word, L.chunk_word, L.chunk_flag, L.n_rows, L.tile_shift | (L.chunk_tiles_shift << 8),
+                  tile, rows, verts);
+}
+
+// Host streaming: wait until the source list holds rows [0, need) (the copy
+// stream writes src_ready behind each block's copy).  Bounded: a copy that
+// never lands raises a device error instead of hanging the GPU.
+// Returns the rows known resident.
+static __device__ __noinline__ uint64_t wait_sources(const unsigned int* src_ready, uint32_t src_shift, int* error_word,
+                                              uint64_t need) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned int r;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(src_ready) : "memory");
+        const uint64_t have = static_cast<uint64_t>(r) << src_shift;
+        if (have >= need) return have;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10000000000ull) {  // 10 s
+            atomicCAS(error_word, 0, WF_ERR_CUDA);
+            return ~0ull;
+        }
+        __nanosleep(200);
+    }
 }
 
 __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint32_t p, uint32_t v,
@@ -910,7 +991,12 @@ constexpr int walk_min_blocks() {
 #endif
 constexpr uint32_t kClaim = WF_CLAIM;
 
-template <int K, int S, int F>
+// ST: the host-streaming instantiation (run_to_host): the source list may
+// land during the run (src_ready) and, when tile_word is set, finished rows
+// report to their tile / chunk words.
+// A separate instantiation keeps the device-output kernels' registers as they
+// were (the reports cost ~10 registers, which would cost C3/C5 a block/SM).
+template <int K, int S, int F, bool ST>
 __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kernel(const WalkLaunch L) {
     using P = Program<K>;
     const int lane = threadIdx.x & 31;
@@ -949,10 +1035,13 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
     // atomic whose round trip was the refill's top stall (ncu, C2); the rest
     // is claimed through the cursor for balance.
     __shared__ uint32_t claim_k[kBlock / 32];
+    // host streaming: source rows this warp has seen resident
+    __shared__ unsigned long long src_seen[kBlock / 32];
     if (lane == 0) {
         claim_next[wid] = 0;
         claim_left[wid] = 0;
         claim_k[wid] = 0;
+        src_seen[wid] = 0;
     }
     __syncwarp();
     unsigned long long steps = 0;
@@ -990,12 +1079,20 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     drained = drained || !active;
                     continue;
                 }
+                if (ST && L.src_ready && wnext + wleft > src_seen[wid]) {
+                    if (lane == 0) {
+                        const uint64_t have =
+                            wait_sources(L.src_ready, L.src_shift, L.error_word, L.src_row0 + wnext + wleft);
+                        src_seen[wid] = have == ~0ull ? have : have - L.src_row0;
+                    }
+                    __syncwarp();
+                }
                 {
                     uint32_t src = 0;
                     unsigned long long word = 0;
                     if (static_cast<uint32_t>(lane) < wleft) {
                         const uint64_t qid = L.qid_map ? __ldg(L.qid_map + wnext + lane) : L.qid_begin + wnext + lane;
-                        src = source_at(L, qid);
+                        src = source_at<ST>(L, qid);
                         if (src < L.g.V) word = start_word<K, S, F>(L, src);
                     }
                     claim_src[wid][lane] = src;
@@ -1032,6 +1129,10 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     q.len = 1;
                     if (P::prechecked && P::finished(L.prog, q)) {
                         finish(L, q, WF_WALK_COMPLETE, ps);  // walk_already_finished, program.hpp:86-93
+                        if (ST && L.tile_word) {
+                            __threadfence();
+                            stream_report(L, static_cast<uint32_t>(row >> L.tile_shift), 1, 1);
+                        }
                     } else {
                         const unsigned long long w = claim_word[wid][slot];
                         active = true;
@@ -1095,6 +1196,31 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
             } else {
                 finish(L, q, WF_WALK_DEAD_END, ps);
                 active = false;
+            }
+        }
+        if (ST && L.tile_word) {
+            // host streaming: the rows finished this iteration report to their
+            // tiles, one atomic per tile per warp
+            const bool f = ready && !active;
+            unsigned fm = __ballot_sync(kFull, f);
+            if (fm) {
+                // the finished rows' stores are ordered before each leader's
+                // release (warp barrier, then a release fence: cumulative over
+                // what the barrier made it observe)
+                __syncwarp();
+                const uint32_t tile = static_cast<uint32_t>(q.row >> L.tile_shift);
+                do {  // usually one round: a warp's rows come from one or two tiles
+                    const int leader = __ffs(fm) - 1;
+                    const uint32_t lt = __shfl_sync(kFull, tile, leader);
+                    const bool mine = f && tile == lt;
+                    const unsigned grp = __ballot_sync(kFull, mine);
+                    const uint32_t verts = __reduce_add_sync(kFull, mine ? q.len : 0u);
+                    if (lane == leader) {
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        stream_report(L, lt, __popc(grp), verts);
+                    }
+                    fm &= ~grp;
+                } while (fm);
             }
         }
     }

@@ -149,12 +149,24 @@ struct WalkSetStore {
     uint32_t max_length = 0;
 };
 
+// Host streaming of a launch (run_to_host): see WalkLaunch's fields.
+struct StreamLaunch {
+    unsigned long long* tile_word = nullptr;   // device, per tile, zeroed
+    unsigned long long* chunk_word = nullptr;  // device, per chunk, zeroed
+    unsigned long long* chunk_flag = nullptr;  // host-mapped, per chunk, zeroed
+    uint32_t tile_shift = 10;
+    uint32_t chunk_tiles_shift = 6;
+    const unsigned int* src_ready = nullptr;  // device, or null
+    uint32_t src_shift = 16;
+    uint64_t src_row0 = 0;  // rows of the list (src_ready's count) before the launch's first row
+};
+
 // walk.cu
 void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sources,
                  uint64_t qid_begin, uint64_t qid_end, const uint64_t* qid_map, uint32_t* paths,
                  uint32_t stride, uint32_t* lengths, uint8_t* status, uint32_t* visit_counts,
                  unsigned long long* steps_out, unsigned long long* overflow_out,
-                 unsigned long long* cursor, cudaStream_t st);
+                 unsigned long long* cursor, cudaStream_t st, const StreamLaunch* stream = nullptr);
 int occupancy_grid(const Session& s);
 int row_bucket(uint64_t n_rows);  // tuner key: ceil(log2(rows))
 

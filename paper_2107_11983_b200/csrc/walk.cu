@@ -5,51 +5,22 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <tuple>
 
+#include "kernel_table.cuh"
 #include "runtime.hpp"
 
 namespace wf {
 
-using KernelFn = void (*)(const WalkLaunch);
-
 namespace {
 
-template <int K, int S, int F>
-constexpr KernelFn kfn() {
-    return &walk_kernel<K, S, F>;
-}
-
-// Every program × sampler × flow the reference accepts.
+// Every program x sampler x flow the reference accepts; the host-streaming
+// instantiations live in walk_stream.cu (compiled in parallel).
 KernelFn select_kernel(int prog, int sampler, int flow) {
 #define WF_CASE(P, S, F) \
-    if (prog == P && sampler == S && flow == F) return kfn<P, S, F>();
-#define WF_UNBIASED(P)                                             \
-    WF_CASE(P, WF_SAMPLER_NAIVE, kDirect)                          \
-    WF_CASE(P, WF_SAMPLER_OREJ, kDirect)                           \
-    WF_CASE(P, WF_SAMPLER_ITS, kTables)                            \
-    WF_CASE(P, WF_SAMPLER_ALIAS, kTables)                          \
-    WF_CASE(P, WF_SAMPLER_REJ, kTables)                            \
-    WF_CASE(P, WF_SAMPLER_ITS, kGathered)                          \
-    WF_CASE(P, WF_SAMPLER_ALIAS, kGathered)                        \
-    WF_CASE(P, WF_SAMPLER_REJ, kGathered)
-    WF_UNBIASED(WF_PROGRAM_PPR)
-    WF_UNBIASED(WF_PROGRAM_UNIFORM)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_OREJ, kDirect)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ITS, kTables)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ALIAS, kTables)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_REJ, kTables)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ITS, kGathered)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_ALIAS, kGathered)
-    WF_CASE(WF_PROGRAM_DEEPWALK, WF_SAMPLER_REJ, kGathered)
-    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_OREJ, kDirect)
-    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_ITS, kGathered)
-    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_ALIAS, kGathered)
-    WF_CASE(WF_PROGRAM_NODE2VEC, WF_SAMPLER_REJ, kGathered)
-    WF_CASE(WF_PROGRAM_METAPATH, WF_SAMPLER_ITS, kGathered)
-    WF_CASE(WF_PROGRAM_METAPATH, WF_SAMPLER_ALIAS, kGathered)
-    WF_CASE(WF_PROGRAM_METAPATH, WF_SAMPLER_REJ, kGathered)
-#undef WF_UNBIASED
+    if (prog == P && sampler == S && flow == F) return &walk_kernel<P, S, F, false>;
+    WF_FOR_EACH_COMBO(WF_CASE)
 #undef WF_CASE
     config_error("no kernel for this program/sampler/flow combination");
 }
@@ -73,11 +44,12 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
                  uint64_t qid_begin, uint64_t qid_end, const uint64_t* qid_map, uint32_t* paths,
                  uint32_t stride, uint32_t* lengths, uint8_t* status, uint32_t* visit_counts,
                  unsigned long long* steps_out, unsigned long long* overflow_out,
-                 unsigned long long* cursor, cudaStream_t st) {
+                 unsigned long long* cursor, cudaStream_t st, const StreamLaunch* stream) {
     GraphStore& g = *s.g;
     if (qid_end <= qid_begin) return;
     if (stride == 0) config_error("path stride must be >= 1");
-    KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
+    KernelFn fn = stream ? select_stream_kernel(s.desc.kind, s.kind, s.flow)
+                         : select_kernel(s.desc.kind, s.kind, s.flow);
     WalkLaunch L{};
     L.g = g.view();
     if (!s.use_edge_hash) L.g.ehash = nullptr;  // per-session choice (B-tree opt-in)
@@ -110,6 +82,16 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.alias_wide = s.alias_wide ? 1 : 0;
     L.adj = s.adj.get();
     L.mp_adj = s.mp_adj.get();
+    if (stream) {
+        L.tile_word = stream->tile_word;
+        L.chunk_word = stream->chunk_word;
+        L.chunk_flag = stream->chunk_flag;
+        L.tile_shift = stream->tile_shift;
+        L.chunk_tiles_shift = stream->chunk_tiles_shift;
+        L.src_ready = stream->src_ready;
+        L.src_shift = stream->src_shift;
+        L.src_row0 = stream->src_row0;
+    }
     int grid = s.grid > 0 ? s.grid : occupancy_grid(s);
     if (!s.tuned_blocks.empty()) {
         // wf_session_tune's pick for the nearest tuned launch size (row buckets
@@ -125,6 +107,27 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
             }
         }
         if (best > 0 && dist <= 3) grid = best * sm_count(g.device);
+    }
+    if (stream && stream->tile_word) {
+        // host streaming: leave two compaction blocks' registers (128 threads
+        // x 32 each) free on every SM, so the chunk compactions run beside the
+        // walk kernel instead of after it
+        static std::mutex mu;
+        static std::map<KernelFn, int> regs;  // cudaFuncGetAttributes costs the host a few us
+        int nregs;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            auto it = regs.find(fn);
+            if (it == regs.end()) {
+                cudaFuncAttributes fa{};
+                WF_CUDA(cudaFuncGetAttributes(&fa, fn));
+                it = regs.emplace(fn, fa.numRegs).first;
+            }
+            nregs = it->second;
+        }
+        const int per_block = ((nregs + 7) / 8 * 8) * kBlock;
+        const int fit = std::max(1, (65536 - 8192) / std::max(per_block, 1));
+        grid = std::min(grid, fit * sm_count(g.device));
     }
     uint64_t lanes_needed = (L.n_rows + 31) / 32 * 32;
     int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));

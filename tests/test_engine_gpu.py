@@ -400,6 +400,36 @@ def test_run_host_streaming_equals_run(rmat12, prog, chunk, nsrc):
     assert np.array_equal(st, whole.status[lo:hi])
 
 
+@pytest.mark.parametrize("mode", ["whole", "chunks"])
+@pytest.mark.parametrize("stage_bytes", [None, 3 << 17])
+def test_run_host_modes_and_segments(rmat12, monkeypatch, mode, stage_bytes):
+    """Both host-streaming modes (whole-launch publication for short walks,
+    in-kernel chunk reports for long ones) give every program's exact walk
+    set, also when a small staging budget splits the run into several
+    launches (segments) and the chunks into batches."""
+    dg, hg = rmat12
+    monkeypatch.setenv("WF_STREAM_MODE", mode)
+    if stage_bytes:
+        monkeypatch.setenv("WF_STREAM_STAGE_BYTES", str(stage_bytes))
+    src = np.random.default_rng(21).integers(0, hg.vertex_count, 30000).astype(np.uint32)
+    spec = QuerySpec.from_list(src)
+    for prog, chunk in [(PprProgram(0.2), 1 << 10), (DeepWalkProgram(20, True), 0),
+                        (Node2VecProgram(2.0, 0.5, 12, False), 1 << 12), (UniformProgram(9), 100),
+                        (MetaPathProgram([i % 5 for i in range(10)]), 1 << 11)]:
+        opts = ExecOptions(seed=29, path_stride=16)
+        whole = E.run_sequential(dg, spec, prog, opts).walks
+        sess = E.Session(dg, prog, opts)
+        res = sess.run_to_numpy(spec, chunk=chunk)
+        assert res.walks.equals(whole), (type(prog).__name__, mode, stage_bytes)
+        n, total = src.size, int(whole.offsets[-1])
+        rec = np.zeros(n, np.uint32)
+        verts = np.zeros(total, np.uint32)
+        sess.run_host_records(spec, rec.ctypes.data, verts.ctypes.data, total, chunk=chunk)
+        assert np.array_equal(rec & 0x7FFFFFFF, np.diff(whole.offsets).astype(np.uint32))
+        assert np.array_equal((rec >> 31).astype(np.uint8), whole.status)
+        assert np.array_equal(verts, whole.vertices)
+
+
 def test_launch_tuner_keeps_results(rmat12):
     """wf_session_tune only changes the grid: walks are identical before and after."""
     import torch
