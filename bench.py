@@ -428,6 +428,27 @@ def cpu_baseline(key, cfg, dg, spec, threads=None):
                        f"no-op sink, one warm-up run")
 
 
+def ncu_traffic():
+    """profiles/ncu_traffic.json: DRAM bytes (read + write) per walk-kernel launch
+    and per move, from ncu captures of each config at its tuned grid."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def measured_sectors_block(key, moves_per_s, peak):
+    """BASELINE's roofline: HBM bandwidth / measured DRAM bytes per step (ncu,
+    cold cache; every random 32 B request that misses L2 costs a 128 B line)."""
+    bpm = ncu_traffic().get(f"{key}_bytes_per_move")
+    if not bpm:
+        return None
+    ceiling = peak / bpm * 1e9
+    return {"bytes_per_move": bpm, "ceiling_steps_per_s": ceiling, "frac": moves_per_s / ceiling,
+            "source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
+
+
 def extras(args, rank, world, local_rank, dist):
     """GPU-only numbers for the other configs (not bench lines; evidence)."""
     out = {}
@@ -445,6 +466,7 @@ def extras(args, rank, world, local_rank, dist):
             out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=rate, blocks_per_sm=r["tuned"],
                             ms_per_step=ms, moves=r["moves"], achieved_gbs=ach,
                             roofline_frac=ach / peak, bytes_per_move=b, bytes_model=bdesc,
+                            measured_sectors=measured_sectors_block(key, rate, peak),
                             random_access=random_access_block(rate, reads),
                             E=r["info"]["E"])
             del r
@@ -570,12 +592,7 @@ def main():
     b, b_desc, reads = s_alg_bytes(cfg, r["stats"], moves, r["layout"], walks=r["n"])
     mean_launch_s = total_ms / args.steps * 1e-3
     achieved = moves * b / mean_launch_s / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(args.config)
-    except Exception:
-        pass
+    traffic = ncu_traffic().get(args.config)
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

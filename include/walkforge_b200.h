@@ -270,9 +270,12 @@ int wf_session_sync(wf_session* s, void* stream);
  *   offsets  u64[n+1]   path of query i = vertices[offsets[i] .. offsets[i+1])
  *   vertices u32[vertices_capacity]
  *   status   u8[n]
- * Queries run in chunks of `chunk_queries` (0 = auto); chunk k's walks are
- * compacted and copied to the host while chunk k+1 runs.  Pinned host memory
- * gives full copy bandwidth.  A FROM_LIST spec takes a HOST source list.
+ * One persistent launch covers the queries (several for very large runs);
+ * completed chunks of `chunk_queries` rows (0 = auto, 64 Ki; rounded up to a
+ * power of two) are compacted and copied to the host while the rest still
+ * run.  Pinned host memory gives full copy bandwidth, and a pinned source
+ * list is streamed in while the kernel starts.  A FROM_LIST spec takes a HOST
+ * source list.
  * Only queries [qid_begin, qid_end) run (qid_end 0 = all; a shard of a
  * multi-GPU job); outputs are indexed relative to qid_begin.
  * WF_ERR_INVALID_ARG if the walks need more than vertices_capacity entries. */

@@ -67,6 +67,8 @@ def main():
         with torch.cuda.graph(graph):
             launch()
         torch.cuda.synchronize()
+    # ncu --nvtx --nvtx-include "timed/" captures only these launches (not the tuner's)
+    torch.cuda.nvtx.range_push("timed")
     for i in range(args.launches):
         steps.zero_()
         if l2buf is not None:
@@ -101,6 +103,8 @@ def main():
                 if sel.any():
                     print(f"  length [{lo},{hi}): n={sel.sum()} mean finish {t[sel].mean():.1f} us, "
                           f"max {t[sel].max():.1f} us")
+
+    torch.cuda.nvtx.range_pop()
 
 
 if __name__ == "__main__":
