@@ -194,7 +194,7 @@ struct HostPipe {
     cudaStream_t c = nullptr;  // host -> device source copies
     cudaStream_t d = nullptr;  // chunk compaction
     std::vector<cudaEvent_t> ev_chunk;  // chunk k compacted
-    cudaEvent_t ev_src0 = nullptr, ev_walk = nullptr, ev_compact = nullptr, ev_copy = nullptr;
+    cudaEvent_t ev_src0 = nullptr, ev_walk = nullptr, ev_copy = nullptr;
     cudaEvent_t ev_trace_src = nullptr;  // WF_TRACE_HOST: sources resident
     uint64_t cap_rows = 0;  // segment rows the buffers hold
     uint32_t cap_stride = 0;
@@ -213,7 +213,7 @@ struct HostPipe {
 
     explicit HostPipe(int dev) : device(dev) {
         for (cudaStream_t* s : {&a, &b, &c, &d}) WF_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&ev_src0, &ev_walk, &ev_compact, &ev_copy})
+        for (cudaEvent_t* e : {&ev_src0, &ev_walk, &ev_copy})
             WF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         ctr.allocate(2);
         src_ready.allocate(1);
@@ -234,7 +234,7 @@ struct HostPipe {
         for (cudaStream_t s : {a, b, c, d})
             if (s) cudaStreamDestroy(s);
         for (cudaEvent_t e : ev_chunk) cudaEventDestroy(e);
-        for (cudaEvent_t e : {ev_src0, ev_walk, ev_compact, ev_copy})
+        for (cudaEvent_t e : {ev_src0, ev_walk, ev_copy})
             if (e) cudaEventDestroy(e);
         if (flags) cudaFreeHost(flags);
         if (h_end) cudaFreeHost(h_end);
