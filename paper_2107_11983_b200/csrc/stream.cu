@@ -338,6 +338,17 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         SL.chunk_flag = P.flags;
         SL.tile_shift = tile_shift;
         SL.chunk_tiles_shift = chunk_shift - tile_shift;
+        // whole mode: the first launch covers ~a quarter of the rows (below)
+        const uint64_t split = whole && nch >= 4 ? ((nch + 3) / 4) << chunk_shift : sn;
+        uint64_t src_rest = sn;  // source rows still to queue (before the launch that needs them)
+        auto copy_src = [&](uint64_t r0, uint64_t r1) {
+            if (r1 <= r0) return;
+            WF_CUDA(cudaMemcpyAsync(P.src.get() + r0, host_sources + qb + s0 + r0, (r1 - r0) * 4,
+                                    cudaMemcpyHostToDevice, C));
+            CUresult cr = P.write_value32(reinterpret_cast<CUstream>(C), reinterpret_cast<CUdeviceptr>(P.src_ready.get()),
+                                          static_cast<cuuint32_t>((r1 + 1023) >> 10), 0);
+            if (cr != CUDA_SUCCESS) raise(WF_ERR_CUDA, "cuStreamWriteValue32 failed");
+        };
         const uint32_t* src_by_qid = nullptr;
         if (list) {
             src_by_qid = P.src.get() - (qb + s0);
@@ -351,22 +362,20 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             if (P.write_value32 && pinned) {
                 // the kernel starts once the first piece of the list has
                 // landed and waits for the rest only where it gets ahead of the
-                // copies (src_ready, in 1024-row units).  Pieces double from
-                // 64 Ki rows: a short first copy, few copies overall (each
-                // costs the host a few us).
+                // copies (src_ready, in 1024-row units).  Every piece is
+                // queued before the first launch that may wait on it: a copy
+                // queued behind a spinning kernel can be held up by it
+                // (streams may share a hardware queue), which would deadlock.
+                // Few pieces: each costs the host a few us before the launch.
                 WF_CUDA(cudaMemsetAsync(P.src_ready.get(), 0, 4, C));
                 WF_CUDA(cudaEventRecord(P.ev_src0, C));
-                // (queued before the launch: the kernel waits on them, and a
-                // copy queued behind a spinning kernel can be held up by it —
-                // streams may share a hardware queue — which would deadlock)
-                for (uint64_t r0 = 0, piece = kSrcFirstPiece; r0 < sn; r0 += piece, piece *= 2) {
-                    const uint64_t r1 = std::min<uint64_t>(sn, r0 + piece);
-                    WF_CUDA(cudaMemcpyAsync(P.src.get() + r0, host_sources + qb + s0 + r0, (r1 - r0) * 4,
-                                            cudaMemcpyHostToDevice, C));
-                    CUresult cr = P.write_value32(reinterpret_cast<CUstream>(C),
-                                                  reinterpret_cast<CUdeviceptr>(P.src_ready.get()),
-                                                  static_cast<cuuint32_t>((r1 + 1023) >> 10), 0);
-                    if (cr != CUDA_SUCCESS) raise(WF_ERR_CUDA, "cuStreamWriteValue32 failed");
+                copy_src(0, std::min<uint64_t>(sn, kSrcFirstPiece));
+                if (whole) {
+                    copy_src(std::min<uint64_t>(sn, kSrcFirstPiece), split);  // the first launch's rows
+                    src_rest = split;  // queued before the second launch
+                } else {
+                    for (uint64_t r0 = kSrcFirstPiece, piece = kSrcFirstPiece; r0 < sn; r0 += piece, piece *= 2)
+                        copy_src(r0, std::min<uint64_t>(sn, r0 + piece));
                 }
                 if (trace_on) {
                     WF_CUDA(cudaEventCreate(&P.ev_trace_src));
@@ -395,13 +404,17 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             // are published (and their copies start) while the second runs.
             // One launch would publish everything only at its end; halves
             // would make the first copy wait longer.
-            const uint64_t split = nch >= 4 ? ((nch + 3) / 4) << chunk_shift : sn;
             for (uint64_t a = 0; a < sn;) {
                 const uint64_t b = a == 0 ? split : sn;
+                if (a == src_rest) {
+                    copy_src(src_rest, sn);
+                    src_rest = sn;
+                }
                 SL.src_row0 = a;
                 launch_walk(s, spec, src_by_qid, qb + s0 + a, qb + s0 + b, nullptr, P.rows.get() + a * stride,
                             stride, P.lens.get() + a, P.stat.get() + a, nullptr, P.ctr.get(), P.ctr.get() + 1,
                             s.cursor.get(), A, &SL);
+                trace("launch queued, first row", static_cast<long long>(s0 + a));
                 const uint64_t t0 = a >> tile_shift, c0 = a >> chunk_shift;
                 const uint64_t nt = ((b - a) + (1ull << tile_shift) - 1) >> tile_shift;
                 const uint64_t nc = ((b - a) + chunk_rows - 1) >> chunk_shift;
