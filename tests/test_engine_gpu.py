@@ -430,6 +430,37 @@ def test_run_host_modes_and_segments(rmat12, monkeypatch, mode, stage_bytes):
         assert np.array_equal(verts, whole.vertices)
 
 
+@pytest.mark.parametrize("mode", ["whole", "chunks"])
+def test_run_host_errors_in_both_modes(rmat12, monkeypatch, mode):
+    """Device-side errors surface from the streaming pipeline as the reference's
+    exception classes, with pinned (streamed) and pageable source lists, and
+    the session stays usable: a non-vertex source (ConfigError) and a trial cap
+    the O-REJ bound cannot meet (RejectionCapError)."""
+    import torch
+    dg, hg = rmat12
+    monkeypatch.setenv("WF_STREAM_MODE", mode)
+    n = 1 << 16
+    src = np.random.default_rng(4).integers(0, hg.vertex_count, n).astype(np.uint32)
+    src[n - 5] = hg.vertex_count + 3
+    pinned = torch.from_numpy(src.view(np.int32)).pin_memory()
+    sess = E.Session(dg, PprProgram(0.2), ExecOptions(seed=2, path_stride=64))
+    verts = torch.zeros(n * 64, dtype=torch.int32).pin_memory()
+    rec = torch.zeros(n, dtype=torch.int32).pin_memory()
+    for sources in (src, pinned.numpy().view(np.uint32)):
+        with pytest.raises(abi.ConfigError, match=str(hg.vertex_count + 3)):
+            sess.run_host_records(QuerySpec.from_list(sources), rec.data_ptr(), verts.data_ptr(), n * 64,
+                                  chunk=1 << 12)
+    good = src.copy()
+    good[n - 5] = 7
+    whole = E.run_sequential(dg, QuerySpec.from_list(good), PprProgram(0.2), ExecOptions(seed=2)).walks
+    sess.run_host_records(QuerySpec.from_list(good), rec.data_ptr(), verts.data_ptr(), n * 64, chunk=1 << 12)
+    total = int(whole.offsets[-1])
+    assert np.array_equal(verts.numpy()[:total].view(np.uint32), whole.vertices)
+    n2v = E.Session(dg, Node2VecProgram(0.01, 0.5, 10, False), ExecOptions(seed=1, rej_trial_cap=1))
+    with pytest.raises(abi.RejectionCapError):
+        n2v.run_to_numpy(QuerySpec.one_per_vertex())
+
+
 def test_launch_tuner_keeps_results(rmat12):
     """wf_session_tune only changes the grid: walks are identical before and after."""
     import torch
