@@ -1,19 +1,23 @@
 // Run + stream the walk set to host memory.  This is the end-to-end path: the
 // reference hands its walks back in host memory (RunResult::walks,
 // engine.hpp:448-452) or through a BlockSink per worker block
-// (engine.hpp:76-79, output.cpp:133-200).
+// (engine.hpp:76-79, output.cpp:133-200).  DESIGN.md 5.2.
 //
-// One persistent walk launch covers the whole batch (a segment of it when the
-// rows would not fit a 4 GiB staging budget).  Its rows are grouped in chunks;
-// the walk kernel publishes each completed chunk's vertex total to host-mapped
-// memory (walk_kernel<..., true>, stream_report), and this thread, polling
-// those flags, queues the chunk's compaction on a side stream and its
-// device->host copies on the copy stream while the kernel is still running.
-// The source list is copied in the same chunks on a third stream, and the
-// kernel waits per chunk for it (src_ready) instead of the launch waiting for
-// all of it.  So the PCIe copies start as soon as the first chunk is done and
-// overlap the rest of the run; no launch pays a separate tail of long walks.
-// Streams, events, mapped flags and staging buffers are cached on the session
+// Rows are grouped in chunks; each chunk's vertex total is published to
+// host-mapped memory as soon as all its walks are done, and this thread,
+// polling those flags, queues the compaction of every published chunk (a
+// batch) on a side stream and its device->host copies on the copy stream
+// while the walks go on:
+//   * fixed-length walks (chunks mode): one persistent launch whose streaming
+//     instantiation (walk_kernel<..., true>) reports finished rows per tile
+//     and publishes each chunk itself (stream_report);
+//   * short geometric walks (whole mode, PPR): they end all at once near the
+//     end of any launch, so the batch runs as two launches (a quarter, then
+//     the rest), each followed by k_tile_sums + k_publish.
+// A pinned source list is copied in a few pieces on a third stream and the
+// kernel waits (src_ready) only where its claims get ahead of them.  Large
+// runs are split into segments that fit a 4 GiB staging budget.  Streams,
+// events, mapped flags and staging buffers are cached on the session
 // (HostPipe): repeated calls pay no allocation.
 #include <cub/cub.cuh>
 #include <cuda.h>
