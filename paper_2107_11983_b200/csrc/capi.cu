@@ -378,7 +378,7 @@ int wf_graph_original_ids(const wf_graph* g, uint64_t* out) {
 
 void wf_graph_destroy(wf_graph* g) {
     if (g) {
-        DeviceGuard guard(g->g->device);
+        DeviceGuard guard(g->g->device, std::nothrow);
         delete g;
     }
 }
@@ -478,7 +478,7 @@ int wf_session_layout(const wf_session* sh, uint32_t* flags) {
 
 void wf_session_destroy(wf_session* s) {
     if (s) {
-        DeviceGuard guard(s->s->g->device);
+        DeviceGuard guard(s->s->g->device, std::nothrow);
         delete s;
     }
 }
@@ -792,7 +792,7 @@ int wf_walkset_write(const wf_walkset* w, const char* path, int format, uint64_t
 
 void wf_walkset_destroy(wf_walkset* w) {
     if (w) {
-        DeviceGuard guard(w->w->device);
+        DeviceGuard guard(w->w->device, std::nothrow);
         delete w;
     }
 }

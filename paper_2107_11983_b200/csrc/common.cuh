@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <new>
+
 #include <atomic>
 #include <cstdint>
 #include <stdexcept>
@@ -76,6 +78,16 @@ struct DeviceGuard {
     explicit DeviceGuard(int dev) {
         WF_CUDA(cudaGetDevice(&prev));
         if (prev != dev) WF_CUDA(cudaSetDevice(dev));
+    }
+    // For destructors and the *_destroy entry points, which must not throw: at
+    // interpreter / process shutdown the runtime may already be torn down.
+    DeviceGuard(int dev, std::nothrow_t) noexcept {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            cudaGetLastError();
+            return;
+        }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
     }
     ~DeviceGuard() {
         int cur = -1;

@@ -234,7 +234,7 @@ struct HostPipe {
             cudaGetLastError();
     }
     ~HostPipe() {
-        DeviceGuard guard(device);
+        DeviceGuard guard(device, std::nothrow);
         for (cudaStream_t s : {a, b, c, d})
             if (s) cudaStreamDestroy(s);
         for (cudaEvent_t e : ev_chunk) cudaEventDestroy(e);

@@ -1,4 +1,4 @@
-"""Full BASELINE-size configurations (SURVEY §8 d: C1-C4) on the GPU.
+"""Full BASELINE-size configurations (SURVEY §8 d: C1-C5) on the GPU.
 
 * sampled parity: a few hundred query ids of each full-size run are replayed by
   the unmodified reference (oracle/_ref run_qids: its own ResolvedRun +
@@ -8,6 +8,10 @@
   no usable edge, MetaPath edges carry the schema label, PPR's mean length is
   the geometric 1/0.2, total steps = sum of path lengths - n, visit counts sum
   to the number of path vertices, and repeated runs are identical.
+* C5 (s26, 2^26 walks, ~110 GB of HBM): the sampled walks are replayed in
+  Python from the reference's own primitives (the C restatement's
+  alias_init over each visited vertex's weights and its RngStream draws), so
+  no 50 GB host-side preprocess_static is needed.
 """
 import numpy as np
 import pytest
@@ -138,3 +142,62 @@ def test_c4_metapath_s22_full_size(s22):
         want_label = schema[lens[q] - 1]
         assert not np.any(hg.labels[hg.offsets[last]:hg.offsets[last + 1]] == want_label)
     _sample_parity(hg, spec, prog, opts, got, k=300)
+
+
+def _replay_deepwalk_alias(hg, port, qid, length, seed, cache):
+    """DeepWalk on static ALIAS tables (engine.hpp:379-384, 423-424; sampler.hpp
+    89-120): x = uniform_index(d), y = uniform_real(1.0), first if y < split."""
+    draws = port.rng_probe(seed, qid, 2 * (length - 1))
+    path = [qid]
+    for i in range(length - 1):
+        v = path[-1]
+        lo, hi = int(hg.offsets[v]), int(hg.offsets[v + 1])
+        d = hi - lo
+        if d == 0:
+            return path, 1
+        if v not in cache:
+            cache[v] = port.alias_init(hg.weights[lo:hi].astype(np.float64))
+        split, first, second = cache[v]
+        x = (int(draws[2 * i]) * d) >> 64
+        y = (int(draws[2 * i + 1]) >> 11) * 2.0 ** -53
+        pick = first[x] if (y < split[x] or second[x] == 0xFFFFFFFF) else second[x]
+        path.append(int(hg.neighbors[lo + int(pick)]))
+    return path, 0
+
+
+def test_c5_deepwalk_s26_full_size():
+    import torch
+    if torch.cuda.get_device_properties(0).total_memory < (150 << 30):
+        pytest.skip("C5 needs ~110 GB of device memory")
+    dg = E.DeviceGraph.rmat(26, 16, seed=1, weighted=True)
+    prog, opts = DeepWalkProgram(80, True), ExecOptions(seed=1)
+    sess = E.Session(dg, prog, opts)
+    ws = sess.run(QuerySpec.one_per_vertex())
+    hg = dg.download()
+    V = hg.vertex_count
+    assert V == 1 << 26 and hg.edge_count > 2_000_000_000
+    deg = np.diff(hg.offsets)
+    # every walk, in slices: 80 vertices unless the source is isolated
+    total = 0
+    step = 1 << 24
+    for a in range(0, V, step):
+        part = ws.to_host(a, a + step)
+        lens = part.lengths()
+        d = deg[a:a + step]
+        assert np.all(lens[d > 0] == 80) and np.all(part.status[d > 0] == 0)
+        # an isolated source dead-ends at once (no draws)
+        assert np.all(lens[d == 0] == 1) and np.all(part.status[d == 0] == 1)
+        total += int(lens.sum()) - lens.size
+        del part
+    ok, *_ = _edges_ok(hg, ws.to_host(0, 1 << 17))
+    assert ok
+    assert ws.metrics.total_steps == total
+    # sampled parity against a replay from the reference's primitives
+    port = PortOracle()
+    cache = {}
+    for q in np.random.default_rng(26).integers(0, V, 48):
+        q = int(q)
+        want, st = _replay_deepwalk_alias(hg, port, q, 80, 1, cache)
+        got = ws.to_host(q, q + 1)
+        assert int(got.status[0]) == st, q
+        assert np.array_equal(got.path(0), np.asarray(want, np.uint32)), q
