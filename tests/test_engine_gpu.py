@@ -594,3 +594,7 @@ def test_degenerate_inputs_match_reference():
                 want = rg.run(spec, prog, opts)
                 assert got.walks.equals(want.walks), (V, prog, spec.mode)
                 assert got.metrics.total_steps == want.metrics.total_steps == 0
+                # and through the host-streaming pipeline
+                streamed = E.Session(dg, prog, opts).run_to_numpy(spec)
+                assert streamed.walks.equals(want.walks), (V, prog, spec.mode)
+                assert streamed.metrics.total_steps == 0
