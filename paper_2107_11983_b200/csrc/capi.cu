@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <chrono>
 #include <cmath>
@@ -718,6 +719,9 @@ int wf_session_tune(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begi
                 WF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
                 if (rep > 0) mn = std::min(mn, ms);
             }
+            if (getenv("WF_TRACE_TUNE"))  // diagnostics: every candidate's time
+                std::fprintf(stderr, "[tune] rows %llu: %d blocks/SM %.4f ms\n",
+                             static_cast<unsigned long long>(n), c, mn);
             if (mn < best) {
                 best = mn;
                 pick = c;
