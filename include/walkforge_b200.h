@@ -296,6 +296,23 @@ int wf_session_run_host_records(wf_session* s, const wf_query_spec* spec, uint64
                                 uint64_t vertices_capacity, uint64_t chunk_queries,
                                 wf_run_metrics* metrics);
 
+/* The BlockSink form (engine.hpp:76-79: the sink gets one block per worker,
+ * records in qid order, output.cpp's OrderedBlockSink merges them): as
+ * wf_session_run_host_records, and `on_block(user, block, qid_begin, qid_end,
+ * vertex_begin)` is called on the calling thread, in qid order, as soon as the
+ * records [qid_begin, qid_end) and their vertices (from vertex_begin) have
+ * landed in the host buffers — while later queries are still walking.  qids
+ * are relative to the call's qid_begin; blocks are consecutive and cover the
+ * run; `block` counts from 0.  Blocks holding a walk longer than the session's
+ * row capacity are delivered after the run, once patched.  A non-zero return
+ * stops the run with WF_ERR_IO (in-flight work is drained first). */
+typedef int (*wf_block_fn)(void* user, uint64_t block, uint64_t qid_begin, uint64_t qid_end,
+                           uint64_t vertex_begin);
+int wf_session_run_host_blocks(wf_session* s, const wf_query_spec* spec, uint64_t qid_begin,
+                               uint64_t qid_end, uint32_t* records, uint32_t* vertices,
+                               uint64_t vertices_capacity, uint64_t chunk_queries, wf_block_fn on_block,
+                               void* user, wf_run_metrics* metrics);
+
 /* Instrumentation (measurement only; no reference counterpart): when enabled,
  * launches accumulate logical access counts used for the algorithmic sector
  * figure of SURVEY §8 d — out[0] rejection trials, out[1] adjacency-search

@@ -15,10 +15,12 @@
 //     worker threads); k / k' of run_interleaved are validated then ignored.
 #pragma once
 
+#include <algorithm>
 #include <cctype>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
+#include <exception>
 #include <fstream>
 #include <functional>
 #include <memory>
@@ -26,6 +28,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../walkforge_b200.h"
@@ -433,6 +436,65 @@ private:
 
 // ---- run_sequential / run_interleaved (engine.hpp:440-504, interleave.hpp:391-556) ---
 namespace detail {
+inline std::pair<uint64_t, uint64_t> worker_range(uint64_t n, uint32_t workers, uint32_t w) {
+    return {n * w / workers, n * (w + 1) / workers};  // engine.hpp:296-298
+}
+
+// Turns the streamed records + vertices into WalkRecords as blocks land, and
+// hands the sink one block per worker range (engine.hpp:446-495: `workers` =
+// max(1, threads) contiguous qid ranges, sink(w, block) once each, in order).
+struct StreamSink {
+    const uint32_t* records = nullptr;
+    const uint32_t* vertices = nullptr;
+    uint64_t n = 0;
+    uint32_t workers = 1;
+    uint32_t next_worker = 0;
+    uint64_t next_q = 0, next_v = 0;
+    WalkSet* all = nullptr;  // no sink: the whole walk set
+    const BlockSink* sink = nullptr;
+    WalkSet block;
+    bool delivered = false;
+    std::exception_ptr error;
+
+    void flush_empty_workers() {  // ranges with no queries still get their (empty) block
+        while (sink && next_worker < workers && worker_range(n, workers, next_worker).second <= next_q) {
+            (*sink)(next_worker++, std::move(block));
+            block.clear();
+        }
+    }
+    void take(uint64_t q1) {
+        for (uint64_t q = next_q; q < q1; ++q) {
+            const uint32_t rec = records[q];
+            const uint32_t len = rec & 0x7FFFFFFFu;
+            WalkRecord r{q, (rec >> 31) ? WalkStatus::DeadEnd : WalkStatus::Complete,
+                         std::vector<VertexId>(vertices + next_v, vertices + next_v + len)};
+            next_v += len;
+            if (all) (*all)[q] = std::move(r);
+            else block.push_back(std::move(r));
+            next_q = q + 1;
+            delivered = true;
+            flush_empty_workers();
+        }
+    }
+    static int on_block(void* user, uint64_t, uint64_t, uint64_t q1, uint64_t) {
+        auto* self = static_cast<StreamSink*>(user);
+        try {
+            self->take(q1);
+            return 0;
+        } catch (...) {
+            self->error = std::current_exception();
+            return 1;
+        }
+    }
+};
+
+// Upper bound on path vertices per query (0: unbounded, PPR).
+inline uint64_t max_path_vertices(const wf_program_desc& d) {
+    if (d.kind == WF_PROGRAM_METAPATH) return static_cast<uint64_t>(d.schema_len) + 1;
+    if (d.kind == WF_PROGRAM_PPR) return 0;
+    return d.target_length;
+}
+
 template <typename P>
 RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts) {
     wf_program_desc d = prog.to_desc();
@@ -443,30 +505,47 @@ RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOp
     o.rej_trial_cap = opts.rej_trial_cap;
     o.threads = opts.threads;
     wf_query_spec q = spec.to_c();
-    wf_walkset* ws = nullptr;
-    wf_run_metrics m{};
-    check(wf_run(g.handle(), &d, &q, &o, &ws, &m));
-    std::unique_ptr<wf_walkset, void (*)(wf_walkset*)> guard(ws, wf_walkset_destroy);
-    uint64_t n = 0, total = 0;
-    uint32_t maxlen = 0;
-    check(wf_walkset_info(ws, &n, &total, &maxlen));
-    std::vector<uint64_t> off(n + 1);
-    std::vector<uint32_t> verts(total);
-    std::vector<uint8_t> st(n);
-    check(wf_walkset_copy(ws, 0, n, off.data(), verts.data(), st.data()));
+    // QuerySpec::validate before any work (walker.cpp:8-109), as the
+    // reference does: no block may reach a sink for an invalid query set
+    const uint64_t n = spec.total(g);
+    if (spec.mode == QuerySpec::Mode::FromSource && spec.source >= g.vertex_count())
+        throw ConfigError("query source " + std::to_string(spec.source) + " is not a vertex (V=" +
+                          std::to_string(g.vertex_count()) + ")");
+    if (spec.mode == QuerySpec::Mode::FromFile)
+        for (VertexId v : spec.sources)
+            if (v >= g.vertex_count())
+                throw ConfigError("query source " + std::to_string(v) + " is not a vertex (V=" +
+                                  std::to_string(g.vertex_count()) + ")");
+    wf_session* s = nullptr;
+    check(wf_session_create(g.handle(), &d, &o, &s));
+    std::unique_ptr<wf_session, void (*)(wf_session*)> guard(s, wf_session_destroy);
+
+    // the walks stream into host memory block by block (wf_session_run_host_blocks)
+    // and become WalkRecords while later queries are still walking
+    uint64_t per = max_path_vertices(d);
+    if (per == 0) per = static_cast<uint64_t>(2.0 / d.termination) + 24;  // PPR: ~5x its mean length
+    const uint64_t cap = n * per + 4096;
+    std::unique_ptr<uint32_t[]> records(new uint32_t[std::max<uint64_t>(n, 1)]);
+    std::unique_ptr<uint32_t[]> vertices(new uint32_t[cap]);
     RunResult r;
-    r.metrics = {m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight};
-    WalkSet walks(n);
-    for (uint64_t i = 0; i < n; ++i) {
-        walks[i].query_id = i;
-        walks[i].status = static_cast<WalkStatus>(st[i]);
-        walks[i].path.assign(verts.begin() + off[i], verts.begin() + off[i + 1]);
-    }
+    StreamSink st;
+    st.records = records.get();
+    st.vertices = vertices.get();
+    st.n = n;
+    st.workers = std::max<uint32_t>(1, opts.threads);
     if (opts.sink) {
-        opts.sink(0, std::move(walks));  // one device worker: one block, qid order
+        st.sink = &opts.sink;
     } else {
-        r.walks = std::move(walks);
+        r.walks.resize(n);
+        st.all = &r.walks;
     }
+    wf_run_metrics m{};
+    const int rc = wf_session_run_host_blocks(s, &q, 0, 0, records.get(), vertices.get(), cap, 0,
+                                              &StreamSink::on_block, &st, &m);
+    if (st.error) std::rethrow_exception(st.error);
+    check(rc);
+    st.flush_empty_workers();
+    r.metrics = {m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight};
     return r;
 }
 }  // namespace detail

@@ -232,6 +232,7 @@ EXPORTED_SYMBOLS = [
     "wf_graph_read_wfg1", "wf_graph_write_wfg1", "wf_graph_load_edge_list", "wf_graph_original_ids",
     "wf_session_create", "wf_session_describe", "wf_session_destroy", "wf_session_run",
     "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_run_host_records",
+    "wf_session_run_host_blocks",
     "wf_session_set_stats",
     "wf_session_stats", "wf_session_layout", "wf_session_tune",
     "wf_walkset_info", "wf_walkset_copy", "wf_walkset_visit_counts", "wf_walkset_destroy",

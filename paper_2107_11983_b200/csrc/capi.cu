@@ -601,7 +601,8 @@ int wf_session_run(wf_session* sh, const wf_query_spec* spec, wf_walkset** out,
 namespace {
 void run_host_checked(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin, uint64_t qid_end,
                       uint64_t* offsets, uint32_t* vertices, uint64_t vertices_capacity, uint8_t* status,
-                      uint64_t chunk_queries, wf_run_metrics* metrics, uint32_t* records) {
+                      uint64_t chunk_queries, wf_run_metrics* metrics, uint32_t* records,
+                      wf_block_fn on_block = nullptr, void* user = nullptr) {
     require(sh && spec && vertices, "null argument");
     Session& s = *sh->s;
     GraphStore& g = *s.g;
@@ -618,7 +619,7 @@ void run_host_checked(wf_session* sh, const wf_query_spec* spec, uint64_t qid_be
         // sources are range-checked by the walk kernel (ConfigError after the run)
     }
     run_to_host(s, *spec, spec->sources, qid_begin, qid_end, offsets, vertices, vertices_capacity, status,
-                chunk_queries, metrics, records);
+                chunk_queries, metrics, records, on_block, user);
 }
 }  // namespace
 
@@ -629,6 +630,17 @@ int wf_session_run_host_records(wf_session* sh, const wf_query_spec* spec, uint6
         require(records != nullptr, "null argument");
         run_host_checked(sh, spec, qid_begin, qid_end, nullptr, vertices, vertices_capacity, nullptr,
                          chunk_queries, metrics, records);
+    });
+}
+
+int wf_session_run_host_blocks(wf_session* sh, const wf_query_spec* spec, uint64_t qid_begin,
+                               uint64_t qid_end, uint32_t* records, uint32_t* vertices,
+                               uint64_t vertices_capacity, uint64_t chunk_queries, wf_block_fn on_block,
+                               void* user, wf_run_metrics* metrics) {
+    return guarded([&] {
+        require(records != nullptr && on_block != nullptr, "null argument");
+        run_host_checked(sh, spec, qid_begin, qid_end, nullptr, vertices, vertices_capacity, nullptr,
+                         chunk_queries, metrics, records, on_block, user);
     });
 }
 

@@ -197,7 +197,8 @@ struct WidenU64 {
 // stream.cu: pipelined run + copy of the walk set into host buffers
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
-                 uint64_t chunk, wf_run_metrics* metrics, uint32_t* records = nullptr);
+                 uint64_t chunk, wf_run_metrics* metrics, uint32_t* records = nullptr,
+                 wf_block_fn on_block = nullptr, void* user = nullptr);
 
 // output.cu: record encoding (text / binary, byte-identical to output.cpp)
 uint64_t encode_walks(const uint64_t* offsets, const uint32_t* vertices, const uint8_t* status,

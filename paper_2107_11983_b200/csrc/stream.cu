@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kCompactThreads, 16) k_stream_compact(
     const uint8_t* __restrict__ stat, const unsigned long long* __restrict__ tile_word,
     const unsigned long long* __restrict__ chunk_word, uint32_t tile_shift, uint32_t chunk_tiles_shift,
     uint64_t row0, uint64_t nrows, uint32_t* __restrict__ out, uint64_t cap, uint32_t* __restrict__ records,
-    uint64_t* __restrict__ offs, uint64_t off_base) {
+    uint64_t* __restrict__ offs, uint64_t off_base, volatile unsigned int* over_flag) {
     using Scan = cub::BlockScan<unsigned long long, kCompactThreads>;
     using Reduce = cub::BlockReduce<unsigned long long, kCompactThreads>;
     __shared__ union {
@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kCompactThreads, 16) k_stream_compact(
             const uint64_t row = row0 + r;
             if (records) records[row] = len[i] | (static_cast<uint32_t>(stat[row]) << 31);
             if (offs) offs[row] = off_base + base + pos;
+            if (over_flag && len[i] > stride) *over_flag = 1u;  // host-mapped: patched after the run
             s_start[r - r_first] = pos;
         }
         pos += len[i];
@@ -211,6 +212,9 @@ struct HostPipe {
     DeviceBuffer<unsigned long long> ctr;
     unsigned long long* flags = nullptr;  // host-mapped chunk flags
     unsigned long long* h_end = nullptr;  // pinned: steps, overflow, error word
+    unsigned int* h_over = nullptr;       // host-mapped, per block: a walk outgrew its row
+    uint64_t cap_over = 0;
+    std::vector<cudaEvent_t> ev_block;    // block k's copies landed (wf_session_run_host_blocks)
     uint64_t cap_flags = 0;
     using WriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
     WriteValue32 write_value32 = nullptr;
@@ -242,6 +246,23 @@ struct HostPipe {
             if (e) cudaEventDestroy(e);
         if (flags) cudaFreeHost(flags);
         if (h_end) cudaFreeHost(h_end);
+        if (h_over) cudaFreeHost(h_over);
+        for (cudaEvent_t e : ev_block) cudaEventDestroy(e);
+    }
+    // per-block state of a wf_session_run_host_blocks call with up to `blocks` blocks
+    void reserve_blocks(uint64_t blocks) {
+        while (ev_block.size() < blocks) {
+            cudaEvent_t e;
+            WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev_block.push_back(e);
+        }
+        if (blocks > cap_over) {
+            if (h_over) WF_CUDA(cudaFreeHost(h_over));
+            h_over = nullptr;
+            WF_CUDA(cudaHostAlloc(&h_over, blocks * sizeof(unsigned int), cudaHostAllocMapped));
+            cap_over = blocks;
+        }
+        std::fill(h_over, h_over + blocks, 0u);
     }
     void reserve(uint64_t seg_rows, uint32_t stride, uint64_t nchunks) {
         while (ev_chunk.size() < nchunks) {
@@ -282,7 +303,8 @@ void raise_device_error(const Session& s, int code) {
 
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
-                 uint64_t chunk, wf_run_metrics* metrics, uint32_t* records) {
+                 uint64_t chunk, wf_run_metrics* metrics, uint32_t* records, wf_block_fn on_block,
+                 void* user) {
     GraphStore& g = *s.g;
     DeviceGuard guard(g.device);
     auto t0 = std::chrono::steady_clock::now();
@@ -322,6 +344,39 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     if (list && P.src.size() < seg_rows) P.src.allocate(seg_rows);
     cudaStream_t A = P.a, B = P.b, C = P.c, D = P.d;
 
+    // wf_session_run_host_blocks: blocks (batches) are handed to the caller in
+    // qid order as their copies land; one holding a walk longer than its row
+    // (patched after the run) holds back itself and everything after it
+    struct Block {
+        uint64_t q0, q1, v0, slot;
+    };
+    std::vector<Block> pending;
+    size_t next_block = 0;
+    uint64_t nblocks = 0;
+    bool patched = false;
+    auto drain = [&] {
+        for (cudaStream_t st : {P.a, P.b, P.c, P.d}) cudaStreamSynchronize(st);
+    };
+    if (on_block) P.reserve_blocks(((n + chunk_rows - 1) >> chunk_shift) + (n + seg_rows - 1) / seg_rows);
+    auto deliver = [&](bool wait) {
+        while (next_block < pending.size()) {
+            const Block& b = pending[next_block];
+            cudaEvent_t ev = P.ev_block[b.slot];
+            if (!wait) {
+                const cudaError_t e = cudaEventQuery(ev);
+                if (e == cudaErrorNotReady) return;
+                WF_CUDA(e);
+            } else {
+                WF_CUDA(cudaEventSynchronize(ev));
+            }
+            if (!patched && P.h_over[b.slot]) return;
+            if (on_block(user, next_block, b.q0, b.q1, b.v0) != 0) {
+                drain();
+                raise(WF_ERR_IO, "the block callback stopped the run at block " + std::to_string(next_block));
+            }
+            ++next_block;
+        }
+    };
     WF_CUDA(cudaMemsetAsync(P.ctr.get(), 0, 16, A));
     uint64_t total = 0;  // vertices written before the current chunk
     bool first_seg = true;
@@ -454,6 +509,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             uint64_t spins = 0;
             while (flags[k] == 0) {
                 if ((++spins & 255) == 0) {
+                    if (on_block) deliver(false);
                     cudaError_t e = cudaStreamQuery(A);
                     if (e == cudaSuccess) {
                         if (flags[k] != 0) break;
@@ -471,7 +527,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             trace("chunks published up to", static_cast<long long>(k1 - 1));
             if (total + cnt > capacity) {
                 // drain what is in flight into the caller's buffers before unwinding
-                for (cudaStream_t st : {A, B, C, D}) cudaStreamSynchronize(st);
+                drain();
                 raise(WF_ERR_INVALID_ARG, "vertices_capacity too small for the walk set");
             }
             const uint64_t slot_cap = nr * stride;
@@ -483,7 +539,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
                 k_stream_compact<<<tiles, kCompactThreads, 0, st>>>(
                     P.rows.get(), stride, P.lens.get(), P.stat.get(), P.tile_word.get(), P.chunk_word.get(),
                     tile_shift, chunk_shift - tile_shift, r0, nr, out, cap, records ? P.packed.get() : nullptr,
-                    offsets ? P.offs.get() : nullptr, total);
+                    offsets ? P.offs.get() : nullptr, total, on_block ? P.h_over + nblocks : nullptr);
                 WF_LAUNCHED();
             };
             if (cnt <= slot_cap) {
@@ -511,10 +567,16 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
                 WF_CUDA(cudaMemcpyAsync(status + s0 + r0, P.stat.get() + r0, nr, cudaMemcpyDeviceToHost, B));
             if (records)
                 WF_CUDA(cudaMemcpyAsync(records + s0 + r0, P.packed.get() + r0, nr * 4, cudaMemcpyDeviceToHost, B));
+            if (on_block) {
+                WF_CUDA(cudaEventRecord(P.ev_block[nblocks], B));
+                pending.push_back({s0 + r0, s0 + r1, total, nblocks});
+                ++nblocks;
+            }
             total += cnt;
             if (trace_on) WF_CUDA(cudaEventRecord(cev[3 * k + 2], B));
             trace("copies queued", static_cast<long long>(k1 - 1));
             k = k1;
+            if (on_block) deliver(false);
         }
         WF_CUDA(cudaEventRecord(P.ev_copy, B));
         if (trace_on) {
@@ -610,6 +672,10 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             std::copy(hp.begin() + i * mx, hp.begin() + i * mx + (offsets[r + 1] - offsets[r]),
                       vertices + offsets[r]);
         }
+    }
+    if (on_block) {
+        patched = true;
+        deliver(true);
     }
     trace("done", -1);
     if (metrics) {

@@ -27,6 +27,8 @@ LIB_PATH = os.environ.get("WF_LIB") or os.path.join(os.path.dirname(os.path.absp
                                                  "libwalkforge_b200.so")
 
 _u64p = C.POINTER(C.c_uint64)
+# wf_block_fn: int (*)(void* user, uint64_t block, uint64_t qid_begin, uint64_t qid_end, uint64_t vertex_begin)
+_BLOCK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64)
 _u32p = C.POINTER(C.c_uint32)
 _u8p = C.POINTER(C.c_uint8)
 _f32p = C.POINTER(C.c_float)
@@ -313,6 +315,25 @@ class Session:
         _check(load_library().wf_session_run_host_records(
             self.h, C.byref(cs), C.c_uint64(qid_begin), C.c_uint64(qid_end), _vp(records_ptr),
             _vp(vertices_ptr), C.c_uint64(capacity), C.c_uint64(chunk), C.byref(m)))
+        return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
+
+    def run_host_blocks(self, spec: QuerySpec, records_ptr: int, vertices_ptr: int, capacity: int,
+                        on_block, chunk: int = 0, qid_begin: int = 0, qid_end: int = 0) -> RunMetrics:
+        """wf_session_run_host_blocks (the BlockSink form): as run_host_records,
+        and on_block(block, qid_begin, qid_end, vertex_begin) -> bool|None is
+        called in qid order as each block lands; returning True stops the run
+        (IoError)."""
+        def tramp(_user, block, q0, q1, v0):
+            try:
+                return 1 if on_block(block, q0, q1, v0) else 0
+            except Exception:  # a Python error stops the run instead of crossing the C frame
+                return 1
+        cb = _BLOCK_FN(tramp)
+        cs = spec.to_c()
+        m = RunMetricsC()
+        _check(load_library().wf_session_run_host_blocks(
+            self.h, C.byref(cs), C.c_uint64(qid_begin), C.c_uint64(qid_end), _vp(records_ptr),
+            _vp(vertices_ptr), C.c_uint64(capacity), C.c_uint64(chunk), cb, None, C.byref(m)))
         return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
 
     def run_to_numpy(self, spec: QuerySpec, chunk: int = 0) -> RunResult:

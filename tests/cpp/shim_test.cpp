@@ -125,6 +125,33 @@ int main(int argc, char** argv) {
         w.finish();
         std::printf("written_%s %s\n", fmt ? "bin" : "txt", of.c_str());
     }
+    // the reference CLI's exact pattern with several workers (walkforge.cpp:
+    // OrderedBlockSink(writer, threads), sink(w, block) once per worker range)
+    {
+        const std::string of = std::string(argv[1]) + ".walks4.txt";
+        DoubleBufferedWriter w(of, OutputFormat::Text, kMinOutputBuffer);
+        ExecOptions wo = eo;
+        wo.threads = 5;
+        OrderedBlockSink sink(w, wo.threads);
+        std::vector<int> calls(wo.threads, 0);
+        wo.sink = [&](uint32_t worker, WalkSet&& block) {
+            calls.at(worker) += 1;
+            sink.push(worker, std::move(block));
+        };
+        run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 20, true), wo);
+        sink.finish();
+        w.finish();
+        bool once = true;
+        for (int c : calls) once = once && c == 1;
+        std::printf("written_txt_workers %s %s\n", of.c_str(), once ? "each_once" : "miscounted");
+        // an empty query set still hands every worker its (empty) block
+        std::vector<int> empty_calls(3, 0);
+        ExecOptions eo3 = eo;
+        eo3.threads = 3;
+        eo3.sink = [&](uint32_t worker, WalkSet&& block) { empty_calls.at(worker) += block.empty() ? 1 : 100; };
+        run_sequential(g, QuerySpec::from_source(0, 0), DeepWalkProgram(g, 20, true), eo3);
+        std::printf("empty_workers %d %d %d\n", empty_calls[0], empty_calls[1], empty_calls[2]);
+    }
     try {
         DoubleBufferedWriter bad("/nonexistent_dir/x.txt", OutputFormat::Text);
     } catch (const IoError&) {

@@ -461,6 +461,55 @@ def test_run_host_errors_in_both_modes(rmat12, monkeypatch, mode):
         n2v.run_to_numpy(QuerySpec.one_per_vertex())
 
 
+@pytest.mark.parametrize("mode", ["whole", "chunks"])
+@pytest.mark.parametrize("prog,stride", [(PprProgram(0.2), 64), (PprProgram(0.1), 8),
+                                         (DeepWalkProgram(24, True), 0),
+                                         (Node2VecProgram(2.0, 0.5, 16, False), 0)])
+def test_run_host_blocks_deliver_final_bytes_in_order(rmat12, monkeypatch, mode, prog, stride):
+    """wf_session_run_host_blocks (the BlockSink form): blocks arrive in qid
+    order, consecutive, covering the run, and what the host buffers hold for a
+    block AT ITS CALLBACK is already the final walk set (blocks with walks
+    longer than their row, stride 8, come after the patch).  A callback that
+    returns non-zero stops the run with IoError; the session stays usable."""
+    import torch
+    dg, hg = rmat12
+    monkeypatch.setenv("WF_STREAM_MODE", mode)
+    src = np.random.default_rng(31).integers(0, hg.vertex_count, 1 << 17).astype(np.uint32)
+    spec = QuerySpec.from_list(src)
+    opts = ExecOptions(seed=47, path_stride=stride)
+    whole = E.run_sequential(dg, spec, prog, opts).walks
+    n, total = src.size, int(whole.offsets[-1])
+    sess = E.Session(dg, prog, opts)
+    h_rec = torch.zeros(n, dtype=torch.int32).pin_memory()
+    h_vert = torch.zeros(total + 64, dtype=torch.int32).pin_memory()
+    rec_np, vert_np = h_rec.numpy().view(np.uint32), h_vert.numpy().view(np.uint32)
+    seen = []
+
+    def on_block(b, q0, q1, v0):
+        rec = rec_np[q0:q1].copy()
+        nv = int((rec & 0x7FFFFFFF).astype(np.int64).sum())
+        seen.append((b, q0, q1, v0, rec, vert_np[v0:v0 + nv].copy()))
+
+    m = sess.run_host_blocks(spec, h_rec.data_ptr(), h_vert.data_ptr(), total + 64, on_block, chunk=1 << 12)
+    assert m.total_steps == total - n
+    assert [b for b, *_ in seen] == list(range(len(seen))) and len(seen) > 1
+    assert seen[0][1] == 0 and seen[-1][2] == n
+    for (_, q0, q1, v0, rec, verts), nxt in zip(seen, seen[1:] + [None]):
+        if nxt is not None:
+            assert nxt[1] == q1
+        assert v0 == int(whole.offsets[q0])
+        assert np.array_equal(rec & 0x7FFFFFFF, np.diff(whole.offsets[q0:q1 + 1]).astype(np.uint32))
+        assert np.array_equal((rec >> 31).astype(np.uint8), whole.status[q0:q1])
+        assert np.array_equal(verts, whole.vertices[v0:int(whole.offsets[q1])])
+    # stopping the run from the callback
+    with pytest.raises(abi.IoError):
+        sess.run_host_blocks(spec, h_rec.data_ptr(), h_vert.data_ptr(), total + 64,
+                             lambda b, *_: b == 1, chunk=1 << 12)
+    h_vert.fill_(0)
+    sess.run_host_records(spec, h_rec.data_ptr(), h_vert.data_ptr(), total + 64, chunk=1 << 12)
+    assert np.array_equal(vert_np[:total], whole.vertices)
+
+
 def test_launch_tuner_keeps_results(rmat12):
     """wf_session_tune only changes the grid: walks are identical before and after."""
     import torch

@@ -66,9 +66,11 @@ def test_shim_reproduces_golden_walks():
         # output.hpp's writer + ordered sink: the reference's record bytes
         # (wf_encode_walks is pinned byte-identical to output.cpp elsewhere)
         dw = gu.walks({c["name"]: c for c in gu.cases()}["pl_deepwalk_w_alias"])
-        for key, fmt in [("written_txt", 0), ("written_bin", 1)]:
+        for key, fmt in [("written_txt", 0), ("written_bin", 1), ("written_txt_workers", 0)]:
             with open(res[key][0], "rb") as f:
                 assert f.read() == E.encode_walks(dw, fmt), key
+        assert res["written_txt_workers"][1] == "each_once"
+        assert res["empty_workers"] == ["1", "1", "1"]
     cases = {c["name"]: c for c in gu.cases()}
     for key, case in [("deepwalk_alias", "pl_deepwalk_w_alias"),
                       ("node2vec_orej", "pl_node2vec_w_orej"),
