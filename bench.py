@@ -19,10 +19,14 @@ generated on the device; the paper's real graphs are not in this container.
 value     device-resident throughput: moves / s, inputs in HBM, CUDA events on
           the launching stream, max over ranks.
 e2e       same metric through the C-ABI call that returns walks in HOST memory
-          (wf_session_run_host): H2D of the step's source list from pinned host
-          memory + D2H of the whole walk set (ragged) into pinned host memory.
+          (wf_session_run_host_records; offsets_api: wf_session_run_host): H2D
+          of the step's source list from pinned host memory + D2H of the whole
+          walk set (ragged) into pinned host memory; L2 flushed before each
+          step as for `value` (small graphs).
 roofline  algorithmic bytes per launch (S_alg x moves) / mean launch time vs the
-          measured HBM copy bandwidth (MEASURED_PEAKS.json).
+          measured HBM copy bandwidth (MEASURED_PEAKS.json); measured_sectors:
+          BASELINE's definition, HBM bandwidth / measured DRAM bytes per move
+          (ncu, profiles/ncu_traffic.json).
 cpu_baseline  the unmodified reference (oracle/_ref, run_interleaved k=64 k'=32,
           all host threads, no-op sink) on a bounded sample, rank 0 at N=1.
 
@@ -357,6 +361,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                           qid_begin=lo, qid_end=hi)
         e2e_s = []
         for _ in range(args.steps):
+            if l2buf is not None:
+                flush_l2(l2buf)  # cold L2 for every timed step, as for `value`
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -374,6 +380,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         sess.run_host_records(hspec, h_rec.data_ptr(), h_vert.data_ptr(), cap, qid_begin=lo, qid_end=hi)
         e2e_s = []
         for _ in range(args.steps):
+            if l2buf is not None:
+                flush_l2(l2buf)
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
