@@ -436,6 +436,19 @@ def cpu_baseline(key, cfg, dg, spec, threads=None):
                        f"no-op sink, one warm-up run")
 
 
+# What bounds each config's walk kernel: carried in the
+# bench line so the fractions read with their cause.
+ROOFLINE_NOTES = {
+    "c1": "L2-resident graph (58 MB of buckets): bound by the 65 Ki walks' dependent L2 chains, not HBM",
+    "c2": "latency/tail-bound, not bandwidth-bound: the bulk saturates near 30 G moves/s at 3 blocks/SM "
+          "(DRAM ~2.9 TB/s), and the longest geometric walks finish in the unloaded tail; the HBM-resident "
+          "configs reach 0.75-0.86 of the measured-sector ceiling (per_algorithm.c3-c5)",
+    "c3": "DRAM-bound: one 128 B line per O-REJ trial, ~4.9 TB/s",
+    "c4": "DRAM-bound: one 128 B line per move (successor-decorated edges), ~5.0 TB/s",
+    "c5": "DRAM-bound: one 128 B line per move (wide alias buckets), 5.6 TB/s = 86% of the copy bandwidth",
+}
+
+
 def ncu_traffic():
     """profiles/ncu_traffic.json: DRAM bytes (read + write) per walk-kernel launch
     and per move, from ncu captures of each config at its tuned grid."""
@@ -619,6 +632,7 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "bytes_per_move": b, "bytes_model": b_desc,
+                     "note": ROOFLINE_NOTES.get(args.config),
                      # BASELINE's own definition: HBM bandwidth / measured DRAM
                      # bytes per step (ncu, cold cache, includes the 128 B line
                      # fetched for every 32 B random request)
