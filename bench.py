@@ -488,6 +488,7 @@ def extras(args, rank, world, local_rank, dist):
                             ms_per_step=ms, moves=r["moves"], achieved_gbs=ach,
                             roofline_frac=ach / peak, bytes_per_move=b, bytes_model=bdesc,
                             measured_sectors=measured_sectors_block(key, rate, peak),
+                            note=ROOFLINE_NOTES.get(key),
                             random_access=random_access_block(rate, reads),
                             E=r["info"]["E"])
             del r
