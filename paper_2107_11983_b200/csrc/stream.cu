@@ -12,7 +12,7 @@
 //     instantiation (walk_kernel<..., true>) reports finished rows per tile
 //     and publishes each chunk itself (stream_report);
 //   * short geometric walks (whole mode, PPR): they end all at once near the
-//     end of any launch, so the batch runs as two launches (a quarter, then
+//     end of any launch, so the batch runs as two launches (5/16, then
 //     the rest), each followed by k_tile_sums + k_publish.
 // A pinned source list is copied in a few pieces on a third stream and the
 // kernel waits (src_ready) only where its claims get ahead of them.  Large
@@ -397,8 +397,10 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         SL.chunk_flag = P.flags;
         SL.tile_shift = tile_shift;
         SL.chunk_tiles_shift = chunk_shift - tile_shift;
-        // whole mode: the first launch covers ~a quarter of the rows (below)
-        const uint64_t split = whole && nch >= 4 ? ((nch + 3) / 4) << chunk_shift : sn;
+        // whole mode: the first launch covers 5/16 of the chunks (C2 e2e: 3/16
+        // 0.636, 4/16 0.615, 5/16 0.606, 6/16 0.616 ms) — long enough that
+        // its copies cover the second launch, short enough to start them early
+        const uint64_t split = whole && nch >= 4 ? ((nch * 5 + 15) / 16) << chunk_shift : sn;
         uint64_t src_rest = sn;  // source rows still to queue (before the launch that needs them)
         auto copy_src = [&](uint64_t r0, uint64_t r1) {
             if (r1 <= r0) return;
@@ -459,7 +461,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             launch_walk(s, spec, src_by_qid, qb + s0, qb + s1, nullptr, P.rows.get(), stride, P.lens.get(),
                         P.stat.get(), nullptr, P.ctr.get(), P.ctr.get() + 1, s.cursor.get(), A, &SL);
         } else {
-            // Two launches, the first over ~a quarter of the rows: its chunks
+            // Two launches, the first over ~5/16 of the rows: its chunks
             // are published (and their copies start) while the second runs.
             // One launch would publish everything only at its end; halves
             // would make the first copy wait longer.
