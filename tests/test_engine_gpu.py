@@ -428,6 +428,15 @@ def test_run_host_modes_and_segments(rmat12, monkeypatch, mode, stage_bytes):
         assert np.array_equal(rec & 0x7FFFFFFF, np.diff(whole.offsets).astype(np.uint32))
         assert np.array_equal((rec >> 31).astype(np.uint8), whole.status)
         assert np.array_equal(verts, whole.vertices)
+        # a pinned source list streams in while the kernels run (src_ready)
+        import torch
+        pinned = torch.from_numpy(src.view(np.int32)).pin_memory()
+        h_rec = torch.zeros(n, dtype=torch.int32).pin_memory()
+        h_vert = torch.zeros(total, dtype=torch.int32).pin_memory()
+        sess.run_host_records(QuerySpec.from_list(pinned.numpy().view(np.uint32)), h_rec.data_ptr(),
+                              h_vert.data_ptr(), total, chunk=chunk)
+        assert np.array_equal(h_rec.numpy().view(np.uint32), rec)
+        assert np.array_equal(h_vert.numpy().view(np.uint32), whole.vertices)
 
 
 @pytest.mark.parametrize("mode", ["whole", "chunks"])
