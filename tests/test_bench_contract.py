@@ -28,3 +28,16 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "steps/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_roofline_evidence_covers_every_config():
+    """Every config's bench entry can carry BASELINE's measured-sector roofline
+    (profiles/ncu_traffic.json, from committed ncu captures) and a note on what
+    bounds its kernel."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for key in bench.CONFIGS:
+        assert bench.ROOFLINE_NOTES.get(key), key
+        block = bench.measured_sectors_block(key, 1e10, 6547.5)
+        assert block is not None and block["bytes_per_move"] > 0, key
+        assert 0 < block["frac"] and block["ceiling_steps_per_s"] > 0, key
