@@ -510,6 +510,17 @@ def test_run_host_blocks_deliver_final_bytes_in_order(rmat12, monkeypatch, mode,
         assert np.array_equal(rec & 0x7FFFFFFF, np.diff(whole.offsets[q0:q1 + 1]).astype(np.uint32))
         assert np.array_equal((rec >> 31).astype(np.uint8), whole.status[q0:q1])
         assert np.array_equal(verts, whole.vertices[v0:int(whole.offsets[q1])])
+    # a shard [lo, hi): qids and vertex offsets relative to lo
+    lo, hi = 12345, 100000
+    got = []
+    sess.run_host_blocks(spec, h_rec.data_ptr(), h_vert.data_ptr(), total + 64,
+                         lambda b, q0, q1, v0: got.append((q0, q1, v0)), chunk=1 << 12, qid_begin=lo, qid_end=hi)
+    assert got[0][0] == 0 and got[-1][1] == hi - lo
+    base = int(whole.offsets[lo])
+    for q0, q1, v0 in got:
+        assert v0 == int(whole.offsets[lo + q0]) - base
+    nv = int(whole.offsets[hi]) - base
+    assert np.array_equal(vert_np[:nv], whole.vertices[base:base + nv])
     # stopping the run from the callback
     with pytest.raises(abi.IoError):
         sess.run_host_blocks(spec, h_rec.data_ptr(), h_vert.data_ptr(), total + 64,
