@@ -301,6 +301,58 @@ void raise_device_error(const Session& s, int code) {
     raise(code, "device-side contract violation");
 }
 
+// A device-side error word after a run: the reference's exception, naming a
+// non-vertex source as QuerySpec::validate would (walker.cpp:8-109).
+[[noreturn]] void raise_run_error(const Session& s, const wf_query_spec& spec, const uint32_t* host_sources,
+                                  uint64_t qb, uint64_t qe, int err) {
+    WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
+    if (err == WF_ERR_CONFIG && spec.mode == WF_QUERY_FROM_LIST) {
+        for (uint64_t i = qb; i < qe; ++i)
+            if (host_sources[i] >= s.g->V)
+                config_error("query source " + std::to_string(host_sources[i]) + " is not a vertex (V=" +
+                             std::to_string(s.g->V) + ")");
+    }
+    raise_device_error(s, err);
+}
+
+// Walks longer than a row (rare: PPR beyond the row capacity) left gaps in
+// the streamed vertices: re-run exactly those queries with rows long enough
+// and patch their paths in place.  `offsets` are relative to qb.
+void patch_long_walks(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
+                      uint64_t n, uint32_t stride, const uint64_t* offsets, uint32_t* vertices) {
+    std::vector<uint64_t> qids;
+    uint32_t mx = 0;
+    for (uint64_t r = 0; r < n; ++r) {
+        const uint64_t len = offsets[r + 1] - offsets[r];
+        if (len > stride) {
+            qids.push_back(qb + r);
+            mx = std::max<uint32_t>(mx, static_cast<uint32_t>(len));
+        }
+    }
+    if (qids.empty()) return;
+    DeviceBuffer<uint64_t> dq(qids.size());
+    WF_CUDA(cudaMemcpy(dq.get(), qids.data(), qids.size() * 8, cudaMemcpyHostToDevice));
+    DeviceBuffer<uint32_t> p(qids.size() * static_cast<uint64_t>(mx)), l(qids.size());
+    DeviceBuffer<uint8_t> sst(qids.size());
+    DeviceBuffer<unsigned long long> c2(2);
+    WF_CUDA(cudaMemset(c2.get(), 0, 16));
+    DeviceBuffer<uint32_t> all_src;  // the shard's sources, addressed by qid
+    const uint32_t* src_by_qid = nullptr;
+    if (host_sources) {
+        all_src.allocate(n);
+        WF_CUDA(cudaMemcpy(all_src.get(), host_sources + qb, n * 4, cudaMemcpyHostToDevice));
+        src_by_qid = all_src.get() - qb;
+    }
+    launch_walk(s, spec, src_by_qid, 0, qids.size(), dq.get(), p.get(), mx, l.get(), sst.get(), nullptr,
+                c2.get(), c2.get() + 1, s.cursor.get(), nullptr);
+    std::vector<uint32_t> hp(qids.size() * static_cast<uint64_t>(mx));
+    WF_CUDA(cudaMemcpy(hp.data(), p.get(), hp.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < qids.size(); ++i) {
+        const uint64_t r = qids[i] - qb;
+        std::copy(hp.begin() + i * mx, hp.begin() + i * mx + (offsets[r + 1] - offsets[r]), vertices + offsets[r]);
+    }
+}
+
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics, uint32_t* records, wf_block_fn on_block,
@@ -635,17 +687,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
     WF_CUDA(cudaStreamSynchronize(A));
     WF_CUDA(cudaStreamSynchronize(D));
     const int err = static_cast<int>(P.h_end[2] & 0xFFFFFFFFu);
-    if (err) {
-        WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
-        if (err == WF_ERR_CONFIG && spec.mode == WF_QUERY_FROM_LIST) {
-            // the kernel flagged a source outside [0, V): name it as the host check would
-            for (uint64_t i = qb; i < qe; ++i)
-                if (host_sources[i] >= g.V)
-                    config_error("query source " + std::to_string(host_sources[i]) +
-                                 " is not a vertex (V=" + std::to_string(g.V) + ")");
-        }
-        raise_device_error(s, err);
-    }
+    if (err) raise_run_error(s, spec, host_sources, qb, qe, err);
     if (offsets) offsets[n] = total;
     const unsigned long long hc[2] = {P.h_end[0], P.h_end[1]};
     std::vector<uint64_t> rec_offs;  // records mode: offsets rebuilt on the host when needed
@@ -656,39 +698,8 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         offsets = rec_offs.data();
     }
     if (hc[1] > 0) {
-        // walks longer than a row: re-run them whole and patch their paths
         if (!offsets) raise(WF_ERR_INVALID_ARG, "offsets are required to place overflowing walks");
-        std::vector<uint64_t> qids;
-        uint32_t mx = 0;
-        for (uint64_t r = 0; r < n; ++r) {
-            uint64_t len = offsets[r + 1] - offsets[r];
-            if (len > stride) {
-                qids.push_back(qb + r);
-                mx = std::max<uint32_t>(mx, static_cast<uint32_t>(len));
-            }
-        }
-        DeviceBuffer<uint64_t> dq(qids.size());
-        WF_CUDA(cudaMemcpy(dq.get(), qids.data(), qids.size() * 8, cudaMemcpyHostToDevice));
-        DeviceBuffer<uint32_t> p(qids.size() * static_cast<uint64_t>(mx)), l(qids.size());
-        DeviceBuffer<uint8_t> sst(qids.size());
-        DeviceBuffer<unsigned long long> c2(2);
-        WF_CUDA(cudaMemset(c2.get(), 0, 16));
-        DeviceBuffer<uint32_t> all_src;  // the shard's sources, addressed by qid
-        const uint32_t* src_by_qid = nullptr;
-        if (list) {
-            all_src.allocate(n);
-            WF_CUDA(cudaMemcpy(all_src.get(), host_sources + qb, n * 4, cudaMemcpyHostToDevice));
-            src_by_qid = all_src.get() - qb;
-        }
-        launch_walk(s, spec, src_by_qid, 0, qids.size(), dq.get(), p.get(), mx, l.get(), sst.get(),
-                    nullptr, c2.get(), c2.get() + 1, s.cursor.get(), nullptr);
-        std::vector<uint32_t> hp(qids.size() * static_cast<uint64_t>(mx));
-        WF_CUDA(cudaMemcpy(hp.data(), p.get(), hp.size() * 4, cudaMemcpyDeviceToHost));
-        for (size_t i = 0; i < qids.size(); ++i) {
-            uint64_t r = qids[i] - qb;
-            std::copy(hp.begin() + i * mx, hp.begin() + i * mx + (offsets[r + 1] - offsets[r]),
-                      vertices + offsets[r]);
-        }
+        patch_long_walks(s, spec, list ? host_sources : nullptr, qb, n, stride, offsets, vertices);
     }
     if (on_block) {
         patched = true;
