@@ -353,6 +353,38 @@ void patch_long_walks(Session& s, const wf_query_spec& spec, const uint32_t* hos
     }
 }
 
+// WF_TRACE_HOST: the device timeline of one segment relative to its first
+// kernel's start (tev: kernel start / end, copies end; cev: per batch
+// compaction end, copy start, copy end); destroys the events.
+void print_segment_timeline(uint64_t s0, cudaEvent_t (&tev)[3], std::vector<cudaEvent_t>& cev, uint64_t nch,
+                            cudaEvent_t& ev_src) {
+    WF_CUDA(cudaEventSynchronize(tev[2]));
+    float kms = 0, cms = 0;
+    WF_CUDA(cudaEventElapsedTime(&kms, tev[0], tev[1]));
+    WF_CUDA(cudaEventElapsedTime(&cms, tev[0], tev[2]));
+    std::fprintf(stderr, "[run_host] segment %llu: kernel %.1f us, copies end %.1f us after kernel start\n",
+                 static_cast<unsigned long long>(s0), kms * 1e3, cms * 1e3);
+    if (ev_src) {
+        float sms = 0;
+        if (cudaEventElapsedTime(&sms, tev[0], ev_src) == cudaSuccess)
+            std::fprintf(stderr, "[run_host] sources resident %.1f us after kernel start\n", sms * 1e3);
+        cudaEventDestroy(ev_src);
+        ev_src = nullptr;
+    }
+    for (uint64_t k = 0; k < nch; ++k) {  // batches start at the chunks with events
+        float t[3] = {0, 0, 0};
+        bool any = false;
+        for (int i = 0; i < 3; ++i)
+            if (cudaEventElapsedTime(&t[i], tev[0], cev[3 * k + i]) == cudaSuccess) any = true;
+        if (!any) continue;
+        std::fprintf(stderr, "[run_host]   batch at chunk %llu: compacted %.1f us, copy %.1f -> %.1f us\n",
+                     static_cast<unsigned long long>(k), t[0] * 1e3, t[1] * 1e3, t[2] * 1e3);
+    }
+    cudaGetLastError();
+    for (cudaEvent_t e : cev) cudaEventDestroy(e);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+}
+
 void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sources, uint64_t qb,
                  uint64_t qe, uint64_t* offsets, uint32_t* vertices, uint64_t capacity, uint8_t* status,
                  uint64_t chunk, wf_run_metrics* metrics, uint32_t* records, wf_block_fn on_block,
@@ -650,31 +682,7 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
         WF_CUDA(cudaEventRecord(P.ev_copy, B));
         if (trace_on) {
             WF_CUDA(cudaEventRecord(tev[2], B));
-            WF_CUDA(cudaEventSynchronize(tev[2]));
-            float kms = 0, cms = 0;
-            WF_CUDA(cudaEventElapsedTime(&kms, tev[0], tev[1]));
-            WF_CUDA(cudaEventElapsedTime(&cms, tev[0], tev[2]));
-            std::fprintf(stderr, "[run_host] segment %llu: kernel %.1f us, copies end %.1f us after kernel start\n",
-                         static_cast<unsigned long long>(s0), kms * 1e3, cms * 1e3);
-            if (P.ev_trace_src) {
-                float sms = 0;
-                if (cudaEventElapsedTime(&sms, tev[0], P.ev_trace_src) == cudaSuccess)
-                    std::fprintf(stderr, "[run_host] sources resident %.1f us after kernel start\n", sms * 1e3);
-                cudaEventDestroy(P.ev_trace_src);
-                P.ev_trace_src = nullptr;
-            }
-            for (uint64_t k = 0; k < nch; ++k) {  // batches start at the chunks with events
-                float t[3] = {0, 0, 0};
-                bool any = false;
-                for (int i = 0; i < 3; ++i)
-                    if (cudaEventElapsedTime(&t[i], tev[0], cev[3 * k + i]) == cudaSuccess) any = true;
-                if (!any) continue;
-                std::fprintf(stderr, "[run_host]   batch at chunk %llu: compacted %.1f us, copy %.1f -> %.1f us\n",
-                             static_cast<unsigned long long>(k), t[0] * 1e3, t[1] * 1e3, t[2] * 1e3);
-            }
-            cudaGetLastError();
-            for (cudaEvent_t e : cev) cudaEventDestroy(e);
-            for (cudaEvent_t e : tev) cudaEventDestroy(e);
+            print_segment_timeline(s0, tev, cev, nch, P.ev_trace_src);
         }
         first_seg = false;
     }
