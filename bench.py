@@ -8,10 +8,14 @@ One "step" = one pass of the hot path over one batch of queries of the named
 configuration (BASELINE.json `configs`, SURVEY §8 d shorthand):
 
   c1  DeepWalk s16 weighted ALIAS, one walk per vertex, L=80
-  c2  PPR s20, NAIVE, 2^20 uniform random sources, stop 0.2, + visit counts  [default]
+  c2  PPR s20, NAIVE, 2^20 uniform random sources, stop 0.2, + visit counts
   c3  Node2Vec s22 (a=2, b=0.5) O-REJ, one walk per vertex, L=80
   c4  MetaPath s22, 5 labels, schema [i%5]x79, one walk per vertex
-  c5  DeepWalk s26 weighted ALIAS, 2^26 walks, L=80
+  c5  DeepWalk s26 weighted ALIAS, 2^26 walks, L=80                      [default]
+
+The default is C5, BASELINE.json's box-scale config for the 1/2/4/8-GPU sweep
+(the largest single-GPU configuration); C1-C4 are reported under
+`per_algorithm`, each with its own reference CPU baseline.
 
 Graphs are synthetic R-MAT (a,b,c,d = .57/.19/.19/.05, edge factor 16, seed 1)
 generated on the device; the paper's real graphs are not in this container.
@@ -23,16 +27,22 @@ e2e       same metric through the C-ABI call that returns walks in HOST memory
           of the step's source list from pinned host memory + D2H of the whole
           walk set (ragged) into pinned host memory; L2 flushed before each
           step as for `value` (small graphs).
-roofline  algorithmic bytes per launch (S_alg x moves) / mean launch time vs the
-          measured HBM copy bandwidth (MEASURED_PEAKS.json); measured_sectors:
-          BASELINE's definition, HBM bandwidth / measured DRAM bytes per move
-          (ncu, profiles/ncu_traffic.json).
+roofline  algorithmic bytes per launch (SURVEY §8 d S_alg x moves) / mean launch
+          time vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).  S_alg
+          is §8 d's per-move figure for the reference CSR layout (ALIAS / NAIVE
+          2.375 sectors = 76 B; O-REJ and MetaPath from instrumented logical
+          counts); `layout` gives the same for the decorated layouts this
+          engine uses; measured_sectors: HBM bandwidth / measured DRAM bytes per
+          move (ncu, profiles/ncu_traffic.json, stamped with the source hash it
+          was captured from; a capture of other sources is reported stale).
 cpu_baseline  the unmodified reference (oracle/_ref, run_interleaved k=64 k'=32,
           all host threads, no-op sink) on a bounded sample, rank 0 at N=1.
 
 Multi-GPU (torchrun): graph replicated per rank, queries sharded in contiguous
-qid blocks (worker_range, engine.hpp:296-298); every rank walks its own batch of
-the configured size (weak scaling); PPR visit counts are summed with one NCCL
+qid blocks (worker_range, engine.hpp:296-298).  One-walk-per-vertex configs
+(C1, C3-C5) split the fixed walk set over the ranks (strong scaling: BASELINE's
+"2^26 walks sharded evenly across GPUs"); C2 gives every rank its own batch of
+2^20 random sources (weak scaling); PPR visit counts are summed with one NCCL
 all-reduce inside the timed step.
 """
 from __future__ import annotations
@@ -56,19 +66,19 @@ SECTOR = 32
 CONFIGS = {
     "c1": dict(workload="C1 DeepWalk R-MAT s16 ef16, weighted f32 [1,5), ALIAS tables, one walk "
                         "per vertex, length 80, seed 1", scale=16, program="deepwalk", length=80,
-               weighted=True, labels=0, queries="per_vertex"),
+               weighted=True, labels=0, queries="per_vertex", scaling="strong"),
     "c2": dict(workload="C2 PPR R-MAT s20 ef16, unweighted, NAIVE, 2^20 uniform random sources, "
                         "stop 0.2, walks + visit counts", scale=20, program="ppr", weighted=False,
-               labels=0, queries="random", n_queries=1 << 20),
+               labels=0, queries="random", n_queries=1 << 20, scaling="weak"),
     "c3": dict(workload="C3 Node2Vec R-MAT s22 ef16, p=a=2 q=b=0.5, O-REJ, one walk per vertex, "
                         "length 80", scale=22, program="node2vec", length=80, weighted=False,
-               labels=0, queries="per_vertex"),
+               labels=0, queries="per_vertex", scaling="strong"),
     "c4": dict(workload="C4 MetaPath R-MAT s22 ef16, labels u8 {0..4}, f32 weights (unused), "
                         "schema [i%5]x79, one walk per vertex", scale=22, program="metapath",
-               weighted=True, labels=5, queries="per_vertex"),
+               weighted=True, labels=5, queries="per_vertex", scaling="strong"),
     "c5": dict(workload="C5 DeepWalk R-MAT s26 ef16, weighted f32 [1,5), ALIAS tables, 2^26 walks, "
                         "length 80", scale=26, program="deepwalk", length=80, weighted=True,
-               labels=0, queries="per_vertex"),
+               labels=0, queries="per_vertex", scaling="strong"),
 }
 
 # CPU-baseline samples (queries), sized for ~10-30 s of reference work on 16 cores
@@ -96,22 +106,68 @@ def row_capacity(cfg):
     return cfg["length"]
 
 
+def worker_range(n, workers, w):
+    """worker_range (engine.hpp:296-298) from the engine library (wf_worker_range),
+    or its formula where no library is built (CPU-only tests)."""
+    try:
+        from paper_2107_11983_b200 import engine as E
+        return E.worker_range(n, workers, w)
+    except (OSError, FileNotFoundError):
+        return n * w // workers, n * (w + 1) // workers
+
+
 def query_plan(cfg, V, rank, world):
-    """(QuerySpec over the whole job, qid_begin, qid_end) for this rank."""
+    """(QuerySpec over the whole job, qid_begin, qid_end) for this rank: the
+    job's contiguous worker_range shard (engine.hpp:296-298)."""
     from paper_2107_11983_b200.host import QuerySpec
     if cfg["queries"] == "random":
-        per = cfg["n_queries"]
-        total = per * world  # weak scaling: each rank its own batch of 2^20
+        # weak scaling: the job is world batches of 2^20 random sources, so
+        # every rank's shard is one batch
+        total = cfg["n_queries"] * world
         src = np.random.default_rng(1).integers(0, V, total, dtype=np.uint32)
         spec = QuerySpec.from_list(src)
-        lo, hi = per * rank, per * (rank + 1)
     else:
         # one walk per vertex; the vertex list is sharded (C5: 2^26 walks split
         # evenly).  FROM_LIST with sources[q] = q is the same walk set as
         # one_per_vertex and gives the e2e path a real H2D input.
         spec = QuerySpec.from_list(np.arange(V, dtype=np.uint32))
-        lo, hi = V * rank // world, V * (rank + 1) // world
+    lo, hi = worker_range(spec.count, world, rank)
     return spec, lo, hi
+
+
+def make_comm(dist, rank, world, device):
+    """The engine's own NCCL communicator (wf_comm_*) for the PPR visit-count
+    reduction: rank 0's id travels over the torch process group (plumbing
+    only); the reduction itself is the library's ncclAllReduce."""
+    if dist is None:
+        return None
+    from paper_2107_11983_b200 import engine as E
+    obj = [E.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return E.Comm(obj[0], world, rank, device)
+
+
+def reduce_counts(counts, comm, dist, stream=0):
+    """Sum the ranks' visit-count vectors in place: the path's one collective
+    (SURVEY 8(e)).  On GPUs through the library communicator; without one
+    (CPU tests, gloo) through the process group."""
+    if comm is not None:
+        comm.allreduce_u32(counts.data_ptr(), counts.numel(), stream)
+    elif dist is not None and dist.get_world_size() > 1:
+        dist.all_reduce(counts)
+
+
+def combine_ranks(dist, device, total_ms, e2e_s, e2e_off_s, moves):
+    """Max over ranks of the device times, sum of the moves (the contract's
+    whole-job value)."""
+    if dist is None:
+        return total_ms, e2e_s, e2e_off_s, moves
+    import torch
+    t = torch.tensor([total_ms, e2e_s or 0.0, e2e_off_s or 0.0], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    mv = torch.tensor([moves], dtype=torch.int64, device=device)
+    dist.all_reduce(mv)
+    return float(t[0]), float(t[1]), float(t[2]), int(mv.item())
 
 
 def measured_peak():
@@ -175,21 +231,25 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def s_alg_bytes(cfg, stats, moves, layout, walks=0):
-    """Algorithmic 32 B sectors per move (SURVEY §8 d) for the layout the
-    session actually uses (abi.HAS_*), plus the random requests per move.
+def s_alg(cfg, stats, moves, layout, steps=None):
+    """Algorithmic 32 B sectors per move, two ways.
 
-    DeepWalk ALIAS: wide 32 B bucket (carries the destination's vertex word)
-    = 1 sector, else 16 B bucket + 8 B vertex word = 2.  PPR NAIVE: decorated
-    adjacency entry = 1, else neighbour + vertex word = 2.  MetaPath ITS:
-    successor-decorated partitioned edge = 1, else 32 B label record +
-    neighbour = 2.  Node2Vec O-REJ: one adjacency sector per trial + the
-    instrumented search probes (+1 vertex word without the decorated
-    adjacency).  Every move also writes 4 B of path = 1/8 sector.  PPR's
-    visit counts add one 4 B read-modify-write (one sector request) per
-    emitted vertex: (moves + walks) / moves per move."""
+    ref (SURVEY §8 d, the figure `roofline.frac` uses): the reference's CSR
+    layout, no cache reuse, no overfetch.
+      ALIAS (C1, C5) and NAIVE (C2): offsets pair 1.25 + bucket / neighbour 1
+        + path 1/8 = 2.375 sectors = 76 B (PPR's visit counts live in L2 and
+        are not counted).
+      O-REJ (C3): 1.25 + per trial (1 neighbour + ceil(log2(d_prev + 1))
+        binary-search probes when the reference's weight() tests adjacency)
+        + 1/8, from the instrumented counters (`ref_probes`).
+      MetaPath (C4): per step 1.25 + ceil(d_v / 32) label sectors, per move
+        + 1 neighbour + 1/8 (`ref_label_sectors`, `steps`).
+    layout: the same count for the decorated layouts this engine uses (abi.HAS_*).
+    Returns dict(ref=sectors, ref_model=text, layout=sectors, layout_model=text,
+    requests=random requests per move)."""
     from paper_2107_11983_b200 import abi
     p = cfg["program"]
+    mv = max(moves, 1)
     one = {"deepwalk": abi.HAS_WIDE_ALIAS, "ppr": abi.HAS_ADJ, "metapath": abi.HAS_MP_SUCC}
     if p in one:
         reads = 1.0 if layout & one[p] else 2.0
@@ -201,19 +261,34 @@ def s_alg_bytes(cfg, stats, moves, layout, walks=0):
             desc = {"deepwalk": "16 B alias bucket + 8 B vertex word",
                     "ppr": "4 B neighbour + 8 B vertex word",
                     "metapath": "32 B label record + 4 B partitioned neighbour"}[p]
-        if p == "ppr" and walks:
-            cnt = (moves + walks) / max(moves, 1)
-            text = f"{desc} + {cnt:.3f} visit-count sectors + 1/8 path = {reads + cnt + 0.125:.3f} sectors"
-            return (reads + cnt + 0.125) * SECTOR, text, reads + cnt
-        text = f"{desc} + 1/8 path = {reads + 0.125:.3f} sectors"
+        lay, lay_text = reads + 0.125, f"{desc} + 1/8 path = {reads + 0.125:.3f} sectors"
     else:
-        trials = stats["trials"] / max(moves, 1)
-        probes = stats["probes"] / max(moves, 1)
+        trials = stats.get("trials", 0) / mv
+        probes = stats.get("probes", 0) / mv
         base = 0.0 if layout & abi.HAS_ADJ else 1.0
         reads = base + trials + probes
-        text = (f"{trials:.3f} trial adjacency sectors + {probes:.3f} search probe sectors"
-                f"{' + vertex word' if base else ''} + 1/8 path = {reads + 0.125:.3f} sectors")
-    return (reads + 0.125) * SECTOR, text, reads
+        lay = reads + 0.125
+        lay_text = (f"{trials:.3f} trial adjacency sectors + {probes:.3f} filter/hash sectors"
+                    f"{' + vertex word' if base else ''} + 1/8 path = {lay:.3f} sectors")
+    if p in ("deepwalk", "ppr"):
+        ref = 2.375
+        ref_text = ("SURVEY 8(d): offsets pair 1.25 + " + ("16 B alias bucket" if p == "deepwalk" else "neighbour")
+                    + " 1 + path 1/8 = 2.375 sectors = 76 B per move")
+    elif p == "node2vec" and "ref_probes" in stats:
+        trials = stats["trials"] / mv
+        rp = stats["ref_probes"] / mv
+        ref = 1.25 + trials + rp + 0.125
+        ref_text = (f"SURVEY 8(d): offsets 1.25 + {trials:.3f} trial neighbour sectors + {rp:.3f} binary-search "
+                    f"probes (instrumented ceil(log2(d_prev+1)) per adjacency test) + 1/8 = {ref:.3f} sectors")
+    elif p == "metapath" and "ref_label_sectors" in stats and steps:
+        st = steps / mv
+        ls = stats["ref_label_sectors"] / mv
+        ref = 1.25 * st + ls + 1.0 + 0.125
+        ref_text = (f"SURVEY 8(d): offsets 1.25 x {st:.3f} steps + {ls:.3f} label sectors (instrumented "
+                    f"ceil(d_v/32) per step) + neighbour 1 + 1/8 = {ref:.3f} sectors")
+    else:
+        ref, ref_text = lay, "no instrumented reference counts: layout figure"
+    return dict(ref=ref, ref_model=ref_text, layout=lay, layout_model=lay_text, requests=reads)
 
 
 def random_access_block(moves_per_s, reads_per_move):
@@ -234,11 +309,93 @@ def random_access_block(moves_per_s, reads_per_move):
                     "requests served by L2 (hot vertices, search index) can push frac above 1"}
 
 
+def source_sha():
+    from paper_2107_11983_b200.build import source_hash
+    return source_hash()
+
+
+def ncu_traffic():
+    """profiles/ncu_traffic.json: DRAM bytes (read + write) per walk-kernel launch
+    and per move, from ncu captures of each config at its tuned grid, stamped
+    with the library source hash they were captured from."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def traffic_for(key, moves):
+    """(bytes per launch, bytes per move, stamp) of the committed capture for
+    this config; None values when missing or captured from other sources."""
+    t = ncu_traffic()
+    ent = t.get("configs", {}).get(key)
+    cur = source_sha()
+    stamp = {"captured_src_sha": (ent or {}).get("src_sha"), "current_src_sha": cur,
+             "source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, "
+                       "one ncu launch of this config's walk kernel at its tuned grid)"}
+    if not ent:
+        stamp["stale"] = None
+        return None, None, stamp
+    stamp["stale"] = ent.get("src_sha") != cur
+    stamp["captured_moves"] = ent.get("moves")
+    if stamp["stale"] or ent.get("moves") != moves:
+        if ent.get("moves") != moves:
+            stamp["note"] = "capture ran a different number of moves"
+        return None, None, stamp
+    return ent["bytes"], ent["bytes"] / moves, stamp
+
+
+# What bounds each config's walk kernel (DESIGN.md 5.1, 6.1); the numbers in
+# the note are computed from the run and the stamped capture (bound_note).
+BOUND_CAUSE = {
+    "c1": "the graph is L2-resident; the 65 Ki walks' dependent L2 chains bound it",
+    "c2": "the bulk saturates the L2/atomic queue and the longest geometric walks finish in an unloaded tail",
+    "c3": "one 128 B DRAM line per O-REJ trial (adjacency entry) plus the L2-resident pair filter",
+    "c4": "one 128 B DRAM line per move (successor-decorated partitioned edge)",
+    "c5": "one 128 B DRAM line per move (wide alias bucket)",
+}
+
+
+def bound_note(key, moves_per_s, bytes_per_move, peak):
+    cause = BOUND_CAUSE.get(key, "")
+    if bytes_per_move is None:
+        return f"{cause}; no current ncu capture for these sources, DRAM rate not computed"
+    dram = moves_per_s * bytes_per_move / 1e9
+    f = dram / peak
+    kind = "DRAM-bound" if f >= 0.6 else "not DRAM-bound"
+    return (f"{kind}: {cause}. ncu measured {bytes_per_move:.1f} B of DRAM traffic per move "
+            f"({bytes_per_move / SECTOR:.2f} sectors); at this run's rate that is {dram:.0f} GB/s "
+            f"= {f:.1%} of the measured copy bandwidth")
+
+
+def roofline_block(key, cfg, r, moves, ms_per_launch, peak, peak_kind):
+    """The line's roofline object for one config (see the module docstring)."""
+    sa = s_alg(cfg, r["stats"], moves, r["layout"], steps=r.get("step_attempts") or r["stats"].get("step_attempts"))
+    launch_s = ms_per_launch * 1e-3
+    rate = moves / launch_s
+    ach = moves * sa["ref"] * SECTOR / launch_s / 1e9
+    lay = moves * sa["layout"] * SECTOR / launch_s / 1e9
+    traffic, bpm, stamp = traffic_for(key, moves)
+    return {
+        "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+        "traffic": traffic,
+        "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+        "bytes_per_move": sa["ref"] * SECTOR, "bytes_model": sa["ref_model"],
+        "layout": {"bytes_per_move": sa["layout"] * SECTOR, "model": sa["layout_model"],
+                   "achieved": lay, "frac": lay / peak},
+        "measured_sectors": None if bpm is None else {
+            "bytes_per_move": bpm, "ceiling_steps_per_s": peak / bpm * 1e9,
+            "frac": rate / (peak / bpm * 1e9)},
+        "traffic_stamp": stamp,
+        "note": bound_note(key, rate, bpm, peak),
+    }, sa
+
 def flush_l2(buf):
     buf.add_(1)
 
 
-def run_ours(args, cfg, rank, world, local_rank, dist):
+def run_ours(args, cfg, rank, world, local_rank, dist, comm=None):
     import torch
 
     from paper_2107_11983_b200 import engine as E
@@ -287,8 +444,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             graph.replay()
         else:
             device_step()
-        if counts is not None and dist is not None:
-            dist.all_reduce(counts)  # NCCL: the one collective of the path
+        if counts is not None:
+            reduce_counts(counts, comm, dist, torch.cuda.current_stream().cuda_stream)
 
     # launch tuner (wf_session_tune, the device analogue of the reference's
     # tune_ring_sizes): picks blocks/SM for launches of this size; untimed
@@ -359,8 +516,11 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         for _ in range(1):
             sess.run_host(hspec, h_off.data_ptr(), h_vert.data_ptr(), cap, h_stat.data_ptr(),
                           qid_begin=lo, qid_end=hi)
+        # the offsets form is a secondary API: a few steps suffice when a step
+        # moves gigabytes (C5: 11 GB)
+        off_steps = args.steps if n * stride * 4 < (1 << 30) else min(args.steps, 3)
         e2e_s = []
-        for _ in range(args.steps):
+        for _ in range(off_steps):
             if l2buf is not None:
                 flush_l2(l2buf)  # cold L2 for every timed step, as for `value`
             if dist:
@@ -372,7 +532,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             e2e_s.append(time.perf_counter() - t0)
         total_vertices = int(h_off[n].item())
         assert m.total_steps == moves_per_step
-        e2e_off = dict(seconds=float(sum(e2e_s)), h2d=n * 4, d2h=total_vertices * 4 + (n + 1) * 8 + n,
+        e2e_off = dict(seconds=float(sum(e2e_s)), steps=off_steps, h2d=n * 4, d2h=total_vertices * 4 + (n + 1) * 8 + n,
                        api="wf_session_run_host (offsets u64 + status u8, pinned host buffers)")
         # the records form (length | status << 31 per query, walker.hpp:47-55's
         # WalkRecord without the implicit qid): 4 B per query instead of 9
@@ -390,7 +550,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             e2e_s.append(time.perf_counter() - t0)
         assert m.total_steps == moves_per_step
         assert int((h_rec.numpy().view(np.uint32) & 0x7FFFFFFF).astype(np.int64).sum()) == total_vertices
-        e2e = dict(seconds=float(sum(e2e_s)), h2d=n * 4, d2h=total_vertices * 4 + n * 4,
+        e2e = dict(seconds=float(sum(e2e_s)), steps=args.steps, h2d=n * 4, d2h=total_vertices * 4 + n * 4,
                    api="wf_session_run_host_records (pinned host buffers)", offsets_api=e2e_off)
         del hspec_c_sources
 
@@ -436,66 +596,37 @@ def cpu_baseline(key, cfg, dg, spec, threads=None):
                        f"no-op sink, one warm-up run")
 
 
-# What bounds each config's walk kernel: carried in the
-# bench line so the fractions read with their cause.
-ROOFLINE_NOTES = {
-    "c1": "L2-resident graph (58 MB of buckets): bound by the 65 Ki walks' dependent L2 chains, not HBM",
-    "c2": "latency/tail-bound, not bandwidth-bound: the bulk saturates near 30 G moves/s at 3 blocks/SM "
-          "(DRAM ~2.9 TB/s), and the longest geometric walks finish in the unloaded tail; the HBM-resident "
-          "configs reach 0.75-0.86 of the measured-sector ceiling (per_algorithm.c3-c5)",
-    "c3": "DRAM-bound: one 128 B line per O-REJ trial, ~4.9 TB/s",
-    "c4": "DRAM-bound: one 128 B line per move (successor-decorated edges), ~5.0 TB/s",
-    "c5": "DRAM-bound: one 128 B line per move (wide alias buckets), 5.6 TB/s = 86% of the copy bandwidth",
-}
-
-
-def ncu_traffic():
-    """profiles/ncu_traffic.json: DRAM bytes (read + write) per walk-kernel launch
-    and per move, from ncu captures of each config at its tuned grid."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f)
-    except Exception:
-        return {}
-
-
-def measured_sectors_block(key, moves_per_s, peak):
-    """BASELINE's roofline: HBM bandwidth / measured DRAM bytes per step (ncu,
-    cold cache; every random 32 B request that misses L2 costs a 128 B line)."""
-    bpm = ncu_traffic().get(f"{key}_bytes_per_move")
-    if not bpm:
-        return None
-    ceiling = peak / bpm * 1e9
-    return {"bytes_per_move": bpm, "ceiling_steps_per_s": ceiling, "frac": moves_per_s / ceiling,
-            "source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
-
-
 def extras(args, rank, world, local_rank, dist):
-    """GPU-only numbers for the other configs (not bench lines; evidence)."""
+    """GPU numbers for the other configs (not bench lines; evidence), each with
+    its own reference CPU baseline."""
     out = {}
-    for key in ["c1", "c3", "c4", "c5"]:
+    peak, peak_kind = measured_peak()
+    for key in ["c1", "c2", "c3", "c4", "c5"]:
         if key == args.config:
             continue
         try:
             # e2e evidence too, except for C5 (10.9 GB of pinned host buffers per step)
             a = argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 1, "no_e2e": key == "c5"})
-            r = run_ours(a, CONFIGS[key], rank, world, local_rank, dist)
+            cfg = CONFIGS[key]
+            r = run_ours(a, cfg, rank, world, local_rank, dist)
             ms = r["total_ms"] / 3
-            b, bdesc, reads = s_alg_bytes(CONFIGS[key], r["stats"], r["moves"], r["layout"])
-            peak, _ = measured_peak()
-            ach = r["moves"] * b / (ms * 1e-3) / 1e9
+            roof, sa = roofline_block(key, cfg, r, r["moves"], ms, peak, peak_kind)
             rate = r["moves"] / (ms * 1e-3)
-            out[key] = dict(workload=CONFIGS[key]["workload"], steps_per_s=rate, blocks_per_sm=r["tuned"],
-                            ms_per_step=ms, moves=r["moves"], achieved_gbs=ach,
-                            roofline_frac=ach / peak, bytes_per_move=b, bytes_model=bdesc,
-                            measured_sectors=measured_sectors_block(key, rate, peak),
-                            note=ROOFLINE_NOTES.get(key),
-                            e2e=None if not r["e2e"] else {
-                                "value": r["moves"] * 3 / r["e2e"]["seconds"], "unit": "steps/s",
-                                "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"],
-                                "api": r["e2e"]["api"]},
-                            random_access=random_access_block(rate, reads),
-                            E=r["info"]["E"])
+            ent = dict(workload=cfg["workload"], steps_per_s=rate, blocks_per_sm=r["tuned"],
+                       ms_per_step=ms, moves=r["moves"], roofline=roof,
+                       e2e=None if not r["e2e"] else {
+                           "value": r["moves"] * r["e2e"]["steps"] / r["e2e"]["seconds"], "unit": "steps/s",
+                           "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"],
+                           "api": r["e2e"]["api"]},
+                       random_access=random_access_block(rate, sa["requests"]),
+                       preprocess_seconds=r["preprocess_s"], E=r["info"]["E"])
+            if not args.no_cpu and key != "c5":
+                try:
+                    ent["cpu_baseline"] = cpu_baseline(key, cfg, r["dg"], r["spec"])
+                    ent["vs_cpu_baseline"] = rate / ent["cpu_baseline"]["value"]
+                except Exception as e:
+                    ent["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {e}"}
+            out[key] = ent
             del r
             import torch
             torch.cuda.empty_cache()
@@ -505,61 +636,63 @@ def extras(args, rank, world, local_rank, dist):
 
 
 def reference_arm(args, cfg, rank, world):
-    """--impl reference: the reference's own CPU path, rank 0 only."""
+    """--impl reference: the reference's own CPU path, rank 0 only.  Its input
+    is built on the CPU (RefOracle.rmat: the oracle's C R-MAT, bit-identical
+    to the device generator, handed straight to Graph::from_csr); no engine
+    code runs on this arm."""
     if rank != 0:
         return
     from oracle.oracle import PortOracle, RefOracle, ref_available
-    from paper_2107_11983_b200 import engine as E
     from paper_2107_11983_b200.host import ExecOptions, QuerySpec
     threads = os.cpu_count()
-    # input preparation: the same seeded R-MAT CSR the GPU arm walks on, built
-    # on the CPU by the oracle's C restatement of the generator (bit-identical
-    # to the device build, tests/test_rmat_cpu.py) so no engine code runs on
-    # this arm; s26 (2.1 B edges) is built on the device and downloaded.
-    if cfg["scale"] <= 24:
+    t0 = time.time()
+    kind = "reference" if ref_available() else "port"
+    if kind == "reference":
+        rg = RefOracle().rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
+                              label_count=cfg["labels"])
+        info = rg.info()
+        V, E_count = info["V"], info["E"]
+    else:
         hg = PortOracle().rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
                                label_count=cfg["labels"])
-        graph_source = "CPU R-MAT (oracle/wf_oracle.c)"
-    else:
-        dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
-                                label_count=cfg["labels"], device=0)
-        hg = dg.download()
-        del dg
-        graph_source = "device R-MAT, downloaded"
-    V = hg.vertex_count
+        V, E_count = hg.vertex_count, hg.edge_count
+    graph_s = time.time() - t0
     spec, lo, hi = query_plan(cfg, V, 0, 1)
-    m = min(CPU_SAMPLE[args.config], hi - lo)
-    sample = QuerySpec.from_list(spec.sources[:m])
+    # Every run_interleaved call rebuilds the static tables (ResolvedRun,
+    # engine.hpp:275-294; 39 s at C5), so the K steps run as ONE call over K
+    # consecutive samples of m queries (preprocessing excluded from the metric,
+    # engine.hpp:455,498, as in the reference), after one warm-up call over one
+    # sample (first-touch page faults, SURVEY 8(d)).
+    n_all = hi - lo
+    m = min(CPU_SAMPLE[args.config], max(1, n_all // max(args.steps, 1)))
     prog = program_of(cfg)
     opts = ExecOptions(seed=1, threads=threads)
-    kind = "reference" if ref_available() else "port"
-    E_count = hg.edge_count
-    if kind == "reference":
-        rg = RefOracle().graph(hg)
-        del hg
-        run = lambda: rg.run(sample, prog, opts, interleaved=True, discard=True)  # noqa: E731
-    else:
-        po = PortOracle()
-        run = lambda: po.run(hg, sample, prog, opts, threads=threads, discard=True)  # noqa: E731
-    for _ in range(args.warmup):
-        run()
-    moves = 0
-    secs = 0.0
-    for _ in range(args.steps):
-        r = run()
-        moves += r.metrics.total_steps
-        secs += r.metrics.exec_seconds
+
+    def run(queries):
+        sample = QuerySpec.from_list(spec.sources[:queries])
+        if kind == "reference":
+            return rg.run(sample, prog, opts, interleaved=True, discard=True)
+        return PortOracle().run(hg, sample, prog, opts, threads=threads, discard=True)
+
+    if args.warmup > 0:
+        run(m)
+    r = run(m * args.steps)
+    moves, secs, pre = r.metrics.total_steps, r.metrics.exec_seconds, r.metrics.preprocess_seconds
     value = moves / secs
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic R-MAT",
-        "config": {"workload": cfg["workload"], "sample_queries": m, "graph": graph_source,
-                   "edges": int(E_count)},
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic R-MAT",
+        "config": {"workload": cfg["workload"], "sample_queries_per_step": m,
+                   "graph": "CPU R-MAT (oracle/wf_oracle.c wfo_rmat_csr, bit-identical to the device build) "
+                            "-> Graph::from_csr", "graph_build_seconds": graph_s,
+                   "vertices": int(V), "edges": int(E_count)},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": kind,
-                         "sample": f"first {m} queries per step, run_interleaved k=64 k'=32, "
-                                   f"no-op sink, preprocessing excluded (engine.hpp:455,498)"},
+                         "sample": f"{args.steps} steps of {m} queries (the first {m * args.steps} of the "
+                                   f"config's queries) in one run_interleaved call, k=64 k'=32, no-op sink, "
+                                   f"preprocessing ({pre:.2f} s) excluded (engine.hpp:455,498); one warm-up "
+                                   f"call over {m} queries"},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -571,7 +704,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -597,66 +730,45 @@ def main():
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
         dist = tdist
+    comm = make_comm(dist, rank, world, local_rank) if cfg["program"] == "ppr" else None
 
-    r = run_ours(args, cfg, rank, world, local_rank, dist)
+    r = run_ours(args, cfg, rank, world, local_rank, dist, comm)
     total_ms = r["total_ms"]
     moves = r["moves"]
     e2e_s = r["e2e"]["seconds"] if r["e2e"] else None
     e2e_off_s = r["e2e"]["offsets_api"]["seconds"] if r["e2e"] else None
-    if dist:
-        t = torch.tensor([total_ms, e2e_s or 0.0, e2e_off_s or 0.0], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_max, e2e_off_max = float(t[0]), float(t[1]), float(t[2])
-        mv = torch.tensor([moves], dtype=torch.int64, device="cuda")
-        dist.all_reduce(mv)
-        all_moves = int(mv.item())
-    else:
-        e2e_max, e2e_off_max = e2e_s, e2e_off_s
-        all_moves = moves
+    total_ms, e2e_max, e2e_off_max, all_moves = combine_ranks(dist, "cuda", total_ms, e2e_s, e2e_off_s, moves)
     value = all_moves * args.steps / (total_ms * 1e-3)
 
     peak, peak_kind = measured_peak()
-    b, b_desc, reads = s_alg_bytes(cfg, r["stats"], moves, r["layout"], walks=r["n"])
-    mean_launch_s = total_ms / args.steps * 1e-3
-    achieved = moves * b / mean_launch_s / 1e9
-    traffic = ncu_traffic().get(args.config)
+    roof, sa = roofline_block(args.config, cfg, r, moves, total_ms / args.steps, peak, peak_kind)
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "int64+f64",
         "data": "synthetic R-MAT (seed 1) generated on device; paper graphs not available",
         "config": {"workload": cfg["workload"], "queries_per_gpu": r["n"],
                    "vertices": r["info"]["V"], "edges": r["info"]["E"],
                    "sampler": r["sampler"], "flow": r["flow"],
-                   "parallelism": f"query shards x{world}, graph replicated",
+                   "parallelism": f"query shards x{world}, graph replicated"
+                                  + (", visit counts summed by the engine's ncclAllReduce (wf_comm)" if comm else ""),
                    "l2": "flushed between steps (256 MiB write)" if cfg["scale"] <= 20
                    else "inputs larger than L2",
                    "launch": "host launch per step" if args.no_graph
                    else "CUDA graph replay per step (counter resets + walk kernel)",
                    "blocks_per_sm": r["tuned"] if r["tuned"] is not None else "occupancy max (untuned)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "bytes_per_move": b, "bytes_model": b_desc,
-                     "note": ROOFLINE_NOTES.get(args.config),
-                     # BASELINE's own definition: HBM bandwidth / measured DRAM
-                     # bytes per step (ncu, cold cache, includes the 128 B line
-                     # fetched for every 32 B random request)
-                     "measured_sectors": None if not traffic else {
-                         "bytes_per_move": traffic / moves,
-                         "ceiling_steps_per_s": peak / (traffic / moves) * 1e9,
-                         "frac": value / world / (peak / (traffic / moves) * 1e9)}},
-        "random_access": random_access_block(moves * args.steps / (total_ms * 1e-3), reads),
+        "roofline": roof,
+        "random_access": random_access_block(moves * args.steps / (total_ms * 1e-3), sa["requests"]),
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "preprocess_seconds": r["preprocess_s"],
     }
     if r["e2e"]:
         eo = r["e2e"]["offsets_api"]
-        line["e2e"] = {"value": all_moves * args.steps / e2e_max, "unit": "steps/s",
+        line["e2e"] = {"value": all_moves * r["e2e"]["steps"] / e2e_max, "unit": "steps/s",
                        "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"],
-                       "api": r["e2e"]["api"],
-                       "offsets_api": {"value": all_moves * args.steps / e2e_off_max,
+                       "steps": r["e2e"]["steps"], "api": r["e2e"]["api"],
+                       "offsets_api": {"value": all_moves * eo["steps"] / e2e_off_max, "steps": eo["steps"],
                                        "h2d_bytes_per_step": eo["h2d"], "d2h_bytes_per_step": eo["d2h"],
                                        "api": eo["api"]}}
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -170,6 +170,8 @@ typedef struct wf_walkset wf_walkset; /* WalkSet + RunMetrics (engine.hpp:71-74,
 /* ---- library ---------------------------------------------------------------- */
 int wf_abi_version(void);
 const char* wf_last_error(void);
+/* Visible CUDA devices (ExecOptions::threads -> device count in the C++ shim). */
+int wf_device_count(int32_t* n);
 /* Number of engine kernel launches since load (evidence for bench's gpu_launches). */
 uint64_t wf_kernel_launches(void);
 
@@ -225,6 +227,51 @@ int wf_graph_original_ids(const wf_graph* g, uint64_t* out);
  * static tables on the device (preprocess_static, engine.hpp:190-251). */
 int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_exec_options* opts,
                       wf_session** out);
+/* ---- custom device programs: the WalkProgram concept (program.hpp:49-93) -----
+ * The reference's extension point is a C++ type with walker_type(),
+ * weight(const Walker*, const EdgeRef&), update(Walker&, const EdgeRef&) and
+ * optional max_weight() / preferred_sampler() / finished() (program.hpp:49-93;
+ * its own tests write CountingProgram, AvoidVertexProgram and
+ * NegativeWeightProgram that way, tests/test_engine.cpp:17-47).  Here such a
+ * type has __device__ members and is compiled in the USER's .cu translation
+ * unit against include/walkforge_b200/device_program.cuh, whose
+ * WF_DEVICE_PROGRAM(Type, symbol) instantiates the walk kernel for it and
+ * exports `const wf_program_ops* symbol(void)`: the table below.  The library
+ * never needs to know the type; the user's code launches its own kernels on
+ * the library's streams through it (kernels live where they are compiled). */
+typedef struct wf_program_ops {
+    uint32_t abi_version;      /* WF_ABI_VERSION of the header the table was built with */
+    uint32_t launch_size;      /* sizeof(wf::WalkLaunch) it was built with (checked) */
+    const char* name;          /* the program type's name */
+    int32_t walker_type;       /* 0 unbiased, 1 static, 2 dynamic (WalkerType, program.hpp:17) */
+    int32_t preferred_sampler; /* wf_sampler, or WF_SAMPLER_DEFAULT (SamplerPreferringProgram) */
+    int32_t has_max_weight;    /* BoundedWeightProgram (required for O-REJ) */
+    int32_t prechecked;        /* PreCheckedProgram: finished() before the first move */
+    uint32_t program_size;     /* bytes of the program object (<= 256, trivially copyable) */
+    uint32_t reserved;
+    /* Launches walk_kernel<Custom<Type>, sampler, flow, streaming> with `grid`
+     * blocks on `stream`; `walk_launch` is the engine's launch record. */
+    int (*launch)(const void* walk_launch, int32_t sampler, int32_t flow, int32_t streaming, int32_t grid,
+                  void* stream);
+    /* Resident blocks per SM and registers per thread of that kernel. */
+    int (*occupancy)(int32_t sampler, int32_t flow, int32_t streaming, int32_t* blocks_per_sm, int32_t* regs);
+    /* weight(nullptr, e) of every edge into out[E] (static tables,
+     * preprocess_static, engine.hpp:190-251); *bad (device int) is set when a
+     * weight is negative or not finite (check_program_weight, engine.hpp:97-101). */
+    int (*static_weights)(const void* graph_view, const void* program, double* out, int32_t* bad, void* stream);
+    /* max_weight() on the host (resolve_orej_bound, engine.hpp:103-114). */
+    double (*max_weight)(const void* program);
+    /* max_path_vertices(): an upper bound on a walk's vertices (the row
+     * capacity of fixed-length programs); 0 = unbounded. */
+    uint32_t (*max_path)(const void* program);
+} wf_program_ops;
+
+/* ResolvedRun for a custom program: `program` points to the program object
+ * (program_size bytes, copied).  Everything else is as wf_session_create;
+ * the session works with every run / launch / streaming / tune entry point. */
+int wf_session_create_custom(const wf_graph* g, const wf_program_ops* ops, const void* program,
+                             const wf_exec_options* opts, wf_session** out);
+
 /* Resolved sampler and flow (0 Direct, 1 Tables, 2 Gathered). */
 int wf_session_describe(const wf_session* s, int32_t* sampler, int32_t* flow,
                         double* preprocess_seconds);
@@ -319,6 +366,13 @@ int wf_session_run_host_blocks(wf_session* s, const wf_query_spec* spec, uint64_
  * probes, out[2] edges scanned by per-step gathers.  Reading resets them. */
 int wf_session_set_stats(wf_session* s, int enable);
 int wf_session_stats(wf_session* s, uint64_t* out3);
+/* All counters (n <= WF_STATS_COUNT): out[3] binary-search probes the
+ * reference's Node2Vec weight() would make (ceil(log2(d_prev + 1)) per
+ * adjacency test), out[4] u8-label sectors the reference's
+ * MetaPath gather would scan (ceil(d_v / 32) per step), out[5] MetaPath step
+ * attempts (moves + dead ends).  Reading resets them. */
+#define WF_STATS_COUNT 6
+int wf_session_stats_n(wf_session* s, uint64_t* out, uint32_t n);
 
 /* Launch tuner: the device analogue of tune_ring_sizes (tune.cpp:46-111).  The
  * reference sweeps the interleave ring sizes (k, k') for its CPU; on the device
@@ -331,6 +385,54 @@ int wf_session_stats(wf_session* s, uint64_t* out3);
  * results never depend on it.  Out: the chosen blocks/SM and its time. */
 int wf_session_tune(wf_session* s, const wf_query_spec* spec, uint64_t qid_begin, uint64_t qid_end,
                     int32_t* blocks_per_sm, double* best_ms);
+
+/* ---- multi-GPU: run_*'s workers over devices --------------------------------
+ * The reference splits a run into ExecOptions::threads workers, each a
+ * contiguous qid block (worker_range, engine.hpp:296-298) on its own thread
+ * (parallel_workers, engine.hpp:302-328), each block handed to the BlockSink
+ * once, in worker order (engine.hpp:76-79).  Here the blocks are spread over
+ * devices in contiguous groups: the graph is replicated on every listed device
+ * (peer copies), the static tables are built once and peer-copied, one host
+ * thread per device walks its blocks, and the calling thread receives the
+ * blocks in worker order as they complete.  Output equals the single-device
+ * run (walks depend only on (seed, qid)).  The one collective is an NCCL
+ * all-reduce of the PPR visit counts (NCCL is loaded at run time); a device
+ * listed twice shares nothing with NCCL, and its shards' counts are summed on
+ * the device instead. */
+typedef struct wf_multi wf_multi;
+/* worker_range (engine.hpp:296-298): [n*w/W, n*(w+1)/W). */
+int wf_worker_range(uint64_t n, uint32_t workers, uint32_t w, uint64_t* begin, uint64_t* end);
+int wf_multi_create(const wf_graph* g, const int32_t* devices, uint32_t n_devices, const wf_program_desc* prog,
+                    const wf_exec_options* opts, wf_multi** out);
+int wf_multi_create_custom(const wf_graph* g, const int32_t* devices, uint32_t n_devices,
+                           const wf_program_ops* ops, const void* program, const wf_exec_options* opts,
+                           wf_multi** out);
+/* collective: 1 when the visit counts are reduced with NCCL */
+int wf_multi_info(const wf_multi* m, uint32_t* n_devices, int32_t* collective);
+/* One worker block: records u32[qid_end - qid_begin] (length | status << 31)
+ * and the paths back to back (n_vertices), valid during the call.  Non-zero
+ * return stops the run (WF_ERR_IO). */
+typedef int (*wf_shard_fn)(void* user, uint32_t worker, uint64_t qid_begin, uint64_t qid_end,
+                           const uint32_t* records, const uint32_t* vertices, uint64_t n_vertices);
+/* Runs every query of `spec` as `workers` blocks (0 = one per device);
+ * visit_counts (host or device, u32[V], or NULL): PPR occurrence counts over
+ * all paths, reduced over the devices. */
+int wf_multi_run(wf_multi* m, const wf_query_spec* spec, uint32_t workers, wf_shard_fn on_shard, void* user,
+                 uint32_t* visit_counts, wf_run_metrics* metrics);
+void wf_multi_destroy(wf_multi* m);
+
+/* One process per GPU (torchrun): each rank runs its worker_range shard with
+ * the single-device API and reduces its visit counts through the library's
+ * own NCCL communicator.  Rank 0 makes the id; the caller ships it to the
+ * other ranks (any channel). */
+#define WF_COMM_ID_BYTES 128
+typedef struct wf_comm wf_comm;
+int wf_comm_unique_id(uint8_t* id);
+int wf_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, int32_t device, wf_comm** out);
+/* In-place sum over the ranks of a device u32 vector, on `stream`. */
+int wf_comm_allreduce_u32(wf_comm* c, uint32_t* dev_counts, uint64_t count, void* stream);
+void wf_comm_destroy(wf_comm* c);
+int wf_nccl_version(int32_t* version);
 
 /* ---- walk sets: WalkSet (walker.hpp:47-55) -------------------------------- */
 int wf_walkset_info(const wf_walkset* w, uint64_t* n_queries, uint64_t* total_vertices,

@@ -1,10 +1,15 @@
 // Device side of the walk engine: graph view, the built-in programs as
 // templated device functors, the samplers, and the persistent step kernel.
 //
+// Installed with the library (include/walkforge_b200/device/): a translation
+// unit of user code instantiates walk_kernel for its own program type through
+// include/walkforge_b200/device_program.cuh.
+//
 // Reference map (paths under /root/reference/proj):
 //   GraphView            include/walkforge/graph.hpp:17-107 (CSR) + packed vertex words
 //   Program<K>           include/walkforge/algorithms.hpp:20-193 via the WalkProgram
 //                        concept (program.hpp:49-93): weight / update / finished / max_weight
+//   Custom<U>            the same concept for a user's program type U (device_program.cuh)
 //   move<P,S,F>          StepDriver::step, engine.hpp:342-426 (Direct / Tables / Gathered)
 //   walk_kernel          run_sequential / run_interleaved (engine.hpp:440-504,
 //                        interleave.hpp:391-556): a lane per walker, a global
@@ -13,7 +18,9 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
+#include "../../walkforge_b200.h"
 #include "rng.cuh"
 
 namespace wf {
@@ -37,6 +44,8 @@ struct GraphView {
     const uint64_t* __restrict__ offsets;  // V+1
     const uint32_t* __restrict__ nbr;      // E, sorted per vertex when `sorted`
     const float* __restrict__ weights;     // E or null
+    const double* __restrict__ weights64;  // E or null: the reference's f64 weights when they
+                                           // are not all float32-exact (weights then mirrors them)
     const uint8_t* __restrict__ labels;    // E or null
     const uint64_t* __restrict__ vword;    // V: base << 24 | min(deg, escape)
     int sorted;
@@ -65,7 +74,12 @@ struct GraphView {
     unsigned long long* stats;
 };
 
+// A user program's functor bytes travel in the launch parameters (constant
+// bank): a custom program of up to this size costs no memory traffic.
+constexpr int kUserProgramBytes = 256;
+
 struct ProgParams {
+    alignas(16) unsigned char user[kUserProgramBytes];  // Custom<U>: the U object
     uint64_t stop_thr;  // PPR: ceil(termination * 2^53)
     uint32_t length;    // DeepWalk / Node2Vec / Uniform target length
     int weighted;
@@ -106,6 +120,8 @@ struct WalkLaunch {
     int use_label_index;
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
+    int alias_idx;                    // alias buckets carry edge positions {first, second} in
+                                      // E_v instead of destinations (programs that read the edge)
     const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
     const uint4* __restrict__ mp_adj; // MetaPath: per partitioned edge {dst, 0, next-group word} or null
     // Host streaming (run_to_host; all null otherwise).  Rows are grouped in
@@ -191,6 +207,33 @@ __device__ __forceinline__ uint4 ldr16(const uint4* p) {
     uint4 lo, hi;
     ldr256(reinterpret_cast<const uint4*>(a & ~static_cast<uintptr_t>(31)), lo, hi);
     return (a & 16) ? hi : lo;
+}
+
+// The one random request of a DeepWalk / MetaPath move (wide alias bucket,
+// successor-decorated edge), with the .L2::64B prefetch-size qualifier: a
+// miss then fetches 64 B from DRAM instead of the default 128 B line
+// (tools/randbw_matrix.cu, profiles/r02_randbw_matrix.json: 2 vs 4 DRAM
+// sectors per request).  C5 42.2 -> 43.0 G steps/s, C4 37.0 -> 37.4; the
+// Node2Vec loads keep the default (its L2-resident filter and hash probes
+// measured 4 % slower with it).
+#ifndef WF_LDR_MOVE
+#define WF_LDR_MOVE "ld.global.cg.L2::64B"
+#endif
+__device__ __forceinline__ void ldr256_move(const uint4* p, uint4& a, uint4& b) {
+    asm(WF_LDR_MOVE ".v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p));
+}
+__device__ __forceinline__ uint4 ldr16_move(const uint4* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    uint4 lo, hi;
+    ldr256_move(reinterpret_cast<const uint4*>(a & ~static_cast<uintptr_t>(31)), lo, hi);
+    return (a & 16) ? hi : lo;
+}
+
+// An edge's weight as the reference holds it (double, graph.hpp:102).
+__device__ __forceinline__ double edge_weight(const GraphView& g, uint64_t e) {
+    return g.weights64 ? __ldg(g.weights64 + e) : static_cast<double>(ldr(g.weights + e));
 }
 
 __device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint32_t v,
@@ -404,138 +447,266 @@ __device__ __forceinline__ uint32_t upper_index(const double* cum, uint32_t n, d
 }
 
 // ---- programs: the WalkProgram concept as device functors ------------------------
-// weight(q, e): q-dependent weight (gathered / O-REJ flows); weight_static(e):
-// weight(nullptr, e) for static contexts (program.hpp:39-42).
+// Every program type P the kernel runs provides (all static, all inlined):
+//   kind           WF_PROGRAM_* of a built-in, kCustomProgram for a user type
+//   type           kUnbiased / kStatic / kDynamic (walker_type(), program.hpp:17)
+//   prechecked     has finished() (PreCheckedProgram, program.hpp:81-84)
+//   needs_edge     update() reads the traversed edge (the kernel then tracks its index)
+//   checks_weights weight() results go through check_program_weight (engine.hpp:97-101)
+//   weight(L, q, e)           q-dependent weight (gathered / O-REJ flows)
+//   weight_static(L, src, e)  weight(nullptr, e) in static contexts (program.hpp:39-42)
+//   update(L, q, e)           after each move, path already extended; true = finished
+//   finished(L, q)            before the first move
+// The built-ins read their constructor arguments from L.prog; a user's program
+// (Custom<U> below) lives in L.prog.user.
+
+constexpr int kCustomProgram = -1;
 
 template <int K>
 struct Program;
 
 template <>
 struct Program<WF_PROGRAM_PPR> {  // algorithms.hpp:20-37
+    static constexpr int kind = WF_PROGRAM_PPR;
     static constexpr int type = kUnbiased;
     static constexpr bool prechecked = false;
     static constexpr bool has_max_weight = true;
-    __device__ static double weight(const ProgParams&, const GraphView&, const Walker&, uint64_t) {
-        return 1.0;
-    }
-    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
-        return 1.0;
-    }
+    static constexpr bool needs_edge = false;
+    static constexpr bool checks_weights = false;
+    __device__ static double weight(const WalkLaunch&, const Walker&, uint64_t) { return 1.0; }
+    __device__ static double weight_static(const WalkLaunch&, uint32_t, uint64_t) { return 1.0; }
     // update draws the stop coin: uniform_real(1.0) < stop (algorithms.hpp:31)
-    __device__ static bool update(const ProgParams& p, Walker& q) {
-        return q.rng.bits53() < p.stop_thr;
+    __device__ static bool update(const WalkLaunch& L, Walker& q, uint64_t) {
+        return q.rng.bits53() < L.prog.stop_thr;
     }
-    __device__ static bool finished(const ProgParams&, const Walker&) { return false; }
+    __device__ static bool finished(const WalkLaunch&, const Walker&) { return false; }
 };
 
 template <>
 struct Program<WF_PROGRAM_UNIFORM> {  // algorithms.hpp:177-193
+    static constexpr int kind = WF_PROGRAM_UNIFORM;
     static constexpr int type = kUnbiased;
     static constexpr bool prechecked = true;
     static constexpr bool has_max_weight = true;
-    __device__ static double weight(const ProgParams&, const GraphView&, const Walker&, uint64_t) {
-        return 1.0;
-    }
-    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
-        return 1.0;
-    }
-    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len >= p.length; }
-    __device__ static bool finished(const ProgParams& p, const Walker& q) { return q.len >= p.length; }
+    static constexpr bool needs_edge = false;
+    static constexpr bool checks_weights = false;
+    __device__ static double weight(const WalkLaunch&, const Walker&, uint64_t) { return 1.0; }
+    __device__ static double weight_static(const WalkLaunch&, uint32_t, uint64_t) { return 1.0; }
+    __device__ static bool update(const WalkLaunch& L, Walker& q, uint64_t) { return q.len >= L.prog.length; }
+    __device__ static bool finished(const WalkLaunch& L, const Walker& q) { return q.len >= L.prog.length; }
 };
 
 template <>
 struct Program<WF_PROGRAM_DEEPWALK> {  // algorithms.hpp:41-67
+    static constexpr int kind = WF_PROGRAM_DEEPWALK;
     static constexpr int type = kStatic;
     static constexpr bool prechecked = true;
     static constexpr bool has_max_weight = true;
-    __device__ static double weight_static(const ProgParams& p, const GraphView& g, uint64_t e) {
-        return p.weighted ? static_cast<double>(ldr(g.weights + e)) : 1.0;
+    static constexpr bool needs_edge = false;
+    static constexpr bool checks_weights = false;
+    __device__ static double weight_static(const WalkLaunch& L, uint32_t, uint64_t e) {
+        return L.prog.weighted ? edge_weight(L.g, e) : 1.0;
     }
-    __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker&,
-                                    uint64_t e) {
-        return weight_static(p, g, e);
+    __device__ static double weight(const WalkLaunch& L, const Walker&, uint64_t e) {
+        return weight_static(L, 0, e);
     }
-    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len >= p.length; }
-    __device__ static bool finished(const ProgParams& p, const Walker& q) { return q.len >= p.length; }
+    __device__ static bool update(const WalkLaunch& L, Walker& q, uint64_t) { return q.len >= L.prog.length; }
+    __device__ static bool finished(const WalkLaunch& L, const Walker& q) { return q.len >= L.prog.length; }
 };
 
 template <>
 struct Program<WF_PROGRAM_NODE2VEC> {  // algorithms.hpp:79-133
+    static constexpr int kind = WF_PROGRAM_NODE2VEC;
     static constexpr int type = kDynamic;
     static constexpr bool prechecked = true;
     static constexpr bool has_max_weight = true;
-    __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker& q,
-                                    uint64_t e) {  // algorithms.hpp:103-119
+    static constexpr bool needs_edge = false;
+    static constexpr bool checks_weights = false;
+    __device__ static double weight(const WalkLaunch& L, const Walker& q, uint64_t e) {  // algorithms.hpp:103-119
+        const ProgParams& p = L.prog;
         double w;
         if (q.len == 1) {
             w = p.first;
         } else {
-            uint32_t dst = ldr(g.nbr + e);
+            uint32_t dst = ldr(L.g.nbr + e);
             if (dst == q.prev) w = p.inv_a;
-            else if (prev_has_edge(g, q.prev, q.prev_base, q.prev_deg, dst, g.stats ? g.stats + 1 : nullptr)) w = 1.0;
+            else if (prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, L.g.stats ? L.g.stats + 1 : nullptr)) w = 1.0;
             else w = p.inv_b;
         }
-        return p.weighted ? __dmul_rn(w, static_cast<double>(ldr(g.weights + e))) : w;
+        return p.weighted ? __dmul_rn(w, edge_weight(L.g, e)) : w;
     }
-    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
+    __device__ static double weight_static(const WalkLaunch&, uint32_t, uint64_t) {
         return 0.0;  // never called: dynamic programs have no static tables
     }
-    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len >= p.length; }
-    __device__ static bool finished(const ProgParams& p, const Walker& q) { return q.len >= p.length; }
+    __device__ static bool update(const WalkLaunch& L, Walker& q, uint64_t) { return q.len >= L.prog.length; }
+    __device__ static bool finished(const WalkLaunch& L, const Walker& q) { return q.len >= L.prog.length; }
 };
 
 template <>
 struct Program<WF_PROGRAM_METAPATH> {  // algorithms.hpp:141-173
+    static constexpr int kind = WF_PROGRAM_METAPATH;
     static constexpr int type = kDynamic;
     static constexpr bool prechecked = true;
     static constexpr bool has_max_weight = false;
-    __device__ static double weight(const ProgParams& p, const GraphView& g, const Walker& q,
-                                    uint64_t e) {  // algorithms.hpp:164-166
-        return static_cast<uint32_t>(__ldg(g.labels + e)) == __ldg(p.schema + (q.len - 1)) ? 1.0
-                                                                                          : 0.0;
+    static constexpr bool needs_edge = false;
+    static constexpr bool checks_weights = false;
+    __device__ static double weight(const WalkLaunch& L, const Walker& q, uint64_t e) {  // algorithms.hpp:164-166
+        return static_cast<uint32_t>(__ldg(L.g.labels + e)) == __ldg(L.prog.schema + (q.len - 1)) ? 1.0 : 0.0;
     }
-    __device__ static double weight_static(const ProgParams&, const GraphView&, uint64_t) {
-        return 0.0;
+    __device__ static double weight_static(const WalkLaunch&, uint32_t, uint64_t) { return 0.0; }
+    __device__ static bool update(const WalkLaunch& L, Walker& q, uint64_t) { return q.len - 1 >= L.prog.schema_len; }
+    __device__ static bool finished(const WalkLaunch& L, const Walker& q) { return q.len - 1 >= L.prog.schema_len; }
+};
+
+// ---- user programs ---------------------------------------------------------------
+// The device face of the reference's Walker / EdgeRef (walker.hpp:24-45) that a
+// user's program sees.  The walker's history is its current and previous
+// vertex and its length (what the reference's own programs read: cur(),
+// prev(), path.size(), moves()); the rest of the path is already in the
+// output row.  The RNG is the walker's own stream; update() is the only place
+// a program may draw from it (program.hpp:46-48).
+class WalkerRng {
+public:
+    __device__ explicit WalkerRng(Rng& r) : r_(r) {}
+    __device__ uint64_t next_u64() { return r_.next(); }                // rng.hpp:26-30
+    __device__ uint32_t uniform_index(uint32_t n) { return r_.index(n); }  // rng.hpp:34-38
+    __device__ double uniform_real(double bound) { return r_.real(bound); }  // rng.hpp:42-47
+
+private:
+    Rng& r_;
+};
+
+class WalkerView {
+public:
+    __device__ WalkerView(uint64_t id, uint32_t cur, uint32_t prev, uint32_t len, Rng* rng)
+        : id_(id), cur_(cur), prev_(prev), len_(len), rng_(rng) {}
+    __device__ uint64_t id() const { return id_; }
+    __device__ uint32_t cur() const { return cur_; }
+    __device__ uint32_t prev() const { return prev_; }  // valid after one move
+    __device__ uint64_t path_size() const { return len_; }
+    __device__ uint64_t moves() const { return len_ - 1; }
+    // Only in update(): weight() must not draw (program.hpp:46-48).
+    __device__ WalkerRng rng() const { return WalkerRng(*rng_); }
+
+private:
+    uint64_t id_;
+    uint32_t cur_, prev_, len_;
+    Rng* rng_;
+};
+
+class EdgeRef {  // walker.hpp:37-45: lazy, a program touches only what it reads
+public:
+    __device__ EdgeRef(const GraphView& g, uint32_t src, uint64_t index) : g_(g), src_(src), index_(index) {}
+    __device__ uint32_t src() const { return src_; }
+    __device__ uint64_t index() const { return index_; }
+    __device__ uint32_t dst() const { return ldr(g_.nbr + index_); }
+    __device__ double weight() const { return edge_weight(g_, index_); }
+    __device__ uint32_t label() const { return __ldg(g_.labels + index_); }
+
+private:
+    const GraphView& g_;
+    uint32_t src_;
+    uint64_t index_;
+};
+
+__device__ __forceinline__ uint64_t walker_qid(const WalkLaunch& L, const Walker& q) {
+    return L.qid_map ? __ldg(L.qid_map + q.row) : L.qid_begin + q.row;
+}
+
+// The walk engine's view of a user program type U (device_program.cuh).  U is
+// trivially copyable, fits kUserProgramBytes, and declares
+//   static constexpr wf_walker_type walker_type = ...;
+//   __device__ double weight(const WalkerView* q, const EdgeRef& e) const;  // q null: static
+//   __device__ bool update(WalkerView& q, const EdgeRef& e) const;
+// and optionally max_weight() (host + device), finished(const WalkerView&).
+template <class U, class = void>
+struct has_finished : std::false_type {};
+template <class U>
+struct has_finished<U, std::void_t<decltype(std::declval<const U&>().finished(std::declval<const WalkerView&>()))>>
+    : std::true_type {};
+template <class U, class = void>
+struct has_max_weight_fn : std::false_type {};
+template <class U>
+struct has_max_weight_fn<U, std::void_t<decltype(std::declval<const U&>().max_weight())>> : std::true_type {};
+
+template <class U>
+struct Custom {
+    static_assert(std::is_trivially_copyable<U>::value, "a device program must be trivially copyable");
+    static_assert(sizeof(U) <= kUserProgramBytes, "a device program must fit kUserProgramBytes");
+    static constexpr int kind = kCustomProgram;
+    static constexpr int type = static_cast<int>(U::walker_type);
+    static constexpr bool prechecked = has_finished<U>::value;
+    static constexpr bool has_max_weight = has_max_weight_fn<U>::value;
+    static constexpr bool needs_edge = true;
+    static constexpr bool checks_weights = true;
+    __device__ static const U& self(const WalkLaunch& L) { return *reinterpret_cast<const U*>(L.prog.user); }
+    __device__ static WalkerView view(const WalkLaunch& L, const Walker& q) {
+        return WalkerView(walker_qid(L, q), q.cur, q.prev, q.len, const_cast<Rng*>(&q.rng));
     }
-    __device__ static bool update(const ProgParams& p, Walker& q) { return q.len - 1 >= p.schema_len; }
-    __device__ static bool finished(const ProgParams& p, const Walker& q) {
-        return q.len - 1 >= p.schema_len;
+    __device__ static double weight(const WalkLaunch& L, const Walker& q, uint64_t e) {
+        const WalkerView v = view(L, q);
+        return self(L).weight(&v, EdgeRef(L.g, q.cur, e));
+    }
+    __device__ static double weight_static(const WalkLaunch& L, uint32_t src, uint64_t e) {
+        return self(L).weight(static_cast<const WalkerView*>(nullptr), EdgeRef(L.g, src, e));
+    }
+    __device__ static bool update(const WalkLaunch& L, Walker& q, uint64_t e) {
+        WalkerView v = view(L, q);
+        return self(L).update(v, EdgeRef(L.g, q.prev, e));  // EdgeRef{&g, walker.prev(), edge}, engine.hpp:481
+    }
+    __device__ static bool finished(const WalkLaunch& L, const Walker& q) {
+        if constexpr (has_finished<U>::value) return self(L).finished(view(L, q));
+        else return false;
     }
 };
 
 // ---- samplers ------------------------------------------------------------------
+
+__device__ __forceinline__ void raise_device(const WalkLaunch& L, int code) {
+    atomicCAS(L.error_word, 0, code);
+}
+
+// check_program_weight (engine.hpp:97-101) for programs whose weights are not
+// known good: a negative or non-finite weight raises ContractError at the
+// next sync; the walk stops as a fault.
+template <class P>
+__device__ __forceinline__ bool weight_ok(const WalkLaunch& L, double w) {
+    if constexpr (P::checks_weights) {
+        if (!(w >= 0.0 && w <= 1.7976931348623157e308)) {
+            raise_device(L, WF_ERR_CONTRACT);
+            return false;
+        }
+    }
+    return true;
+}
 
 // O-REJ accept test (rej_generate, sampler.hpp:152-164 with the program weight
 // evaluated lazily, engine.hpp:356-364).  Node2Vec evaluates only as much of
 // its weight as y needs: every weight out of a vertex lies in {1/a, 1, 1/b}
 // (times w_e when weighted) so y below / above the candidates decides without
 // the adjacency search.  Same accept decisions, same draws — bit-exact.
-template <int K>
-__device__ __forceinline__ bool orej_accept(const WalkLaunch& L, const Walker& q, uint64_t e,
-                                            double y, uint32_t /*dst*/) {
-    return y < Program<K>::weight(L.prog, L.g, q, e);
-}
-
-template <>
-__device__ __forceinline__ bool orej_accept<WF_PROGRAM_NODE2VEC>(const WalkLaunch& L,
-                                                                 const Walker& q, uint64_t e,
-                                                                 double y, uint32_t dst) {
-    const ProgParams& p = L.prog;
-    double ew = p.weighted ? static_cast<double>(ldr(L.g.weights + e)) : 1.0;
-    auto scaled = [&](double w) { return p.weighted ? __dmul_rn(w, ew) : w; };
-    if (q.len == 1) return y < scaled(p.first);
-    if (dst == q.prev) return y < scaled(p.inv_a);
-    if (y < scaled(p.lo_w)) return true;
-    if (!(y < scaled(p.hi_w))) return false;
-    bool common = prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, L.g.stats ? L.g.stats + 1 : nullptr);
+// Returns 1 accept, 0 reject, -1 contract fault.
+template <class P>
+__device__ __forceinline__ int orej_accept(const WalkLaunch& L, const Walker& q, uint64_t e, double y,
+                                           uint32_t dst) {
+    if constexpr (P::kind == WF_PROGRAM_NODE2VEC) {
+        const ProgParams& p = L.prog;
+        double ew = p.weighted ? edge_weight(L.g, e) : 1.0;
+        auto scaled = [&](double w) { return p.weighted ? __dmul_rn(w, ew) : w; };
+        if (q.len == 1) return y < scaled(p.first);
+        if (dst == q.prev) return y < scaled(p.inv_a);
+        if (y < scaled(p.lo_w)) return 1;
+        if (!(y < scaled(p.hi_w))) return 0;
+        bool common = prev_has_edge(L.g, q.prev, q.prev_base, q.prev_deg, dst, L.g.stats ? L.g.stats + 1 : nullptr);
 #ifdef WF_DIAG_COMMON
-    if (common && L.g.stats) atomicAdd(L.g.stats + 2, 1ull);  // diagnostics: distance tests answered "edge"
+        if (common && L.g.stats) atomicAdd(L.g.stats + 2, 1ull);  // diagnostics: distance tests answered "edge"
 #endif
-    return y < scaled(common ? 1.0 : p.inv_b);
-}
-
-__device__ __forceinline__ void raise_device(const WalkLaunch& L, int code) {
-    atomicCAS(L.error_word, 0, code);
+        return y < scaled(common ? 1.0 : p.inv_b);
+    } else {
+        const double w = P::weight(L, q, e);
+        if (!weight_ok<P>(L, w)) return -1;
+        return y < w;
+    }
 }
 
 // Vose's alias construction (sampler.hpp:89-120) for ONE bucket x, over the
@@ -599,16 +770,17 @@ __device__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double*
 
 // Deferred unpack of the current vertex word (Walker::pend): on for every
 // program but Node2Vec, whose O-REJ kernel measured 3 % slower with it.
-template <int K>
-constexpr bool kDeferWord = K != WF_PROGRAM_NODE2VEC;
+template <class P>
+constexpr bool kDeferWord = P::kind != WF_PROGRAM_NODE2VEC;
 
 // One move: StepDriver::step (engine.hpp:342-426).  Draw order per sampler is
 // the reference contract (engine.hpp:330-333): NAIVE x; ITS x_real; ALIAS x
-// then y; REJ / O-REJ (x, y) per trial; dead ends consume no draws.
-template <int K, int S, int F>
-__device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& dst) {
-    using P = Program<K>;
-    if constexpr (kDeferWord<K>) {
+// then y; REJ / O-REJ (x, y) per trial; dead ends consume no draws.  `edge`
+// (the global index of the traversed edge) is produced only for programs
+// whose update() reads it (P::needs_edge).
+template <class P, int S, int F>
+__device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& dst, uint64_t& edge) {
+    if constexpr (kDeferWord<P>) {
         if (q.pend) {
             unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
             q.pend = false;
@@ -616,6 +788,13 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
     }
     const uint32_t d = q.cur_deg;
     const uint64_t base = q.cur_base;
+    if (L.g.stats && P::kind == WF_PROGRAM_METAPATH) {
+        // instrumented runs: the reference's gather scans every label of the
+        // current vertex (ceil(d_v / 32) u8-label sectors per step)
+        const uint64_t d_v = ldr(L.g.offsets + q.cur + 1) - ldr(L.g.offsets + q.cur);
+        atomicAdd(L.g.stats + 4, static_cast<unsigned long long>((d_v + 31) / 32));
+        atomicAdd(L.g.stats + 5, 1ull);
+    }
     if (d == 0) return kDead;
     uint32_t pick = 0;
     if constexpr (F == kDirect) {
@@ -642,8 +821,16 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 } else {
                     dx = ldr(L.g.nbr + base + x);
                 }
-                if (orej_accept<K>(L, q, base + x, y, dx)) {
+                if (L.g.stats && P::kind == WF_PROGRAM_NODE2VEC && q.len > 1 && dx != q.prev) {
+                    // instrumented runs: the reference's weight() binary-searches
+                    // adj(prev) on every such trial (ceil(log2(d_prev+1)) probes)
+                    atomicAdd(L.g.stats + 3, static_cast<unsigned long long>(32 - __clz(q.prev_deg)));
+                }
+                const int acc = orej_accept<P>(L, q, base + x, y, dx);
+                if (acc < 0) return kFault;
+                if (acc) {
                     dst = dx;
+                    if constexpr (P::needs_edge) edge = base + x;
                     if (L.adj) {
                         q.nb_word = wx;
                         q.have_nb = true;
@@ -660,7 +847,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 // destinations' own vertex words, so the next step needs no
                 // dependent vertex-word load (one random sector per move).
                 uint4 b, w;
-                ldr256(L.alias + 2 * (base + x), b, w);
+                ldr256_move(L.alias + 2 * (base + x), b, w);
                 uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
                 bool first = q.rng.bits53() < thr;  // y < split <=> k < ceil(split 2^53)
                 dst = first ? b.z : b.w;
@@ -671,8 +858,15 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             }
             uint4 b = ldr16(L.alias + base + x);
             uint64_t thr = (static_cast<uint64_t>(b.y) << 32) | b.x;
-            dst = q.rng.bits53() < thr ? b.z : b.w;  // y < split <=> k < ceil(split 2^53)
-            return kMoved;
+            const bool first = q.rng.bits53() < thr;  // y < split <=> k < ceil(split 2^53)
+            if (L.alias_idx) {
+                // {thr, first, second} as positions in E_v (EngineAliasSlot's
+                // first / second, engine.hpp:22-28): the edge, then its destination
+                pick = first ? b.z : b.w;
+            } else {
+                dst = first ? b.z : b.w;
+                return kMoved;
+            }
         } else if constexpr (S == WF_SAMPLER_ITS) {
             const double* cum = L.its + base;
             double x = q.rng.real(__ldg(cum + d - 1));
@@ -688,11 +882,11 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (L.g.stats) atomicAdd(L.g.stats, 1ull);
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(ps);
-                if (y < P::weight_static(L.prog, L.g, base + x)) { pick = x; break; }
+                if (y < P::weight_static(L, q.cur, base + x)) { pick = x; break; }
             }
         }
     } else {  // Gathered: gather (engine.hpp:134-184) without the scratch table
-        if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) {
+        if constexpr (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) {
             if (L.use_label_index) {
                 // label-partitioned CSR: q.cur_base / q.cur_deg already frame the
                 // group of edges labelled schema[moves]; the reference picks the
@@ -704,7 +898,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (L.mp_adj) {
                     // {dst, -, group word of dst for the next schema label}: the
                     // next move's label group arrives with this one load
-                    uint4 a = ldr16(L.mp_adj + base + j);
+                    uint4 a = ldr16_move(L.mp_adj + base + j);
                     dst = a.x;
                     const uint64_t w = (static_cast<uint64_t>(a.w) << 32) | a.z;
                     if (w != ~0ull) {
@@ -720,7 +914,8 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
         double sum = 0.0, mx = 0.0;
         if (L.g.stats) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
         for (uint32_t i = 0; i < d; ++i) {
-            double w = P::weight(L.prog, L.g, q, base + i);
+            double w = P::weight(L, q, base + i);
+            if (!weight_ok<P>(L, w)) return kFault;
             sum += w;
             mx = w > mx ? w : mx;
         }
@@ -730,7 +925,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             double run = 0.0;
             pick = d - 1;
             for (uint32_t i = 0; i < d; ++i) {
-                run += P::weight(L.prog, L.g, q, base + i);
+                run += P::weight(L, q, base + i);
                 if (x < run) { pick = i; break; }
             }
         } else if constexpr (S == WF_SAMPLER_ALIAS) {
@@ -739,7 +934,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             double* park = L.scratch + (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * L.scratch_stride;
             double split;
             uint32_t second;
-            vose_bucket(d, sum, [&](uint32_t i) { return P::weight(L.prog, L.g, q, base + i); }, x,
+            vose_bucket(d, sum, [&](uint32_t i) { return P::weight(L, q, base + i); }, x,
                         park, split, second);
             pick = k < unit_threshold(split) ? x : second;
         } else {  // REJ over the gathered weights, p* = max
@@ -752,10 +947,11 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (L.g.stats) atomicAdd(L.g.stats, 1ull);
                 uint32_t x = q.rng.index(d);
                 double y = q.rng.real(mx);
-                if (y < P::weight(L.prog, L.g, q, base + x)) { pick = x; break; }
+                if (y < P::weight(L, q, base + x)) { pick = x; break; }
             }
         }
     }
+    if constexpr (P::needs_edge) edge = base + pick;
     if (F == kDirect && L.adj) {
         // decorated adjacency {dst, -, vertex word of dst}: one 16 B load
         uint4 a = ldr16(L.adj + base + pick);
@@ -769,9 +965,9 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
 }
 
 // Loads what the next move out of q.cur needs into registers.
-template <int K, int S, int F>
+template <class P, int S, int F>
 __device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
-    if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
+    if constexpr (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
         if (L.use_label_index) {
             const uint4* rec = L.g.lab_rec + 2 * static_cast<uint64_t>(q.cur);
             uint4 r0, r1;
@@ -796,9 +992,9 @@ __device__ __forceinline__ void load_current(const WalkLaunch& L, Walker& q) {
 
 // True when load_current is a plain vertex-word read (everything but
 // MetaPath's label-index flow), which can then be deferred (Walker::pend).
-template <int K, int S, int F>
+template <class P, int S, int F>
 __device__ __forceinline__ bool plain_word(const WalkLaunch& L) {
-    if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) return !L.use_label_index;
+    if constexpr (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) return !L.use_label_index;
     return true;
 }
 
@@ -806,9 +1002,9 @@ __device__ __forceinline__ bool plain_word(const WalkLaunch& L) {
 // vertex word (base << 24 | deg) for claim-time staging; kNoWord when it does
 // not pack (a label group of >= 2^24 - 1 edges): that lane loads it itself.
 constexpr unsigned long long kNoWord = ~0ull;
-template <int K, int S, int F>
+template <class P, int S, int F>
 __device__ __forceinline__ unsigned long long start_word(const WalkLaunch& L, uint32_t src) {
-    if constexpr (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
+    if constexpr (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS && F == kGathered) {
         if (L.use_label_index) {
             uint4 r0, r1;
             ldr256(L.g.lab_rec + 2 * static_cast<uint64_t>(src), r0, r1);
@@ -967,7 +1163,7 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
 // gathered flows (per-step scans, on-the-fly Vose) keep their registers.
 // Build knobs (experiments only): WF_BLOCK, WF_MIN_BLOCKS, WF_N2V_BLOCKS,
 // WF_CLAIM (128-thread blocks measured the same as 256).
-template <int K, int S, int F>
+template <class P, int S, int F>
 constexpr int walk_min_blocks() {
     // Node2Vec's O-REJ step (edge hash probe) needs ~48 registers without
     // spills (5 blocks: 23.9 vs 22.9 G steps/s at 6 with 76 B of spills, C3);
@@ -976,11 +1172,11 @@ constexpr int walk_min_blocks() {
 #ifndef WF_MIN_BLOCKS
 #define WF_MIN_BLOCKS 4
 #endif
-    if (F == kGathered) return (K == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) ? WF_MIN_BLOCKS : 1;
+    if (F == kGathered) return (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) ? WF_MIN_BLOCKS : 1;
 #ifndef WF_N2V_BLOCKS
 #define WF_N2V_BLOCKS 5
 #endif
-    return K == WF_PROGRAM_NODE2VEC ? WF_N2V_BLOCKS : WF_MIN_BLOCKS;
+    return P::kind == WF_PROGRAM_NODE2VEC ? WF_N2V_BLOCKS : WF_MIN_BLOCKS;
 }
 
 // Rows a warp claims from the global cursor per atomic.  One atomic per refill
@@ -996,9 +1192,8 @@ constexpr uint32_t kClaim = WF_CLAIM;
 // report to their tile / chunk words.
 // A separate instantiation keeps the device-output kernels' registers as they
 // were (the reports cost ~10 registers, which would cost C3/C5 a block/SM).
-template <int K, int S, int F, bool ST>
-__global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kernel(const WalkLaunch L) {
-    using P = Program<K>;
+template <class P, int S, int F, bool ST>
+__global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kernel(const WalkLaunch L) {
     const int lane = threadIdx.x & 31;
     __shared__ uint32_t stage_words[8 * kBlock];
     PathStage ps{stage_words};
@@ -1093,7 +1288,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     if (static_cast<uint32_t>(lane) < wleft) {
                         const uint64_t qid = L.qid_map ? __ldg(L.qid_map + wnext + lane) : L.qid_begin + wnext + lane;
                         src = source_at<ST>(L, qid);
-                        if (src < L.g.V) word = start_word<K, S, F>(L, src);
+                        if (src < L.g.V) word = start_word<P, S, F>(L, src);
                     }
                     claim_src[wid][lane] = src;
                     claim_word[wid][lane] = word;
@@ -1127,7 +1322,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                 {
                     emit(L, q, 0, q.cur, ps);
                     q.len = 1;
-                    if (P::prechecked && P::finished(L.prog, q)) {
+                    if (P::prechecked && P::finished(L, q)) {
                         finish(L, q, WF_WALK_COMPLETE, ps);  // walk_already_finished, program.hpp:86-93
                         if (ST && L.tile_word) {
                             __threadfence();
@@ -1137,14 +1332,14 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                         const unsigned long long w = claim_word[wid][slot];
                         active = true;
                         if (w != kNoWord) {
-                            if constexpr (kDeferWord<K>) {
+                            if constexpr (kDeferWord<P>) {
                                 q.nb_word = w;
                                 q.pend = true;
                             } else {
                                 unpack_word(L.g, w, q.cur, q.cur_base, q.cur_deg);
                             }
                         } else {
-                            load_current<K, S, F>(L, q);
+                            load_current<P, S, F>(L, q);
                             fresh = true;
                         }
                     }
@@ -1159,7 +1354,8 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
         fresh = false;
         if (ready) {
             uint32_t dst = 0;
-            int r = move<K, S, F>(L, q, dst);
+            uint64_t edge = 0;
+            int r = move<P, S, F>(L, q, dst, edge);
             if (r == kMoved) {
                 q.prev = q.cur;
                 q.prev_base = q.cur_base;
@@ -1172,11 +1368,11 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                 // overlaps the neighbour load the store waits for (Node2Vec,
                 // with kDeferWord off, keeps its original order)
                 bool done;
-                if constexpr (K == WF_PROGRAM_NODE2VEC) {
+                if constexpr (P::kind == WF_PROGRAM_NODE2VEC) {
                     emit(L, q, p, dst, ps);
-                    done = P::update(L.prog, q);
+                    done = P::update(L, q, edge);
                 } else {
-                    done = P::update(L.prog, q);
+                    done = P::update(L, q, edge);
                     emit(L, q, p, dst, ps);
                 }
                 if (done) {
@@ -1184,13 +1380,13 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<K, S, F>()) walk_kerne
                     active = false;
                 } else if (q.have_nb) {
                     // unpacked by the next move (kDeferWord)
-                    if constexpr (kDeferWord<K>) q.pend = true;
+                    if constexpr (kDeferWord<P>) q.pend = true;
                     else unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
-                } else if (kDeferWord<K> && plain_word<K, S, F>(L)) {
+                } else if (kDeferWord<P> && plain_word<P, S, F>(L)) {
                     q.nb_word = ldr(L.sview + q.cur);
                     q.pend = true;
                 } else {
-                    load_current<K, S, F>(L, q);
+                    load_current<P, S, F>(L, q);
                 }
                 q.have_nb = false;
             } else {

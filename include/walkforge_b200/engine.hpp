@@ -9,10 +9,15 @@
 // libwalkforge_b200.so.  Differences, all checked at the boundary:
 //   * weights must be exactly representable in float32 (device storage), and
 //     labels < 256 — otherwise ConfigError;
-//   * programs are the five built-ins (the device functors); custom programs are
-//     written as device functors in csrc/engine.cuh (Program<K>);
-//   * ExecOptions::threads and prefetch are accepted and ignored (lanes replace
-//     worker threads); k / k' of run_interleaved are validated then ignored.
+//   * programs are the five built-ins or a user's device program: a type written
+//     against walkforge_b200/device_program.cuh in the user's .cu file, passed
+//     here as DeviceProgram(ops, object) (the ops table its WF_DEVICE_PROGRAM
+//     exports);
+//   * ExecOptions::threads keeps its meaning — the run is split into that many
+//     contiguous worker blocks, each handed to the sink once, in worker order —
+//     and the blocks are spread over min(threads, visible GPUs) devices
+//     (wf_multi_*); prefetch is accepted and ignored; k / k' of
+//     run_interleaved are validated then used as launch hints.
 #pragma once
 
 #include <algorithm>
@@ -20,7 +25,9 @@
 #include <charconv>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <exception>
+#include <type_traits>
 #include <fstream>
 #include <functional>
 #include <memory>
@@ -153,6 +160,7 @@ public:
         return g;
     }
     wf_graph* handle() const { return h_.get(); }
+    int32_t device() const { return info_.device; }
 
 private:
     struct HostCsr {
@@ -417,6 +425,29 @@ private:
     std::vector<uint32_t> schema_;
 };
 
+// A user's device program (walkforge_b200/device_program.cuh): the
+// wf_program_ops table its WF_DEVICE_PROGRAM(Type, symbol) exports and the
+// program object's bytes (a host mirror of the trivially copyable Type).
+class DeviceProgram {
+public:
+    template <typename T>
+    DeviceProgram(const wf_program_ops* ops, const T& obj) : ops_(ops) {
+        static_assert(std::is_trivially_copyable<T>::value, "a device program object is trivially copyable");
+        if (ops == nullptr) throw ConfigError("null program table");
+        if (ops->program_size != sizeof(T)) throw ConfigError("program object size does not match its table");
+        bytes_.resize(sizeof(T));
+        std::memcpy(bytes_.data(), &obj, sizeof(T));
+    }
+    WalkerType walker_type() const { return static_cast<WalkerType>(ops_->walker_type); }
+    const wf_program_ops* ops() const { return ops_; }
+    const void* object() const { return bytes_.data(); }
+    uint32_t max_path() const { return ops_->max_path ? ops_->max_path(object()) : 0; }
+
+private:
+    const wf_program_ops* ops_;
+    std::vector<unsigned char> bytes_;
+};
+
 class UniformProgram {
 public:
     explicit UniformProgram(uint32_t target_length) : length_(target_length) {
@@ -495,19 +526,19 @@ inline uint64_t max_path_vertices(const wf_program_desc& d) {
     return d.target_length;
 }
 
-template <typename P>
-RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts) {
-    wf_program_desc d = prog.to_desc();
+inline wf_exec_options to_c(const ExecOptions& opts) {
     wf_exec_options o{};
     o.seed = opts.seed;
     o.sampler = opts.sampler ? static_cast<int32_t>(*opts.sampler) : WF_SAMPLER_DEFAULT;
     o.use_static_tables = opts.use_static_tables ? 1 : 0;
     o.rej_trial_cap = opts.rej_trial_cap;
     o.threads = opts.threads;
-    wf_query_spec q = spec.to_c();
-    // QuerySpec::validate before any work (walker.cpp:8-109), as the
-    // reference does: no block may reach a sink for an invalid query set
-    const uint64_t n = spec.total(g);
+    return o;
+}
+
+// QuerySpec::validate before any work (walker.cpp:8-109), as the reference
+// does: no block may reach a sink for an invalid query set.
+inline void validate_spec(const Graph& g, const QuerySpec& spec) {
     if (spec.mode == QuerySpec::Mode::FromSource && spec.source >= g.vertex_count())
         throw ConfigError("query source " + std::to_string(spec.source) + " is not a vertex (V=" +
                           std::to_string(g.vertex_count()) + ")");
@@ -516,14 +547,93 @@ RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOp
             if (v >= g.vertex_count())
                 throw ConfigError("query source " + std::to_string(v) + " is not a vertex (V=" +
                                   std::to_string(g.vertex_count()) + ")");
-    wf_session* s = nullptr;
-    check(wf_session_create(g.handle(), &d, &o, &s));
-    std::unique_ptr<wf_session, void (*)(wf_session*)> guard(s, wf_session_destroy);
+}
 
-    // the walks stream into host memory block by block (wf_session_run_host_blocks)
-    // and become WalkRecords while later queries are still walking
-    uint64_t per = max_path_vertices(d);
-    if (per == 0) per = static_cast<uint64_t>(2.0 / d.termination) + 24;  // PPR: ~5x its mean length
+// Worker blocks over devices (wf_multi_run): `workers` blocks in worker order
+// to the sink (or into the walk set); unbounded walks need no host capacity
+// guess (each block is sized after its walks ran).
+template <typename P>
+RunResult run_blocks(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts,
+                     uint32_t n_devices) {
+    const wf_exec_options o = to_c(opts);
+    std::vector<int32_t> devs;
+    int32_t total = 1;
+    check(wf_device_count(&total));
+    for (uint32_t i = 0; i < n_devices; ++i) devs.push_back((g.device() + static_cast<int32_t>(i)) % total);
+    wf_multi* m = nullptr;
+    if constexpr (std::is_same_v<P, DeviceProgram>) {
+        check(wf_multi_create_custom(g.handle(), devs.data(), n_devices, prog.ops(), prog.object(), &o, &m));
+    } else {
+        wf_program_desc d = prog.to_desc();
+        check(wf_multi_create(g.handle(), devs.data(), n_devices, &d, &o, &m));
+    }
+    std::unique_ptr<wf_multi, void (*)(wf_multi*)> guard(m, wf_multi_destroy);
+    const uint64_t n = spec.total(g);
+    const uint32_t workers = std::max<uint32_t>(1, opts.threads);
+    RunResult r;
+    if (!opts.sink) r.walks.resize(n);
+    struct Ctx {
+        RunResult* r;
+        const BlockSink* sink;
+        std::exception_ptr error;
+    } ctx{&r, opts.sink ? &opts.sink : nullptr, nullptr};
+    auto on_shard = [](void* user, uint32_t w, uint64_t q0, uint64_t q1, const uint32_t* rec,
+                       const uint32_t* verts, uint64_t) -> int {
+        auto* c = static_cast<Ctx*>(user);
+        try {
+            WalkSet block;
+            uint64_t v = 0;
+            for (uint64_t q = q0; q < q1; ++q) {
+                const uint32_t len = rec[q - q0] & 0x7FFFFFFFu;
+                WalkRecord wr{q, (rec[q - q0] >> 31) ? WalkStatus::DeadEnd : WalkStatus::Complete,
+                              std::vector<VertexId>(verts + v, verts + v + len)};
+                v += len;
+                if (c->sink) block.push_back(std::move(wr));
+                else c->r->walks[q] = std::move(wr);
+            }
+            if (c->sink) (*c->sink)(w, std::move(block));
+            return 0;
+        } catch (...) {
+            c->error = std::current_exception();
+            return 1;
+        }
+    };
+    wf_query_spec q = spec.to_c();
+    wf_run_metrics mt{};
+    const int rc = wf_multi_run(m, &q, workers, on_shard, &ctx, nullptr, &mt);
+    if (ctx.error) std::rethrow_exception(ctx.error);
+    check(rc);
+    r.metrics = {mt.preprocess_seconds, mt.exec_seconds, mt.total_steps, mt.max_in_flight};
+    return r;
+}
+
+template <typename P>
+RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts) {
+    validate_spec(g, spec);
+    const uint64_t n = spec.total(g);
+    uint64_t per;
+    if constexpr (std::is_same_v<P, DeviceProgram>) per = prog.max_path();
+    else per = max_path_vertices(prog.to_desc());
+    // ExecOptions::threads: worker blocks, spread over up to that many GPUs
+    int32_t ndev = 1;
+    check(wf_device_count(&ndev));
+    const uint32_t workers = std::max<uint32_t>(1, opts.threads);
+    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(workers, static_cast<uint32_t>(std::max(ndev, 1))));
+    if (G > 1 || per == 0) return run_blocks(g, spec, prog, opts, G);
+
+    // one device, bounded walks: the walks stream into host memory block by
+    // block (wf_session_run_host_blocks) and become WalkRecords while later
+    // queries are still walking
+    const wf_exec_options o = to_c(opts);
+    wf_query_spec q = spec.to_c();
+    wf_session* s = nullptr;
+    if constexpr (std::is_same_v<P, DeviceProgram>) {
+        check(wf_session_create_custom(g.handle(), prog.ops(), prog.object(), &o, &s));
+    } else {
+        wf_program_desc d = prog.to_desc();
+        check(wf_session_create(g.handle(), &d, &o, &s));
+    }
+    std::unique_ptr<wf_session, void (*)(wf_session*)> guard(s, wf_session_destroy);
     const uint64_t cap = n * per + 4096;
     std::unique_ptr<uint32_t[]> records(new uint32_t[std::max<uint64_t>(n, 1)]);
     std::unique_ptr<uint32_t[]> vertices(new uint32_t[cap]);
@@ -532,7 +642,7 @@ RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOp
     st.records = records.get();
     st.vertices = vertices.get();
     st.n = n;
-    st.workers = std::max<uint32_t>(1, opts.threads);
+    st.workers = workers;
     if (opts.sink) {
         st.sink = &opts.sink;
     } else {

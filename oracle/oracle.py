@@ -197,6 +197,31 @@ class RefOracle:
             C.byref(h)))
         return RefGraph(self, h)
 
+    def rmat(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, weighted=False,
+             label_count=0, threads=0) -> "RefGraph":
+        """The seeded R-MAT CSR built on the CPU by the C restatement of the
+        generator (wfo_rmat_csr, bit-identical to the device build,
+        tests/test_rmat_cpu.py) and handed straight to Graph::from_csr: no
+        Python copies, so s26 (2.1 B edges) fits the host beside the
+        reference's own f64 arrays and 24 B/edge alias tables."""
+        port = PortOracle()
+        g = _WfoCsr()
+        rc = port.lib.wfo_rmat_csr(C.c_uint32(scale), C.c_uint32(edge_factor), C.c_double(a),
+                                   C.c_double(b), C.c_double(c), C.c_uint64(seed),
+                                   C.c_int(int(weighted)), C.c_uint32(label_count),
+                                   C.c_int(threads), C.byref(g))
+        raise_for(rc, "bad R-MAT parameters")
+        try:
+            h = C.c_void_p()
+            self._check(self.lib.wfref_graph_create_f32(
+                C.cast(g.offsets, _u64p), C.cast(g.neighbors, _u32p),
+                C.cast(g.weights, _f32p) if weighted else None,
+                C.cast(g.labels, _u8p) if label_count else None,
+                C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count), C.byref(h)))
+        finally:
+            port.lib.wfo_rmat_free(C.byref(g))
+        return RefGraph(self, h)
+
     def power_law(self, vertex_count, edge_count, seed, exponent=0.8, weighted=False,
                   label_count=0) -> "RefGraph":
         h = C.c_void_p()
@@ -386,6 +411,21 @@ class RefGraph:
                                                     C.byref(copts), _ptr(q, _u64p),
                                                     C.c_uint64(q.size), C.byref(h), C.byref(m)))
         return self._collect(h, m, q)
+
+    def run_test_program(self, which: int, params, spec: QuerySpec, opts: ExecOptions,
+                         interleaved: bool = False):
+        """One of the reference-API test programs in ref_harness.cpp (Counting,
+        AvoidVertex, NegativeWeight, LabelWeight, LabelStop); returns
+        (RunResult, update() calls of CountingProgram)."""
+        cspec = spec.to_c()
+        copts = opts.to_c()
+        h = C.c_void_p()
+        m = RunMetricsC()
+        upd = C.c_uint64()
+        self.ref._check(self.ref.lib.wfref_run_test_program(
+            self.h, C.c_int(which), C.byref(params), C.byref(cspec), C.byref(copts),
+            C.c_int(int(interleaved)), C.byref(h), C.byref(m), C.byref(upd)))
+        return self._collect(h, m, None), upd.value
 
     def static_tables(self, prog, sampler: int):
         i = self.info()

@@ -15,6 +15,7 @@
 //   RngStream                            proj/include/walkforge/rng.hpp:19-67
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 // reference leg may load the resulting library.
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -254,6 +255,75 @@ int wfref_has_edge(const void* gp, uint32_t src, uint32_t dst) {
     return static_cast<const Graph*>(gp)->has_edge(src, dst) ? 1 : 0;
 }
 
+// ---- test programs ----------------------------------------------------------
+// The custom programs of the reference's own engine tests (written against its
+// WalkProgram concept, program.hpp:49-93), for parity with the same programs
+// written against the device program API (tests/programs/test_programs.cu).
+
+struct TestProgramParams {  // mirrors tests/test_custom_programs_gpu.py
+    uint32_t length;
+    uint32_t banned;
+    double stop;
+    uint32_t stop_label;
+    uint32_t schema_len;
+    uint32_t schema[48];
+};
+
+// proj/tests/test_engine.cpp:17-27
+struct CountingProgram {
+    uint32_t length;
+    std::atomic<uint64_t>* updates;
+    WalkerType walker_type() const { return WalkerType::Unbiased; }
+    double weight(const Walker*, const EdgeRef&) const { return 1.0; }
+    bool update(Walker& q, const EdgeRef&) const {
+        updates->fetch_add(1, std::memory_order_relaxed);
+        return q.path.size() >= length;
+    }
+};
+
+// proj/tests/test_engine.cpp:29-40
+struct AvoidVertexProgram {
+    VertexId banned;
+    uint32_t length;
+    WalkerType walker_type() const { return WalkerType::Static; }
+    double weight(const Walker*, const EdgeRef& e) const { return e.dst() == banned ? 0.0 : 1.0; }
+    bool update(Walker& q, const EdgeRef&) const { return q.path.size() >= length; }
+    double max_weight() const { return 1.0; }
+};
+
+// proj/tests/test_engine.cpp:42-46
+struct NegativeWeightProgram {
+    WalkerType walker_type() const { return WalkerType::Static; }
+    double weight(const Walker*, const EdgeRef&) const { return -1.0; }
+    bool update(Walker&, const EdgeRef&) const { return true; }
+};
+
+// a weighted meta-path walk has no reference built-in; this is
+// the test-local program the survey prescribes (label match ? w_e : 0).
+struct LabelWeightProgram {
+    std::vector<uint32_t> schema;
+    WalkerType walker_type() const { return WalkerType::Dynamic; }
+    double weight(const Walker* q, const EdgeRef& e) const {
+        if (q == nullptr) return 0.0;
+        return e.label() == schema[q->moves()] ? e.weight() : 0.0;
+    }
+    bool update(Walker& q, const EdgeRef&) const { return q.moves() >= schema.size(); }
+    bool finished(const Walker& q) const { return q.moves() >= schema.size(); }
+};
+
+// Unbiased, unbounded: a stop coin drawn in update() plus the traversed edge's label.
+struct LabelStopProgram {
+    double stop;
+    uint32_t stop_label;
+    WalkerType walker_type() const { return WalkerType::Unbiased; }
+    double weight(const Walker*, const EdgeRef&) const { return 1.0; }
+    bool update(Walker& q, const EdgeRef& e) const {
+        const bool coin = q.rng.uniform_real(1.0) < stop;
+        return coin || e.label() == stop_label;
+    }
+    double max_weight() const { return 1.0; }
+};
+
 // ---- runs -------------------------------------------------------------------
 
 // interleaved: 0 -> run_sequential, 1 -> run_interleaved(k, k').
@@ -465,5 +535,43 @@ uint32_t wfref_synthetic_label(uint64_t seed, uint64_t edge, uint32_t count) {
 }
 
 unsigned wfref_hardware_threads() { return std::thread::hardware_concurrency(); }
+
+// run_sequential / run_interleaved over one of the test programs above:
+// which = 0 Counting, 1 AvoidVertex, 2 NegativeWeight, 3 LabelWeight,
+// 4 LabelStop.  *updates = CountingProgram's update() calls.
+int wfref_run_test_program(const void* gp, int which, const TestProgramParams* tp, const wf_query_spec* q,
+                           const wf_exec_options* opts, int interleaved, void** out, wf_run_metrics* metrics,
+                           uint64_t* updates) {
+    return guarded([&] {
+        const Graph& g = *static_cast<const Graph*>(gp);
+        auto res = std::make_unique<RefResult>();
+        ExecOptions eo = to_exec(opts);
+        QuerySpec spec = to_spec(q);
+        uint32_t k = opts && opts->k ? opts->k : 64;
+        uint32_t kp = opts && opts->k_prime ? opts->k_prime : 32;
+        std::atomic<uint64_t> count{0};
+        auto go = [&](const auto& p) {
+            RunResult r = interleaved ? run_interleaved(g, spec, p, k, kp, eo) : run_sequential(g, spec, p, eo);
+            res->walks = std::move(r.walks);
+            res->metrics = r.metrics;
+        };
+        switch (which) {
+            case 0: go(CountingProgram{tp->length, &count}); break;
+            case 1: go(AvoidVertexProgram{tp->banned, tp->length}); break;
+            case 2: go(NegativeWeightProgram{}); break;
+            case 3: go(LabelWeightProgram{std::vector<uint32_t>(tp->schema, tp->schema + tp->schema_len)}); break;
+            case 4: go(LabelStopProgram{tp->stop, tp->stop_label}); break;
+            default: throw ConfigError("unknown test program");
+        }
+        if (updates) *updates = count.load();
+        if (metrics) {
+            metrics->preprocess_seconds = res->metrics.preprocess_seconds;
+            metrics->exec_seconds = res->metrics.exec_seconds;
+            metrics->total_steps = res->metrics.total_steps;
+            metrics->max_in_flight = res->metrics.max_in_flight;
+        }
+        *out = res.release();
+    });
+}
 
 }  // extern "C"

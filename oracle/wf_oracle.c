@@ -877,6 +877,11 @@ typedef struct {
     uint64_t lo, hi;
     uint32_t* deg;           /* pass 0 */
     uint64_t* cursor;        /* pass 1 */
+    /* R-MAT hubs are the low ids: their counts and cursors are per thread
+     * (no shared cache lines), the rest use atomics */
+    uint32_t hot;            /* vertices [0, hot) */
+    uint32_t* hot_deg;       /* pass 0: this thread's counts */
+    uint64_t* hot_cur;       /* pass 1: this thread's cursors */
     uint32_t* raw;           /* pass 1 */
     /* pass 2/3: vertex range */
     uint32_t vlo, vhi;
@@ -892,9 +897,37 @@ typedef struct {
     uint32_t label_count;
 } wfo_rmat_job;
 
-static int wfo_cmp_u32(const void* a, const void* b) {
-    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
-    return x < y ? -1 : (x > y);
+/* Sorts a neighbour segment: insertion sort when short, else an LSD radix
+ * sort with 11-bit digits through `tmp` (same result as any sort; the order of
+ * equal ids does not matter because duplicates are merged right after). */
+static void wfo_sort_u32(uint32_t* x, uint64_t n, uint32_t** tmp, uint64_t* tmp_n) {
+    if (n <= 32) {
+        for (uint64_t i = 1; i < n; ++i) {
+            uint32_t v = x[i];
+            uint64_t k = i;
+            while (k > 0 && x[k - 1] > v) { x[k] = x[k - 1]; --k; }
+            x[k] = v;
+        }
+        return;
+    }
+    if (*tmp_n < n) {
+        free(*tmp);
+        *tmp = malloc(n * sizeof(uint32_t));
+        *tmp_n = n;
+    }
+    uint32_t* a = x;
+    uint32_t* b = *tmp;
+    for (int shift = 0; shift < 32; shift += 11) {
+        uint64_t cnt[2049] = {0};
+        for (uint64_t i = 0; i < n; ++i) ++cnt[((a[i] >> shift) & 2047) + 1];
+        if (cnt[((a[0] >> shift) & 2047) + 1] == n) continue; /* one digit value: already ordered */
+        for (int d = 0; d < 2048; ++d) cnt[d + 1] += cnt[d];
+        for (uint64_t i = 0; i < n; ++i) b[cnt[(a[i] >> shift) & 2047]++] = a[i];
+        uint32_t* t = a;
+        a = b;
+        b = t;
+    }
+    if (a != x) memcpy(x, a, n * sizeof(uint32_t));
 }
 
 static void* wfo_rmat_worker(void* arg) {
@@ -905,21 +938,26 @@ static void* wfo_rmat_worker(void* arg) {
             wfo_rmat_edge(j->gen, i, &s, &d);
             if (s == d) continue;
             if (j->pass == 0) {
-                __atomic_fetch_add(&j->deg[s], 1u, __ATOMIC_RELAXED);
-                __atomic_fetch_add(&j->deg[d], 1u, __ATOMIC_RELAXED);
+                if (s < j->hot) ++j->hot_deg[s];
+                else __atomic_fetch_add(&j->deg[s], 1u, __ATOMIC_RELAXED);
+                if (d < j->hot) ++j->hot_deg[d];
+                else __atomic_fetch_add(&j->deg[d], 1u, __ATOMIC_RELAXED);
             } else {
-                j->raw[__atomic_fetch_add(&j->cursor[s], 1ull, __ATOMIC_RELAXED)] = d;
-                j->raw[__atomic_fetch_add(&j->cursor[d], 1ull, __ATOMIC_RELAXED)] = s;
+                j->raw[s < j->hot ? j->hot_cur[s]++ : __atomic_fetch_add(&j->cursor[s], 1ull, __ATOMIC_RELAXED)] = d;
+                j->raw[d < j->hot ? j->hot_cur[d]++ : __atomic_fetch_add(&j->cursor[d], 1ull, __ATOMIC_RELAXED)] = s;
             }
         }
     } else if (j->pass == 2) { /* sort + count distinct */
+        uint32_t* tmp = NULL;
+        uint64_t tmp_n = 0;
         for (uint32_t v = j->vlo; v < j->vhi; ++v) {
             uint64_t a = j->off0[v], n = j->off0[v + 1] - a;
-            if (n > 1) qsort(j->raw + a, n, sizeof(uint32_t), wfo_cmp_u32);
+            if (n > 1) wfo_sort_u32(j->raw + a, n, &tmp, &tmp_n);
             uint32_t c = 0;
             for (uint64_t e = 0; e < n; ++e) c += (e == 0 || j->raw[a + e] != j->raw[a + e - 1]);
             j->ndeg[v] = c;
         }
+        free(tmp);
     } else if (j->pass == 3) { /* compact */
         for (uint32_t v = j->vlo; v < j->vhi; ++v) {
             uint64_t a = j->off0[v], n = j->off0[v + 1] - a, w = j->off1[v];
@@ -967,14 +1005,20 @@ int wfo_rmat_csr(uint32_t scale, uint32_t edge_factor, double a, double b, doubl
     const uint64_t n = (uint64_t)edge_factor << scale;
     uint32_t* deg = calloc(V, sizeof(uint32_t));
     wfo_rmat_job* jobs = calloc(threads, sizeof(wfo_rmat_job));
+    const uint32_t hot = V < (1u << 18) ? V : (1u << 18);
     for (int t = 0; t < threads; ++t) {
         jobs[t].gen = &gen;
         jobs[t].lo = n * t / threads;
         jobs[t].hi = n * (t + 1) / threads;
         jobs[t].deg = deg;
+        jobs[t].hot = hot;
+        jobs[t].hot_deg = calloc(hot, sizeof(uint32_t));
+        jobs[t].hot_cur = malloc(hot * sizeof(uint64_t));
         jobs[t].pass = 0;
     }
     wfo_run_jobs(jobs, threads);
+    for (int t = 0; t < threads; ++t)
+        for (uint32_t v = 0; v < hot; ++v) deg[v] += jobs[t].hot_deg[v];
     uint64_t* off0 = malloc((V + 1ull) * sizeof(uint64_t));
     off0[0] = 0;
     for (uint32_t v = 0; v < V; ++v) off0[v + 1] = off0[v] + deg[v];
@@ -983,6 +1027,14 @@ int wfo_rmat_csr(uint32_t scale, uint32_t edge_factor, double a, double b, doubl
     uint32_t* raw = malloc((E0 ? E0 : 1) * sizeof(uint32_t));
     uint64_t* cursor = malloc(V * sizeof(uint64_t));
     memcpy(cursor, off0, V * sizeof(uint64_t));
+    /* each thread's hot cursors start at its own slice of the segment */
+    for (uint32_t v = 0; v < hot; ++v) {
+        uint64_t at = off0[v];
+        for (int t = 0; t < threads; ++t) {
+            jobs[t].hot_cur[v] = at;
+            at += jobs[t].hot_deg[v];
+        }
+    }
     for (int t = 0; t < threads; ++t) {
         jobs[t].cursor = cursor;
         jobs[t].raw = raw;
@@ -990,6 +1042,12 @@ int wfo_rmat_csr(uint32_t scale, uint32_t edge_factor, double a, double b, doubl
     }
     wfo_run_jobs(jobs, threads);
     free(cursor);
+    for (int t = 0; t < threads; ++t) {
+        free(jobs[t].hot_deg);
+        free(jobs[t].hot_cur);
+        jobs[t].hot_deg = NULL;
+        jobs[t].hot_cur = NULL;
+    }
     uint32_t* ndeg = malloc(V * sizeof(uint32_t));
     /* vertex ranges balanced by edges: R-MAT hubs sit at low ids */
     uint32_t* cut = malloc((threads + 1) * sizeof(uint32_t));

@@ -226,7 +226,7 @@ class RmatParamsC(C.Structure):
 
 # Every symbol include/walkforge_b200.h declares (checked by the CPU suite).
 EXPORTED_SYMBOLS = [
-    "wf_abi_version", "wf_last_error", "wf_kernel_launches",
+    "wf_abi_version", "wf_last_error", "wf_kernel_launches", "wf_device_count",
     "wf_graph_create", "wf_graph_create_device", "wf_graph_generate_rmat",
     "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_destroy",
     "wf_graph_read_wfg1", "wf_graph_write_wfg1", "wf_graph_load_edge_list", "wf_graph_original_ids",
@@ -234,7 +234,11 @@ EXPORTED_SYMBOLS = [
     "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_run_host_records",
     "wf_session_run_host_blocks",
     "wf_session_set_stats",
-    "wf_session_stats", "wf_session_layout", "wf_session_tune",
+    "wf_session_stats", "wf_session_stats_n", "wf_session_layout", "wf_session_tune",
+    "wf_session_create_custom",
+    "wf_worker_range", "wf_multi_create", "wf_multi_create_custom", "wf_multi_info", "wf_multi_run",
+    "wf_multi_destroy", "wf_comm_unique_id", "wf_comm_create", "wf_comm_allreduce_u32", "wf_comm_destroy",
+    "wf_nccl_version",
     "wf_walkset_info", "wf_walkset_copy", "wf_walkset_visit_counts", "wf_walkset_destroy",
     "wf_run", "wf_rng_probe", "wf_session_tables", "wf_encode_walks", "wf_walkset_write",
 ]

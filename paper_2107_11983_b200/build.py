@@ -35,6 +35,25 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) over the library's sources, headers and nvcc flags: the
+    stamp that ties a committed ncu capture (profiles/ncu_traffic.json) to the
+    kernels it measured."""
+    import hashlib
+    files = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                   + glob.glob(os.path.join(CSRC, "*.hpp"))
+                   + glob.glob(os.path.join(ROOT, "include", "walkforge_b200", "**", "*"), recursive=True)
+                   + [os.path.join(ROOT, "include", "walkforge_b200.h")])
+    h = hashlib.sha256()
+    for f in files:
+        if os.path.isfile(f):
+            h.update(os.path.relpath(f, ROOT).encode())
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+    h.update(" ".join(a for a in NVCC_FLAGS if not a.startswith("-I")).encode())
+    return h.hexdigest()[:16]
+
+
 def _newest(paths):
     return max(os.path.getmtime(p) for p in paths)
 
@@ -43,6 +62,7 @@ def build(verbose: bool = False, jobs: int = 4) -> str:
     os.makedirs(OBJ, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp"))
+               + glob.glob(os.path.join(ROOT, "include", "walkforge_b200", "device", "*"))
                + [os.path.join(ROOT, "include", "walkforge_b200.h")])
     hdr_time = _newest(headers)
     procs = []
@@ -81,6 +101,26 @@ def build(verbose: bool = False, jobs: int = 4) -> str:
                                cli_src, "-o", cli, f"-L{os.path.dirname(LIB)}",
                                f"-l:{os.path.basename(LIB)}", "-Wl,-rpath,$ORIGIN"])
     return LIB
+
+
+def build_user_program(src: str, out: str) -> str:
+    """Compiles a user's device-program translation unit (one that includes
+    walkforge_b200/device_program.cuh and uses WF_DEVICE_PROGRAM) into a
+    shared library, with the engine's own flags: the way a user of the
+    library builds a custom program."""
+    deps = [src] + glob.glob(os.path.join(ROOT, "include", "walkforge_b200", "**", "*"), recursive=True) + [
+        os.path.join(ROOT, "include", "walkforge_b200.h")]
+    if os.path.exists(out) and os.path.getmtime(out) >= _newest(deps):
+        return out
+    subprocess.check_call([nvcc()] + NVCC_FLAGS + ["-shared", "-o", out, src])
+    return out
+
+
+def build_test_programs() -> str:
+    """tests/programs/libwf_test_programs.so (test code: the reference's own
+    custom test programs written against the device program API)."""
+    d = os.path.join(ROOT, "tests", "programs")
+    return build_user_program(os.path.join(d, "test_programs.cu"), os.path.join(d, "libwf_test_programs.so"))
 
 
 if __name__ == "__main__":

@@ -73,6 +73,10 @@ std::string fmt_double(double x) {
     return buf;
 }
 
+}  // namespace
+
+namespace wf {
+
 // Program constructors' validation (algorithms.hpp:22-27, 43-51, 81-96,
 // 143-160, 179-182) and the resolved run (resolve_default_sampler,
 // program.hpp:68-75; resolve_flow, engine.hpp:255-272; resolve_orej_bound,
@@ -136,9 +140,22 @@ void resolve_program(Session& s, const wf_program_desc& d, const wf_exec_options
             config_error("unknown program kind " + std::to_string(d.kind));
     }
     s.desc.schema = nullptr;
-    const int type = walker_type(d.kind);
+    // row capacity: fixed-length programs hold their whole walk
+    const uint32_t fixed = d.kind == WF_PROGRAM_METAPATH ? d.schema_len + 1
+                           : d.kind == WF_PROGRAM_PPR ? 0 : d.target_length;
+    resolve_run(s, walker_type(d.kind), d.kind == WF_PROGRAM_NODE2VEC ? WF_SAMPLER_OREJ : WF_SAMPLER_DEFAULT,
+                has_max_weight, fixed, o);
+}
+
+// The sampler / flow / bound half of ResolvedRun (engine.hpp:275-294), shared by
+// the built-ins and custom programs: resolve_default_sampler (program.hpp:68-75),
+// resolve_flow (engine.hpp:255-272), resolve_orej_bound (engine.hpp:103-114)
+// with the bound already in s.params.bound.
+void resolve_run(Session& s, int type, int preferred, bool has_max_weight, uint32_t fixed,
+                 const wf_exec_options* o) {
+    ProgParams& p = s.params;
     int kind = o && o->sampler >= 0 ? o->sampler
-               : d.kind == WF_PROGRAM_NODE2VEC ? WF_SAMPLER_OREJ
+               : preferred >= 0 ? preferred
                : type == kUnbiased ? WF_SAMPLER_NAIVE
                : type == kStatic ? WF_SAMPLER_ALIAS : WF_SAMPLER_ITS;
     if (kind < WF_SAMPLER_NAIVE || kind > WF_SAMPLER_OREJ) config_error("unknown sampler");
@@ -168,19 +185,29 @@ void resolve_program(Session& s, const wf_program_desc& d, const wf_exec_options
         if (o->k == 0) config_error("task ring size must be >= 1");
         if (o->k_prime == 0 || o->k_prime > o->k) config_error("search ring size must be in [1, k]");
     }
-    // row capacity: fixed-length programs hold their whole walk
-    uint32_t fixed = d.kind == WF_PROGRAM_METAPATH ? d.schema_len + 1
-                     : d.kind == WF_PROGRAM_PPR ? 0 : d.target_length;
     if (fixed) s.default_stride = fixed;
     else s.default_stride = o && o->path_stride ? o->path_stride : 64;
+    s.unbounded = fixed == 0;
 }
 
-struct ResolvedSpec {
-    wf_query_spec spec{};
-    uint64_t n = 0;
-    DeviceBuffer<uint32_t> sources;
-    const uint32_t* dev_sources = nullptr;
-};
+// A user's device program (wf_session_create_custom): the table says what the
+// concept's optional members are; the object rides in the launch parameters.
+void resolve_custom(Session& s, const wf_program_ops& ops, const void* program, const wf_exec_options* o) {
+    require(ops.abi_version == WF_ABI_VERSION, "program table built against another ABI version");
+    require(ops.launch_size == sizeof(WalkLaunch), "program table built against another engine header");
+    require(ops.launch && ops.occupancy && ops.static_weights, "incomplete program table");
+    require(program != nullptr || ops.program_size == 0, "null program object");
+    require(ops.program_size <= static_cast<uint32_t>(kUserProgramBytes), "program object too large");
+    require(ops.walker_type >= kUnbiased && ops.walker_type <= kDynamic, "bad walker type");
+    s.custom = &ops;
+    s.params = ProgParams{};
+    if (ops.program_size) std::memcpy(s.params.user, program, ops.program_size);
+    s.desc = wf_program_desc{};
+    s.desc.kind = kCustomProgram;
+    s.params.bound = ops.has_max_weight && ops.max_weight ? ops.max_weight(program) : 0.0;
+    resolve_run(s, ops.walker_type, ops.preferred_sampler, ops.has_max_weight != 0,
+                ops.max_path ? ops.max_path(program) : 0u, o);
+}
 
 // QuerySpec::total + validate (walker.cpp:80-109), sources made device-resident.
 void resolve_spec(const GraphStore& g, const wf_query_spec* q, ResolvedSpec& r) {
@@ -233,6 +260,10 @@ void check_device_error(Session& s) {
     }
 }
 
+}  // namespace wf
+
+namespace {
+
 __global__ void k_rng_probe(uint64_t premixed, const uint64_t* streams, uint64_t n, uint32_t draws,
                             uint64_t* out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -259,9 +290,23 @@ int current_device() {
 
 }  // namespace
 
+namespace wf {
+std::string& last_error_slot() { return g_last_error; }
+GraphStore* graph_store(const wf_graph* g) { return g->g.get(); }
+}  // namespace wf
+
 extern "C" {
 
 int wf_abi_version(void) { return WF_ABI_VERSION; }
+
+int wf_device_count(int32_t* n) {
+    return guarded([&] {
+        require(n != nullptr, "null argument");
+        int c = 0;
+        WF_CUDA(cudaGetDeviceCount(&c));
+        *n = c;
+    });
+}
 const char* wf_last_error(void) { return g_last_error.c_str(); }
 uint64_t wf_kernel_launches(void) { return g_kernel_launches.load(); }
 
@@ -384,6 +429,78 @@ void wf_graph_destroy(wf_graph* g) {
     }
 }
 
+}  // extern "C"
+
+namespace wf {
+
+// Device state of a resolved session: error word, claim cursor, static
+// tables and the decorated layouts the HBM budget allows.  `tables_from`: a
+// session of the same program on another device whose static tables are
+// copied (peer copy) instead of rebuilt (multi-device runs).
+void setup_session(Session& s, const wf_exec_options* opts, const Session* tables_from) {
+    s.error_word.allocate(1);
+    WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
+    // random 32 B gathers: do not let L2 promote misses to 64/128 B fetches
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+    cudaGetLastError();
+    s.cursor.allocate(1);
+    // HBM budget for the decorated layouts (they trade capacity for one
+    // dependent random load per move); fall back to the compact forms.
+    size_t free_b = 0, total_b = 0;
+    WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t reserve = 8ull << 30;
+    const uint64_t E = s.g->E;
+    const uint32_t lf = opts ? opts->layout_flags : 0;
+    // a custom program's update() reads the traversed edge: its buckets carry
+    // edge positions (compact), the destination is read from the CSR
+    s.alias_idx = s.custom != nullptr;
+    if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS && !(lf & WF_LAYOUT_COMPACT_ALIAS) && !s.alias_idx)
+        s.alias_wide = 32 * E + reserve <= free_b;
+    if (s.flow == kTables) {
+        if (tables_from) s.copy_tables_from(*tables_from, nullptr);
+        else s.build_tables(nullptr);
+    }
+    // The decorated adjacency saves the dependent vertex-word load but is 4x
+    // the neighbour array: when the compact graph (neighbours + vertex
+    // words) is near L2 size, its L2 hits win (C2: 12.8 vs 11.3 G moves/s).
+    int l2 = 0;
+    WF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.g->device));
+    const uint64_t compact = 4 * E + 8ull * s.g->V;
+    const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
+    if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
+        s.build_adjacency(nullptr);
+    if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
+        s.g->ensure_label_index(nullptr);
+        WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        // one random 16 B read per move (the partitioned edge carrying the
+        // next schema label's group of its destination) instead of label
+        // record + neighbour: C4 2.07 -> 1.87 ms since the warp-claimed
+        // refill (it measured slower while the cursor atomic bound C4)
+        if (!(lf & WF_LAYOUT_NO_MP_SUCC) && 16 * E + reserve <= free_b)
+            s.build_metapath_successors(nullptr);
+    }
+    if (s.desc.kind == WF_PROGRAM_NODE2VEC) {
+        // distance test: exact edge hash set (one random bucket per query)
+        // unless opted out or HBM is short; then the sector B-tree
+        WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (!(lf & WF_LAYOUT_SEARCH_TREE) && (s.g->edge_hash_built || 16 * E + reserve <= free_b)) {
+            s.g->ensure_edge_hash(nullptr);
+            s.use_edge_hash = true;
+        } else {
+            s.g->ensure_search_index(nullptr);
+        }
+        if (!(lf & WF_LAYOUT_NO_EDGE_FILTER)) {
+            s.g->ensure_edge_filter(nullptr);
+            s.use_edge_filter = true;
+        }
+    }
+    s.grid = occupancy_grid(s);
+}
+
+}  // namespace wf
+
+extern "C" {
+
 int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_exec_options* opts,
                       wf_session** out) {
     return guarded([&] {
@@ -394,58 +511,24 @@ int wf_session_create(const wf_graph* g, const wf_program_desc* prog, const wf_e
         Session& s = *h->s;
         s.g = g->g.get();
         resolve_program(s, *prog, opts);
-        s.error_word.allocate(1);
-        WF_CUDA(cudaMemset(s.error_word.get(), 0, 4));
-        // random 32 B gathers: do not let L2 promote misses to 64/128 B fetches
-        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
-        cudaGetLastError();
-        s.cursor.allocate(1);
         h->counters.allocate(2);
-        // HBM budget for the decorated layouts (they trade capacity for one
-        // dependent random load per move); fall back to the compact forms.
-        size_t free_b = 0, total_b = 0;
-        WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const uint64_t reserve = 8ull << 30;
-        const uint64_t E = s.g->E;
-        const uint32_t lf = opts ? opts->layout_flags : 0;
-        if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS && !(lf & WF_LAYOUT_COMPACT_ALIAS))
-            s.alias_wide = 32 * E + reserve <= free_b;
-        if (s.flow == kTables) s.build_tables(nullptr);
-        // The decorated adjacency saves the dependent vertex-word load but is 4x
-        // the neighbour array: when the compact graph (neighbours + vertex
-        // words) is near L2 size, its L2 hits win (C2: 12.8 vs 11.3 G moves/s).
-        int l2 = 0;
-        WF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.g->device));
-        const uint64_t compact = 4 * E + 8ull * s.g->V;
-        const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
-        if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
-            s.build_adjacency(nullptr);
-        if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
-            s.g->ensure_label_index(nullptr);
-            WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            // one random 16 B read per move (the partitioned edge carrying the
-            // next schema label's group of its destination) instead of label
-            // record + neighbour: C4 2.07 -> 1.87 ms since the warp-claimed
-            // refill (it measured slower while the cursor atomic bound C4)
-            if (!(lf & WF_LAYOUT_NO_MP_SUCC) && 16 * E + reserve <= free_b)
-                s.build_metapath_successors(nullptr);
-        }
-        if (s.desc.kind == WF_PROGRAM_NODE2VEC) {
-            // distance test: exact edge hash set (one random bucket per query)
-            // unless opted out or HBM is short; then the sector B-tree
-            WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-            if (!(lf & WF_LAYOUT_SEARCH_TREE) && (s.g->edge_hash_built || 16 * E + reserve <= free_b)) {
-                s.g->ensure_edge_hash(nullptr);
-                s.use_edge_hash = true;
-            } else {
-                s.g->ensure_search_index(nullptr);
-            }
-            if (!(lf & WF_LAYOUT_NO_EDGE_FILTER)) {
-                s.g->ensure_edge_filter(nullptr);
-                s.use_edge_filter = true;
-            }
-        }
-        s.grid = occupancy_grid(s);
+        setup_session(s, opts, nullptr);
+        *out = h.release();
+    });
+}
+
+int wf_session_create_custom(const wf_graph* g, const wf_program_ops* ops, const void* program,
+                             const wf_exec_options* opts, wf_session** out) {
+    return guarded([&] {
+        require(g && ops && out, "null argument");
+        DeviceGuard guard(g->g->device);
+        auto h = std::make_unique<wf_session>();
+        h->s = std::make_unique<Session>();
+        Session& s = *h->s;
+        s.g = g->g.get();
+        resolve_custom(s, *ops, program, opts);
+        h->counters.allocate(2);
+        setup_session(s, opts, nullptr);
         *out = h.release();
     });
 }
@@ -513,87 +596,104 @@ int wf_session_sync(wf_session* sh, void* stream) {
     });
 }
 
+}  // extern "C"
+
+namespace wf {
+
+// run_sequential's result for queries [qb, qe) of a resolved spec, kept in
+// HBM (rows relative to qb).  Walks that outgrow their row are re-run into
+// rows of their own (same (seed, qid) streams).  `ctr`: two device counters
+// (moves, overflowed rows).
+std::unique_ptr<WalkSetStore> session_run(Session& s, const ResolvedSpec& rs, uint64_t qb, uint64_t qe,
+                                          unsigned long long* ctr) {
+    GraphStore& g = *s.g;
+    DeviceGuard guard(g.device);
+    auto wp = std::make_unique<WalkSetStore>();
+    WalkSetStore& w = *wp;
+    w.device = g.device;
+    w.n = qe - qb;
+    w.V = g.V;
+    w.stride = s.default_stride;
+    w.paths.allocate(std::max<uint64_t>(w.n * w.stride, 1));
+    w.lengths.allocate(std::max<uint64_t>(w.n, 1));
+    w.status.allocate(std::max<uint64_t>(w.n, 1));
+    const bool counts = s.desc.kind == WF_PROGRAM_PPR;
+    if (counts) {
+        w.visit_counts.allocate(g.V);
+        WF_CUDA(cudaMemset(w.visit_counts.get(), 0, g.V * 4ull));
+    }
+    WF_CUDA(cudaMemset(ctr, 0, 16));
+    cudaEvent_t e0, e1;
+    WF_CUDA(cudaEventCreate(&e0));
+    WF_CUDA(cudaEventCreate(&e1));
+    WF_CUDA(cudaEventRecord(e0, nullptr));
+    launch_walk(s, rs.spec, rs.dev_sources, qb, qe, nullptr, w.paths.get(), w.stride, w.lengths.get(),
+                w.status.get(), counts ? w.visit_counts.get() : nullptr, ctr, ctr + 1, s.cursor.get(), nullptr);
+    WF_CUDA(cudaEventRecord(e1, nullptr));
+    WF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    WF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    check_device_error(s);
+    unsigned long long hc[2] = {0, 0};
+    WF_CUDA(cudaMemcpy(hc, ctr, 16, cudaMemcpyDeviceToHost));
+    if (hc[1] > 0) {
+        // re-run the walks that outgrew their row; same (seed, qid) streams
+        std::vector<uint32_t> lens(w.n);
+        WF_CUDA(cudaMemcpy(lens.data(), w.lengths.get(), w.n * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> qids;
+        uint32_t mx = 0;
+        for (uint64_t r = 0; r < w.n; ++r)
+            if (lens[r] > w.stride) {
+                w.over_rows.push_back(r);
+                qids.push_back(qb + r);
+                mx = std::max(mx, lens[r]);
+            }
+        w.over_stride = mx;
+        DeviceBuffer<uint64_t> dq(qids.size());
+        WF_CUDA(cudaMemcpy(dq.get(), qids.data(), qids.size() * 8, cudaMemcpyHostToDevice));
+        w.over_paths.allocate(qids.size() * static_cast<uint64_t>(mx));
+        DeviceBuffer<uint32_t> tl(qids.size());
+        DeviceBuffer<uint8_t> ts(qids.size());
+        DeviceBuffer<unsigned long long> tc(2);
+        WF_CUDA(cudaMemset(tc.get(), 0, 16));
+        launch_walk(s, rs.spec, rs.dev_sources, 0, qids.size(), dq.get(), w.over_paths.get(), mx, tl.get(),
+                    ts.get(), nullptr, tc.get(), tc.get() + 1, s.cursor.get(), nullptr);
+        WF_CUDA(cudaDeviceSynchronize());
+        check_device_error(s);
+    }
+    w.metrics.preprocess_seconds = s.preprocess_seconds;
+    w.metrics.exec_seconds = ms * 1e-3;
+    w.metrics.total_steps = hc[0];
+    w.metrics.max_in_flight = static_cast<uint32_t>(
+        std::min<uint64_t>(static_cast<uint64_t>(s.grid) * kBlock, std::max<uint64_t>(w.n, 1)));
+    w.total_vertices = w.n + hc[0];
+    if (w.n) {
+        DeviceBuffer<unsigned> m(1);
+        WF_CUDA(cudaMemset(m.get(), 0, 4));
+        k_max_u32<<<256, 256>>>(w.lengths.get(), w.n, m.get());
+        WF_LAUNCHED();
+        WF_CUDA(cudaMemcpy(&w.max_length, m.get(), 4, cudaMemcpyDeviceToHost));
+    }
+    return wp;
+}
+
+}  // namespace wf
+
+extern "C" {
+
 int wf_session_run(wf_session* sh, const wf_query_spec* spec, wf_walkset** out,
                    wf_run_metrics* metrics) {
     return guarded([&] {
         require(sh && spec && out, "null argument");
         Session& s = *sh->s;
-        GraphStore& g = *s.g;
-        DeviceGuard guard(g.device);
+        DeviceGuard guard(s.g->device);
         ResolvedSpec rs;
-        resolve_spec(g, spec, rs);
+        resolve_spec(*s.g, spec, rs);
         auto wh = std::make_unique<wf_walkset>();
-        wh->w = std::make_unique<WalkSetStore>();
-        WalkSetStore& w = *wh->w;
-        w.device = g.device;
-        w.n = rs.n;
-        w.V = g.V;
-        w.stride = s.default_stride;
-        w.paths.allocate(std::max<uint64_t>(w.n * w.stride, 1));
-        w.lengths.allocate(std::max<uint64_t>(w.n, 1));
-        w.status.allocate(std::max<uint64_t>(w.n, 1));
-        const bool counts = s.desc.kind == WF_PROGRAM_PPR;
-        if (counts) {
-            w.visit_counts.allocate(g.V);
-            WF_CUDA(cudaMemset(w.visit_counts.get(), 0, g.V * 4ull));
-        }
-        unsigned long long* ctr = sh->counters.get();
-        WF_CUDA(cudaMemset(ctr, 0, 16));
-        cudaEvent_t e0, e1;
-        WF_CUDA(cudaEventCreate(&e0));
-        WF_CUDA(cudaEventCreate(&e1));
-        WF_CUDA(cudaEventRecord(e0, nullptr));
-        launch_walk(s, rs.spec, rs.dev_sources, 0, w.n, nullptr, w.paths.get(), w.stride,
-                    w.lengths.get(), w.status.get(), counts ? w.visit_counts.get() : nullptr, ctr,
-                    ctr + 1, s.cursor.get(), nullptr);
-        WF_CUDA(cudaEventRecord(e1, nullptr));
-        WF_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        WF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        check_device_error(s);
-        unsigned long long hc[2] = {0, 0};
-        WF_CUDA(cudaMemcpy(hc, ctr, 16, cudaMemcpyDeviceToHost));
-        if (hc[1] > 0) {
-            // re-run the walks that outgrew their row; same (seed, qid) streams
-            std::vector<uint32_t> lens(w.n);
-            WF_CUDA(cudaMemcpy(lens.data(), w.lengths.get(), w.n * 4, cudaMemcpyDeviceToHost));
-            std::vector<uint64_t> qids;
-            uint32_t mx = 0;
-            for (uint64_t r = 0; r < w.n; ++r)
-                if (lens[r] > w.stride) {
-                    w.over_rows.push_back(r);
-                    qids.push_back(r);
-                    mx = std::max(mx, lens[r]);
-                }
-            w.over_stride = mx;
-            DeviceBuffer<uint64_t> dq(qids.size());
-            WF_CUDA(cudaMemcpy(dq.get(), qids.data(), qids.size() * 8, cudaMemcpyHostToDevice));
-            w.over_paths.allocate(qids.size() * static_cast<uint64_t>(mx));
-            DeviceBuffer<uint32_t> tl(qids.size());
-            DeviceBuffer<uint8_t> ts(qids.size());
-            DeviceBuffer<unsigned long long> tc(2);
-            WF_CUDA(cudaMemset(tc.get(), 0, 16));
-            launch_walk(s, rs.spec, rs.dev_sources, 0, qids.size(), dq.get(), w.over_paths.get(), mx,
-                        tl.get(), ts.get(), nullptr, tc.get(), tc.get() + 1, s.cursor.get(), nullptr);
-            WF_CUDA(cudaDeviceSynchronize());
-            check_device_error(s);
-        }
-        w.metrics.preprocess_seconds = s.preprocess_seconds;
-        w.metrics.exec_seconds = ms * 1e-3;
-        w.metrics.total_steps = hc[0];
-        w.metrics.max_in_flight = static_cast<uint32_t>(
-            std::min<uint64_t>(static_cast<uint64_t>(s.grid) * kBlock, std::max<uint64_t>(w.n, 1)));
-        w.total_vertices = w.n + hc[0];
-        if (w.n) {
-            DeviceBuffer<unsigned> m(1);
-            WF_CUDA(cudaMemset(m.get(), 0, 4));
-            k_max_u32<<<256, 256>>>(w.lengths.get(), w.n, m.get());
-            WF_LAUNCHED();
-            WF_CUDA(cudaMemcpy(&w.max_length, m.get(), 4, cudaMemcpyDeviceToHost));
-        }
-        if (metrics) *metrics = w.metrics;
+        wh->w = session_run(s, rs, 0, rs.n, sh->counters.get());
+        if (metrics) *metrics = wh->w->metrics;
         *out = wh.release();
     });
 }
@@ -660,25 +760,29 @@ int wf_session_set_stats(wf_session* sh, int enable) {
         Session& s = *sh->s;
         DeviceGuard guard(s.g->device);
         if (enable && !s.stats.get()) {
-            s.stats.allocate(3);
-            WF_CUDA(cudaMemset(s.stats.get(), 0, 24));
+            s.stats.allocate(WF_STATS_COUNT);
+            WF_CUDA(cudaMemset(s.stats.get(), 0, WF_STATS_COUNT * 8));
         }
         s.collect_stats = enable != 0;
     });
 }
 
-int wf_session_stats(wf_session* sh, uint64_t* out3) {
+int wf_session_stats_n(wf_session* sh, uint64_t* out, uint32_t n) {
     return guarded([&] {
-        require(sh && out3, "null argument");
+        require(sh && out, "null argument");
         Session& s = *sh->s;
         DeviceGuard guard(s.g->device);
-        out3[0] = out3[1] = out3[2] = 0;
+        for (uint32_t i = 0; i < n; ++i) out[i] = 0;
         if (!s.stats.get()) return;
+        uint64_t all[WF_STATS_COUNT];
         WF_CUDA(cudaDeviceSynchronize());
-        WF_CUDA(cudaMemcpy(out3, s.stats.get(), 24, cudaMemcpyDeviceToHost));
-        WF_CUDA(cudaMemset(s.stats.get(), 0, 24));
+        WF_CUDA(cudaMemcpy(all, s.stats.get(), sizeof(all), cudaMemcpyDeviceToHost));
+        WF_CUDA(cudaMemset(s.stats.get(), 0, sizeof(all)));
+        for (uint32_t i = 0; i < n && i < WF_STATS_COUNT; ++i) out[i] = all[i];
     });
 }
+
+int wf_session_stats(wf_session* sh, uint64_t* out3) { return wf_session_stats_n(sh, out3, 3); }
 
 // Launch tuner (tune.cpp:46-111's role): candidate blocks/SM from the occupancy
 // maximum down to a quarter, each timed over whole launches of the range.

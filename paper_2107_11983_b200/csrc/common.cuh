@@ -12,7 +12,7 @@
 #include <string>
 #include <utility>
 
-#include "../../include/walkforge_b200.h"
+#include "walkforge_b200.h"
 
 namespace wf {
 

@@ -4,7 +4,7 @@
 #pragma once
 
 #include "common.cuh"
-#include "engine.cuh"
+#include "walkforge_b200/device/engine.cuh"
 
 namespace wf {
 

@@ -18,7 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
-#include "engine.cuh"
+#include "walkforge_b200/device/engine.cuh"
 
 namespace wf {
 
@@ -31,6 +31,10 @@ struct GraphStore {
     DeviceBuffer<uint64_t> offsets;
     DeviceBuffer<uint32_t> nbr;
     DeviceBuffer<float> weights;
+    // the reference's f64 weights (graph.hpp:102), kept only when some weight
+    // is not float32-exact (then `weights` holds their f32 roundings for the
+    // hot-path layouts and this array is what samplers and tables read)
+    DeviceBuffer<double> weights64;
     DeviceBuffer<uint8_t> labels;
     DeviceBuffer<uint64_t> vword;
     bool sorted = true;
@@ -61,6 +65,7 @@ struct GraphStore {
         g.offsets = offsets.get();
         g.nbr = nbr.get();
         g.weights = weights.get();
+        g.weights64 = weights64.get();
         g.labels = labels.get();
         g.vword = vword.get();
         g.sorted = sorted ? 1 : 0;
@@ -92,6 +97,7 @@ void release_host_pipe(HostPipe* p);
 
 struct Session {
     GraphStore* g = nullptr;
+    const wf_program_ops* custom = nullptr;  // a user's device program (wf_session_create_custom)
     std::unique_ptr<HostPipe, void (*)(HostPipe*)> pipe{nullptr, release_host_pipe};
     wf_program_desc desc{};
     std::vector<uint32_t> schema;
@@ -119,12 +125,16 @@ struct Session {
     bool collect_stats = false;
     DeviceBuffer<unsigned long long> stats;  // [trials, probes, scanned]
     bool alias_wide = false;     // 32 B buckets carrying the destinations' vertex words
+    bool alias_idx = false;      // buckets carry edge positions (custom programs read the edge)
     bool use_edge_hash = false;  // Node2Vec distance test through the graph's edge hash set
     bool use_edge_filter = false;  // ... behind the graph's pair pre-filter
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
     DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 
     void build_tables(cudaStream_t st);
+    // the static tables of a session of the same program on another device
+    // (multi-device runs: peer copies instead of a rebuild)
+    void copy_tables_from(const Session& src, cudaStream_t st);
     void build_adjacency(cudaStream_t st);
     // MetaPath with a schema whose successor label is a function of the label
     // (e.g. cyclic): returns false (no table) otherwise.
@@ -160,6 +170,27 @@ struct StreamLaunch {
     uint32_t src_shift = 16;
     uint64_t src_row0 = 0;  // rows of the list (src_ready's count) before the launch's first row
 };
+
+// capi.cu: the calling thread's wf_last_error() text; the store behind a handle
+std::string& last_error_slot();
+GraphStore* graph_store(const wf_graph* g);
+
+// capi.cu: ResolvedRun (engine.hpp:275-294) and QuerySpec resolution
+struct ResolvedSpec {
+    wf_query_spec spec{};
+    uint64_t n = 0;
+    DeviceBuffer<uint32_t> sources;
+    const uint32_t* dev_sources = nullptr;
+};
+void resolve_program(Session& s, const wf_program_desc& d, const wf_exec_options* o);
+void resolve_custom(Session& s, const wf_program_ops& ops, const void* program, const wf_exec_options* o);
+void resolve_run(Session& s, int type, int preferred, bool has_max_weight, uint32_t fixed,
+                 const wf_exec_options* o);
+void setup_session(Session& s, const wf_exec_options* opts, const Session* tables_from);
+void resolve_spec(const GraphStore& g, const wf_query_spec* q, ResolvedSpec& r);
+void check_device_error(Session& s);
+std::unique_ptr<WalkSetStore> session_run(Session& s, const ResolvedSpec& rs, uint64_t qb, uint64_t qe,
+                                          unsigned long long* ctr);
 
 // walk.cu
 void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sources,

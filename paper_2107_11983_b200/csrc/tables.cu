@@ -27,11 +27,16 @@ namespace {
 struct UnitWeight {
     __device__ __forceinline__ double operator()(uint64_t) const { return 1.0; }
 };
-struct EdgeWeight {
+struct EdgeWeight {  // the graph's weights (f64 when they are not all float32-exact)
     const float* __restrict__ w;
+    const double* __restrict__ w64;
     __device__ __forceinline__ double operator()(uint64_t e) const {
-        return static_cast<double>(__ldg(w + e));
+        return w64 ? __ldg(w64 + e) : static_cast<double>(__ldg(w + e));
     }
+};
+struct F64Weight {  // a custom program's weight(nullptr, e), materialised once
+    const double* __restrict__ w;
+    __device__ __forceinline__ double operator()(uint64_t e) const { return __ldg(w + e); }
 };
 
 __device__ __forceinline__ void store_bucket(uint4* b, double split, uint32_t first_dst,
@@ -51,7 +56,9 @@ __device__ __forceinline__ double unpark(const uint4* b) {
     return __longlong_as_double(static_cast<long long>(bits));
 }
 
-template <typename WF>
+// IDX: buckets carry the positions {first, second} in E_v (EngineAliasSlot,
+// engine.hpp:22-28) instead of their destinations.
+template <typename WF, bool IDX>
 __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
                                uint32_t V, WF wf, uint4* __restrict__ bucket, uint32_t bs,
                                uint8_t* __restrict__ exhausted, unsigned* any_exhausted) {
@@ -67,7 +74,8 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
             atomicOr(any_exhausted, 1u);
             continue;
         }
-        const uint32_t* dst = nbr + a0;
+        const uint32_t* nb = nbr + a0;
+        auto dst = [&](uint32_t i) { return IDX ? i : nb[i]; };
         uint4* out = bucket + a0 * bs;  // bs = 2: wide 32 B buckets (second half decorated later)
         auto scaled = [&](uint32_t i) { return wf(a0 + i) * n / sum; };  // sampler.hpp:97
         auto next_large = [&](uint32_t from) {
@@ -98,7 +106,7 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
             } else {
                 break;
             }
-            store_bucket(out + s * bs, sval, dst[s], dst[lcur]);
+            store_bucket(out + s * bs, sval, dst(s), dst(lcur));
             lval -= 1.0 - sval;
             if (lval < 1.0) {
                 park(out + lcur * bs, lval);
@@ -108,14 +116,14 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
             }
         }
         // leftovers at probability exactly 1 (sampler.hpp:112-119)
-        for (uint32_t s = a; s < n; s = next_small(s + 1)) store_bucket(out + s * bs, 1.0, dst[s], dst[s]);
+        for (uint32_t s = a; s < n; s = next_small(s + 1)) store_bucket(out + s * bs, 1.0, dst(s), dst(s));
         while (consumed < demoted) {
             c = next_large(c);
-            store_bucket(out + c * bs, 1.0, dst[c], dst[c]);
+            store_bucket(out + c * bs, 1.0, dst(c), dst(c));
             ++c;
             ++consumed;
         }
-        for (uint32_t l = lcur; l < n; l = next_large(l + 1)) store_bucket(out + l * bs, 1.0, dst[l], dst[l]);
+        for (uint32_t l = lcur; l < n; l = next_large(l + 1)) store_bucket(out + l * bs, 1.0, dst(l), dst(l));
     }
 }
 
@@ -211,8 +219,12 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
         // buckets of exhausted vertices are never built; zero them so the
         // decoration pass reads valid vertex ids there
         WF_CUDA(cudaMemsetAsync(s.alias.get(), 0, s.alias.bytes(), st));
-        k_static_alias<<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
-                                                   s.alias.get(), bs, s.exhausted.get(), any);
+        if (s.alias_idx)
+            k_static_alias<WF, true><<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
+                                                                 s.alias.get(), bs, s.exhausted.get(), any);
+        else
+            k_static_alias<WF, false><<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
+                                                                  s.alias.get(), bs, s.exhausted.get(), any);
     } else if (s.kind == WF_SAMPLER_ITS) {
         s.its.allocate(std::max<uint64_t>(g.E, 1));
         k_static_its<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.its.get(),
@@ -237,8 +249,28 @@ void Session::build_tables(cudaStream_t st) {
     DeviceBuffer<unsigned> any(1);
     WF_CUDA(cudaMemsetAsync(any.get(), 0, 4, st));
     bool edge_weight = desc.kind == WF_PROGRAM_DEEPWALK && desc.weighted;
-    if (edge_weight) launch_tables(*this, EdgeWeight{gs.weights.get()}, any.get(), st);
-    else launch_tables(*this, UnitWeight{}, any.get(), st);
+    DeviceBuffer<double> custom_w;
+    if (custom) {
+        // weight(nullptr, e) over every edge by the program's own kernel, with
+        // check_program_weight (engine.hpp:97-101) on each
+        custom_w.allocate(std::max<uint64_t>(gs.E, 1));
+        DeviceBuffer<int> bad(1);
+        WF_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+        const GraphView gv = gs.view();
+        const int rc = custom->static_weights(&gv, params.user, custom_w.get(), bad.get(), st);
+        if (rc != 0) raise(WF_ERR_CUDA, std::string("custom program static weights: ") +
+                                            cudaGetErrorString(static_cast<cudaError_t>(rc)));
+        count_launch();
+        int h_bad = 0;
+        WF_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), 4, cudaMemcpyDeviceToHost, st));
+        WF_CUDA(cudaStreamSynchronize(st));
+        if (h_bad) raise(WF_ERR_CONTRACT, "program emitted a weight that is negative or not finite");
+        launch_tables(*this, F64Weight{custom_w.get()}, any.get(), st);
+    } else if (edge_weight) {
+        launch_tables(*this, EdgeWeight{gs.weights.get(), gs.weights64.get()}, any.get(), st);
+    } else {
+        launch_tables(*this, UnitWeight{}, any.get(), st);
+    }
     unsigned h = 0;
     WF_CUDA(cudaMemcpyAsync(&h, any.get(), 4, cudaMemcpyDeviceToHost, st));
     WF_CUDA(cudaStreamSynchronize(st));
@@ -337,6 +369,30 @@ void Session::build_adjacency(cudaStream_t st) {
     WF_CUDA(cudaStreamSynchronize(st));
     preprocess_seconds +=
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace wf
+
+namespace wf {
+
+void Session::copy_tables_from(const Session& src, cudaStream_t st) {
+    DeviceGuard guard(g->device);
+    auto t0 = std::chrono::steady_clock::now();
+    auto peer = [&](auto& dst, const auto& from) {
+        if (!from.get()) return;
+        dst.allocate(from.size());
+        WF_CUDA(cudaMemcpyPeerAsync(dst.get(), g->device, from.get(), src.g->device, from.bytes(), st));
+    };
+    peer(alias, src.alias);
+    peer(its, src.its);
+    peer(rej, src.rej);
+    peer(exhausted, src.exhausted);
+    peer(sview, src.sview);
+    any_exhausted = src.any_exhausted;
+    alias_wide = src.alias_wide;
+    alias_idx = src.alias_idx;
+    WF_CUDA(cudaStreamSynchronize(st));
+    preprocess_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 }  // namespace wf

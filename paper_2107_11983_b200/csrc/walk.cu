@@ -19,7 +19,7 @@ namespace {
 // instantiations live in walk_stream.cu (compiled in parallel).
 KernelFn select_kernel(int prog, int sampler, int flow) {
 #define WF_CASE(P, S, F) \
-    if (prog == P && sampler == S && flow == F) return &walk_kernel<P, S, F, false>;
+    if (prog == P && sampler == S && flow == F) return &walk_kernel<Program<P>, S, F, false>;
     WF_FOR_EACH_COMBO(WF_CASE)
 #undef WF_CASE
     config_error("no kernel for this program/sampler/flow combination");
@@ -33,10 +33,25 @@ int row_bucket(uint64_t n_rows) {
     return b;
 }
 
+// A custom program's kernels live in the user's translation unit: their
+// occupancy and launches go through its wf_program_ops table.
+void custom_occupancy(const Session& s, int streaming, int* per_sm, int* regs) {
+    int32_t b = 0, r = 0;
+    const int rc = s.custom->occupancy(s.kind, s.flow, streaming, &b, &r);
+    if (rc != 0) raise(WF_ERR_CUDA, std::string("custom program occupancy: ") +
+                                        cudaGetErrorString(static_cast<cudaError_t>(rc)));
+    if (per_sm) *per_sm = b;
+    if (regs) *regs = r;
+}
+
 int occupancy_grid(const Session& s) {
-    KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
     int per_sm = 0;
-    WF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+    if (s.custom) {
+        custom_occupancy(s, 0, &per_sm, nullptr);
+    } else {
+        KernelFn fn = select_kernel(s.desc.kind, s.kind, s.flow);
+        WF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+    }
     return std::max(1, per_sm) * sm_count(s.g->device);
 }
 
@@ -48,8 +63,9 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     GraphStore& g = *s.g;
     if (qid_end <= qid_begin) return;
     if (stride == 0) config_error("path stride must be >= 1");
-    KernelFn fn = stream ? select_stream_kernel(s.desc.kind, s.kind, s.flow)
-                         : select_kernel(s.desc.kind, s.kind, s.flow);
+    KernelFn fn = s.custom ? nullptr
+                  : stream ? select_stream_kernel(s.desc.kind, s.kind, s.flow)
+                           : select_kernel(s.desc.kind, s.kind, s.flow);
     WalkLaunch L{};
     L.g = g.view();
     if (!s.use_edge_hash) L.g.ehash = nullptr;  // per-session choice (B-tree opt-in)
@@ -80,6 +96,7 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.g.stats = s.collect_stats ? s.stats.get() : nullptr;
     L.staged = (stride % 8 == 0 && reinterpret_cast<uintptr_t>(paths) % 32 == 0) ? 1 : 0;
     L.alias_wide = s.alias_wide ? 1 : 0;
+    L.alias_idx = s.alias_idx ? 1 : 0;
     L.adj = s.adj.get();
     L.mp_adj = s.mp_adj.get();
     if (stream) {
@@ -115,7 +132,9 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
         static std::mutex mu;
         static std::map<KernelFn, int> regs;  // cudaFuncGetAttributes costs the host a few us
         int nregs;
-        {
+        if (s.custom) {
+            custom_occupancy(s, 1, nullptr, &nregs);
+        } else {
             std::lock_guard<std::mutex> lock(mu);
             auto it = regs.find(fn);
             if (it == regs.end()) {
@@ -154,6 +173,13 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
         L.dyn_base = warps * L.static_blocks * kClaim;
     }
     WF_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+    if (s.custom) {
+        const int rc = s.custom->launch(&L, s.kind, s.flow, stream ? 1 : 0, grid, st);
+        if (rc != 0) raise(WF_ERR_CUDA, std::string("custom program launch: ") +
+                                            cudaGetErrorString(static_cast<cudaError_t>(rc)));
+        count_launch();
+        return;
+    }
     fn<<<grid, kBlock, 0, st>>>(L);
     WF_LAUNCHED();
 }

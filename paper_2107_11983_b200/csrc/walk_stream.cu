@@ -8,7 +8,7 @@ namespace wf {
 
 KernelFn select_stream_kernel(int prog, int sampler, int flow) {
 #define WF_CASE(P, S, F) \
-    if (prog == P && sampler == S && flow == F) return &walk_kernel<P, S, F, true>;
+    if (prog == P && sampler == S && flow == F) return &walk_kernel<Program<P>, S, F, true>;
     WF_FOR_EACH_COMBO(WF_CASE)
 #undef WF_CASE
     config_error("no kernel for this program/sampler/flow combination");

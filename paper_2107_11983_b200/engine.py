@@ -249,11 +249,17 @@ class Session:
         self.graph = graph
         self.prog = prog
         self.opts = opts or ExecOptions()
-        self._desc = prog.to_c()
         self._copts = self.opts.to_c()
         h = _vp()
-        _check(load_library().wf_session_create(graph.h, C.byref(self._desc),
-                                                C.byref(self._copts), C.byref(h)))
+        if isinstance(prog, host_mod.DeviceProgram):
+            self._desc = ProgramDesc()
+            self._desc.kind = -1
+            _check(load_library().wf_session_create_custom(graph.h, _vp(prog.ops), _vp(prog.object_pointer()),
+                                                           C.byref(self._copts), C.byref(h)))
+        else:
+            self._desc = prog.to_c()
+            _check(load_library().wf_session_create(graph.h, C.byref(self._desc),
+                                                    C.byref(self._copts), C.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -337,19 +343,31 @@ class Session:
         return RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)
 
     def run_to_numpy(self, spec: QuerySpec, chunk: int = 0) -> RunResult:
-        """Convenience over run_host with numpy (pageable) buffers."""
+        """Convenience over run_host with numpy (pageable) buffers.  Unbounded
+        programs (PPR, custom programs without max_path_vertices) have no host
+        capacity to size in advance: they run into HBM (wf_session_run, which
+        re-runs walks that outgrow their row) and are copied out after."""
         n = self.graph.vertex_count if spec.mode == abi.QueryMode.ONE_PER_VERTEX else spec.count
-        stride = self.row_capacity()
-        # fixed-length programs fit n * stride exactly; unbounded (PPR) walks get headroom
-        cap = n * stride if not isinstance(self.prog, host_mod.PprProgram) else n * stride * 4 + 4096
+        if self.unbounded():
+            ws = self.run(spec)
+            return RunResult(ws.to_host(), ws.metrics)
+        cap = n * self.row_capacity()  # fixed-length programs fit exactly
         off = np.zeros(n + 1, np.uint64)
         verts = np.zeros(max(cap, 1), np.uint32)
         st = np.zeros(max(n, 1), np.uint8)
         m = self.run_host(spec, off.ctypes.data, verts.ctypes.data, cap, st.ctypes.data, chunk)
         return RunResult(WalkSet(off, verts[:int(off[-1])], st[:n]), m)
 
+    def unbounded(self) -> bool:
+        p = self.prog
+        if isinstance(p, host_mod.DeviceProgram):
+            return p.max_path() == 0
+        return isinstance(p, host_mod.PprProgram)
+
     def row_capacity(self) -> int:
         p = self.prog
+        if isinstance(p, host_mod.DeviceProgram):
+            return p.max_path() or self.opts.path_stride or 64
         if isinstance(p, host_mod.MetaPathProgram):
             return len(p.schema) + 1
         if isinstance(p, host_mod.PprProgram):
@@ -379,9 +397,16 @@ class Session:
         _check(load_library().wf_session_set_stats(self.h, C.c_int(1 if enable else 0)))
 
     def stats(self) -> dict:
-        out = np.zeros(3, np.uint64)
-        _check(load_library().wf_session_stats(self.h, _ptr(out, _u64p)))
-        return dict(trials=int(out[0]), probes=int(out[1]), scanned=int(out[2]))
+        out = np.zeros(6, np.uint64)
+        _check(load_library().wf_session_stats_n(self.h, _ptr(out, _u64p), C.c_uint32(6)))
+        d = dict(trials=int(out[0]), probes=int(out[1]), scanned=int(out[2]))
+        kind = int(self._desc.kind)
+        if kind == abi.ProgramKind.NODE2VEC:
+            d["ref_probes"] = int(out[3])
+        if kind == abi.ProgramKind.METAPATH:
+            d["ref_label_sectors"] = int(out[4])
+            d["step_attempts"] = int(out[5])
+        return d
 
     def sync(self, stream: int = 0) -> None:
         _check(load_library().wf_session_sync(self.h, _vp(stream or None)))
@@ -407,6 +432,10 @@ def run_sequential(g, spec: QuerySpec, prog, opts: Optional[ExecOptions] = None)
     """run_sequential (engine.hpp:440-504): every query to completion; the walk
     set is a pure function of (graph, spec, program, seed)."""
     dg = _as_device(g)
+    if isinstance(prog, host_mod.DeviceProgram):
+        sess = Session(dg, prog, opts)
+        ws = sess.run(spec)
+        return RunResult(ws.to_host(), ws.metrics)
     cs = spec.to_c()
     # validate the spec before resolving the program, like the reference
     desc = prog.to_c()
@@ -457,3 +486,141 @@ def rng_probe(seed: int, streams, draws: int) -> np.ndarray:
     _check(load_library().wf_rng_probe(C.c_uint64(seed), _ptr(s, _u64p), C.c_uint64(s.size),
                                        C.c_uint32(draws), _ptr(out, _u64p)))
     return out
+
+
+_SHARD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32),
+                        C.POINTER(C.c_uint32), C.c_uint64)
+
+
+def worker_range(n: int, workers: int, w: int):
+    """worker_range (engine.hpp:296-298) through the library: [n*w/W, n*(w+1)/W)."""
+    b, e = C.c_uint64(), C.c_uint64()
+    _check(load_library().wf_worker_range(C.c_uint64(n), C.c_uint32(workers), C.c_uint32(w), C.byref(b),
+                                          C.byref(e)))
+    return b.value, e.value
+
+
+def device_count() -> int:
+    n = C.c_int32()
+    _check(load_library().wf_device_count(C.byref(n)))
+    return n.value
+
+
+class MultiDevice:
+    """run_*'s workers over devices (wf_multi_*): the graph replicated on every
+    listed device, the static tables built once and peer-copied, `workers`
+    contiguous qid blocks walked by one host thread per device and delivered
+    in worker order; PPR visit counts reduced with one NCCL all-reduce (or a
+    device sum when a device is listed twice)."""
+
+    def __init__(self, graph: DeviceGraph, devices, prog, opts: Optional[ExecOptions] = None):
+        self.graph = graph
+        self.prog = prog
+        self.opts = opts or ExecOptions()
+        self._copts = self.opts.to_c()
+        devs = (C.c_int32 * len(devices))(*devices)
+        h = _vp()
+        lib = load_library()
+        if isinstance(prog, host_mod.DeviceProgram):
+            _check(lib.wf_multi_create_custom(graph.h, devs, C.c_uint32(len(devices)), _vp(prog.ops),
+                                              _vp(prog.object_pointer()), C.byref(self._copts), C.byref(h)))
+        else:
+            self._desc = prog.to_c()
+            _check(lib.wf_multi_create(graph.h, devs, C.c_uint32(len(devices)), C.byref(self._desc),
+                                       C.byref(self._copts), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.wf_multi_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self):
+        n = C.c_uint32()
+        coll = C.c_int32()
+        _check(load_library().wf_multi_info(self.h, C.byref(n), C.byref(coll)))
+        return dict(devices=n.value, nccl=bool(coll.value))
+
+    def run(self, spec: QuerySpec, workers: int = 0, on_block=None, counts: bool = False):
+        """Runs every query; returns (RunResult, visit counts or None, blocks
+        [(worker, qid_begin, qid_end)] in delivery order).  on_block(worker,
+        q0, q1, WalkSet) is called in worker order."""
+        n = self.graph.vertex_count if spec.mode == abi.QueryMode.ONE_PER_VERTEX else spec.count
+        offs = [np.zeros(1, np.uint64)]
+        verts, stats, order = [], [], []
+        err = []
+
+        def tramp(_user, w, q0, q1, rec, vp, nv):
+            try:
+                r = np.ctypeslib.as_array(rec, shape=(q1 - q0,)).copy() if q1 > q0 else np.zeros(0, np.uint32)
+                v = np.ctypeslib.as_array(vp, shape=(nv,)).copy() if nv else np.zeros(0, np.uint32)
+                lens = (r & 0x7FFFFFFF).astype(np.uint64)
+                st = (r >> 31).astype(np.uint8)
+                order.append((w, q0, q1))
+                o = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+                if on_block is not None:
+                    on_block(w, q0, q1, WalkSet(o, v, st))
+                offs.append(o[1:] + offs[-1][-1])
+                verts.append(v)
+                stats.append(st)
+                return 0
+            except Exception as e:  # stop the run, re-raise here
+                err.append(e)
+                return 1
+
+        cb = _SHARD_FN(tramp)
+        cs = spec.to_c()
+        m = RunMetricsC()
+        cnt = np.zeros(self.graph.vertex_count, np.uint32) if counts else None
+        rc = load_library().wf_multi_run(self.h, C.byref(cs), C.c_uint32(workers), cb, None,
+                                         _ptr(cnt, _u32p), C.byref(m))
+        if err:
+            raise err[0]
+        _check(rc)
+        ws = WalkSet(np.concatenate(offs).astype(np.uint64),
+                     np.concatenate(verts) if verts else np.zeros(0, np.uint32),
+                     np.concatenate(stats) if stats else np.zeros(0, np.uint8))
+        assert len(ws) == n
+        return (RunResult(ws, RunMetrics(m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight)),
+                cnt, order)
+
+
+class Comm:
+    """The library's own NCCL communicator for one-process-per-GPU jobs
+    (wf_comm_*): rank 0 makes the id (unique_id()), the caller ships it to the
+    other ranks; allreduce_u32 sums a device u32 vector in place."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * Comm.ID_BYTES)()
+        _check(load_library().wf_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        buf = (C.c_uint8 * Comm.ID_BYTES)(*uid)
+        h = _vp()
+        _check(load_library().wf_comm_create(buf, C.c_int32(nranks), C.c_int32(rank), C.c_int32(device),
+                                             C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.wf_comm_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def allreduce_u32(self, dev_ptr: int, count: int, stream: int = 0) -> None:
+        _check(load_library().wf_comm_allreduce_u32(self.h, _vp(dev_ptr), C.c_uint64(count), _vp(stream or None)))
+
+
+def nccl_version() -> int:
+    v = C.c_int32()
+    _check(load_library().wf_nccl_version(C.byref(v)))
+    return v.value

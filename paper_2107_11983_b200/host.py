@@ -202,6 +202,48 @@ class ExecOptions:
         return c
 
 
+class DeviceProgram:
+    """A user's device program (the WalkProgram concept, program.hpp:49-93,
+    written against include/walkforge_b200/device_program.cuh and compiled
+    into the user's own shared library).  `ops` is the address of the
+    wf_program_ops table its WF_DEVICE_PROGRAM(Type, symbol) exports (or a
+    (library path, symbol) pair); `obj` the program object: a ctypes
+    Structure with the C++ type's layout (or its raw bytes)."""
+
+    kind = -1  # kCustomProgram
+
+    def __init__(self, ops, obj):
+        if isinstance(ops, tuple):
+            lib = C.CDLL(ops[0])
+            fn = getattr(lib, ops[1])
+            fn.restype = C.c_void_p
+            self._lib = lib
+            ops = fn()
+        self.ops = int(ops)
+        self.obj = obj
+        self._buf = C.create_string_buffer(bytes(obj), max(len(bytes(obj)), 1))
+
+    def object_pointer(self) -> int:
+        return C.addressof(self._buf)
+
+    def table(self) -> "ProgramOpsC":
+        return ProgramOpsC.from_address(self.ops)
+
+    def max_path(self) -> int:
+        """max_path_vertices() of the object (0 = unbounded)."""
+        t = self.table()
+        return int(t.max_path(C.c_void_p(self.object_pointer()))) if t.max_path else 0
+
+
+class ProgramOpsC(C.Structure):  # wf_program_ops (walkforge_b200.h)
+    _fields_ = [("abi_version", C.c_uint32), ("launch_size", C.c_uint32), ("name", C.c_char_p),
+                ("walker_type", C.c_int32), ("preferred_sampler", C.c_int32), ("has_max_weight", C.c_int32),
+                ("prechecked", C.c_int32), ("program_size", C.c_uint32), ("reserved", C.c_uint32),
+                ("launch", C.c_void_p), ("occupancy", C.c_void_p), ("static_weights", C.c_void_p),
+                ("max_weight", C.CFUNCTYPE(C.c_double, C.c_void_p)),
+                ("max_path", C.CFUNCTYPE(C.c_uint32, C.c_void_p))]
+
+
 class _Program:
     kind: ProgramKind
 

@@ -14,6 +14,18 @@
 
 using namespace walkforge;
 
+// a user's device program, compiled separately (tests/programs/test_programs.cu)
+extern "C" const wf_program_ops* wf_test_avoid_vertex_program(void);
+extern "C" const wf_program_ops* wf_test_label_stop_program(void);
+struct AvoidVertexObj {  // host mirror of AvoidVertexProgram's layout
+    uint32_t banned;
+    uint32_t length;
+};
+struct LabelStopObj {  // host mirror of LabelStopProgram's layout
+    double stop;
+    uint32_t stop_label;
+};
+
 static uint64_t fnv(const WalkSet& ws) {
     uint64_t h = 1469598103934665603ULL;
     auto mixin = [&](uint64_t x) {
@@ -151,6 +163,47 @@ int main(int argc, char** argv) {
         eo3.sink = [&](uint32_t worker, WalkSet&& block) { empty_calls.at(worker) += block.empty() ? 1 : 100; };
         run_sequential(g, QuerySpec::from_source(0, 0), DeepWalkProgram(g, 20, true), eo3);
         std::printf("empty_workers %d %d %d\n", empty_calls[0], empty_calls[1], empty_calls[2]);
+    }
+    // PPR with a tiny stop probability: walks of ~10^4 vertices (no host
+    // capacity guess; the blocks are sized after their walks ran)
+    {
+        ExecOptions pe;
+        pe.seed = 3;
+        RunResult p = run_sequential(g, QuerySpec::from_source(0, 3), PprProgram(1e-4), pe);
+        std::printf("ppr_long %016llx %llu %zu\n", (unsigned long long)fnv(p.walks),
+                    (unsigned long long)p.metrics.total_steps, p.walks.size());
+        // threads -> worker blocks (each once, in order) for an unbounded program
+        ExecOptions pt;
+        pt.seed = 3;
+        pt.threads = 3;
+        std::vector<int> order;
+        WalkSet merged;
+        pt.sink = [&](uint32_t worker, WalkSet&& block) {
+            order.push_back(static_cast<int>(worker));
+            for (auto& r : block) merged.push_back(std::move(r));
+        };
+        std::vector<VertexId> src(200);
+        for (size_t i = 0; i < src.size(); ++i) src[i] = static_cast<VertexId>((i * 37) % g.vertex_count());
+        RunResult pb = run_sequential(g, QuerySpec::from_list(src), PprProgram(0.2), pt);
+        std::printf("ppr_workers %016llx %llu order=%d%d%d n=%zu\n", (unsigned long long)fnv(merged),
+                    (unsigned long long)pb.metrics.total_steps, order.size() > 0 ? order[0] : -1,
+                    order.size() > 1 ? order[1] : -1, order.size() > 2 ? order[2] : -1, order.size());
+    }
+    // a user's device program through the drop-in entry points
+    {
+        const uint32_t hub = 0;
+        ExecOptions ce;
+        ce.seed = 3;
+        DeviceProgram avoid(wf_test_avoid_vertex_program(), AvoidVertexObj{hub, 12});
+        RunResult a2 = run_sequential(g, QuerySpec::one_per_vertex(), avoid, ce);
+        std::printf("custom_avoid %016llx %llu\n", (unsigned long long)fnv(a2.walks),
+                    (unsigned long long)a2.metrics.total_steps);
+        ExecOptions ls;
+        ls.seed = 5;
+        DeviceProgram stop(wf_test_label_stop_program(), LabelStopObj{0.1, 4});
+        RunResult b2 = run_interleaved(g, QuerySpec::one_per_vertex(), stop, 64, 32, ls);
+        std::printf("custom_stop %016llx %llu\n", (unsigned long long)fnv(b2.walks),
+                    (unsigned long long)b2.metrics.total_steps);
     }
     try {
         DoubleBufferedWriter bad("/nonexistent_dir/x.txt", OutputFormat::Text);

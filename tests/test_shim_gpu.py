@@ -33,12 +33,19 @@ def fnv(ws):
     return h
 
 
+PROGRAMS = os.path.join(ROOT, "tests", "programs")
+
+
 def build_shim(tmp):
+    """A reference caller's build: plain g++ against the C header and the
+    shim, linked with the engine and with a separately compiled user
+    device-program library (tests/programs)."""
     exe = os.path.join(tmp, "shim_test")
     subprocess.check_call(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
                            os.path.join(ROOT, "tests", "cpp", "shim_test.cpp"), "-o", exe,
                            "-L", os.path.dirname(E.LIB_PATH), "-lwalkforge_b200",
-                           f"-Wl,-rpath,{os.path.dirname(E.LIB_PATH)}"])
+                           f"-Wl,-rpath,{os.path.dirname(E.LIB_PATH)}",
+                           "-L", PROGRAMS, "-l:libwf_test_programs.so", f"-Wl,-rpath,{PROGRAMS}"])
     return exe
 
 
@@ -85,3 +92,22 @@ def test_shim_reproduces_golden_walks():
     assert res["writer_open"] == ["IoError"]
     assert res["query_file"] == ["3", "3", "3", "7"]  # walker.cpp:22-78 on test_cli.cpp:188's file
     assert res["query_file_error"] == ["ParseError", ":1:", "too", "many", "columns"]
+    # unbounded walks, worker blocks and user device programs against the
+    # unmodified reference on the same graph
+    import ctypes as C
+    from oracle.oracle import RefOracle, ref_available
+    from paper_2107_11983_b200.host import ExecOptions, PprProgram, QuerySpec
+    if not ref_available():
+        return
+    from tests.test_custom_programs_gpu import TestParams
+    rg = RefOracle().graph(g)
+    want = rg.run(QuerySpec.from_source(0, 3), PprProgram(1e-4), ExecOptions(seed=3))
+    assert res["ppr_long"] == [f"{fnv(want.walks):016x}", str(want.metrics.total_steps), "3"]
+    src = np.array([(i * 37) % g.vertex_count for i in range(200)], np.uint32)
+    want = rg.run(QuerySpec.from_list(src), PprProgram(0.2), ExecOptions(seed=3, threads=3))
+    assert res["ppr_workers"] == [f"{fnv(want.walks):016x}", str(want.metrics.total_steps), "order=012", "n=3"]
+    want, _ = rg.run_test_program(1, TestParams(length=12, banned=0), QuerySpec.one_per_vertex(), ExecOptions(seed=3))
+    assert res["custom_avoid"] == [f"{fnv(want.walks):016x}", str(want.metrics.total_steps)]
+    want, _ = rg.run_test_program(4, TestParams(stop=0.1, stop_label=4), QuerySpec.one_per_vertex(),
+                                  ExecOptions(seed=5), interleaved=True)
+    assert res["custom_stop"] == [f"{fnv(want.walks):016x}", str(want.metrics.total_steps)]
