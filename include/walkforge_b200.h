@@ -146,7 +146,7 @@ typedef struct wf_graph_info {
     int32_t adjacency_sorted;
     int32_t device;
     uint32_t label_count; /* max label + 1 (0 if unlabeled) */
-    uint32_t reserved;
+    uint32_t weights_f64; /* 1: some weight is not float32-exact; an f64 copy is resident */
 } wf_graph_info;
 
 /* Synthetic R-MAT generator (ingest; SURVEY §8 d).  Symmetrised,
@@ -182,6 +182,15 @@ uint64_t wf_kernel_launches(void);
 int wf_graph_create(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
                     const uint32_t* labels, uint32_t vertex_count, uint64_t edge_count, int device,
                     wf_graph** out);
+/* Same with the reference's f64 weights (graph.hpp:102): weights that are all
+ * float32-exact are stored as f32 only; otherwise an f64 copy stays resident
+ * and every sampler, table and program reads it (the f32 array then mirrors
+ * it for the hot-path layouts).  Walks equal the reference's either way. */
+int wf_graph_create_f64(const uint64_t* offsets, const uint32_t* neighbors, const double* weights,
+                        const uint32_t* labels, uint32_t vertex_count, uint64_t edge_count, int device,
+                        wf_graph** out);
+/* The weights as the reference holds them (f64[E], HOST). */
+int wf_graph_download_weights_f64(const wf_graph* g, double* weights);
 /* Same from DEVICE pointers (already resident, e.g. torch tensors); copies. */
 int wf_graph_create_device(const uint64_t* offsets, const uint32_t* neighbors,
                            const float* weights, const uint8_t* labels, uint32_t vertex_count,
@@ -200,7 +209,8 @@ void wf_graph_destroy(wf_graph* g);
 /* WFG1 binary files, Graph::read_binary / write_binary: magic "WFG1", u64 V,
  * u64 E, u8 flags, u64 offsets[V+1], u32 neighbors[E], f64 weights[E]?, u32
  * labels[E]?.  Reading applies the reference's FormatError checks; weights
- * must be float32-exact and labels < 256 (device storage, ConfigError). */
+ * keep their f64 values (wf_graph_create_f64); labels must be < 256 (device
+ * storage, ConfigError). */
 int wf_graph_read_wfg1(const char* path, int device, wf_graph** out);
 int wf_graph_write_wfg1(const wf_graph* g, const char* path);
 

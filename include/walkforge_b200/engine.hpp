@@ -7,8 +7,8 @@
 // <walkforge/engine.hpp> + <walkforge/interleave.hpp> + <walkforge/algorithms.hpp>
 // (define WALKFORGE_B200_DROP_IN to alias namespace walkforge) and linking
 // libwalkforge_b200.so.  Differences, all checked at the boundary:
-//   * weights must be exactly representable in float32 (device storage), and
-//     labels < 256 — otherwise ConfigError;
+//   * weights keep their f64 values (an f64 copy stays resident when some
+//     weight is not float32-exact); labels must be < 256 — otherwise ConfigError;
 //   * programs are the five built-ins or a user's device program: a type written
 //     against walkforge_b200/device_program.cuh in the user's .cu file, passed
 //     here as DeviceProgram(ops, object) (the ops table its WF_DEVICE_PROGRAM
@@ -83,18 +83,12 @@ public:
                           std::vector<double> weights = {}, std::vector<uint32_t> labels = {},
                           int device = 0) {
         if (offsets.size() < 2) throw ConfigError("graph must have at least one vertex");
-        std::vector<float> w32(weights.size());
-        for (size_t i = 0; i < weights.size(); ++i) {
-            w32[i] = static_cast<float>(weights[i]);
-            if (std::isfinite(weights[i]) && static_cast<double>(w32[i]) != weights[i])
-                throw ConfigError("edge weights must be exactly representable in float32");
-        }
         if (!weights.empty() && weights.size() != neighbors.size())
             throw ConfigError("weight array does not match edge count");
         if (!labels.empty() && labels.size() != neighbors.size())
             throw ConfigError("label array does not match edge count");
         wf_graph* h = nullptr;
-        check(wf_graph_create(offsets.data(), neighbors.data(), weights.empty() ? nullptr : w32.data(),
+        check(wf_graph_create_f64(offsets.data(), neighbors.data(), weights.empty() ? nullptr : weights.data(),
                               labels.empty() ? nullptr : labels.data(),
                               static_cast<uint32_t>(offsets.size() - 1), neighbors.size(), device, &h));
         Graph g;
@@ -166,7 +160,7 @@ private:
     struct HostCsr {
         std::vector<uint64_t> offsets;
         std::vector<VertexId> neighbors;
-        std::vector<double> weights;  // widened exactly from the device's f32
+        std::vector<double> weights;  // f64, as the reference holds them
         std::vector<uint32_t> labels;
     };
     const HostCsr& host() const {
@@ -174,11 +168,11 @@ private:
             auto c = std::make_shared<HostCsr>();
             c->offsets.resize(vertex_count() + 1ull);
             c->neighbors.resize(edge_count());
-            std::vector<float> w(has_weights() ? edge_count() : 0);
             std::vector<uint8_t> l(has_labels() ? edge_count() : 0);
-            check(wf_graph_download(h_.get(), c->offsets.data(), c->neighbors.data(),
-                                    w.empty() ? nullptr : w.data(), l.empty() ? nullptr : l.data()));
-            c->weights.assign(w.begin(), w.end());
+            check(wf_graph_download(h_.get(), c->offsets.data(), c->neighbors.data(), nullptr,
+                                    l.empty() ? nullptr : l.data()));
+            c->weights.resize(has_weights() ? edge_count() : 0);
+            if (!c->weights.empty()) check(wf_graph_download_weights_f64(h_.get(), c->weights.data()));
             c->labels.assign(l.begin(), l.end());
             csr_ = std::move(c);
         }

@@ -87,6 +87,8 @@ class PortOracle:
         self.lib = lib
 
     def _graph(self, g: Graph) -> _WfoGraph:
+        if g.weights is not None and g.weights.dtype != np.float32:
+            raise ValueError("the C restatement holds f32 weights; f64 graphs are checked against RefOracle")
         cg = _WfoGraph()
         cg.offsets = _ptr(g.offsets, _u64p)
         cg.neighbors = _ptr(g.neighbors, _u32p)
@@ -191,6 +193,12 @@ class RefOracle:
         """Graph::from_csr over the device formats (f32 weights widened to f64,
         u8 labels widened to u32 inside the reference's own vectors)."""
         h = C.c_void_p()
+        if g.weights is not None and g.weights.dtype == np.float64:
+            lab = None if g.labels is None else np.ascontiguousarray(g.labels, dtype=np.uint32)
+            self._check(self.lib.wfref_graph_create(
+                _ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p), _ptr(g.weights, _f64p),
+                _ptr(lab, _u32p), C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count), C.byref(h)))
+            return RefGraph(self, h)
         self._check(self.lib.wfref_graph_create_f32(
             _ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p), _ptr(g.weights, _f32p),
             _ptr(g.labels, _u8p), C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),

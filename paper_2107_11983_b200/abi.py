@@ -197,7 +197,7 @@ class GraphInfoC(C.Structure):
         ("adjacency_sorted", C.c_int32),
         ("device", C.c_int32),
         ("label_count", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("weights_f64", C.c_uint32),
     ]
 
 
@@ -227,7 +227,8 @@ class RmatParamsC(C.Structure):
 # Every symbol include/walkforge_b200.h declares (checked by the CPU suite).
 EXPORTED_SYMBOLS = [
     "wf_abi_version", "wf_last_error", "wf_kernel_launches", "wf_device_count",
-    "wf_graph_create", "wf_graph_create_device", "wf_graph_generate_rmat",
+    "wf_graph_create", "wf_graph_create_f64", "wf_graph_download_weights_f64",
+    "wf_graph_create_device", "wf_graph_generate_rmat",
     "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_destroy",
     "wf_graph_read_wfg1", "wf_graph_write_wfg1", "wf_graph_load_edge_list", "wf_graph_original_ids",
     "wf_session_create", "wf_session_describe", "wf_session_destroy", "wf_session_run",

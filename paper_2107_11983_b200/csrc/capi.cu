@@ -322,6 +322,34 @@ int wf_graph_create(const uint64_t* offsets, const uint32_t* neighbors, const fl
     });
 }
 
+int wf_graph_create_f64(const uint64_t* offsets, const uint32_t* neighbors, const double* weights,
+                        const uint32_t* labels, uint32_t vertex_count, uint64_t edge_count, int device,
+                        wf_graph** out) {
+    return guarded([&] {
+        require(out && offsets && (neighbors || edge_count == 0), "null argument");
+        auto h = std::make_unique<wf_graph>();
+        h->g.reset(graph_from_host_f64(offsets, neighbors, weights, labels, vertex_count, edge_count,
+                                       device < 0 ? current_device() : device));
+        *out = h.release();
+    });
+}
+
+int wf_graph_download_weights_f64(const wf_graph* g, double* weights) {
+    return guarded([&] {
+        require(g && weights, "null argument");
+        const GraphStore& s = *g->g;
+        DeviceGuard guard(s.device);
+        if (!s.has_weights() || !s.E) return;
+        if (s.weights64.get()) {
+            WF_CUDA(cudaMemcpy(weights, s.weights64.get(), s.E * 8, cudaMemcpyDefault));
+        } else {
+            std::vector<float> w(s.E);
+            WF_CUDA(cudaMemcpy(w.data(), s.weights.get(), s.E * 4, cudaMemcpyDefault));
+            for (uint64_t e = 0; e < s.E; ++e) weights[e] = w[e];
+        }
+    });
+}
+
 int wf_graph_create_device(const uint64_t* offsets, const uint32_t* neighbors,
                            const float* weights, const uint8_t* labels, uint32_t vertex_count,
                            uint64_t edge_count, int device, wf_graph** out) {
@@ -357,6 +385,7 @@ int wf_graph_info_get(const wf_graph* g, wf_graph_info* out) {
         out->adjacency_sorted = s.sorted;
         out->device = s.device;
         out->label_count = s.label_count;
+        out->weights_f64 = s.weights64.get() != nullptr;
     });
 }
 

@@ -67,6 +67,32 @@ __global__ void k_check_weights(const float* __restrict__ w, uint64_t E, unsigne
     if ((threadIdx.x & 31) == 0) atomicMax(max_bits, mx);
 }
 
+// The reference's f64 weights (graph.hpp:102): validated (finite,
+// non-negative), their maximum, whether any is not float32-exact, and the
+// f32 mirror the hot-path layouts read (saturated, never inf).
+__global__ void k_weights_f64(const double* __restrict__ w64, uint64_t E, float* __restrict__ w32,
+                              unsigned* flags, unsigned long long* max_bits) {
+    bool bad = false, inexact = false;
+    unsigned long long mx = 0;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = w64[e];
+        if (!(x >= 0.0 && x <= 1.7976931348623157e308)) {
+            bad = true;
+            w32[e] = 0.0f;
+            continue;
+        }
+        const float f = static_cast<float>(fmin(x, 3.4028234663852886e38));
+        w32[e] = f;
+        inexact = inexact || static_cast<double>(f) != x;
+        mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(x)));  // x >= 0: bits order as values
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, kBadWeight);
+    if (__any_sync(kFull, inexact) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u << 30);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(max_bits, mx);
+}
+
 __global__ void k_narrow_labels(const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
                                 uint64_t E, unsigned* flags) {
     bool bad = false;
@@ -284,6 +310,33 @@ struct FlagBlock {
 
 }  // namespace
 
+void GraphStore::adopt_weights64(DeviceBuffer<double>&& w64, cudaStream_t st) {
+    DeviceGuard guard(device);
+    weights.allocate(std::max<uint64_t>(E, 1));
+    DeviceBuffer<unsigned> flags(1);
+    DeviceBuffer<unsigned long long> mx(1);
+    WF_CUDA(cudaMemsetAsync(flags.get(), 0, 4, st));
+    WF_CUDA(cudaMemsetAsync(mx.get(), 0, 8, st));
+    if (E) {
+        k_weights_f64<<<blocks_for(E, 256, device), 256, 0, st>>>(w64.get(), E, weights.get(), flags.get(), mx.get());
+        WF_LAUNCHED();
+    }
+    unsigned hf = 0;
+    unsigned long long hm = 0;
+    WF_CUDA(cudaMemcpyAsync(&hf, flags.get(), 4, cudaMemcpyDeviceToHost, st));
+    WF_CUDA(cudaMemcpyAsync(&hm, mx.get(), 8, cudaMemcpyDeviceToHost, st));
+    WF_CUDA(cudaStreamSynchronize(st));
+    if (hf & kBadWeight) config_error("edge weights must be finite and non-negative");
+    if (hf & (1u << 30)) {
+        // some weight is not float32-exact: the f64 array is what samplers,
+        // tables and programs read (edge_weight); the f32 one mirrors it
+        weights64 = std::move(w64);
+        std::memcpy(&max_weight64, &hm, 8);
+    } else {
+        weights64.release();
+    }
+}
+
 void GraphStore::finalize(cudaStream_t st) {
     DeviceGuard guard(device);
     if (E >= (1ULL << 40)) config_error("edge count exceeds the 40-bit packed vertex word range");
@@ -327,6 +380,7 @@ void GraphStore::finalize(cudaStream_t st) {
     float mw;
     std::memcpy(&mw, &h.max_weight_bits, 4);
     max_weight = weights.get() ? static_cast<double>(mw) : 0.0;
+    if (weights64.get()) max_weight = max_weight64;  // graph.hpp:56 over the f64 weights
     label_present.assign(256, 0);
     label_count = 0;
     if (labels.get()) {
@@ -496,7 +550,7 @@ static std::unique_ptr<GraphStore> alloc_graph(uint32_t V, uint64_t E, bool w, b
 }
 
 GraphStore* graph_from_host(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
-                            const uint32_t* labels, uint32_t V, uint64_t E, int device) {
+                            const uint32_t* labels, uint32_t V, uint64_t E, int device, bool finalize) {
     DeviceGuard guard(device);
     auto g = alloc_graph(V, E, weights != nullptr, labels != nullptr, device);
     cudaStream_t st = nullptr;
@@ -514,7 +568,19 @@ GraphStore* graph_from_host(const uint64_t* offsets, const uint32_t* neighbors, 
         WF_CUDA(cudaMemcpy(&h, flag.get(), 4, cudaMemcpyDeviceToHost));
         if (h) config_error("edge labels must be < 256 on the device");
     }
-    g->finalize(st);
+    if (finalize) g->finalize(st);
+    return g.release();
+}
+
+GraphStore* graph_from_host_f64(const uint64_t* offsets, const uint32_t* neighbors, const double* weights,
+                                const uint32_t* labels, uint32_t V, uint64_t E, int device) {
+    if (!weights) return graph_from_host(offsets, neighbors, nullptr, labels, V, E, device);
+    DeviceGuard guard(device);
+    std::unique_ptr<GraphStore> g(graph_from_host(offsets, neighbors, nullptr, labels, V, E, device, false));
+    DeviceBuffer<double> w64(std::max<uint64_t>(E, 1));
+    if (E) WF_CUDA(cudaMemcpy(w64.get(), weights, E * 8, cudaMemcpyHostToDevice));
+    g->adopt_weights64(std::move(w64), nullptr);
+    g->finalize(nullptr);
     return g.release();
 }
 

@@ -34,16 +34,6 @@ struct File {
     }
 };
 
-std::vector<float> narrow_weights(const double* w, uint64_t n) {
-    std::vector<float> out(n);
-    for (uint64_t i = 0; i < n; ++i) {
-        out[i] = static_cast<float>(w[i]);
-        if (std::isfinite(w[i]) && static_cast<double>(out[i]) != w[i])
-            config_error("edge weights must be exactly representable in float32 (device storage)");
-    }
-    return out;
-}
-
 __global__ void k_lower_bound(const uint64_t* __restrict__ ids, uint64_t nids,
                               const uint64_t* __restrict__ q, uint64_t n, uint32_t* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -97,13 +87,13 @@ __global__ void k_gather_attr(const T* __restrict__ in, const uint64_t* __restri
     }
 }
 
-__global__ void k_synthetic_attrs(uint64_t E, uint64_t wmix, uint64_t lmix, float* __restrict__ w,
+__global__ void k_synthetic_attrs(uint64_t E, uint64_t wmix, uint64_t lmix, double* __restrict__ w,
                                   uint8_t* __restrict__ lab, uint32_t label_count) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
          e += (uint64_t)gridDim.x * blockDim.x) {
         if (w) {
             Rng r{stream_state(wmix, e)};
-            w[e] = static_cast<float>(1.0 + r.real(4.0));
+            w[e] = 1.0 + r.real(4.0);  // synthetic_weight (graph.cpp:279-283), f64 like the reference
         }
         if (lab) {
             Rng r{stream_state(lmix, e)};
@@ -181,14 +171,10 @@ GraphStore* graph_read_wfg1(const char* path, int device) {
     }
     if (!ok) raise(WF_ERR_FORMAT, p + " ended unexpectedly");
     try {
-        std::vector<float> w32;
-        if (!w.empty()) {
-            for (double x : w)
-                if (!std::isfinite(x) || x < 0.0) config_error("edge weights must be finite and non-negative");
-            w32 = narrow_weights(w.data(), e);
-        }
-        return graph_from_host(off.data(), nbr.data(), w.empty() ? nullptr : w32.data(),
-                               lab.empty() ? nullptr : lab.data(), static_cast<uint32_t>(v), e, device);
+        // f64 weights as on disk (graph.cpp:206-208); a separate f64 array is
+        // kept only when some weight is not float32-exact
+        return graph_from_host_f64(off.data(), nbr.data(), w.empty() ? nullptr : w.data(),
+                                   lab.empty() ? nullptr : lab.data(), static_cast<uint32_t>(v), e, device);
     } catch (const Error& err) {
         if (err.code == WF_ERR_CONFIG) raise(WF_ERR_FORMAT, p + " fails validation: " + err.what());
         throw;
@@ -216,7 +202,9 @@ void graph_write_wfg1(const GraphStore& g, const char* path) {
     };
     dump(g.offsets.get(), v + 1, 8);
     dump(g.nbr.get(), e, 4);
-    if (g.has_weights()) {  // f64 on disk (graph.cpp:206-208): the f32 values widened exactly
+    if (g.weights64.get()) {  // f64 on disk (graph.cpp:206-208)
+        dump(g.weights64.get(), e, 8);
+    } else if (g.has_weights()) {  // the f32 values widened exactly
         std::vector<float> w;
         std::vector<double> w64;
         for (uint64_t i = 0; ok && i < e; i += kChunk) {
@@ -314,8 +302,6 @@ GraphStore* graph_load_edge_list(const char* path, const wf_edge_list_options& o
     }
     if (!line.empty()) handle(line);
     if (src.empty()) raise(WF_ERR_PARSE, std::string(path) + ": no edges");
-    std::vector<float> fw32;
-    if (want_w) fw32 = narrow_weights(fw.data(), fw.size());
     for (uint32_t l : fl)
         if (l > 255) config_error("edge labels must be < 256 on the device");
 
@@ -400,13 +386,15 @@ GraphStore* graph_load_edge_list(const char* path, const wf_edge_list_options& o
     key2.release();
     // attributes: from the file (permuted with the edges) or synthetic on the
     // final edge order (graph.cpp:430-446)
-    if (want_w || o.weights == WF_ATTR_RANDOM) g->weights.allocate(std::max<uint64_t>(E, 1));
+    // weights in f64, as the reference reads and synthesises them (graph.hpp:102)
+    DeviceBuffer<double> w64;
+    if (want_w || o.weights == WF_ATTR_RANDOM) w64.allocate(std::max<uint64_t>(E, 1));
     if (want_l || o.labels == WF_ATTR_RANDOM) g->labels.allocate(std::max<uint64_t>(E, 1));
     if (want_w) {
-        DeviceBuffer<float> in(m);
-        WF_CUDA(cudaMemcpy(in.get(), fw32.data(), m * 4, cudaMemcpyHostToDevice));
-        k_gather_attr<float><<<grid_for(E, device), 256, 0, st>>>(in.get(), val2.get(), E, undirected ? 1 : 0,
-                                                                  g->weights.get());
+        DeviceBuffer<double> in(m);
+        WF_CUDA(cudaMemcpy(in.get(), fw.data(), m * 8, cudaMemcpyHostToDevice));
+        k_gather_attr<double><<<grid_for(E, device), 256, 0, st>>>(in.get(), val2.get(), E, undirected ? 1 : 0,
+                                                                   w64.get());
         WF_LAUNCHED();
     }
     if (want_l) {
@@ -422,11 +410,12 @@ GraphStore* graph_load_edge_list(const char* path, const wf_edge_list_options& o
     if (o.weights == WF_ATTR_RANDOM || o.labels == WF_ATTR_RANDOM) {
         k_synthetic_attrs<<<grid_for(E, device), 256, 0, st>>>(
             E, seed_premix(o.seed ^ kWeightSalt), seed_premix(o.seed ^ kLabelSalt),
-            o.weights == WF_ATTR_RANDOM ? g->weights.get() : nullptr,
+            o.weights == WF_ATTR_RANDOM ? w64.get() : nullptr,
             o.labels == WF_ATTR_RANDOM ? g->labels.get() : nullptr, o.label_count);
         WF_LAUNCHED();
     }
     WF_CUDA(cudaStreamSynchronize(st));
+    if (w64.get()) g->adopt_weights64(std::move(w64), st);
     g->finalize(st);
     return g.release();
 }

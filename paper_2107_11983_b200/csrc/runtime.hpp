@@ -35,6 +35,7 @@ struct GraphStore {
     // is not float32-exact (then `weights` holds their f32 roundings for the
     // hot-path layouts and this array is what samplers and tables read)
     DeviceBuffer<double> weights64;
+    double max_weight64 = 0.0;
     DeviceBuffer<uint8_t> labels;
     DeviceBuffer<uint64_t> vword;
     bool sorted = true;
@@ -86,6 +87,9 @@ struct GraphStore {
     // After offsets/nbr/weights/labels are resident: validate (from_csr),
     // compute stats, build vertex words.  `labels_checked` = labels already u8.
     void finalize(cudaStream_t st);
+    // takes the reference's f64 weights (device): fills the f32 mirror and
+    // keeps the f64 array only when some weight is not float32-exact
+    void adopt_weights64(DeviceBuffer<double>&& w64, cudaStream_t st);
     void ensure_label_index(cudaStream_t st);
     void ensure_search_index(cudaStream_t st);
     void ensure_edge_hash(cudaStream_t st);
@@ -203,7 +207,9 @@ int row_bucket(uint64_t n_rows);  // tuner key: ceil(log2(rows))
 
 // graph.cu
 GraphStore* graph_from_host(const uint64_t* offsets, const uint32_t* neighbors, const float* weights,
-                            const uint32_t* labels, uint32_t V, uint64_t E, int device);
+                            const uint32_t* labels, uint32_t V, uint64_t E, int device, bool finalize = true);
+GraphStore* graph_from_host_f64(const uint64_t* offsets, const uint32_t* neighbors, const double* weights,
+                                const uint32_t* labels, uint32_t V, uint64_t E, int device);
 GraphStore* graph_from_device(const uint64_t* offsets, const uint32_t* neighbors,
                               const float* weights, const uint8_t* labels, uint32_t V, uint64_t E,
                               int device);

@@ -298,6 +298,8 @@ void raise_device_error(const Session& s, int code) {
                         " trials; asserted bound does not match the weights");
     if (code == WF_ERR_CONFIG) raise(code, "query source is not a vertex");
     if (code == WF_ERR_CUDA) raise(code, "walk kernel timed out waiting for its source list");
+    if (code == WF_ERR_CONTRACT)  // check_program_weight, engine.hpp:97-101
+        raise(code, "program emitted a weight that is negative or not finite");
     raise(code, "device-side contract violation");
 }
 
@@ -345,6 +347,11 @@ void patch_long_walks(Session& s, const wf_query_spec& spec, const uint32_t* hos
     }
     launch_walk(s, spec, src_by_qid, 0, qids.size(), dq.get(), p.get(), mx, l.get(), sst.get(), nullptr,
                 c2.get(), c2.get() + 1, s.cursor.get(), nullptr);
+    // a device error of the re-run (e.g. the rejection cap) is the run's error
+    WF_CUDA(cudaDeviceSynchronize());
+    int err = 0;
+    WF_CUDA(cudaMemcpy(&err, s.error_word.get(), 4, cudaMemcpyDeviceToHost));
+    if (err) raise_run_error(s, spec, host_sources, qb, qb + n, err);
     std::vector<uint32_t> hp(qids.size() * static_cast<uint64_t>(mx));
     WF_CUDA(cudaMemcpy(hp.data(), p.get(), hp.size() * 4, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < qids.size(); ++i) {
@@ -490,8 +497,12 @@ void run_to_host(Session& s, const wf_query_spec& spec, const uint32_t* host_sou
             if (r1 <= r0) return;
             WF_CUDA(cudaMemcpyAsync(P.src.get() + r0, host_sources + qb + s0 + r0, (r1 - r0) * 4,
                                     cudaMemcpyHostToDevice, C));
+            // resident 1024-row blocks: a piece ending inside a block leaves
+            // that block unpublished until the piece that completes it (or the
+            // list's end) lands; the claims past it wait for that copy
+            const uint64_t blocks = r1 == sn ? (r1 + 1023) >> 10 : r1 >> 10;
             CUresult cr = P.write_value32(reinterpret_cast<CUstream>(C), reinterpret_cast<CUdeviceptr>(P.src_ready.get()),
-                                          static_cast<cuuint32_t>((r1 + 1023) >> 10), 0);
+                                          static_cast<cuuint32_t>(blocks), 0);
             if (cr != CUDA_SUCCESS) raise(WF_ERR_CUDA, "cuStreamWriteValue32 failed");
         };
         const uint32_t* src_by_qid = nullptr;

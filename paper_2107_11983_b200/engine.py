@@ -80,6 +80,14 @@ class DeviceGraph:
         lib = load_library()
         h = _vp()
         lab = None if g.labels is None else g.labels.astype(np.uint32)
+        if g.weights is not None and g.weights.dtype == np.float64:
+            # the reference's f64 weights (wf_graph_create_f64)
+            w = np.ascontiguousarray(g.weights)
+            _check(lib.wf_graph_create_f64(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
+                                           w.ctypes.data_as(C.POINTER(C.c_double)), _ptr(lab, _u32p),
+                                           C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),
+                                           C.c_int(device), C.byref(h)))
+            return cls(h)
         _check(lib.wf_graph_create(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
                                    _ptr(g.weights, _f32p), _ptr(lab, _u32p),
                                    C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),
@@ -152,7 +160,8 @@ class DeviceGraph:
             self._info = dict(V=i.vertex_count, E=i.edge_count, max_degree=i.max_degree,
                               max_weight=i.max_weight, has_weights=bool(i.has_weights),
                               has_labels=bool(i.has_labels), sorted=bool(i.adjacency_sorted),
-                              device=i.device, label_count=i.label_count)
+                              device=i.device, label_count=i.label_count,
+                              weights_f64=bool(i.weights_f64))
         return self._info
 
     @property
@@ -171,6 +180,9 @@ class DeviceGraph:
         lab = np.zeros(i["E"], np.uint8) if i["has_labels"] else None
         _check(load_library().wf_graph_download(self.h, _ptr(off, _u64p), _ptr(nbr, _u32p),
                                                 _ptr(w, _f32p), _ptr(lab, _u8p)))
+        if i.get("weights_f64"):  # weights that are not float32-exact: the f64 values
+            w = np.zeros(i["E"], np.float64)
+            _check(load_library().wf_graph_download_weights_f64(self.h, w.ctypes.data_as(C.POINTER(C.c_double))))
         return Graph(off, nbr, w, lab)
 
     def has_edge(self, src, dst) -> np.ndarray:

@@ -23,12 +23,16 @@ from .abi import (ConfigError, ExecOptionsC, ProgramDesc, ProgramKind, QueryMode
 
 
 class Graph:
-    """CSR graph: offsets u64[V+1], neighbors u32[E], weights f32[E]?, labels u8[E]?"""
+    """CSR graph: offsets u64[V+1], neighbors u32[E], weights f32[E] or f64[E]
+    (the reference's own type, graph.hpp:102; kept when given), labels u8[E]?"""
 
     def __init__(self, offsets, neighbors, weights=None, labels=None):
         self.offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
         self.neighbors = np.ascontiguousarray(neighbors, dtype=np.uint32)
-        self.weights = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+        if weights is not None:
+            w = np.asarray(weights)
+            weights = np.ascontiguousarray(w, dtype=np.float64 if w.dtype == np.float64 else np.float32)
+        self.weights = weights
         self.labels = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint8)
 
     @classmethod
@@ -49,12 +53,12 @@ class Graph:
             w64 = np.asarray(weights)
             if w64.size != neighbors.size:
                 raise ConfigError("weight array does not match edge count")
-            w32 = w64.astype(np.float32)
-            if not np.all(np.isfinite(w32)) or np.any(w32 < 0):
+            wd = w64.astype(np.float64)
+            if not np.all(np.isfinite(wd)) or np.any(wd < 0):
                 raise ConfigError("edge weights must be finite and non-negative")
-            if w64.dtype != np.float32 and not np.array_equal(w32.astype(np.float64), w64.astype(np.float64)):
-                raise ConfigError("edge weights must be exactly representable in float32")
-            weights = w32
+            w32 = wd.astype(np.float32)
+            # float32-exact weights are stored as f32; others keep their f64 values
+            weights = w32 if np.array_equal(w32.astype(np.float64), wd) else wd
         if labels is not None:
             labels = np.asarray(labels)
             if labels.size != neighbors.size:
