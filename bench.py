@@ -81,8 +81,38 @@ CONFIGS = {
                labels=0, queries="per_vertex", scaling="strong"),
 }
 
+# Gathered flows (a per-step gather over every edge of the current vertex,
+# engine.hpp:134-184) on the s22 graph: not BASELINE configs, but the flows
+# whose hub steps run warp-cooperatively (coop_step); reported under
+# per_algorithm with their own reference baselines.
+GATHERED = {
+    "g1": dict(workload="G1 Node2Vec R-MAT s22 (a=2, b=0.5), ITS gathered (per-step gather), 2^16 walks from "
+                        "uniform random sources, length 80", scale=22, program="node2vec", length=80, weighted=False,
+               labels=0, queries="random", n_queries=1 << 16, scaling="weak", sampler="ITS", tables=True),
+    "g2": dict(workload="G2 MetaPath R-MAT s22, ALIAS gathered (Vose per step), schema [i%5]x79, 2^16 walks "
+                        "from uniform random sources", scale=22, program="metapath", weighted=True, labels=5,
+               queries="random", n_queries=1 << 16, scaling="weak", sampler="ALIAS", tables=True),
+    "g3": dict(workload="G3 DeepWalk R-MAT s22 weighted, ALIAS without static tables (Vose per step), 2^16 "
+                        "walks from uniform random sources, length 80", scale=22, program="deepwalk", length=80,
+               weighted=True, labels=0, queries="random", n_queries=1 << 16, scaling="weak", sampler="ALIAS",
+               tables=False),
+}
+
+
+def exec_extra(cfg):
+    """ExecOptions overrides of a config (sampler / static tables)."""
+    from paper_2107_11983_b200 import abi
+    out = {}
+    if cfg.get("sampler"):
+        out["sampler"] = int(getattr(abi.Sampler, cfg["sampler"]))
+    if "tables" in cfg:
+        out["use_static_tables"] = bool(cfg["tables"])
+    return out
+
+
 # CPU-baseline samples (queries), sized for ~10-30 s of reference work on 16 cores
-CPU_SAMPLE = {"c1": 1 << 16, "c2": 1 << 20, "c3": 1 << 20, "c4": 1 << 15, "c5": 1 << 22}
+CPU_SAMPLE = {"c1": 1 << 16, "c2": 1 << 20, "c3": 1 << 20, "c4": 1 << 15, "c5": 1 << 22,
+              "g1": 1 << 12, "g2": 1 << 12, "g3": 1 << 12}
 
 
 def program_of(cfg):
@@ -250,6 +280,16 @@ def s_alg(cfg, stats, moves, layout, steps=None):
     from paper_2107_11983_b200 import abi
     p = cfg["program"]
     mv = max(moves, 1)
+    if cfg.get("sampler") and (p in ("node2vec", "metapath") or not cfg.get("tables", True)):
+        # gathered flows: the per-step gather reads every edge's weight input
+        # (u8 label, f32 weight, or u32 neighbour + adjacency test)
+        eb = {"metapath": 1, "deepwalk": 4, "node2vec": 4}[p]
+        sc = stats.get("scanned", 0) / mv
+        pr = stats.get("probes", 0) / mv
+        ref = 1.25 + sc * eb / SECTOR + pr + 1.0 + 0.125
+        text = (f"gathered: offsets 1.25 + {sc:.1f} edges x {eb} B / 32 + {pr:.2f} adjacency-test sectors "
+                f"+ neighbour 1 + 1/8 = {ref:.3f} sectors (instrumented edges scanned per move)")
+        return dict(ref=ref, ref_model=text, layout=ref, layout_model=text, requests=1.0 + pr)
     one = {"deepwalk": abi.HAS_WIDE_ALIAS, "ppr": abi.HAS_ADJ, "metapath": abi.HAS_MP_SUCC}
     if p in one:
         reads = 1.0 if layout & one[p] else 2.0
@@ -352,8 +392,12 @@ BOUND_CAUSE = {
     "c1": "the graph is L2-resident; the 65 Ki walks' dependent L2 chains bound it",
     "c2": "the bulk saturates the L2/atomic queue and the longest geometric walks finish in an unloaded tail",
     "c3": "one 128 B DRAM line per O-REJ trial (adjacency entry) plus the L2-resident pair filter",
-    "c4": "one 128 B DRAM line per move (successor-decorated partitioned edge)",
-    "c5": "one 128 B DRAM line per move (wide alias bucket)",
+    "c4": "one random DRAM request per move (successor-decorated partitioned edge, 64 B fetch)",
+    "c5": "one random DRAM request per move (wide alias bucket, 64 B fetch): the random-request rate of HBM",
+    "g1": "per-step gathers over the current vertex's edges (hub steps warp-cooperative), each a Node2Vec "
+          "adjacency test",
+    "g2": "per-step gathers of the current vertex's labels and Vose's construction per step",
+    "g3": "per-step gathers of the current vertex's weights and Vose's construction per step",
 }
 
 
@@ -409,7 +453,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist, comm=None):
     info = dg.info()
     V = info["V"]
     prog = program_of(cfg)
-    opts = ExecOptions(seed=1, path_stride=row_capacity(cfg))
+    opts = ExecOptions(seed=1, path_stride=row_capacity(cfg), **exec_extra(cfg))
     sess = E.Session(dg, prog, opts)
     sampler, flow, pre_s = sess.describe()
     layout = sess.layout()
@@ -570,7 +614,7 @@ def cpu_baseline(key, cfg, dg, spec, threads=None):
     sample = QuerySpec.from_list(spec.sources[:m])
     hg = dg.download()
     prog = program_of(cfg)
-    opts = ExecOptions(seed=1, threads=threads)
+    opts = ExecOptions(seed=1, threads=threads, **exec_extra(cfg))
     if ref_available():
         rg = RefOracle().graph(hg)
         del hg
@@ -601,13 +645,14 @@ def extras(args, rank, world, local_rank, dist):
     its own reference CPU baseline."""
     out = {}
     peak, peak_kind = measured_peak()
-    for key in ["c1", "c2", "c3", "c4", "c5"]:
+    for key in ["c1", "c2", "c3", "c4", "c5"] + sorted(GATHERED):
         if key == args.config:
             continue
         try:
             # e2e evidence too, except for C5 (10.9 GB of pinned host buffers per step)
-            a = argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 1, "no_e2e": key == "c5"})
-            cfg = CONFIGS[key]
+            a = argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 1,
+                                      "no_e2e": key == "c5" or key in GATHERED})
+            cfg = CONFIGS[key] if key in CONFIGS else GATHERED[key]
             r = run_ours(a, cfg, rank, world, local_rank, dist)
             ms = r["total_ms"] / 3
             roof, sa = roofline_block(key, cfg, r, r["moves"], ms, peak, peak_kind)
@@ -666,7 +711,7 @@ def reference_arm(args, cfg, rank, world):
     n_all = hi - lo
     m = min(CPU_SAMPLE[args.config], max(1, n_all // max(args.steps, 1)))
     prog = program_of(cfg)
-    opts = ExecOptions(seed=1, threads=threads)
+    opts = ExecOptions(seed=1, threads=threads, **exec_extra(cfg))
 
     def run(queries):
         sample = QuerySpec.from_list(spec.sources[:queries])
@@ -704,7 +749,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS) + sorted(GATHERED))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -713,7 +758,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS[args.config] if args.config in CONFIGS else GATHERED[args.config]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -32,6 +32,10 @@ constexpr uint32_t kDegEscape = (1u << kDegBits) - 1;  // degree >= this: read o
 #endif
 constexpr int kBlock = WF_BLOCK;  // walk kernel threads per block
 constexpr unsigned kFull = 0xFFFFFFFFu;
+#ifndef WF_COOP_DEGREE
+#define WF_COOP_DEGREE 32
+#endif
+constexpr uint32_t kCoopDegree = WF_COOP_DEGREE;  // gathered flows: warp-cooperative gather from this degree
 constexpr int kMaxIndexedLabels = 6;  // 32 B label record: u64 base + 6 u32 group ends
 
 enum Flow : int { kDirect = 0, kTables = 1, kGathered = 2 };
@@ -115,8 +119,8 @@ struct WalkLaunch {
     unsigned long long* overflow_out;
     unsigned long long* cursor;
     int* error_word;
-    double* scratch;  // gathered ALIAS: per-lane park area
-    uint64_t scratch_stride;
+    double* scratch;  // gathered ALIAS: per-warp weights + park areas for hub steps
+    uint64_t scratch_stride;  // doubles per warp area (>= max degree)
     int use_label_index;
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
@@ -159,7 +163,13 @@ struct Walker {
     // draw, so the RNG arithmetic overlaps the word's load instead of waiting
     // behind the unpack's escape branch
     bool pend;
+    // gathered flows: the outcome of this step's warp-cooperative gather
+    // (coop_step) for a hub vertex, consumed by move(); kCoopNone otherwise
+    uint8_t coop;
+    uint32_t coop_pick;
 };
+
+enum CoopState : uint8_t { kCoopNone = 0, kCoopPick = 1, kCoopDead = 2, kCoopFault = 3 };
 
 // ---- graph helpers -------------------------------------------------------------
 
@@ -911,6 +921,15 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 return kMoved;
             }
         }
+        if (q.coop != kCoopNone) {  // the warp gathered this hub step (coop_step)
+            const uint8_t c = q.coop;
+            q.coop = kCoopNone;
+            if (c == kCoopDead) return kDead;
+            if (c == kCoopFault) return kFault;
+            if constexpr (P::needs_edge) edge = base + q.coop_pick;
+            dst = ldr(L.g.nbr + base + q.coop_pick);
+            return kMoved;
+        }
         double sum = 0.0, mx = 0.0;
         if (L.g.stats) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
         for (uint32_t i = 0; i < d; ++i) {
@@ -929,9 +948,11 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (x < run) { pick = i; break; }
             }
         } else if constexpr (S == WF_SAMPLER_ALIAS) {
+            // below kCoopDegree (hubs go through coop_step): the demoted
+            // larges park in a lane-local array
             uint32_t x = q.rng.index(d);
             uint64_t k = q.rng.bits53();
-            double* park = L.scratch + (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * L.scratch_stride;
+            double park[kCoopDegree];
             double split;
             uint32_t second;
             vose_bucket(d, sum, [&](uint32_t i) { return P::weight(L, q, base + i); }, x,
@@ -962,6 +983,154 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
     }
     dst = ldr(L.g.nbr + base + pick);
     return kMoved;
+}
+
+// ---- warp-cooperative gather for hub vertices (gathered flows) -------------------
+// gather (engine.hpp:134-184) evaluates weight(Q, e) over all d edges of the
+// current vertex every step.  A lane doing that alone for a hub serialises d
+// dependent loads (for Node2Vec each one an adjacency test) while its warp
+// waits.  Instead, when a lane's current vertex has >= kCoopDegree edges, the
+// whole warp evaluates its weights, 32 edges per round, and the lane samples
+// from the result:
+//   ITS   the pick is the first i with x < cumulative[i]: a warp-wide inclusive
+//         scan per round of 32 weights, x drawn by the owner from its own stream;
+//   ALIAS the weights go to the warp's scratch row; the owner runs Vose's
+//         construction for its bucket over it (vose_bucket, no re-evaluation);
+//   REJ   p* = max weight (exact in any order); the owner runs the trials.
+// Bit-exactness: the reference sums in edge order.  A reordered fp64 sum is
+// the same number when every partial sum is exact, i.e. when all weights are
+// multiples of a common power of two q and the total stays below 2^52 q (the
+// survey checked this reordering for f32-valued weights).  Each
+// step checks that certificate; without it ITS falls back to the owner's
+// sequential scan and ALIAS sums the scratch row in edge order.  Dead ends
+// (all weights zero) consume no draws; contract violations set the error word.
+// Exponent of the lowest set bit of a positive finite double (its quantum).
+__device__ __forceinline__ int quantum_exp(double w) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(w));
+    const int e = static_cast<int>((b >> 52) & 0x7FF);
+    const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (e ? (1ull << 52) : 0ull);
+    return (e ? e : 1) - 1075 + __ffsll(static_cast<long long>(m)) - 1;
+}
+
+template <class P, int S>
+__device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int leader, double* wrow) {
+    const int lane = threadIdx.x & 31;
+    Walker h = q;  // the owner's walker, as every lane sees it
+    h.row = __shfl_sync(kFull, q.row, leader);
+    h.cur = __shfl_sync(kFull, q.cur, leader);
+    h.prev = __shfl_sync(kFull, q.prev, leader);
+    h.cur_base = __shfl_sync(kFull, q.cur_base, leader);
+    h.prev_base = __shfl_sync(kFull, q.prev_base, leader);
+    h.cur_deg = __shfl_sync(kFull, q.cur_deg, leader);
+    h.prev_deg = __shfl_sync(kFull, q.prev_deg, leader);
+    h.len = __shfl_sync(kFull, q.len, leader);
+    const uint32_t d = h.cur_deg;
+    const uint64_t base = h.cur_base;
+    if (L.g.stats && lane == leader) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
+    // pass 1: weights, validity, partial sums, max, smallest quantum
+    double lsum = 0.0, lmax = 0.0;
+    int qexp = 0x7FFFFFFF;
+    bool bad = false;
+    for (uint32_t i = lane; i < d; i += 32) {
+        const double w = P::weight(L, h, base + i);
+        if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
+        if (S == WF_SAMPLER_ALIAS) wrow[i] = w;
+        if (w > 0.0) qexp = min(qexp, quantum_exp(w));
+        lsum += w;
+        lmax = w > lmax ? w : lmax;
+    }
+    if (__any_sync(kFull, bad)) {  // check_program_weight (engine.hpp:97-101)
+        if (lane == leader) {
+            raise_device(L, WF_ERR_CONTRACT);
+            q.coop = kCoopFault;
+        }
+        return;
+    }
+    double sum = lsum, mx = lmax;
+    for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(kFull, sum, o);
+        const double m2 = __shfl_xor_sync(kFull, mx, o);
+        mx = m2 > mx ? m2 : mx;
+        qexp = min(qexp, __shfl_xor_sync(kFull, qexp, o));
+    }
+    if (!(sum > 0.0)) {  // all weights zero (exact in any order): dead end, no draws
+        if (lane == leader) q.coop = kCoopDead;
+        return;
+    }
+    // every partial sum a multiple of 2^qexp below 2^52 * 2^qexp: exact
+    const bool exact = sum < ldexp(1.0, 52 + max(qexp, -1000));
+    if constexpr (S == WF_SAMPLER_ITS) {
+        if (!exact) return;  // the owner scans sequentially in move()
+        double x = 0.0;
+        if (lane == leader) x = q.rng.real(sum);  // == cumulative[d-1]
+        x = __shfl_sync(kFull, x, leader);
+        // pass 2: first i with x < cumulative[i] (engine.hpp:373-377)
+        double running = 0.0;
+        uint32_t pick = d - 1;
+        for (uint32_t c = 0; c < d; c += 32) {
+            const uint32_t i = c + lane;
+            double v = i < d ? P::weight(L, h, base + i) : 0.0;
+            for (int o = 1; o < 32; o <<= 1) {  // inclusive scan (exact)
+                const double u = __shfl_up_sync(kFull, v, o);
+                if (lane >= o) v += u;
+            }
+            const unsigned hit = __ballot_sync(kFull, i < d && x < running + v);
+            if (hit) {
+                pick = c + __ffs(hit) - 1;
+                break;
+            }
+            running += __shfl_sync(kFull, v, 31);
+        }
+        if (lane == leader) {
+            q.coop = kCoopPick;
+            q.coop_pick = pick;
+        }
+    } else if constexpr (S == WF_SAMPLER_ALIAS) {
+        __syncwarp();  // the scratch row is complete
+        if (lane == leader) {
+            double total = sum;
+            if (!exact) {  // the reference's edge-order sum
+                total = 0.0;
+                for (uint32_t i = 0; i < d; ++i) total += wrow[i];
+            }
+            const uint32_t x = q.rng.index(d);
+            const uint64_t k = q.rng.bits53();
+            double split;
+            uint32_t second;
+            vose_bucket(d, total, [&](uint32_t i) { return wrow[i]; }, x, wrow + L.scratch_stride, split,
+                        second);
+            q.coop = kCoopPick;
+            q.coop_pick = k < unit_threshold(split) ? x : second;
+        }
+        __syncwarp();  // the row is free for the next hub
+    } else {  // REJ over the gathered weights, p* = max (sampler.hpp:152-164)
+        if (lane == leader) {
+            for (uint32_t t = 0;; ++t) {
+                if (t >= L.trial_cap) {
+                    raise_device(L, WF_ERR_REJECTION_CAP);
+                    q.coop = kCoopFault;
+                    return;
+                }
+                if (L.g.stats) atomicAdd(L.g.stats, 1ull);
+                const uint32_t x = q.rng.index(d);
+                const double y = q.rng.real(mx);
+                if (y < P::weight(L, q, base + x)) {
+                    q.coop = kCoopPick;
+                    q.coop_pick = x;
+                    return;
+                }
+            }
+        }
+    }
+}
+
+// Whether a gathered launch takes the cooperative hub path (MetaPath's
+// label-index ITS needs no gather at all).
+template <class P, int S, int F>
+__device__ __forceinline__ bool coop_gathered(const WalkLaunch& L) {
+    if constexpr (F != kGathered) return false;
+    if constexpr (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) return !L.use_label_index;
+    return true;
 }
 
 // Loads what the next move out of q.cur needs into registers.
@@ -1207,6 +1376,8 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
     q.nb_word = 0;
     q.have_nb = false;
     q.pend = false;
+    q.coop = kCoopNone;
+    q.coop_pick = 0;
     bool active = false;
     bool fresh = false;
     bool drained = false;
@@ -1352,6 +1523,26 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
         // and consuming it now would stall the whole warp on that load.
         const bool ready = active && !fresh;
         fresh = false;
+        if constexpr (F == kGathered) {
+            if (coop_gathered<P, S, F>(L)) {
+                if constexpr (kDeferWord<P>) {
+                    if (ready && q.pend) {
+                        unpack_word(L.g, q.nb_word, q.cur, q.cur_base, q.cur_deg);
+                        q.pend = false;
+                    }
+                }
+                // hub steps of this warp, one after the other, by the whole warp
+                unsigned hubs = __ballot_sync(kFull, ready && q.cur_deg >= kCoopDegree);
+                double* wrow = L.scratch ? L.scratch + ((blockIdx.x * static_cast<uint64_t>(kBlock) + threadIdx.x) >> 5) *
+                                                           (2 * L.scratch_stride)
+                                         : nullptr;
+                while (hubs) {
+                    const int leader = __ffs(hubs) - 1;
+                    hubs &= hubs - 1;
+                    coop_step<P, S>(L, q, leader, wrow);
+                }
+            }
+        }
         if (ready) {
             uint32_t dst = 0;
             uint64_t edge = 0;

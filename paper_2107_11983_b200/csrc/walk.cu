@@ -151,16 +151,18 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     uint64_t lanes_needed = (L.n_rows + 31) / 32 * 32;
     int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));
     grid = std::max(1, std::min(grid, grid_needed));
-    if (s.kind == WF_SAMPLER_ALIAS && s.flow == kGathered) {
-        // per-lane park area for the on-the-fly Vose construction
-        uint64_t per_lane = std::max<uint32_t>(g.max_degree, 1);
-        uint64_t budget = 4ull << 30;
-        uint64_t lanes = std::max<uint64_t>(kBlock, budget / (per_lane * 8));
-        grid = std::max(1, std::min<int>(grid, static_cast<int>(lanes / kBlock)));
-        uint64_t need = static_cast<uint64_t>(grid) * kBlock * per_lane;
+    if (s.kind == WF_SAMPLER_ALIAS && s.flow == kGathered && g.max_degree >= kCoopDegree) {
+        // per-warp rows for the cooperative hub steps (coop_step): the hub's
+        // weights and Vose's park area, max_degree doubles each; lanes below
+        // kCoopDegree park in registers / local memory
+        const uint64_t per_warp = 2ull * g.max_degree;
+        const uint64_t budget = 8ull << 30;
+        const uint64_t warps = std::max<uint64_t>(kBlock / 32, budget / (per_warp * 8));
+        grid = std::max(1, std::min<int>(grid, static_cast<int>(warps / (kBlock / 32))));
+        const uint64_t need = static_cast<uint64_t>(grid) * (kBlock / 32) * per_warp;
         if (s.scratch.size() < need) s.scratch.allocate(need);
         L.scratch = s.scratch.get();
-        L.scratch_stride = per_lane;
+        L.scratch_stride = g.max_degree;
     }
     {
         // PPR's short geometric walks refill a lane every few moves: half of

@@ -8,11 +8,17 @@
   no usable edge, MetaPath edges carry the schema label, PPR's mean length is
   the geometric 1/0.2, total steps = sum of path lengths - n, visit counts sum
   to the number of path vertices, and repeated runs are identical.
-* C5 (s26, 2^26 walks, ~110 GB of HBM): the sampled walks are replayed in
-  Python from the reference's own primitives (the C restatement's
-  alias_init over each visited vertex's weights and its RngStream draws), so
-  no 50 GB host-side preprocess_static is needed.
+* whole-run parity against the unmodified reference: C1, C2 and C3 (Node2Vec
+  s22, 4.2 M walks, 189 M moves; the reference on all host cores);
+* sampled parity at the largest sizes: C4 (MetaPath s22) on 20 k query ids and
+  C5 (DeepWalk s26, 2^26 walks, ~110 GB of HBM) on 10 k query ids, replayed by
+  the reference's own ResolvedRun + StepDriver (run_qids) over the downloaded
+  2.1 B-edge CSR (its preprocess_static builds 50 GB of alias tables on the
+  host); the 48-walk Python replay from the reference's primitives stays as a
+  second, independent check.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -115,9 +121,16 @@ def test_c3_node2vec_s22_full_size(s22):
     # symmetric graph: only isolated sources dead-end; everything else has 80 vertices
     assert np.all(got.lengths()[deg > 0] == 80)
     assert np.all(got.lengths()[deg == 0] == 1)
-    _sample_parity(hg, spec, prog, opts, got, k=200)
     again = E.run_sequential(dg, spec, prog, opts).walks
     assert again.equals(got)
+    # the whole run against the unmodified reference (all host cores)
+    if ref_available():
+        want = RefOracle().graph(hg).run(spec, prog, ExecOptions(seed=1, threads=os.cpu_count()))
+        bad = got.first_mismatch(want.walks)
+        assert bad is None, f"walk {bad} differs"
+        assert int(got.vertices.size - got.status.size) == want.metrics.total_steps
+    else:
+        _sample_parity(hg, spec, prog, opts, got, k=2000)
 
 
 def test_c4_metapath_s22_full_size(s22):
@@ -141,7 +154,7 @@ def test_c4_metapath_s22_full_size(s22):
         last = int(got.path(int(q))[-1])
         want_label = schema[lens[q] - 1]
         assert not np.any(hg.labels[hg.offsets[last]:hg.offsets[last + 1]] == want_label)
-    _sample_parity(hg, spec, prog, opts, got, k=300)
+    _sample_parity(hg, spec, prog, opts, got, k=20000)
 
 
 def _replay_deepwalk_alias(hg, port, qid, length, seed, cache):
@@ -192,6 +205,23 @@ def test_c5_deepwalk_s26_full_size():
     ok, *_ = _edges_ok(hg, ws.to_host(0, 1 << 17))
     assert ok
     assert ws.metrics.total_steps == total
+    # 10 k query ids (10 blocks of 1024 at random offsets) against the
+    # unmodified reference's ResolvedRun + StepDriver over this CSR
+    if ref_available():
+        starts = np.sort(np.random.default_rng(5).choice(V // 1024, 10, replace=False)) * 1024
+        qids = np.concatenate([np.arange(a, a + 1024) for a in starts]).astype(np.uint64)
+        rg = RefOracle().graph(hg)
+        del hg.weights  # the reference holds its own f64 copy now
+        want = rg.run_qids(QuerySpec.one_per_vertex(), prog, opts, qids).walks
+        del rg
+        i = 0
+        for a in starts:
+            got = ws.to_host(int(a), int(a) + 1024)
+            for j in range(1024):
+                assert int(got.status[j]) == int(want.status[i]), int(a) + j
+                assert np.array_equal(got.path(j), want.path(i)), int(a) + j
+                i += 1
+        hg = dg.download()
     # sampled parity against a replay from the reference's primitives
     port = PortOracle()
     cache = {}

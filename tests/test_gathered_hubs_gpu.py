@@ -1,0 +1,85 @@
+"""Gathered flows (a gather over all d edges per step, engine.hpp:134-184) on an
+R-MAT graph whose hubs have thousands of edges: hub steps run warp-
+cooperatively (coop_step: weights 32 edges per round, the ITS pick by a
+warp-wide exact scan, ALIAS over the warp's scratch row, REJ's p* as a warp
+max), lighter vertices per lane.  Every walk must equal the unmodified
+reference's, including where the exactness certificate fails (f64 weights)
+and the owner falls back to the reference's edge-order sum."""
+import numpy as np
+import pytest
+
+from oracle.oracle import RefOracle, ref_available
+from paper_2107_11983_b200 import abi
+from paper_2107_11983_b200 import engine as E
+from paper_2107_11983_b200.host import (DeepWalkProgram, ExecOptions, Graph, MetaPathProgram, Node2VecProgram,
+                                        QuerySpec)
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")]
+
+GATHERED = [abi.Sampler.ITS, abi.Sampler.ALIAS, abi.Sampler.REJ]
+
+
+@pytest.fixture(scope="module")
+def rmat():
+    # 10 labels: more than the label index holds, so MetaPath ITS also gathers
+    dg = E.DeviceGraph.rmat(14, 16, seed=3, weighted=True, label_count=10)
+    hg = dg.download()
+    assert np.diff(hg.offsets).max() > 1000  # real hubs
+    return dg, hg, RefOracle().graph(hg)
+
+
+def same(got, want):
+    bad = got.walks.first_mismatch(want.walks)
+    assert bad is None, f"walk {bad} differs"
+    assert got.metrics.total_steps == want.metrics.total_steps
+
+
+@pytest.mark.parametrize("sampler", GATHERED)
+@pytest.mark.parametrize("prog", [DeepWalkProgram(30, True), Node2VecProgram(2.0, 0.5, 30, False),
+                                  Node2VecProgram(0.5, 2.0, 30, True), MetaPathProgram([i % 10 for i in range(20)])],
+                         ids=["deepwalk_w", "node2vec", "node2vec_w", "metapath10"])
+def test_gathered_hub_steps_match_reference(rmat, prog, sampler):
+    dg, hg, rg = rmat
+    opts = ExecOptions(seed=12, sampler=int(sampler), use_static_tables=False)
+    spec = QuerySpec.one_per_vertex()
+    sess = E.Session(dg, prog, opts)
+    s, f, _ = sess.describe()
+    assert f == abi.Flow.GATHERED
+    same(E.run_sequential(dg, spec, prog, opts), rg.run(spec, prog, opts))
+
+
+def test_gathered_hubs_without_exactness_certificate():
+    """f64 weights that are not float32-exact: the reordered sum is not
+    certified, so ITS scans in the owner lane and ALIAS sums the scratch row
+    in edge order — still the reference's walks."""
+    ref = RefOracle()
+    rg = ref.power_law(3000, 60000, seed=17, weighted=True)
+    off, nbr, w, _ = rg.export()
+    assert np.diff(off).max() >= 64
+    dg = E.DeviceGraph.from_host(Graph(off, nbr, w))
+    for sampler in GATHERED:
+        opts = ExecOptions(seed=4, sampler=int(sampler), use_static_tables=False)
+        prog = DeepWalkProgram(25, True)
+        same(E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, opts),
+             rg.run(QuerySpec.one_per_vertex(), prog, opts))
+
+
+def test_quantum_certificate_mixed_scales():
+    """Weights of very different scales (1e-12 .. 1e12, exactly representable
+    in f32): the certificate must reject the reordered sum where it would
+    round, and the walks still match."""
+    rng = np.random.default_rng(8)
+    V = 400
+    deg = np.where(np.arange(V) < 4, 300, 3)
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    nbr = np.concatenate([np.sort(rng.choice(V, d, replace=False)) for d in deg]).astype(np.uint32)
+    scale = rng.choice([1e-12, 1.0, 3.0, 1e12], nbr.size)
+    w = (scale * rng.integers(1, 100, nbr.size)).astype(np.float32)
+    hg = Graph(off, nbr, w)
+    dg = E.DeviceGraph.from_host(hg)
+    rg = RefOracle().graph(hg)
+    for sampler in GATHERED:
+        opts = ExecOptions(seed=2, sampler=int(sampler), use_static_tables=False)
+        prog = DeepWalkProgram(20, True)
+        same(E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, opts),
+             rg.run(QuerySpec.one_per_vertex(), prog, opts))
