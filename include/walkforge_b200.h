@@ -258,7 +258,7 @@ typedef struct wf_program_ops {
     int32_t has_max_weight;    /* BoundedWeightProgram (required for O-REJ) */
     int32_t prechecked;        /* PreCheckedProgram: finished() before the first move */
     uint32_t program_size;     /* bytes of the program object (<= 256, trivially copyable) */
-    uint32_t reserved;
+    uint32_t engine_abi;       /* wf::kEngineAbi of the device headers it was compiled with (checked) */
     /* Launches walk_kernel<Custom<Type>, sampler, flow, streaming> with `grid`
      * blocks on `stream`; `walk_launch` is the engine's launch record. */
     int (*launch)(const void* walk_launch, int32_t sampler, int32_t flow, int32_t streaming, int32_t grid,

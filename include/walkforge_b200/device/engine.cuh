@@ -230,9 +230,19 @@ __device__ __forceinline__ uint4 ldr16(const uint4* p) {
 #define WF_LDR_MOVE "ld.global.cg.L2::64B"
 #endif
 __device__ __forceinline__ void ldr256_move(const uint4* p, uint4& a, uint4& b) {
+#ifdef WF_MOVE_EVICT_FIRST
+    // experiment: evict-first L2 policy on the move's random line (keeps L2 for
+    // the path rows' partial lines)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm("ld.global.L2::cache_hint.L2::64B.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p), "l"(pol));
+#else
     asm(WF_LDR_MOVE ".v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
         : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
         : "l"(p));
+#endif
 }
 __device__ __forceinline__ uint4 ldr16_move(const uint4* p) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(p);
@@ -471,6 +481,11 @@ __device__ __forceinline__ uint32_t upper_index(const double* cum, uint32_t n, d
 // (Custom<U> below) lives in L.prog.user.
 
 constexpr int kCustomProgram = -1;
+
+// Version of the launch record's meaning (WalkLaunch fields, scratch layout,
+// program adapter): a user program library compiled against another value is
+// refused at wf_session_create_custom (its kernels would misread the launch).
+constexpr uint32_t kEngineAbi = 2;
 
 template <int K>
 struct Program;
@@ -725,10 +740,21 @@ __device__ __forceinline__ int orej_accept(const WalkLaunch& L, const Walker& q,
 // demoted in ascending order, so three ascending cursors replay it exactly.
 // Demoted larges park their final scaled value in park[] until consumed.
 // Returns split of bucket x and its alias index (x itself when none).
+// `scaled(i)` = w_i * n / sum (sampler.hpp:97): computed on demand, or read
+// from a row the warp filled in parallel (vose_bucket_scaled).
+template <typename Scaled>
+__device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double* park, double& split_out,
+                                   uint32_t& second_out);
+
 template <typename WFn>
-__device__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double* park,
-                            double& split_out, uint32_t& second_out) {
-    auto scaled = [&](uint32_t i) { return wfn(i) * n / sum; };
+__device__ __forceinline__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double* park,
+                                            double& split_out, uint32_t& second_out) {
+    vose_bucket_scaled(n, [&](uint32_t i) { return wfn(i) * n / sum; }, x, park, split_out, second_out);
+}
+
+template <typename Scaled>
+__device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double* park, double& split_out,
+                                   uint32_t& second_out) {
     uint32_t a = 0;        // next initial-small candidate
     uint32_t c = 0;        // next demoted-large candidate (trails the large cursor)
     uint32_t demoted = 0;  // larges demoted so far
@@ -772,6 +798,80 @@ __device__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double*
             demoted += 1;
             lcur = next_large(lcur + 1);
             if (lcur < n) lval = scaled(lcur);
+        }
+    }
+    split_out = 1.0;  // leftover: probability exactly 1, no alias (sampler.hpp:112-119)
+    second_out = x;
+}
+
+// ---- Vose's worklists by a warp -------------------------------------------------
+// The replay of the FIFO worklists (vose_bucket_scaled) advances three
+// ascending cursors over the scaled weights; a lone lane doing that over a
+// hub's row waits an L2 round trip per element.  Here the whole warp scans 32
+// elements per step with a ballot and every lane carries the (uniform)
+// cursor state, so a cursor advance costs one coalesced load per 32 elements;
+// the pairing arithmetic (lval -= 1 - sval, order-dependent fp64) is the same
+// sequence as the reference's.
+
+// First i in [from, n) whose value satisfies `pred`, and its value; n if none.
+template <class Pred>
+__device__ __forceinline__ uint32_t warp_find(const double* __restrict__ row, uint32_t from, uint32_t n, Pred pred,
+                                              double& val) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t b = from; b < n; b += 32) {
+        const uint32_t i = b + lane;
+        const double v = i < n ? row[i] : 0.0;
+        const unsigned m = __ballot_sync(kFull, i < n && pred(v));
+        if (m) {
+            const int l = __ffs(m) - 1;
+            val = __shfl_sync(kFull, v, l);
+            return b + l;
+        }
+    }
+    return n;
+}
+
+// vose_bucket_scaled for bucket x over `row` (scaled weights), by the whole
+// warp; `park` (n doubles) holds demoted larges' final values.  Every lane
+// returns the split and alias of bucket x.
+__device__ __forceinline__ void vose_bucket_warp(uint32_t n, const double* __restrict__ row, uint32_t x,
+                                                 double* __restrict__ park, double& split_out,
+                                                 uint32_t& second_out) {
+    const int lane = threadIdx.x & 31;
+    auto small = [](double v) { return v < 1.0; };
+    auto large = [](double v) { return v >= 1.0; };
+    double lval = 0.0, aval = 0.0, dummy = 0.0;
+    uint32_t lcur = warp_find(row, 0, n, large, lval);
+    uint32_t a = warp_find(row, 0, n, small, aval);
+    uint32_t c = 0, demoted = 0, consumed = 0;
+    while (lcur < n) {  // sampler.hpp:103-111
+        uint32_t sidx;
+        double sval;
+        if (a < n) {
+            sidx = a;
+            sval = aval;
+            a = warp_find(row, a + 1, n, small, aval);
+        } else if (consumed < demoted) {
+            c = warp_find(row, c, n, large, dummy);
+            sidx = c;
+            double pv = 0.0;
+            if (lane == 0) pv = park[c];  // written by lane 0 when demoted
+            sval = __shfl_sync(kFull, pv, 0);
+            ++c;
+            ++consumed;
+        } else {
+            break;
+        }
+        if (sidx == x) {
+            split_out = sval;
+            second_out = lcur;
+            return;
+        }
+        lval -= 1.0 - sval;
+        if (lval < 1.0) {
+            if (lane == 0) park[lcur] = lval;
+            ++demoted;
+            lcur = warp_find(row, lcur + 1, n, large, lval);
         }
     }
     split_out = 1.0;  // leftover: probability exactly 1, no alias (sampler.hpp:112-119)
@@ -1031,6 +1131,7 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
     double lsum = 0.0, lmax = 0.0;
     int qexp = 0x7FFFFFFF;
     bool bad = false;
+#pragma unroll 4
     for (uint32_t i = lane; i < d; i += 32) {
         const double w = P::weight(L, h, base + i);
         if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
@@ -1087,18 +1188,28 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         }
     } else if constexpr (S == WF_SAMPLER_ALIAS) {
         __syncwarp();  // the scratch row is complete
+        double total = sum;
+        if (!exact) {  // the reference's edge-order sum, by the owner
+            double seq = 0.0;
+            if (lane == leader)
+                for (uint32_t i = 0; i < d; ++i) seq += wrow[i];
+            total = __shfl_sync(kFull, seq, leader);
+        }
+        // the scaled weights (one division each, sampler.hpp:97) by the warp,
+        // so the owner's replay of Vose's worklists only reads the row
+        for (uint32_t i = lane; i < d; i += 32) wrow[i] = wrow[i] * d / total;
+        __syncwarp();
+        uint32_t x = 0;
+        uint64_t k = 0;
         if (lane == leader) {
-            double total = sum;
-            if (!exact) {  // the reference's edge-order sum
-                total = 0.0;
-                for (uint32_t i = 0; i < d; ++i) total += wrow[i];
-            }
-            const uint32_t x = q.rng.index(d);
-            const uint64_t k = q.rng.bits53();
-            double split;
-            uint32_t second;
-            vose_bucket(d, total, [&](uint32_t i) { return wrow[i]; }, x, wrow + L.scratch_stride, split,
-                        second);
+            x = q.rng.index(d);
+            k = q.rng.bits53();
+        }
+        x = __shfl_sync(kFull, x, leader);
+        double split;
+        uint32_t second;
+        vose_bucket_warp(d, wrow, x, wrow + L.scratch_stride, split, second);
+        if (lane == leader) {
             q.coop = kCoopPick;
             q.coop_pick = k < unit_threshold(split) ? x : second;
         }
@@ -1222,6 +1333,17 @@ struct PathStage {
 
 // One 256-bit store (st.global.v8, sm_100) of a lane's staged 8-word group.
 __device__ __forceinline__ void store_group(uint32_t* dst, PathStage ps) {
+#ifdef WF_PATH_EVICT_LAST
+    // experiment: evict-last L2 policy on the path sectors (their line fills
+    // over four groups)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(dst),
+                 "r"(ps.at(0)), "r"(ps.at(1)), "r"(ps.at(2)), "r"(ps.at(3)), "r"(ps.at(4)), "r"(ps.at(5)),
+                 "r"(ps.at(6)), "r"(ps.at(7)), "l"(pol)
+                 : "memory");
+    return;
+#endif
     asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(ps.at(0)),
                  "r"(ps.at(1)), "r"(ps.at(2)), "r"(ps.at(3)), "r"(ps.at(4)), "r"(ps.at(5)), "r"(ps.at(6)),
                  "r"(ps.at(7))

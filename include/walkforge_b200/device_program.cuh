@@ -206,7 +206,7 @@ const wf_program_ops* ops_for(const char* name) {
         P::has_max_weight ? 1 : 0,
         P::prechecked ? 1 : 0,
         static_cast<uint32_t>(sizeof(U)),
-        0u,
+        wf::kEngineAbi,
         &launch<U>,
         &occupancy<U>,
         &static_weights<U>,

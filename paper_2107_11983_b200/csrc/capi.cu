@@ -194,7 +194,8 @@ void resolve_run(Session& s, int type, int preferred, bool has_max_weight, uint3
 // concept's optional members are; the object rides in the launch parameters.
 void resolve_custom(Session& s, const wf_program_ops& ops, const void* program, const wf_exec_options* o) {
     require(ops.abi_version == WF_ABI_VERSION, "program table built against another ABI version");
-    require(ops.launch_size == sizeof(WalkLaunch), "program table built against another engine header");
+    require(ops.launch_size == sizeof(WalkLaunch) && ops.engine_abi == kEngineAbi,
+            "program table built against another engine header: rebuild the program library");
     require(ops.launch && ops.occupancy && ops.static_weights, "incomplete program table");
     require(program != nullptr || ops.program_size == 0, "null program object");
     require(ops.program_size <= static_cast<uint32_t>(kUserProgramBytes), "program object too large");

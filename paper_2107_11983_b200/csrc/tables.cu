@@ -17,6 +17,8 @@
 // u32 second_dst}; `y < split` with y = uniform_real(1.0) is exactly
 // `(r >> 11) < thr` (rng.cuh unit_threshold).
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "runtime.hpp"
 
@@ -58,26 +60,24 @@ __device__ __forceinline__ double unpark(const uint4* b) {
 
 // IDX: buckets carry the positions {first, second} in E_v (EngineAliasSlot,
 // engine.hpp:22-28) instead of their destinations.
-template <typename WF, bool IDX>
-__global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
-                               uint32_t V, WF wf, uint4* __restrict__ bucket, uint32_t bs,
-                               uint8_t* __restrict__ exhausted, unsigned* any_exhausted) {
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t a0 = off[v];
-        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
-        if (n == 0) continue;
-        double sum = 0.0;
-        for (uint32_t i = 0; i < n; ++i) sum += wf(a0 + i);
-        if (!(sum > 0.0)) {
-            exhausted[v] = 1;
-            atomicOr(any_exhausted, 1u);
-            continue;
-        }
-        const uint32_t* nb = nbr + a0;
-        auto dst = [&](uint32_t i) { return IDX ? i : nb[i]; };
-        uint4* out = bucket + a0 * bs;  // bs = 2: wide 32 B buckets (second half decorated later)
-        auto scaled = [&](uint32_t i) { return wf(a0 + i) * n / sum; };  // sampler.hpp:97
+// Vertices with at least kHubDeg edges are built by a warp (k_*_warp below);
+// the rest one thread per vertex.  ALIAS keeps Vose's pairing loop serial in
+// lane 0 (the worklist replay is order-dependent fp64), so only its heaviest
+// vertices move to a warp, where the parallel sum and scaled weights pay:
+// with the ITS / REJ threshold (64) the C5 build took 12.5 s against 2.6 s
+// thread-per-vertex — too few warps for millions of mid-degree vertices.
+constexpr uint32_t kHubDeg = 64;
+constexpr uint32_t kHubDegAlias = 1024;
+
+// Vose's construction for one vertex of n edges (sampler.hpp:89-120) with the
+// scaled weights given by `scaled(i)` (w_i * n / sum, sampler.hpp:97), three
+// ascending cursors replaying the FIFO worklists, demoted larges parked in
+// their own output bucket.
+template <bool IDX, typename Scaled>
+__device__ void vose_vertex(uint32_t n, Scaled scaled, const uint32_t* __restrict__ nb, uint4* __restrict__ out,
+                            uint32_t bs) {
+    auto dst = [&](uint32_t i) { return IDX ? i : nb[i]; };
+    {
         auto next_large = [&](uint32_t from) {
             while (from < n && !(scaled(from) >= 1.0)) ++from;
             return from;
@@ -127,6 +127,152 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
     }
 }
 
+template <typename WF, bool IDX>
+__global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                               uint32_t V, WF wf, uint4* __restrict__ bucket, uint32_t bs,
+                               uint8_t* __restrict__ exhausted, unsigned* any_exhausted) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n == 0 || n >= kHubDegAlias) continue;
+        double sum = 0.0;
+        for (uint32_t i = 0; i < n; ++i) sum += wf(a0 + i);  // engine.hpp:218-226
+        if (!(sum > 0.0)) {
+            exhausted[v] = 1;
+            atomicOr(any_exhausted, 1u);
+            continue;
+        }
+        vose_vertex<IDX>(n, [&](uint32_t i) { return wf(a0 + i) * n / sum; }, nbr + a0, bucket + a0 * bs, bs);
+    }
+}
+
+// ---- hubs: a warp per vertex ---------------------------------------------------------
+// The reference sums a vertex's weights in edge order (engine.hpp:218-226).  A
+// warp's reordered sum is the same number when every partial sum is exact:
+// all weights multiples of 2^q and the total below 2^(52+q) (f32 weights in
+// [1,5) qualify with room to spare; SURVEY 8(a) verified the reordered ITS
+// scan on 32 M entries).  Otherwise lane 0 sums in edge order.
+__device__ __forceinline__ int quantum_of(double w) {  // exponent of the lowest set bit of w > 0
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(w));
+    const int e = static_cast<int>((b >> 52) & 0x7FF);
+    const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (e ? (1ull << 52) : 0ull);
+    return (e ? e : 1) - 1075 + __ffsll(static_cast<long long>(m)) - 1;
+}
+
+// Sum and max of a vertex's weights as the reference computes them; every
+// lane returns the same values.
+template <typename WF>
+__device__ __forceinline__ void warp_sum_max(WF wf, uint64_t a0, uint32_t n, double& sum, double& mx, bool& exact) {
+    const int lane = threadIdx.x & 31;
+    double ls = 0.0, lm = 0.0;
+    int q = 0x7FFFFFFF;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const double w = wf(a0 + i);
+        ls += w;
+        lm = w > lm ? w : lm;
+        if (w > 0.0) q = min(q, quantum_of(w));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
+        const double m2 = __shfl_xor_sync(0xFFFFFFFFu, lm, o);
+        lm = m2 > lm ? m2 : lm;
+        q = min(q, __shfl_xor_sync(0xFFFFFFFFu, q, o));
+    }
+    exact = ls < ldexp(1.0, 52 + max(q, -1000));
+    if (!exact) {  // the edge-order sum, by lane 0
+        double seq = 0.0;
+        if (lane == 0)
+            for (uint32_t i = 0; i < n; ++i) seq += wf(a0 + i);
+        ls = __shfl_sync(0xFFFFFFFFu, seq, 0);
+    }
+    sum = ls;
+    mx = lm;
+}
+
+// vose_vertex by a warp over a row of scaled weights: the cursors advance
+// by ballots over 32 elements (warp_find, engine.cuh), lane 0 stores the
+// buckets and parks demoted larges' values in their own bucket; the leftovers
+// (probability exactly 1) are stored in parallel.
+template <bool IDX>
+__device__ void vose_vertex_warp(uint32_t n, const double* __restrict__ row, const uint32_t* __restrict__ nb,
+                                 uint4* __restrict__ out, uint32_t bs) {
+    const int lane = threadIdx.x & 31;
+    auto dst = [&](uint32_t i) { return IDX ? i : nb[i]; };
+    auto small = [](double v) { return v < 1.0; };
+    auto large = [](double v) { return v >= 1.0; };
+    double lval = 0.0, aval = 0.0, dummy = 0.0;
+    uint32_t lcur = warp_find(row, 0, n, large, lval);
+    uint32_t a = warp_find(row, 0, n, small, aval);
+    uint32_t c = 0, demoted = 0, consumed = 0;
+    while (lcur < n) {  // sampler.hpp:103-111
+        uint32_t sidx;
+        double sval;
+        if (a < n) {
+            sidx = a;
+            sval = aval;
+            a = warp_find(row, a + 1, n, small, aval);
+        } else if (consumed < demoted) {
+            c = warp_find(row, c, n, large, dummy);
+            sidx = c;
+            double pv = 0.0;
+            if (lane == 0) pv = unpark(out + c * bs);
+            sval = __shfl_sync(0xFFFFFFFFu, pv, 0);
+            ++c;
+            ++consumed;
+        } else {
+            break;
+        }
+        if (lane == 0) store_bucket(out + sidx * bs, sval, dst(sidx), dst(lcur));
+        lval -= 1.0 - sval;
+        if (lval < 1.0) {
+            if (lane == 0) park(out + lcur * bs, lval);
+            ++demoted;
+            lcur = warp_find(row, lcur + 1, n, large, lval);
+        }
+    }
+    // leftovers (sampler.hpp:112-119): the smalls from a, the larges from c
+    // (demoted and never consumed, then lcur onward) — probability 1, no alias
+    __syncwarp();
+    for (uint32_t i = min(a, c) + lane; i < n; i += 32) {
+        const double v = row[i];
+        if ((v < 1.0 && i >= a) || (v >= 1.0 && i >= c)) store_bucket(out + i * bs, 1.0, dst(i), dst(i));
+    }
+}
+
+// ALIAS for hub vertices: the warp sums, writes the scaled weights
+// (w_i * n / sum, one division each) to its scratch row, and replays Vose's
+// worklists over the row (vose_vertex_warp).
+template <typename WF, bool IDX>
+__global__ void k_static_alias_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
+                                    uint32_t V, WF wf, uint4* __restrict__ bucket, uint32_t bs,
+                                    uint8_t* __restrict__ exhausted, unsigned* any_exhausted,
+                                    double* __restrict__ rows, uint64_t row_stride) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    double* row = rows + warp * row_stride;
+    for (uint64_t v = warp; v < V; v += nwarps) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n < kHubDegAlias) continue;
+        double sum, mx;
+        bool exact;
+        warp_sum_max(wf, a0, n, sum, mx, exact);
+        if (!(sum > 0.0)) {
+            if (lane == 0) {
+                exhausted[v] = 1;
+                atomicOr(any_exhausted, 1u);
+            }
+            continue;
+        }
+        for (uint32_t i = lane; i < n; i += 32) row[i] = wf(a0 + i) * n / sum;  // sampler.hpp:97
+        __syncwarp();
+        vose_vertex_warp<IDX>(n, row, nbr + a0, bucket + a0 * bs, bs);
+        __syncwarp();
+    }
+}
+
 template <typename WF>
 __global__ void k_static_its(const uint64_t* __restrict__ off, uint32_t V, WF wf,
                              double* __restrict__ cum, uint8_t* __restrict__ exhausted,
@@ -135,13 +281,55 @@ __global__ void k_static_its(const uint64_t* __restrict__ off, uint32_t V, WF wf
          v += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t a0 = off[v];
         const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
-        if (n == 0) continue;
+        if (n == 0 || n >= kHubDeg) continue;
         double run = 0.0;
         for (uint32_t i = 0; i < n; ++i) {
             run += wf(a0 + i);
             cum[a0 + i] = run;
         }
         if (!(run > 0.0)) {
+            exhausted[v] = 1;
+            atomicOr(any_exhausted, 1u);
+        }
+    }
+}
+
+// ITS for hubs: the running sums (engine.hpp:232-238) as a segmented scan, 32
+// edges per round, when the reordering is exact; else lane 0 in edge order.
+template <typename WF>
+__global__ void k_static_its_warp(const uint64_t* __restrict__ off, uint32_t V, WF wf,
+                                  double* __restrict__ cum, uint8_t* __restrict__ exhausted,
+                                  unsigned* any_exhausted) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < V; v += nwarps) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n < kHubDeg) continue;
+        double sum, mx;
+        bool exact;
+        warp_sum_max(wf, a0, n, sum, mx, exact);
+        if (exact) {
+            double running = 0.0;
+            for (uint32_t c = 0; c < n; c += 32) {
+                const uint32_t i = c + lane;
+                double x = i < n ? wf(a0 + i) : 0.0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double u = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                    if (lane >= o) x += u;
+                }
+                if (i < n) cum[a0 + i] = running + x;
+                running += __shfl_sync(0xFFFFFFFFu, x, 31);
+            }
+        } else if (lane == 0) {
+            double run = 0.0;
+            for (uint32_t i = 0; i < n; ++i) {
+                run += wf(a0 + i);
+                cum[a0 + i] = run;
+            }
+        }
+        if (!(sum > 0.0) && lane == 0) {
             exhausted[v] = 1;
             atomicOr(any_exhausted, 1u);
         }
@@ -156,7 +344,7 @@ __global__ void k_static_rej(const uint64_t* __restrict__ off, uint32_t V, WF wf
          v += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t a0 = off[v];
         const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
-        if (n == 0) continue;
+        if (n == 0 || n >= kHubDeg) continue;
         double sum = 0.0, mx = 0.0;
         for (uint32_t i = 0; i < n; ++i) {
             double w = wf(a0 + i);
@@ -168,6 +356,39 @@ __global__ void k_static_rej(const uint64_t* __restrict__ off, uint32_t V, WF wf
             atomicOr(any_exhausted, 1u);
         } else {
             pstar[v] = mx;
+        }
+    }
+}
+
+// REJ for hubs: p* = max weight (engine.hpp:244-246), exact in any order;
+// exhausted iff no weight is positive.
+template <typename WF>
+__global__ void k_static_rej_warp(const uint64_t* __restrict__ off, uint32_t V, WF wf,
+                                  double* __restrict__ pstar, uint8_t* __restrict__ exhausted,
+                                  unsigned* any_exhausted) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < V; v += nwarps) {
+        const uint64_t a0 = off[v];
+        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
+        if (n < kHubDeg) continue;
+        double mx = 0.0;
+        for (uint32_t i = lane; i < n; i += 32) {
+            const double w = wf(a0 + i);
+            mx = w > mx ? w : mx;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double m2 = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+            mx = m2 > mx ? m2 : mx;
+        }
+        if (lane == 0) {
+            if (!(mx > 0.0)) {
+                exhausted[v] = 1;
+                atomicOr(any_exhausted, 1u);
+            } else {
+                pstar[v] = mx;
+            }
         }
     }
 }
@@ -213,29 +434,80 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
     const int threads = 128;
     uint64_t blocks = (g.V + threads - 1) / threads;
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, static_cast<uint64_t>(sm_count(g.device)) * 64));
+    // hubs (>= kHubDeg edges): a warp each, on a second stream beside the
+    // per-thread kernel (the two touch disjoint vertices)
+    const bool hubs = g.max_degree >= (s.kind == WF_SAMPLER_ALIAS ? kHubDegAlias : kHubDeg);
+    const int wblocks = sm_count(g.device) * 16;  // 8 warps per block
+    cudaStream_t hs = st;
+    cudaEvent_t ev = nullptr;
+    if (hubs) {
+        WF_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+        WF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    DeviceBuffer<double> rows;
+    auto fork = [&] {  // the hub stream starts after the buffers are ready
+        if (!hubs) return;
+        WF_CUDA(cudaEventRecord(ev, st));
+        WF_CUDA(cudaStreamWaitEvent(hs, ev, 0));
+    };
     if (s.kind == WF_SAMPLER_ALIAS) {
         const uint32_t bs = s.alias_wide ? 2 : 1;
         s.alias.allocate((g.E + 2) * bs);  // +2: 32 B reads of the last 16 B entry stay in bounds
         // buckets of exhausted vertices are never built; zero them so the
         // decoration pass reads valid vertex ids there
         WF_CUDA(cudaMemsetAsync(s.alias.get(), 0, s.alias.bytes(), st));
+        fork();
         if (s.alias_idx)
             k_static_alias<WF, true><<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
                                                                  s.alias.get(), bs, s.exhausted.get(), any);
         else
             k_static_alias<WF, false><<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
                                                                   s.alias.get(), bs, s.exhausted.get(), any);
+        WF_LAUNCHED();
+        if (hubs) {
+            // a scaled-weight row per warp, within a 4 GiB budget
+            const uint64_t per = g.max_degree;
+            const uint64_t warps =
+                std::max<uint64_t>(8, std::min<uint64_t>(wblocks * 8ull, (4ull << 30) / (per * 8)));
+            const int hb = static_cast<int>(std::max<uint64_t>(1, warps / 8));
+            rows.allocate(static_cast<uint64_t>(hb) * 8 * per);
+            if (s.alias_idx)
+                k_static_alias_warp<WF, true><<<hb, 256, 0, hs>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
+                                                                 s.alias.get(), bs, s.exhausted.get(), any,
+                                                                 rows.get(), per);
+            else
+                k_static_alias_warp<WF, false><<<hb, 256, 0, hs>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
+                                                                  s.alias.get(), bs, s.exhausted.get(), any,
+                                                                  rows.get(), per);
+            WF_LAUNCHED();
+        }
     } else if (s.kind == WF_SAMPLER_ITS) {
         s.its.allocate(std::max<uint64_t>(g.E, 1));
-        k_static_its<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.its.get(),
-                                                 s.exhausted.get(), any);
+        fork();
+        k_static_its<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.its.get(), s.exhausted.get(), any);
+        WF_LAUNCHED();
+        if (hubs) {
+            k_static_its_warp<<<wblocks, 256, 0, hs>>>(g.offsets.get(), g.V, wf, s.its.get(), s.exhausted.get(), any);
+            WF_LAUNCHED();
+        }
     } else {
         s.rej.allocate(g.V);
         WF_CUDA(cudaMemsetAsync(s.rej.get(), 0, g.V * sizeof(double), st));
-        k_static_rej<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.rej.get(),
-                                                 s.exhausted.get(), any);
+        fork();
+        k_static_rej<<<blocks, threads, 0, st>>>(g.offsets.get(), g.V, wf, s.rej.get(), s.exhausted.get(), any);
+        WF_LAUNCHED();
+        if (hubs) {
+            k_static_rej_warp<<<wblocks, 256, 0, hs>>>(g.offsets.get(), g.V, wf, s.rej.get(), s.exhausted.get(), any);
+            WF_LAUNCHED();
+        }
     }
-    WF_LAUNCHED();
+    if (hubs) {  // join: the caller's stream continues after both
+        WF_CUDA(cudaEventRecord(ev, hs));
+        WF_CUDA(cudaStreamWaitEvent(st, ev, 0));
+        WF_CUDA(cudaStreamSynchronize(hs));
+        cudaEventDestroy(ev);
+        cudaStreamDestroy(hs);
+    }
 }
 
 }  // namespace
@@ -274,6 +546,13 @@ void Session::build_tables(cudaStream_t st) {
     unsigned h = 0;
     WF_CUDA(cudaMemcpyAsync(&h, any.get(), 4, cudaMemcpyDeviceToHost, st));
     WF_CUDA(cudaStreamSynchronize(st));
+    const bool trace = getenv("WF_TRACE_PRE") != nullptr;  // diagnostics: phase times
+    auto phase = [&](const char* what) {
+        if (trace)
+            std::fprintf(stderr, "[pre] %s %.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    };
+    phase("tables");
     any_exhausted = h != 0;
     if (any_exhausted) {
         sview.allocate(gs.V);
@@ -289,6 +568,7 @@ void Session::build_tables(cudaStream_t st) {
         k_decorate_alias<<<blocks, 256, 0, st>>>(alias.get(), gs.E, sv);
         WF_LAUNCHED();
         WF_CUDA(cudaStreamSynchronize(st));
+        phase("decorate");
     }
     preprocess_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

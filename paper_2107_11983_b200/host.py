@@ -242,7 +242,7 @@ class DeviceProgram:
 class ProgramOpsC(C.Structure):  # wf_program_ops (walkforge_b200.h)
     _fields_ = [("abi_version", C.c_uint32), ("launch_size", C.c_uint32), ("name", C.c_char_p),
                 ("walker_type", C.c_int32), ("preferred_sampler", C.c_int32), ("has_max_weight", C.c_int32),
-                ("prechecked", C.c_int32), ("program_size", C.c_uint32), ("reserved", C.c_uint32),
+                ("prechecked", C.c_int32), ("program_size", C.c_uint32), ("engine_abi", C.c_uint32),
                 ("launch", C.c_void_p), ("occupancy", C.c_void_p), ("static_weights", C.c_void_p),
                 ("max_weight", C.CFUNCTYPE(C.c_double, C.c_void_p)),
                 ("max_path", C.CFUNCTYPE(C.c_uint32, C.c_void_p))]

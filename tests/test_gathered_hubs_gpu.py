@@ -83,3 +83,43 @@ def test_quantum_certificate_mixed_scales():
         prog = DeepWalkProgram(20, True)
         same(E.run_sequential(dg, QuerySpec.one_per_vertex(), prog, opts),
              rg.run(QuerySpec.one_per_vertex(), prog, opts))
+
+
+def _ceil53(split):
+    from fractions import Fraction
+    x = Fraction(split) * (1 << 53)
+    n = x.numerator // x.denominator
+    return n + (1 if n < x else 0)
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_static_tables_hub_warps_bit_exact(f64):
+    """preprocess_static (engine.hpp:190-251): hub vertices (>= 64 edges) are
+    built by a warp each (certified reordered sums / segmented ITS scan, warp
+    max for REJ, Vose over a scaled-weight row); light ones per thread.  Every
+    table equals the reference's, with f32 weights and with f64 ones (no
+    certificate: edge-order sums)."""
+    dg0 = E.DeviceGraph.rmat(14, 16, seed=7, weighted=True)
+    hg = dg0.download()
+    if f64:
+        w = hg.weights.astype(np.float64) * (1.0 + 1e-9)  # not float32-exact
+        hg = Graph(hg.offsets, hg.neighbors, w)
+    dg = E.DeviceGraph.from_host(hg)
+    assert np.diff(hg.offsets).max() >= 1000 and dg.info()["weights_f64"] == f64
+    rg = RefOracle().graph(hg)
+    prog = DeepWalkProgram(20, True)
+    deg = np.diff(hg.offsets).astype(np.int64)
+    for s in GATHERED:
+        got = E.Session(dg, prog, ExecOptions(sampler=int(s))).tables()
+        want = rg.static_tables(prog, int(s))
+        assert np.array_equal(got["exhausted"], want["exhausted"])
+        live = np.repeat(want["exhausted"] == 0, deg)
+        if s == abi.Sampler.ALIAS:
+            thr = np.array([_ceil53(x) for x in want["alias_split"]], dtype=np.uint64)
+            assert np.array_equal(got["alias_thr"][live], thr[live])
+            assert np.array_equal(got["alias_first_dst"][live], want["alias_first_dst"][live])
+            assert np.array_equal(got["alias_second_dst"][live], want["alias_second_dst"][live])
+        elif s == abi.Sampler.ITS:
+            assert np.array_equal(got["its"], want["its"])
+        else:
+            assert np.array_equal(got["rej_p_star"], want["rej_p_star"])

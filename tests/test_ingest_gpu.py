@@ -38,17 +38,16 @@ def random_edge_list(path, seed, m=3000, sparse=True, with_w=True, with_l=True):
     open(path, "w").write("\n".join(lines) + "\n")
 
 
-def same_graph(dg, rg, ids_ref=None, f32_weights=False):
-    """f32_weights: the reference's weights are synthetic f64 values
-    (synthetic_weight, graph.cpp:279-282); the device stores them rounded to f32."""
+def same_graph(dg, rg, ids_ref=None):
+    """The same CSR, labels and weights: f64 weights (e.g. synthetic_weight,
+    graph.cpp:279-282) come back as the same doubles."""
     h = dg.download()
     off, nbr, w, lab = rg.export()
     assert np.array_equal(h.offsets, off)
     assert np.array_equal(h.neighbors, nbr)
     assert (h.weights is None) == (w is None)
     if w is not None:
-        want = w.astype(np.float32).astype(np.float64) if f32_weights else w
-        assert np.array_equal(h.weights.astype(np.float64), want)
+        assert np.array_equal(h.weights.astype(np.float64), w)
     assert (h.labels is None) == (lab is None)
     if lab is not None:
         assert np.array_equal(h.labels.astype(np.uint32), lab)
@@ -65,9 +64,7 @@ def test_edge_list_loader_matches_reference(undirected, weights, labels):
         random_edge_list(p, seed=weights * 7 + labels + int(undirected))
         rg, ids = ref.load_edge_list(p, undirected, weights, labels, 5, seed=11)
         dg = E.DeviceGraph.load_edge_list(p, undirected, weights, labels, 5, seed=11)
-        same_graph(dg, rg, ids, f32_weights=weights == 2)
-        if weights == 2:  # walk parity on the f32 weights the device holds
-            rg = ref.graph(dg.download())
+        same_graph(dg, rg, ids)
         # walks on the loaded graphs agree too (ingest -> run end to end)
         prog = DeepWalkProgram(12, weights != 0) if weights else Node2VecProgram(2.0, 0.5, 12, False)
         want = rg.run(QuerySpec.one_per_vertex(), prog, ExecOptions(seed=3))
