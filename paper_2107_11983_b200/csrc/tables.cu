@@ -60,14 +60,14 @@ __device__ __forceinline__ double unpark(const uint4* b) {
 
 // IDX: buckets carry the positions {first, second} in E_v (EngineAliasSlot,
 // engine.hpp:22-28) instead of their destinations.
-// Vertices with at least kHubDeg edges are built by a warp (k_*_warp below);
-// the rest one thread per vertex.  ALIAS keeps Vose's pairing loop serial in
-// lane 0 (the worklist replay is order-dependent fp64), so only its heaviest
-// vertices move to a warp, where the parallel sum and scaled weights pay:
-// with the ITS / REJ threshold (64) the C5 build took 12.5 s against 2.6 s
-// thread-per-vertex — too few warps for millions of mid-degree vertices.
+// ITS and REJ: vertices with at least kHubDeg edges are built by a warp
+// (k_*_warp below), the rest one thread per vertex.  ALIAS stays one thread
+// per vertex: Vose's pairing loop is an order-dependent fp64 chain, and a
+// warp replaying it for a hub (cursor scans by ballot over a row of scaled
+// weights) measured far slower at C5 — 11.3 s against 0.12 s for the whole
+// per-thread build: the chain serialises on L2 round trips, and a row per
+// warp left too few warps for the ~10^5 vertices of 1000+ edges.
 constexpr uint32_t kHubDeg = 64;
-constexpr uint32_t kHubDegAlias = 1024;
 
 // Vose's construction for one vertex of n edges (sampler.hpp:89-120) with the
 // scaled weights given by `scaled(i)` (w_i * n / sum, sampler.hpp:97), three
@@ -135,7 +135,7 @@ __global__ void k_static_alias(const uint64_t* __restrict__ off, const uint32_t*
          v += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t a0 = off[v];
         const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
-        if (n == 0 || n >= kHubDegAlias) continue;
+        if (n == 0) continue;
         double sum = 0.0;
         for (uint32_t i = 0; i < n; ++i) sum += wf(a0 + i);  // engine.hpp:218-226
         if (!(sum > 0.0)) {
@@ -188,89 +188,6 @@ __device__ __forceinline__ void warp_sum_max(WF wf, uint64_t a0, uint32_t n, dou
     }
     sum = ls;
     mx = lm;
-}
-
-// vose_vertex by a warp over a row of scaled weights: the cursors advance
-// by ballots over 32 elements (warp_find, engine.cuh), lane 0 stores the
-// buckets and parks demoted larges' values in their own bucket; the leftovers
-// (probability exactly 1) are stored in parallel.
-template <bool IDX>
-__device__ void vose_vertex_warp(uint32_t n, const double* __restrict__ row, const uint32_t* __restrict__ nb,
-                                 uint4* __restrict__ out, uint32_t bs) {
-    const int lane = threadIdx.x & 31;
-    auto dst = [&](uint32_t i) { return IDX ? i : nb[i]; };
-    auto small = [](double v) { return v < 1.0; };
-    auto large = [](double v) { return v >= 1.0; };
-    double lval = 0.0, aval = 0.0, dummy = 0.0;
-    uint32_t lcur = warp_find(row, 0, n, large, lval);
-    uint32_t a = warp_find(row, 0, n, small, aval);
-    uint32_t c = 0, demoted = 0, consumed = 0;
-    while (lcur < n) {  // sampler.hpp:103-111
-        uint32_t sidx;
-        double sval;
-        if (a < n) {
-            sidx = a;
-            sval = aval;
-            a = warp_find(row, a + 1, n, small, aval);
-        } else if (consumed < demoted) {
-            c = warp_find(row, c, n, large, dummy);
-            sidx = c;
-            double pv = 0.0;
-            if (lane == 0) pv = unpark(out + c * bs);
-            sval = __shfl_sync(0xFFFFFFFFu, pv, 0);
-            ++c;
-            ++consumed;
-        } else {
-            break;
-        }
-        if (lane == 0) store_bucket(out + sidx * bs, sval, dst(sidx), dst(lcur));
-        lval -= 1.0 - sval;
-        if (lval < 1.0) {
-            if (lane == 0) park(out + lcur * bs, lval);
-            ++demoted;
-            lcur = warp_find(row, lcur + 1, n, large, lval);
-        }
-    }
-    // leftovers (sampler.hpp:112-119): the smalls from a, the larges from c
-    // (demoted and never consumed, then lcur onward) — probability 1, no alias
-    __syncwarp();
-    for (uint32_t i = min(a, c) + lane; i < n; i += 32) {
-        const double v = row[i];
-        if ((v < 1.0 && i >= a) || (v >= 1.0 && i >= c)) store_bucket(out + i * bs, 1.0, dst(i), dst(i));
-    }
-}
-
-// ALIAS for hub vertices: the warp sums, writes the scaled weights
-// (w_i * n / sum, one division each) to its scratch row, and replays Vose's
-// worklists over the row (vose_vertex_warp).
-template <typename WF, bool IDX>
-__global__ void k_static_alias_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ nbr,
-                                    uint32_t V, WF wf, uint4* __restrict__ bucket, uint32_t bs,
-                                    uint8_t* __restrict__ exhausted, unsigned* any_exhausted,
-                                    double* __restrict__ rows, uint64_t row_stride) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    double* row = rows + warp * row_stride;
-    for (uint64_t v = warp; v < V; v += nwarps) {
-        const uint64_t a0 = off[v];
-        const uint32_t n = static_cast<uint32_t>(off[v + 1] - a0);
-        if (n < kHubDegAlias) continue;
-        double sum, mx;
-        bool exact;
-        warp_sum_max(wf, a0, n, sum, mx, exact);
-        if (!(sum > 0.0)) {
-            if (lane == 0) {
-                exhausted[v] = 1;
-                atomicOr(any_exhausted, 1u);
-            }
-            continue;
-        }
-        for (uint32_t i = lane; i < n; i += 32) row[i] = wf(a0 + i) * n / sum;  // sampler.hpp:97
-        __syncwarp();
-        vose_vertex_warp<IDX>(n, row, nbr + a0, bucket + a0 * bs, bs);
-        __syncwarp();
-    }
 }
 
 template <typename WF>
@@ -436,7 +353,7 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, static_cast<uint64_t>(sm_count(g.device)) * 64));
     // hubs (>= kHubDeg edges): a warp each, on a second stream beside the
     // per-thread kernel (the two touch disjoint vertices)
-    const bool hubs = g.max_degree >= (s.kind == WF_SAMPLER_ALIAS ? kHubDegAlias : kHubDeg);
+    const bool hubs = s.kind != WF_SAMPLER_ALIAS && g.max_degree >= kHubDeg;
     const int wblocks = sm_count(g.device) * 16;  // 8 warps per block
     cudaStream_t hs = st;
     cudaEvent_t ev = nullptr;
@@ -444,7 +361,6 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
         WF_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
         WF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
-    DeviceBuffer<double> rows;
     auto fork = [&] {  // the hub stream starts after the buffers are ready
         if (!hubs) return;
         WF_CUDA(cudaEventRecord(ev, st));
@@ -464,23 +380,6 @@ void launch_tables(Session& s, WF wf, unsigned* any, cudaStream_t st) {
             k_static_alias<WF, false><<<blocks, threads, 0, st>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
                                                                   s.alias.get(), bs, s.exhausted.get(), any);
         WF_LAUNCHED();
-        if (hubs) {
-            // a scaled-weight row per warp, within a 4 GiB budget
-            const uint64_t per = g.max_degree;
-            const uint64_t warps =
-                std::max<uint64_t>(8, std::min<uint64_t>(wblocks * 8ull, (4ull << 30) / (per * 8)));
-            const int hb = static_cast<int>(std::max<uint64_t>(1, warps / 8));
-            rows.allocate(static_cast<uint64_t>(hb) * 8 * per);
-            if (s.alias_idx)
-                k_static_alias_warp<WF, true><<<hb, 256, 0, hs>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
-                                                                 s.alias.get(), bs, s.exhausted.get(), any,
-                                                                 rows.get(), per);
-            else
-                k_static_alias_warp<WF, false><<<hb, 256, 0, hs>>>(g.offsets.get(), g.nbr.get(), g.V, wf,
-                                                                  s.alias.get(), bs, s.exhausted.get(), any,
-                                                                  rows.get(), per);
-            WF_LAUNCHED();
-        }
     } else if (s.kind == WF_SAMPLER_ITS) {
         s.its.allocate(std::max<uint64_t>(g.E, 1));
         fork();

@@ -94,11 +94,11 @@ def _ceil53(split):
 
 @pytest.mark.parametrize("f64", [False, True])
 def test_static_tables_hub_warps_bit_exact(f64):
-    """preprocess_static (engine.hpp:190-251): hub vertices (>= 64 edges) are
-    built by a warp each (certified reordered sums / segmented ITS scan, warp
-    max for REJ, Vose over a scaled-weight row); light ones per thread.  Every
-    table equals the reference's, with f32 weights and with f64 ones (no
-    certificate: edge-order sums)."""
+    """preprocess_static (engine.hpp:190-251): ITS / REJ hub vertices (>= 64
+    edges) are built by a warp each (certified reordered sums / segmented ITS
+    scan, warp max for REJ), light ones and every ALIAS vertex per thread.
+    Every table equals the reference's, with f32 weights and with f64 ones
+    (no certificate: edge-order sums)."""
     dg0 = E.DeviceGraph.rmat(14, 16, seed=7, weighted=True)
     hg = dg0.download()
     if f64:

@@ -31,13 +31,14 @@ def main():
 
     from paper_2107_11983_b200 import engine as E
     from paper_2107_11983_b200.host import ExecOptions
-    cfg = dict(bench.CONFIGS[args.config])
+    cfg = dict(bench.CONFIGS[args.config] if args.config in bench.CONFIGS else bench.GATHERED[args.config])
     if args.scale:
         cfg["scale"] = args.scale
     dg = E.DeviceGraph.rmat(cfg["scale"], 16, seed=1, weighted=cfg["weighted"],
                             label_count=cfg["labels"])
     V = dg.info()["V"]
-    sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=bench.row_capacity(cfg), layout_flags=args.layout))
+    sess = E.Session(dg, bench.program_of(cfg), ExecOptions(seed=1, path_stride=bench.row_capacity(cfg),
+                                                            layout_flags=args.layout, **bench.exec_extra(cfg)))
     if args.queries and cfg["queries"] == "random":
         cfg["n_queries"] = args.queries
     spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
