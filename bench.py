@@ -771,6 +771,10 @@ def main():
     import torch
     dist = None
     if world > 1 or "RANK" in os.environ:  # any torchrun launch, even N=1
+        # NCCL's init log names every rank of the communicators (the engine's
+        # own for the visit counts and torch's for the barriers)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))

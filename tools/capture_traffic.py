@@ -78,6 +78,6 @@ def run(configs):
 
 if __name__ == "__main__":
     if len(sys.argv) >= 2 and sys.argv[1] == "run":
-        run(sys.argv[2:] or ["c1", "c2", "c3", "c4", "c5"])
+        run(sys.argv[2:] or ["c1", "c2", "c3", "c4", "c5", "g1", "g2", "g3"])
     else:
         print(__doc__)
