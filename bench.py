@@ -433,6 +433,10 @@ def roofline_block(key, cfg, r, moves, ms_per_launch, peak, peak_kind):
             "frac": rate / (peak / bpm * 1e9)},
         "traffic_stamp": stamp,
         "note": bound_note(key, rate, bpm, peak),
+        **({"caveat": "frac > 1: SURVEY 8(d)'s S_alg counts the sectors the reference's layout would touch "
+                      "(binary-search probes, label scans) that this engine's layout does not read; "
+                      "layout.frac and measured_sectors.frac are the bytes actually moved"}
+           if ach / peak > 1 else {}),
     }, sa
 
 def flush_l2(buf):
