@@ -119,6 +119,8 @@ typedef struct wf_exec_options {
 #define WF_LAYOUT_SEARCH_TREE 16u  /* Node2Vec: sector B-tree instead of the edge hash set */
 #define WF_LAYOUT_NO_MP_SUCC 32u   /* MetaPath: label records + partitioned neighbours only */
 #define WF_LAYOUT_NO_EDGE_FILTER 64u /* Node2Vec: no pair pre-filter before the exact distance test */
+#define WF_LAYOUT_ADJ8 128u          /* NAIVE too: adjacency packed as (dst, degree, base) in 8 B where it fits
+                                        (O-REJ uses it by default on graphs below the 16 B form's threshold) */
 
 typedef struct wf_query_spec {
     int32_t mode; /* wf_query_mode */
@@ -293,6 +295,7 @@ int wf_session_describe(const wf_session* s, int32_t* sampler, int32_t* flow,
 #define WF_LAYOUT_HAS_SEARCH_INDEX 16u /* adjacency search B-tree (Node2Vec, opt-in) */
 #define WF_LAYOUT_HAS_EDGE_HASH 32u    /* exact edge hash set (Node2Vec default) */
 #define WF_LAYOUT_HAS_EDGE_FILTER 64u  /* blocked Bloom pre-filter of vertex pairs (Node2Vec default) */
+#define WF_LAYOUT_HAS_ADJ8 128u        /* packed 8 B decorated adjacency (NAIVE / O-REJ) */
 int wf_session_layout(const wf_session* s, uint32_t* flags);
 void wf_session_destroy(wf_session* s);
 

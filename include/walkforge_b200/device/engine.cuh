@@ -127,6 +127,10 @@ struct WalkLaunch {
     int alias_idx;                    // alias buckets carry edge positions {first, second} in
                                       // E_v instead of destinations (programs that read the edge)
     const uint4* __restrict__ adj;    // Direct flows: {dst, 0, word lo, word hi} per edge, or null
+    // Direct flows on graphs whose (dst, degree, base) pack into 64 bits: one
+    // u64 per edge, dst | deg << adj8_vbits | base << (adj8_vbits + adj8_dbits)
+    const unsigned long long* __restrict__ adj8;
+    uint32_t adj8_vbits, adj8_dbits;
     const uint4* __restrict__ mp_adj; // MetaPath: per partitioned edge {dst, 0, next-group word} or null
     // Host streaming (run_to_host; all null otherwise).  Rows are grouped in
     // tiles of 2^tile_shift and chunks of 2^chunk_tiles_shift tiles.  Finished
@@ -254,6 +258,15 @@ __device__ __forceinline__ uint4 ldr16_move(const uint4* p) {
 // An edge's weight as the reference holds it (double, graph.hpp:102).
 __device__ __forceinline__ double edge_weight(const GraphView& g, uint64_t e) {
     return g.weights64 ? __ldg(g.weights64 + e) : static_cast<double>(ldr(g.weights + e));
+}
+
+// A packed 8 B adjacency entry: the destination and its vertex word
+// (base << kDegBits | deg) for the next move.
+__device__ __forceinline__ uint32_t adj8_unpack(uint64_t e, uint32_t vbits, uint32_t dbits, uint64_t& word) {
+    const uint32_t dst = static_cast<uint32_t>(e & ((1ull << vbits) - 1));
+    const uint64_t deg = (e >> vbits) & ((1ull << dbits) - 1);
+    word = ((e >> (vbits + dbits)) << kDegBits) | deg;
+    return dst;
 }
 
 __device__ __forceinline__ void unpack_word(const GraphView& g, uint64_t w, uint32_t v,
@@ -485,7 +498,7 @@ constexpr int kCustomProgram = -1;
 // Version of the launch record's meaning (WalkLaunch fields, scratch layout,
 // program adapter): a user program library compiled against another value is
 // refused at wf_session_create_custom (its kernels would misread the launch).
-constexpr uint32_t kEngineAbi = 2;
+constexpr uint32_t kEngineAbi = 3;
 
 template <int K>
 struct Program;
@@ -924,7 +937,10 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 // decorated adjacency, its vertex word for the next step)
                 uint32_t dx;
                 uint64_t wx = 0;
-                if (L.adj) {
+                if (L.adj8) {
+                    dx = adj8_unpack(ldr(reinterpret_cast<const uint64_t*>(L.adj8) + base + x), L.adj8_vbits,
+                                     L.adj8_dbits, wx);
+                } else if (L.adj) {
                     uint4 a = ldr16(L.adj + base + x);
                     dx = a.x;
                     wx = (static_cast<uint64_t>(a.w) << 32) | a.z;
@@ -941,7 +957,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 if (acc) {
                     dst = dx;
                     if constexpr (P::needs_edge) edge = base + x;
-                    if (L.adj) {
+                    if (L.adj || L.adj8) {
                         q.nb_word = wx;
                         q.have_nb = true;
                     }
@@ -1073,6 +1089,15 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
         }
     }
     if constexpr (P::needs_edge) edge = base + pick;
+    if (F == kDirect && L.adj8) {
+        // packed adjacency (dst, degree, base): one 8 B load
+        uint64_t w;
+        dst = adj8_unpack(ldr(reinterpret_cast<const uint64_t*>(L.adj8) + base + pick), L.adj8_vbits, L.adj8_dbits,
+                          w);
+        q.nb_word = w;
+        q.have_nb = true;
+        return kMoved;
+    }
     if (F == kDirect && L.adj) {
         // decorated adjacency {dst, -, vertex word of dst}: one 16 B load
         uint4 a = ldr16(L.adj + base + pick);

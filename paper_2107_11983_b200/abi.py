@@ -157,11 +157,13 @@ LAYOUT_FORCE_ADJ = 8
 LAYOUT_SEARCH_TREE = 16
 LAYOUT_NO_MP_SUCC = 32
 LAYOUT_NO_EDGE_FILTER = 64
+LAYOUT_ADJ8 = 128
 
 HAS_WIDE_ALIAS = 1
 HAS_ADJ = 2
 HAS_MP_SUCC = 4
 HAS_LABEL_INDEX = 8
+HAS_ADJ8 = 128
 HAS_SEARCH_INDEX = 16
 HAS_EDGE_HASH = 32
 HAS_EDGE_FILTER = 64

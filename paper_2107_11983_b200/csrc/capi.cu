@@ -497,8 +497,17 @@ void setup_session(Session& s, const wf_exec_options* opts, const Session* table
     WF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.g->device));
     const uint64_t compact = 4 * E + 8ull * s.g->V;
     const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
-    if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b)
+    // The packed 8 B adjacency (dst, degree, base) when it fits 64 bits: O-REJ
+    // trials by default on graphs small enough to skip the 16 B form
+    // (Node2Vec s20: 20.7 -> 22.6 G steps/s); NAIVE only on request — PPR's
+    // L2-resident vertex words + neighbours beat it (C2: 19.6 vs 18.0).
+    const bool adj8_wanted = (lf & WF_LAYOUT_ADJ8) || (s.kind == WF_SAMPLER_OREJ && !adj_pays);
+    if (s.flow == kDirect && !(lf & WF_LAYOUT_NO_ADJ) && adj8_wanted && 8 * E + reserve <= free_b &&
+        s.build_adjacency8(nullptr)) {
+        // one 8 B load per move / trial carries the next vertex's word
+    } else if (s.flow == kDirect && adj_pays && !(lf & WF_LAYOUT_NO_ADJ) && 16 * E + reserve <= free_b) {
         s.build_adjacency(nullptr);
+    }
     if (s.desc.kind == WF_PROGRAM_METAPATH && s.kind == WF_SAMPLER_ITS) {
         s.g->ensure_label_index(nullptr);
         WF_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -580,6 +589,7 @@ int wf_session_layout(const wf_session* sh, uint32_t* flags) {
         uint32_t f = 0;
         if (s.alias_wide) f |= WF_LAYOUT_HAS_WIDE_ALIAS;
         if (s.adj.get()) f |= WF_LAYOUT_HAS_ADJ;
+        if (s.adj8.get()) f |= WF_LAYOUT_HAS_ADJ8;
         if (s.mp_adj.get()) f |= WF_LAYOUT_HAS_MP_SUCC;
         if (s.use_edge_filter) f |= WF_LAYOUT_HAS_EDGE_FILTER;
         if (s.desc.kind == WF_PROGRAM_METAPATH && s.g->label_index_built) f |= WF_LAYOUT_HAS_LABEL_INDEX;

@@ -133,6 +133,8 @@ struct Session {
     bool use_edge_hash = false;  // Node2Vec distance test through the graph's edge hash set
     bool use_edge_filter = false;  // ... behind the graph's pair pre-filter
     DeviceBuffer<uint4> adj;     // Direct flows: decorated adjacency {dst, 0, word}
+    DeviceBuffer<unsigned long long> adj8;  // ... packed in 8 B when (dst, deg, base) fit
+    uint32_t adj8_vbits = 0, adj8_dbits = 0;
     DeviceBuffer<uint4> mp_adj;  // MetaPath: partitioned edges decorated with the next group
 
     void build_tables(cudaStream_t st);
@@ -140,6 +142,8 @@ struct Session {
     // (multi-device runs: peer copies instead of a rebuild)
     void copy_tables_from(const Session& src, cudaStream_t st);
     void build_adjacency(cudaStream_t st);
+    // the packed form; false when (dst, degree, base) do not fit 64 bits
+    bool build_adjacency8(cudaStream_t st);
     // MetaPath with a schema whose successor label is a function of the label
     // (e.g. cyclic): returns false (no table) otherwise.
     bool build_metapath_successors(cudaStream_t st);

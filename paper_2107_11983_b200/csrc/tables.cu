@@ -334,6 +334,19 @@ __global__ void k_decorate_alias(uint4* __restrict__ bucket, uint64_t E,
     }
 }
 
+// Packed decorated adjacency: dst | deg << vbits | base << (vbits + dbits).
+__global__ void k_decorate_adj8(const uint32_t* __restrict__ nbr, uint64_t E, const uint64_t* __restrict__ vword,
+                                const uint64_t* __restrict__ off, uint32_t vbits, uint32_t dbits,
+                                unsigned long long* __restrict__ adj8) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = nbr[e];
+        const uint64_t base = off[d];
+        const uint64_t deg = off[d + 1] - base;
+        adj8[e] = d | (deg << vbits) | (base << (vbits + dbits));
+    }
+}
+
 // Decorated adjacency for Direct flows (NAIVE / O-REJ): {dst, 0, word(dst)}.
 __global__ void k_decorate_adj(const uint32_t* __restrict__ nbr, uint64_t E,
                                const uint64_t* __restrict__ vword, uint4* __restrict__ adj) {
@@ -531,6 +544,31 @@ bool Session::build_metapath_successors(cudaStream_t st) {
                                                   mp_adj.get());
     WF_LAUNCHED();
     WF_CUDA(cudaStreamSynchronize(st));
+    preprocess_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return true;
+}
+
+bool Session::build_adjacency8(cudaStream_t st) {
+    GraphStore& gs = *g;
+    auto bits = [](uint64_t x) {  // bits to hold values 0..x
+        uint32_t b = 1;
+        while (b < 64 && (x >> b) != 0) ++b;
+        return b;
+    };
+    const uint32_t vb = bits(gs.V - 1), db = bits(gs.max_degree), bb = bits(gs.E);
+    if (vb + db + bb > 64 || gs.max_degree >= kDegEscape || gs.E >= (1ull << 40)) return false;
+    DeviceGuard guard(gs.device);
+    auto t0 = std::chrono::steady_clock::now();
+    adj8.allocate(gs.E + 4);
+    if (gs.E) {
+        int blocks = std::max(1, std::min<int>(static_cast<int>((gs.E + 255) / 256), sm_count(gs.device) * 32));
+        k_decorate_adj8<<<blocks, 256, 0, st>>>(gs.nbr.get(), gs.E, gs.vword.get(), gs.offsets.get(), vb, db,
+                                                adj8.get());
+        WF_LAUNCHED();
+    }
+    WF_CUDA(cudaStreamSynchronize(st));
+    adj8_vbits = vb;
+    adj8_dbits = db;
     preprocess_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return true;
 }

@@ -98,6 +98,9 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     L.alias_wide = s.alias_wide ? 1 : 0;
     L.alias_idx = s.alias_idx ? 1 : 0;
     L.adj = s.adj.get();
+    L.adj8 = s.adj8.get();
+    L.adj8_vbits = s.adj8_vbits;
+    L.adj8_dbits = s.adj8_dbits;
     L.mp_adj = s.mp_adj.get();
     if (stream) {
         L.tile_word = stream->tile_word;

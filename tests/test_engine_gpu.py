@@ -347,6 +347,10 @@ LAYOUT_CASES = [
      abi.HAS_LABEL_INDEX),
     ("metapath_default_succ", lambda: MetaPathProgram([i % 5 for i in range(40)]), 0,
      abi.HAS_MP_SUCC | abi.HAS_LABEL_INDEX),
+    ("ppr_adj8", lambda: PprProgram(0.15), abi.LAYOUT_ADJ8, abi.HAS_ADJ8),
+    ("node2vec_adj8", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_ADJ8,
+     abi.HAS_ADJ8 | abi.HAS_EDGE_HASH | abi.HAS_EDGE_FILTER),
+    ("node2vec_w_adj8", lambda: Node2VecProgram(0.5, 3.0, 30, True), abi.LAYOUT_ADJ8, abi.HAS_ADJ8),
 ]
 
 
