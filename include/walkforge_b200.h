@@ -112,13 +112,15 @@ typedef struct wf_exec_options {
 
 /* Decorated layouts trade HBM capacity for one fewer dependent random load per
  * move; they are used automatically when memory allows unless opted out. */
-#define WF_LAYOUT_COMPACT_ALIAS 1u /* 16 B alias buckets (no destination vertex words) */
+#define WF_LAYOUT_COMPACT_ALIAS 1u /* 16 B alias buckets (no destination vertex words); the default
+                                      while buckets + vertex words fit twice the L2 */
 #define WF_LAYOUT_NO_ADJ 2u        /* no decorated adjacency for NAIVE / O-REJ */
 #define WF_LAYOUT_MP_SUCC 4u       /* MetaPath successor-decorated edges (cyclic schemas; default when HBM allows) */
 #define WF_LAYOUT_FORCE_ADJ 8u     /* decorated adjacency even when the compact graph fits L2 */
 #define WF_LAYOUT_SEARCH_TREE 16u  /* Node2Vec: sector B-tree instead of the edge hash set */
 #define WF_LAYOUT_NO_MP_SUCC 32u   /* MetaPath: label records + partitioned neighbours only */
 #define WF_LAYOUT_NO_EDGE_FILTER 64u /* Node2Vec: no pair pre-filter before the exact distance test */
+#define WF_LAYOUT_WIDE_ALIAS 256u    /* 32 B alias buckets even when the compact form fits the L2 */
 #define WF_LAYOUT_ADJ8 128u          /* NAIVE too: adjacency packed as (dst, degree, base) in 8 B where it fits
                                         (O-REJ uses it by default on graphs below the 16 B form's threshold) */
 

@@ -158,6 +158,7 @@ LAYOUT_SEARCH_TREE = 16
 LAYOUT_NO_MP_SUCC = 32
 LAYOUT_NO_EDGE_FILTER = 64
 LAYOUT_ADJ8 = 128
+LAYOUT_WIDE_ALIAS = 256
 
 HAS_WIDE_ALIAS = 1
 HAS_ADJ = 2

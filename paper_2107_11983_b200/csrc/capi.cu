@@ -481,10 +481,18 @@ void setup_session(Session& s, const wf_exec_options* opts, const Session* table
     const uint64_t reserve = 8ull << 30;
     const uint64_t E = s.g->E;
     const uint32_t lf = opts ? opts->layout_flags : 0;
+    int l2 = 0;
+    WF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.g->device));
     // a custom program's update() reads the traversed edge: its buckets carry
     // edge positions (compact), the destination is read from the CSR
     s.alias_idx = s.custom != nullptr;
-    if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS && !(lf & WF_LAYOUT_COMPACT_ALIAS) && !s.alias_idx)
+    // Wide 32 B buckets (carrying the destinations' vertex words: one random
+    // request per move) pay once the compact form (16 B buckets + vertex
+    // words) outgrows the L2; below that its L2 hits win (C1, s16: 44.8 vs
+    // 38.3 G steps/s compact vs wide; C5, s26: wide).
+    const bool wide_pays = 16 * E + 8ull * s.g->V > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_WIDE_ALIAS);
+    if (s.flow == kTables && s.kind == WF_SAMPLER_ALIAS && !(lf & WF_LAYOUT_COMPACT_ALIAS) && !s.alias_idx &&
+        wide_pays)
         s.alias_wide = 32 * E + reserve <= free_b;
     if (s.flow == kTables) {
         if (tables_from) s.copy_tables_from(*tables_from, nullptr);
@@ -493,8 +501,6 @@ void setup_session(Session& s, const wf_exec_options* opts, const Session* table
     // The decorated adjacency saves the dependent vertex-word load but is 4x
     // the neighbour array: when the compact graph (neighbours + vertex
     // words) is near L2 size, its L2 hits win (C2: 12.8 vs 11.3 G moves/s).
-    int l2 = 0;
-    WF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s.g->device));
     const uint64_t compact = 4 * E + 8ull * s.g->V;
     const bool adj_pays = compact > 2ull * static_cast<uint64_t>(l2) || (lf & WF_LAYOUT_FORCE_ADJ);
     // The packed 8 B adjacency (dst, degree, base) when it fits 64 bits: O-REJ

@@ -322,7 +322,8 @@ def test_has_edge_matches_reference(rmat12):
 
 LAYOUT_CASES = [
     ("deepwalk_compact_alias", lambda: DeepWalkProgram(40, True), abi.LAYOUT_COMPACT_ALIAS, 0),
-    ("deepwalk_wide_alias", lambda: DeepWalkProgram(40, True), 0, abi.HAS_WIDE_ALIAS),
+    ("deepwalk_wide_alias", lambda: DeepWalkProgram(40, True), abi.LAYOUT_WIDE_ALIAS, abi.HAS_WIDE_ALIAS),
+    ("deepwalk_default_alias", lambda: DeepWalkProgram(40, True), 0, 0),  # small graph: compact
     ("ppr_adj", lambda: PprProgram(0.2), abi.LAYOUT_FORCE_ADJ, abi.HAS_ADJ),
     ("ppr_no_adj", lambda: PprProgram(0.2), abi.LAYOUT_NO_ADJ, 0),
     ("node2vec_adj", lambda: Node2VecProgram(2.0, 0.5, 40, False), abi.LAYOUT_FORCE_ADJ,
