@@ -121,6 +121,7 @@ struct WalkLaunch {
     int* error_word;
     double* scratch;  // gathered ALIAS: per-warp weights + park areas for hub steps
     uint64_t scratch_stride;  // doubles per warp area (>= max degree)
+    double* lane_rows;        // gathered ALIAS: per-lane rows (2 x kLaneRow doubles) for hubs up to kLaneRow
     int use_label_index;
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
@@ -171,9 +172,17 @@ struct Walker {
     // (coop_step) for a hub vertex, consumed by move(); kCoopNone otherwise
     uint8_t coop;
     uint32_t coop_pick;
+    uint64_t coop_k;  // gathered ALIAS: the step's second draw, for the lane's own Vose replay
 };
 
-enum CoopState : uint8_t { kCoopNone = 0, kCoopPick = 1, kCoopDead = 2, kCoopFault = 3 };
+// kCoopVose: the warp filled this lane's row with the hub's scaled weights and
+// the owner drew (x, y); the lane replays Vose's worklists on its own row
+enum CoopState : uint8_t { kCoopNone = 0, kCoopPick = 1, kCoopDead = 2, kCoopFault = 3, kCoopVose = 4 };
+
+// Hubs up to this degree get their Vose replay in the owner lane, on a row of
+// its own, so the lanes of a warp replay their hubs in parallel; larger ones
+// are replayed by the whole warp on its warp row (vose_bucket_warp).
+constexpr uint32_t kLaneRow = 4096;
 
 // ---- graph helpers -------------------------------------------------------------
 
@@ -498,7 +507,7 @@ constexpr int kCustomProgram = -1;
 // Version of the launch record's meaning (WalkLaunch fields, scratch layout,
 // program adapter): a user program library compiled against another value is
 // refused at wf_session_create_custom (its kernels would misread the launch).
-constexpr uint32_t kEngineAbi = 3;
+constexpr uint32_t kEngineAbi = 4;
 
 template <int K>
 struct Program;
@@ -1138,7 +1147,7 @@ __device__ __forceinline__ int quantum_exp(double w) {
 }
 
 template <class P, int S>
-__device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int leader, double* wrow) {
+__device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int leader, double* wrow_warp) {
     const int lane = threadIdx.x & 31;
     Walker h = q;  // the owner's walker, as every lane sees it
     h.row = __shfl_sync(kFull, q.row, leader);
@@ -1151,6 +1160,14 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
     h.len = __shfl_sync(kFull, q.len, leader);
     const uint32_t d = h.cur_deg;
     const uint64_t base = h.cur_base;
+    // ALIAS: the owner's own row when the hub fits it (replayed per lane
+    // afterwards), else the warp's row (replayed by the warp now)
+    const bool lane_vose = S == WF_SAMPLER_ALIAS && L.lane_rows != nullptr && d <= kLaneRow;
+    double* wrow = wrow_warp;
+    if (lane_vose) {
+        const uint64_t owner = (blockIdx.x * static_cast<uint64_t>(kBlock) + (threadIdx.x & ~31u)) + leader;
+        wrow = L.lane_rows + owner * (2ull * kLaneRow);
+    }
     if (L.g.stats && lane == leader) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
     // pass 1: weights, validity, partial sums, max, smallest quantum
     double lsum = 0.0, lmax = 0.0;
@@ -1160,7 +1177,7 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
     for (uint32_t i = lane; i < d; i += 32) {
         const double w = P::weight(L, h, base + i);
         if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
-        if (S == WF_SAMPLER_ALIAS) wrow[i] = w;
+        if (S == WF_SAMPLER_ALIAS || (S == WF_SAMPLER_ITS && wrow)) wrow[i] = w;
         if (w > 0.0) qexp = min(qexp, quantum_exp(w));
         lsum += w;
         lmax = w > lmax ? w : lmax;
@@ -1193,9 +1210,12 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         // pass 2: first i with x < cumulative[i] (engine.hpp:373-377)
         double running = 0.0;
         uint32_t pick = d - 1;
+        if (wrow) __syncwarp();  // pass 1's weights are in the row
         for (uint32_t c = 0; c < d; c += 32) {
             const uint32_t i = c + lane;
-            double v = i < d ? P::weight(L, h, base + i) : 0.0;
+            // the weights from pass 1 (an adjacency test each for Node2Vec)
+            // when the launch has warp rows, else evaluated again
+            double v = i < d ? (wrow ? wrow[i] : P::weight(L, h, base + i)) : 0.0;
             for (int o = 1; o < 32; o <<= 1) {  // inclusive scan (exact)
                 const double u = __shfl_up_sync(kFull, v, o);
                 if (lane >= o) v += u;
@@ -1211,6 +1231,7 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
             q.coop = kCoopPick;
             q.coop_pick = pick;
         }
+        if (wrow) __syncwarp();  // the row is free for the next hub
     } else if constexpr (S == WF_SAMPLER_ALIAS) {
         __syncwarp();  // the scratch row is complete
         double total = sum;
@@ -1229,6 +1250,15 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         if (lane == leader) {
             x = q.rng.index(d);
             k = q.rng.bits53();
+        }
+        if (lane_vose) {  // the owner replays on its own row after the hub loop
+            if (lane == leader) {
+                q.coop = kCoopVose;
+                q.coop_pick = x;
+                q.coop_k = k;
+            }
+            __syncwarp();
+            return;
         }
         x = __shfl_sync(kFull, x, leader);
         double split;
@@ -1525,6 +1555,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
     q.pend = false;
     q.coop = kCoopNone;
     q.coop_pick = 0;
+    q.coop_k = 0;
     bool active = false;
     bool fresh = false;
     bool drained = false;
@@ -1687,6 +1718,20 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
                     const int leader = __ffs(hubs) - 1;
                     hubs &= hubs - 1;
                     coop_step<P, S>(L, q, leader, wrow);
+                }
+                if constexpr (S == WF_SAMPLER_ALIAS) {
+                    // the lanes whose hub fitted their own row replay Vose's
+                    // worklists on it, all at once
+                    if (q.coop == kCoopVose) {
+                        const double* row = L.lane_rows +
+                                            (blockIdx.x * static_cast<uint64_t>(kBlock) + threadIdx.x) * (2ull * kLaneRow);
+                        double split;
+                        uint32_t second;
+                        vose_bucket_scaled(q.cur_deg, [&](uint32_t i) { return row[i]; }, q.coop_pick,
+                                           const_cast<double*>(row) + kLaneRow, split, second);
+                        q.coop_pick = q.coop_k < unit_threshold(split) ? q.coop_pick : second;
+                        q.coop = kCoopPick;
+                    }
                 }
             }
         }
