@@ -1375,34 +1375,46 @@ __device__ __forceinline__ uint32_t source_at(const WalkLaunch& L, uint64_t qid)
     return __ldg(L.qsources + qid);
 }
 
-// Path rows are written a full 32 B sector at a time: each lane stages its
-// next 8 vertices in shared memory ([slot][thread], conflict-free) and stores
-// them with one 256-bit store when the group fills or the walk ends.
+// Path rows are written whole 32 B sectors at a time: each lane stages its
+// next kPathGroup vertices in shared memory ([slot][thread], conflict-free)
+// and stores them with 256-bit stores when the group fills or the walk ends.
 // Single 4 B stores to 32 B-strided rows made every step a partial-sector
 // write (ncu: 4x the algorithmic DRAM write bytes).  Used when rows are
 // 32 B-aligned (stride % 8 == 0); otherwise one 4 B store per vertex.
+#ifndef WF_PATH_GROUP
+#define WF_PATH_GROUP 8
+#endif
+constexpr uint32_t kPathGroup = WF_PATH_GROUP;  // 8, 16 or 32 vertices
 struct PathStage {
-    uint32_t* s;  // kBlock * 8 words
+    uint32_t* s;  // kBlock * kPathGroup words
     __device__ __forceinline__ uint32_t& at(uint32_t slot) { return s[slot * kBlock + threadIdx.x]; }
 };
 
-// One 256-bit store (st.global.v8, sm_100) of a lane's staged 8-word group.
-__device__ __forceinline__ void store_group(uint32_t* dst, PathStage ps) {
+// One 256-bit store (st.global.v8, sm_100) of staged words [8k, 8k + 8).
+__device__ __forceinline__ void store_sector(uint32_t* dst, PathStage ps, uint32_t k) {
+    const uint32_t b = 8 * k;
 #ifdef WF_PATH_EVICT_LAST
     // experiment: evict-last L2 policy on the path sectors (their line fills
     // over four groups)
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("st.global.L2::cache_hint.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(dst),
-                 "r"(ps.at(0)), "r"(ps.at(1)), "r"(ps.at(2)), "r"(ps.at(3)), "r"(ps.at(4)), "r"(ps.at(5)),
-                 "r"(ps.at(6)), "r"(ps.at(7)), "l"(pol)
+    asm volatile("st.global.L2::cache_hint.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(dst + b),
+                 "r"(ps.at(b)), "r"(ps.at(b + 1)), "r"(ps.at(b + 2)), "r"(ps.at(b + 3)), "r"(ps.at(b + 4)),
+                 "r"(ps.at(b + 5)), "r"(ps.at(b + 6)), "r"(ps.at(b + 7)), "l"(pol)
                  : "memory");
     return;
 #endif
-    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(ps.at(0)),
-                 "r"(ps.at(1)), "r"(ps.at(2)), "r"(ps.at(3)), "r"(ps.at(4)), "r"(ps.at(5)), "r"(ps.at(6)),
-                 "r"(ps.at(7))
+    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + b), "r"(ps.at(b)),
+                 "r"(ps.at(b + 1)), "r"(ps.at(b + 2)), "r"(ps.at(b + 3)), "r"(ps.at(b + 4)), "r"(ps.at(b + 5)),
+                 "r"(ps.at(b + 6)), "r"(ps.at(b + 7))
                  : "memory");
+}
+
+// The first `nsec` sectors of a lane's staged group.
+__device__ __forceinline__ void store_group(uint32_t* dst, PathStage ps, uint32_t nsec = kPathGroup / 8) {
+#pragma unroll
+    for (uint32_t k = 0; k < kPathGroup / 8; ++k)
+        if (k < nsec) store_sector(dst, ps, k);
 }
 
 __device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int st, PathStage ps) {
@@ -1418,10 +1430,11 @@ __device__ __forceinline__ void finish(const WalkLaunch& L, const Walker& q, int
 #endif
     L.status[q.row] = static_cast<uint8_t>(st);
     if (L.staged) {
-        // the open group as one whole-sector store (words past the length are
+        // the open group as whole-sector stores (words past the length are
         // unspecified row padding, as the rest of the row)
-        const uint32_t g0 = q.len & ~7u;
-        if (g0 < min(q.len, L.stride)) store_group(L.paths + q.row * L.stride + g0, ps);
+        const uint32_t g0 = q.len & ~(kPathGroup - 1);
+        const uint32_t end = min(q.len, L.stride);
+        if (g0 < end) store_group(L.paths + q.row * L.stride + g0, ps, (end - g0 + 7) / 8);
     }
     if (q.len > L.stride) atomicAdd(L.overflow_out, 1ULL);
 }
@@ -1486,8 +1499,9 @@ __device__ __forceinline__ void emit(const WalkLaunch& L, const Walker& q, uint3
                                      PathStage ps) {
     if (p < L.stride) {
         if (L.staged) {
-            ps.at(p & 7) = v;
-            if ((p & 7) == 7) store_group(L.paths + q.row * L.stride + (p - 7), ps);
+            const uint32_t slot = p & (kPathGroup - 1);
+            ps.at(slot) = v;
+            if (slot == kPathGroup - 1) store_group(L.paths + q.row * L.stride + (p - slot), ps);
         } else {
             L.paths[q.row * L.stride + p] = v;
         }
@@ -1541,7 +1555,7 @@ constexpr uint32_t kClaim = WF_CLAIM;
 template <class P, int S, int F, bool ST>
 __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kernel(const WalkLaunch L) {
     const int lane = threadIdx.x & 31;
-    __shared__ uint32_t stage_words[8 * kBlock];
+    __shared__ uint32_t stage_words[kPathGroup * kBlock];
     PathStage ps{stage_words};
     Walker q;
     q.row = 0;

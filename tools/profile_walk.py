@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--tune", action="store_true", help="run the launch tuner first (wf_session_tune)")
     ap.add_argument("--graph", action="store_true", help="replay the launch as a captured CUDA graph")
     ap.add_argument("--flush", action="store_true", help="write 256 MiB between launches (cold L2, as bench.py)")
+    ap.add_argument("--stride", type=int, default=0, help="path row stride override (vertices)")
     args = ap.parse_args()
     import torch
 
@@ -43,7 +44,7 @@ def main():
         cfg["n_queries"] = args.queries
     spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
     n = hi - lo
-    stride = bench.row_capacity(cfg)
+    stride = args.stride or bench.row_capacity(cfg)
     d_src = torch.from_numpy(spec.sources.view("int32")).cuda()
     paths = torch.empty(n * stride, dtype=torch.int32, device="cuda")
     lens = torch.empty(n, dtype=torch.int32, device="cuda")
