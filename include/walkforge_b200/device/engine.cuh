@@ -1146,6 +1146,102 @@ __device__ __forceinline__ int quantum_exp(double w) {
     return (e ? e : 1) - 1075 + __ffsll(static_cast<long long>(m)) - 1;
 }
 
+// Node2Vec's gathered weights over a hub by a warp-wide merge of the sorted
+// neighbour lists.  Every weight out of cur needs "is dst a neighbour of prev"
+// (algorithms.hpp:103-119): over all of N(cur) that is the intersection
+// N(cur) ∩ N(prev).  One adjacency test per edge is d random requests (a
+// filter sector, then a hash bucket for ~6 %), and a warp waits for its
+// slowest lane every round; the merge instead streams both lists in order,
+// 128 entries at a time (coalesced loads), and each lane binary-searches its
+// four cur-neighbours in the window of prev's list staged in shared memory.
+// Same membership answers as Graph::has_edge on sorted adjacency (duplicates
+// included), so the same weights, sums and draws.  Used when both lists are
+// sorted and prev's list is at most kMergeRatio times cur's (else the per-edge
+// tests read less).
+constexpr uint32_t kMergeWin = 128;
+constexpr uint32_t kMergeRatio = 8;
+
+template <class F>
+__device__ __forceinline__ void n2v_merge_weights(const WalkLaunch& L, const Walker& h, F&& emit) {
+    __shared__ uint32_t merge_win[kBlock / 32][kMergeWin];
+    constexpr uint32_t kPer = kMergeWin / 32;
+    const int lane = threadIdx.x & 31;
+    uint32_t* win = merge_win[threadIdx.x >> 5];
+    const uint32_t* A = L.g.nbr + h.cur_base;
+    const uint32_t* B = L.g.nbr + h.prev_base;
+    const uint32_t d = h.cur_deg, dp = h.prev_deg;
+    constexpr uint32_t kPast = 0xFFFFFFFFu;  // above every vertex id
+    // the next window of prev's list and the next block of cur's are loaded
+    // one step ahead (registers), so their round trips overlap the searches
+    uint32_t bn[kPer], an[kPer];
+    auto fetch_b = [&](uint32_t at) {
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            const uint32_t i = at + lane + 32 * k;
+            bn[k] = i < dp ? __ldg(B + i) : kPast;
+        }
+    };
+    auto fetch_a = [&](uint32_t at) {
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            const uint32_t i = at + lane + 32 * k;
+            an[k] = i < d ? __ldg(A + i) : 0u;
+        }
+    };
+    uint32_t ib = 0;
+    auto next_window = [&]() {  // bn -> the window; prefetch the one after it
+        __syncwarp();
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) win[lane + 32 * k] = bn[k];
+        __syncwarp();
+        fetch_b(ib + kMergeWin);  // past the end: kPast, which closes any block
+    };
+    fetch_b(0);
+    fetch_a(0);
+    next_window();
+    uint32_t bmax = win[kMergeWin - 1];
+    unsigned long long windows = 1;
+    for (uint32_t ia = 0; ia < d; ia += kMergeWin) {
+        uint32_t a[kPer];
+        bool found[kPer];
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            a[k] = an[k];
+            found[k] = false;
+        }
+        // the block's largest entry (its last): lane off % 32, slot off / 32
+        const uint32_t off = min(ia + kMergeWin, d) - 1 - ia;
+        uint32_t mine = a[0];
+#pragma unroll
+        for (uint32_t k = 1; k < kPer; ++k) mine = k == off / 32 ? a[k] : mine;
+        const uint32_t amax = __shfl_sync(kFull, mine, off & 31);
+        if (ia + kMergeWin < d) fetch_a(ia + kMergeWin);
+        for (;;) {
+#pragma unroll
+            for (uint32_t k = 0; k < kPer; ++k) {
+                uint32_t lo = 0;  // lower_bound of a[k] in the window
+#pragma unroll
+                for (uint32_t s = kMergeWin / 2; s > 0; s >>= 1) lo = win[lo + s - 1] < a[k] ? lo + s : lo;
+                found[k] = found[k] || (lo < kMergeWin && win[lo] == a[k]);
+            }
+            // prev's entries past this window are >= bmax: the block is done
+            // once the window reaches its largest value
+            if (bmax >= amax) break;
+            ib += kMergeWin;
+            next_window();
+            bmax = win[kMergeWin - 1];
+            ++windows;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            const uint32_t i = ia + lane + 32 * k;
+            if (i < d) emit(i, a[k], found[k]);
+        }
+    }
+    if (L.g.stats && lane == 0)  // instrumented runs: sectors of prev's list streamed
+        atomicAdd(L.g.stats + 1, windows * (kMergeWin * 4 / 32));
+}
+
 template <class P, int S>
 __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int leader, double* wrow_warp) {
     const int lane = threadIdx.x & 31;
@@ -1173,14 +1269,32 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
     double lsum = 0.0, lmax = 0.0;
     int qexp = 0x7FFFFFFF;
     bool bad = false;
+    bool merged = false;
+    if constexpr (P::kind == WF_PROGRAM_NODE2VEC) {
+        if (h.len > 1 && L.g.sorted && h.prev_deg <= kMergeRatio * d) {
+            const ProgParams& p = L.prog;
+            n2v_merge_weights(L, h, [&](uint32_t i, uint32_t dst, bool common) {
+                double w = dst == h.prev ? p.inv_a : common ? 1.0 : p.inv_b;
+                if (p.weighted) w = __dmul_rn(w, edge_weight(L.g, base + i));
+                if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
+                if (S == WF_SAMPLER_ALIAS || (S == WF_SAMPLER_ITS && wrow)) wrow[i] = w;
+                if (w > 0.0) qexp = min(qexp, quantum_exp(w));
+                lsum += w;
+                lmax = w > lmax ? w : lmax;
+            });
+            merged = true;
+        }
+    }
+    if (!merged) {
 #pragma unroll 4
-    for (uint32_t i = lane; i < d; i += 32) {
-        const double w = P::weight(L, h, base + i);
-        if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
-        if (S == WF_SAMPLER_ALIAS || (S == WF_SAMPLER_ITS && wrow)) wrow[i] = w;
-        if (w > 0.0) qexp = min(qexp, quantum_exp(w));
-        lsum += w;
-        lmax = w > lmax ? w : lmax;
+        for (uint32_t i = lane; i < d; i += 32) {
+            const double w = P::weight(L, h, base + i);
+            if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
+            if (S == WF_SAMPLER_ALIAS || (S == WF_SAMPLER_ITS && wrow)) wrow[i] = w;
+            if (w > 0.0) qexp = min(qexp, quantum_exp(w));
+            lsum += w;
+            lmax = w > lmax ? w : lmax;
+        }
     }
     if (__any_sync(kFull, bad)) {  // check_program_weight (engine.hpp:97-101)
         if (lane == leader) {
@@ -1211,11 +1325,40 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         double running = 0.0;
         uint32_t pick = d - 1;
         if (wrow) __syncwarp();  // pass 1's weights are in the row
-        for (uint32_t c = 0; c < d; c += 32) {
+        // with the row: four 32-weight rounds loaded at once, so a hub's scan
+        // waits on one load round trip per 128 weights instead of per 32
+        constexpr uint32_t kG = 4;
+        for (uint32_t c0 = 0; wrow && c0 < d; c0 += 32 * kG) {
+            double v[kG];
+#pragma unroll
+            for (uint32_t k = 0; k < kG; ++k) {
+                const uint32_t i = c0 + 32 * k + lane;
+                v[k] = i < d ? wrow[i] : 0.0;
+            }
+            bool hit_any = false;
+#pragma unroll
+            for (uint32_t k = 0; k < kG; ++k) {
+                const uint32_t c = c0 + 32 * k;
+                if (c >= d) break;
+                double s = v[k];
+                for (int o = 1; o < 32; o <<= 1) {  // inclusive scan (exact)
+                    const double u = __shfl_up_sync(kFull, s, o);
+                    if (lane >= o) s += u;
+                }
+                const unsigned hit = __ballot_sync(kFull, c + lane < d && x < running + s);
+                if (hit) {
+                    pick = c + __ffs(hit) - 1;
+                    hit_any = true;
+                    break;
+                }
+                running += __shfl_sync(kFull, s, 31);
+            }
+            if (hit_any) break;
+        }
+        for (uint32_t c = 0; !wrow && c < d; c += 32) {
             const uint32_t i = c + lane;
-            // the weights from pass 1 (an adjacency test each for Node2Vec)
-            // when the launch has warp rows, else evaluated again
-            double v = i < d ? (wrow ? wrow[i] : P::weight(L, h, base + i)) : 0.0;
+            // no row (pass 1's weights were not kept): evaluated again
+            double v = i < d ? P::weight(L, h, base + i) : 0.0;
             for (int o = 1; o < 32; o <<= 1) {  // inclusive scan (exact)
                 const double u = __shfl_up_sync(kFull, v, o);
                 if (lane >= o) v += u;

@@ -123,3 +123,43 @@ def test_static_tables_hub_warps_bit_exact(f64):
             assert np.array_equal(got["its"], want["its"])
         else:
             assert np.array_equal(got["rej_p_star"], want["rej_p_star"])
+
+
+def _merge_graph(weighted):
+    """Sorted adjacency with multi-edges and self-loops: hubs of 200-3000
+    edges (several 128-entry merge windows), mid vertices of 32-120 edges
+    whose previous vertex is a hub more than 8x larger (the per-edge test
+    path) or comparable (the merge path), and light vertices below 32."""
+    rng = np.random.default_rng(21)
+    V = 2500
+    deg = np.where(np.arange(V) < 12, rng.integers(200, 3000, V),
+                   np.where(np.arange(V) < 400, rng.integers(32, 120, V), rng.integers(1, 31, V)))
+    lists = []
+    for v in range(V):
+        d = int(deg[v])
+        # half the picks among the hubs and mid vertices (shared neighbourhoods), repeats allowed
+        pool = np.where(rng.random(d) < 0.5, rng.integers(0, 400, d), rng.integers(0, V, d))
+        if v % 7 == 0:
+            pool[0] = v  # self-loop
+        lists.append(np.sort(pool))
+    off = np.concatenate([[0], np.cumsum([len(x) for x in lists])]).astype(np.uint64)
+    nbr = np.concatenate(lists).astype(np.uint32)
+    w = (rng.integers(1, 9, nbr.size) * 0.5).astype(np.float32) if weighted else None
+    return Graph(off, nbr, w)
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("sampler", GATHERED)
+def test_node2vec_merge_intersection_matches_reference(weighted, sampler):
+    """Node2Vec hub gathers take the warp merge of N(cur) and N(prev)
+    (n2v_merge_weights) on sorted adjacency: duplicates, self-loops, window
+    boundaries and the fallback to per-edge tests must all give the
+    reference's walks."""
+    hg = _merge_graph(weighted)
+    dg = E.DeviceGraph.from_host(hg)
+    assert dg.info()["sorted"]
+    rg = RefOracle().graph(hg)
+    prog = Node2VecProgram(0.5, 2.0, 40, weighted)
+    opts = ExecOptions(seed=31, sampler=int(sampler))
+    spec = QuerySpec.one_per_vertex()
+    same(E.run_sequential(dg, spec, prog, opts), rg.run(spec, prog, opts))
