@@ -121,7 +121,6 @@ struct WalkLaunch {
     int* error_word;
     double* scratch;  // gathered ALIAS: per-warp weights + park areas for hub steps
     uint64_t scratch_stride;  // doubles per warp area (>= max degree)
-    double* lane_rows;        // gathered ALIAS: per-lane rows (2 x kLaneRow doubles) for hubs up to kLaneRow
     int use_label_index;
     int staged;  // rows 32 B-aligned: sector-sized path stores (PathStage)
     int alias_wide;                   // alias buckets are 32 B (2 x uint4) with dst vertex words
@@ -172,17 +171,9 @@ struct Walker {
     // (coop_step) for a hub vertex, consumed by move(); kCoopNone otherwise
     uint8_t coop;
     uint32_t coop_pick;
-    uint64_t coop_k;  // gathered ALIAS: the step's second draw, for the lane's own Vose replay
 };
 
-// kCoopVose: the warp filled this lane's row with the hub's scaled weights and
-// the owner drew (x, y); the lane replays Vose's worklists on its own row
-enum CoopState : uint8_t { kCoopNone = 0, kCoopPick = 1, kCoopDead = 2, kCoopFault = 3, kCoopVose = 4 };
-
-// Hubs up to this degree get their Vose replay in the owner lane, on a row of
-// its own, so the lanes of a warp replay their hubs in parallel; larger ones
-// are replayed by the whole warp on its warp row (vose_bucket_warp).
-constexpr uint32_t kLaneRow = 4096;
+enum CoopState : uint8_t { kCoopNone = 0, kCoopPick = 1, kCoopDead = 2, kCoopFault = 3 };
 
 // ---- graph helpers -------------------------------------------------------------
 
@@ -507,7 +498,7 @@ constexpr int kCustomProgram = -1;
 // Version of the launch record's meaning (WalkLaunch fields, scratch layout,
 // program adapter): a user program library compiled against another value is
 // refused at wf_session_create_custom (its kernels would misread the launch).
-constexpr uint32_t kEngineAbi = 4;
+constexpr uint32_t kEngineAbi = 5;
 
 template <int K>
 struct Program;
@@ -826,78 +817,142 @@ __device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double
     second_out = x;
 }
 
-// ---- Vose's worklists by a warp -------------------------------------------------
-// The replay of the FIFO worklists (vose_bucket_scaled) advances three
-// ascending cursors over the scaled weights; a lone lane doing that over a
-// hub's row waits an L2 round trip per element.  Here the whole warp scans 32
-// elements per step with a ballot and every lane carries the (uniform)
-// cursor state, so a cursor advance costs one coalesced load per 32 elements;
-// the pairing arithmetic (lval -= 1 - sval, order-dependent fp64) is the same
-// sequence as the reference's.
+// ---- Vose's worklists for a hub, by a warp ---------------------------------------
+// vose_bucket_scaled's replay for bucket x over a hub's weights (`row`, n
+// entries, summed to `total`), with the serial chain on one lane.  Vose's
+// pairing loop is an order-dependent fp64 chain (lval -= 1 - sval), so it
+// cannot be split; everything around it can.  The warp first turns the row
+// into scaled weights (w * n / total, sampler.hpp:97, one division each) and
+// compacts them: the smalls' values in index order to the front of `park`,
+// the larges' values to its back (the j-th large at park[n-1-j]), the larges'
+// indices over the row's front.  Lane 0 then runs the chain over 128-entry
+// batches the warp stages in shared memory — for the smalls their deficits
+// fl(1 - s), computed by the staging lanes (the same rounding as the chain's
+// own subtraction), so a pairing is one subtraction and one compare — and
+// writes each demoted large's final value over its own slot, where the
+// second phase (demoted larges consumed as smalls, in demotion order) reads
+// it.  Same pairing sequence as vose_bucket_scaled.  `row` is overwritten.
+constexpr uint32_t kVoseStage = 128;
 
-// First i in [from, n) whose value satisfies `pred`, and its value; n if none.
-template <class Pred>
-__device__ __forceinline__ uint32_t warp_find(const double* __restrict__ row, uint32_t from, uint32_t n, Pred pred,
-                                              double& val) {
+__device__ __forceinline__ void vose_bucket_staged(uint32_t n, double* __restrict__ row, double total, uint32_t x,
+                                                   double* __restrict__ park, double& split_out,
+                                                   uint32_t& second_out) {
+    __shared__ double vose_stage[kBlock / 32][2][kVoseStage];
     const int lane = threadIdx.x & 31;
-    for (uint32_t b = from; b < n; b += 32) {
-        const uint32_t i = b + lane;
-        const double v = i < n ? row[i] : 0.0;
-        const unsigned m = __ballot_sync(kFull, i < n && pred(v));
-        if (m) {
-            const int l = __ffs(m) - 1;
-            val = __shfl_sync(kFull, v, l);
-            return b + l;
+    double* tb = vose_stage[threadIdx.x >> 5][0];  // deficits: smalls (phase 1) / demoted larges (phase 2)
+    double* lb = vose_stage[threadIdx.x >> 5][1];  // larges' initial values
+    uint32_t* li = reinterpret_cast<uint32_t*>(row);
+    const unsigned lt = (1u << lane) - 1;
+    // 1. scaled weights, compacted; four 32-entry rounds per load batch
+    uint32_t ns = 0, nl = 0, xinfo = 0;  // x: small << 31 | rank among its class
+    for (uint32_t c0 = 0; c0 < n; c0 += 128) {
+        double v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t i = c0 + 32 * r + lane;
+            v[r] = i < n ? row[i] : 0.0;
+        }
+        __syncwarp();  // the batch is read before the large indices overwrite the row's front
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t i = c0 + 32 * r + lane;
+            const double sc = v[r] * n / total;
+            const bool valid = i < n, sm = valid && sc < 1.0;
+            const unsigned bs = __ballot_sync(kFull, sm), bl = __ballot_sync(kFull, valid && !sm);
+            const uint32_t rs = ns + __popc(bs & lt), rl = nl + __popc(bl & lt);
+            if (sm) {
+                park[rs] = sc;
+            } else if (valid) {
+                park[n - 1 - rl] = sc;
+                li[rl] = i;
+            }
+            if (i == x) xinfo = sm ? (0x80000000u | rs) : rl;
+            ns += __popc(bs);
+            nl += __popc(bl);
         }
     }
-    return n;
-}
-
-// vose_bucket_scaled for bucket x over `row` (scaled weights), by the whole
-// warp; `park` (n doubles) holds demoted larges' final values.  Every lane
-// returns the split and alias of bucket x.
-__device__ __forceinline__ void vose_bucket_warp(uint32_t n, const double* __restrict__ row, uint32_t x,
-                                                 double* __restrict__ park, double& split_out,
-                                                 uint32_t& second_out) {
-    const int lane = threadIdx.x & 31;
-    auto small = [](double v) { return v < 1.0; };
-    auto large = [](double v) { return v >= 1.0; };
-    double lval = 0.0, aval = 0.0, dummy = 0.0;
-    uint32_t lcur = warp_find(row, 0, n, large, lval);
-    uint32_t a = warp_find(row, 0, n, small, aval);
-    uint32_t c = 0, demoted = 0, consumed = 0;
-    while (lcur < n) {  // sampler.hpp:103-111
-        uint32_t sidx;
-        double sval;
-        if (a < n) {
-            sidx = a;
-            sval = aval;
-            a = warp_find(row, a + 1, n, small, aval);
-        } else if (consumed < demoted) {
-            c = warp_find(row, c, n, large, dummy);
-            sidx = c;
-            double pv = 0.0;
-            if (lane == 0) pv = park[c];  // written by lane 0 when demoted
-            sval = __shfl_sync(kFull, pv, 0);
-            ++c;
-            ++consumed;
-        } else {
-            break;
+    xinfo = __shfl_sync(kFull, xinfo, x & 31);
+    const bool xs = xinfo >> 31;
+    const uint32_t xr = xinfo & 0x7FFFFFFFu;
+    __syncwarp();
+    // 2. the chain (sampler.hpp:103-111), lane 0, batch by batch
+    uint32_t k = 0, j = 0, dq = 0;  // next small, head large, next demoted large to consume
+    uint32_t tbase = 0, tlen = 0, lbase = 0, llen = 0;
+    int tphase = 0;                 // what tb holds: 0 nothing, 1 smalls, 2 demoted larges
+    int phase = 1;
+    bool head_pending = true, done = nl == 0, found = false;
+    double lval = 0.0;
+    while (!done) {
+        // stage what lane 0 needs next (uniform decisions)
+        if (phase == 1 && k < ns && !(tphase == 1 && k < tbase + tlen)) {
+            tbase = k;
+            tlen = min(kVoseStage, ns - k);
+            for (uint32_t t = lane; t < tlen; t += 32) tb[t] = 1.0 - park[k + t];
+            tphase = 1;
+        } else if (phase == 2 && dq < j && !(tphase == 2 && dq < tbase + tlen)) {
+            tbase = dq;
+            tlen = min(kVoseStage, j - dq);
+            for (uint32_t t = lane; t < tlen; t += 32) tb[t] = 1.0 - park[n - 1 - (dq + t)];
+            tphase = 2;
         }
-        if (sidx == x) {
-            split_out = sval;
-            second_out = lcur;
-            return;
+        if (j < nl && !(j >= lbase && j < lbase + llen)) {
+            lbase = j;
+            llen = min(kVoseStage, nl - j);
+            for (uint32_t t = lane; t < llen; t += 32) lb[t] = park[n - 1 - (j + t)];
         }
-        lval -= 1.0 - sval;
-        if (lval < 1.0) {
-            if (lane == 0) park[lcur] = lval;
-            ++demoted;
-            lcur = warp_find(row, lcur + 1, n, large, lval);
+        __syncwarp();
+        if (lane == 0) {
+            if (head_pending) {
+                lval = lb[j - lbase];
+                head_pending = false;
+            }
+            // pairings until x, the batch's end or the larges' batch end
+            uint32_t& cur = phase == 1 ? k : dq;
+            const uint32_t stop_x = (phase == 1) == xs ? xr : 0xFFFFFFFFu;
+            const uint32_t stop = min(tbase + tlen, stop_x);
+            const uint32_t lend = lbase + llen;
+            bool out = false;
+            while (cur < stop) {
+                lval -= tb[cur - tbase];
+                ++cur;
+                if (lval < 1.0) {
+                    park[n - 1 - j] = lval;  // the demoted value, read back in phase 2
+                    ++j;
+                    if (j == nl || j >= lend || (phase == 2 && cur >= j)) {
+                        out = true;
+                        break;
+                    }
+                    lval = lb[j - lbase];
+                }
+            }
+            if (j == nl) {
+                done = true;  // no large left: every remaining bucket is a leftover
+            } else if (!out && cur == stop_x) {
+                done = found = true;  // x is paired with the head large
+            } else if (j >= lend) {
+                head_pending = true;
+            } else if (phase == 2 && dq >= j) {
+                done = true;  // nothing left to pair: x is a leftover
+            }
+            if (!done && phase == 1 && k >= ns) phase = 2;
+            if (!done && phase == 2 && dq >= j) done = true;
         }
+        k = __shfl_sync(kFull, k, 0);
+        j = __shfl_sync(kFull, j, 0);
+        dq = __shfl_sync(kFull, dq, 0);
+        phase = __shfl_sync(kFull, phase, 0);
+        done = __shfl_sync(kFull, done, 0);
+        head_pending = __shfl_sync(kFull, head_pending, 0);
+        __syncwarp();  // lane 0's demoted values are visible to the next batch's loads
     }
-    split_out = 1.0;  // leftover: probability exactly 1, no alias (sampler.hpp:112-119)
-    second_out = x;
+    found = __shfl_sync(kFull, found, 0);
+    if (found) {  // bucket x: its own (final) value and the head large
+        split_out = xs ? park[xr] : park[n - 1 - xr];
+        second_out = li[j];
+    } else {
+        split_out = 1.0;  // leftover: probability exactly 1, no alias (sampler.hpp:112-119)
+        second_out = x;
+    }
 }
 
 // Deferred unpack of the current vertex word (Walker::pend): on for every
@@ -1256,14 +1311,7 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
     h.len = __shfl_sync(kFull, q.len, leader);
     const uint32_t d = h.cur_deg;
     const uint64_t base = h.cur_base;
-    // ALIAS: the owner's own row when the hub fits it (replayed per lane
-    // afterwards), else the warp's row (replayed by the warp now)
-    const bool lane_vose = S == WF_SAMPLER_ALIAS && L.lane_rows != nullptr && d <= kLaneRow;
-    double* wrow = wrow_warp;
-    if (lane_vose) {
-        const uint64_t owner = (blockIdx.x * static_cast<uint64_t>(kBlock) + (threadIdx.x & ~31u)) + leader;
-        wrow = L.lane_rows + owner * (2ull * kLaneRow);
-    }
+    double* wrow = wrow_warp;  // the warp's row: weights (ITS, ALIAS) + Vose's park area (ALIAS)
     if (L.g.stats && lane == leader) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
     // pass 1: weights, validity, partial sums, max, smallest quantum
     double lsum = 0.0, lmax = 0.0;
@@ -1286,14 +1334,27 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         }
     }
     if (!merged) {
-#pragma unroll 4
-        for (uint32_t i = lane; i < d; i += 32) {
-            const double w = P::weight(L, h, base + i);
-            if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
-            if (S == WF_SAMPLER_ALIAS || (S == WF_SAMPLER_ITS && wrow)) wrow[i] = w;
-            if (w > 0.0) qexp = min(qexp, quantum_exp(w));
-            lsum += w;
-            lmax = w > lmax ? w : lmax;
+        // eight 32-edge rounds per batch: their weight loads are issued
+        // together, ahead of the row stores
+        constexpr int kR = 8;
+        for (uint32_t c0 = 0; c0 < d; c0 += 32 * kR) {
+            double wv[kR];
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const uint32_t i = c0 + 32 * r + lane;
+                wv[r] = i < d ? P::weight(L, h, base + i) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const uint32_t i = c0 + 32 * r + lane;
+                if (i >= d) break;
+                const double w = wv[r];
+                if (!(w >= 0.0 && w <= 1.7976931348623157e308)) bad = true;
+                if (S == WF_SAMPLER_ALIAS || (S == WF_SAMPLER_ITS && wrow)) wrow[i] = w;
+                if (w > 0.0) qexp = min(qexp, quantum_exp(w));
+                lsum += w;
+                lmax = w > lmax ? w : lmax;
+            }
         }
     }
     if (__any_sync(kFull, bad)) {  // check_program_weight (engine.hpp:97-101)
@@ -1384,29 +1445,16 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
                 for (uint32_t i = 0; i < d; ++i) seq += wrow[i];
             total = __shfl_sync(kFull, seq, leader);
         }
-        // the scaled weights (one division each, sampler.hpp:97) by the warp,
-        // so the owner's replay of Vose's worklists only reads the row
-        for (uint32_t i = lane; i < d; i += 32) wrow[i] = wrow[i] * d / total;
-        __syncwarp();
         uint32_t x = 0;
         uint64_t k = 0;
         if (lane == leader) {
             x = q.rng.index(d);
             k = q.rng.bits53();
         }
-        if (lane_vose) {  // the owner replays on its own row after the hub loop
-            if (lane == leader) {
-                q.coop = kCoopVose;
-                q.coop_pick = x;
-                q.coop_k = k;
-            }
-            __syncwarp();
-            return;
-        }
         x = __shfl_sync(kFull, x, leader);
         double split;
         uint32_t second;
-        vose_bucket_warp(d, wrow, x, wrow + L.scratch_stride, split, second);
+        vose_bucket_staged(d, wrow, total, x, wrow + L.scratch_stride, split, second);
         if (lane == leader) {
             q.coop = kCoopPick;
             q.coop_pick = k < unit_threshold(split) ? x : second;
@@ -1712,7 +1760,6 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
     q.pend = false;
     q.coop = kCoopNone;
     q.coop_pick = 0;
-    q.coop_k = 0;
     bool active = false;
     bool fresh = false;
     bool drained = false;
@@ -1875,20 +1922,6 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
                     const int leader = __ffs(hubs) - 1;
                     hubs &= hubs - 1;
                     coop_step<P, S>(L, q, leader, wrow);
-                }
-                if constexpr (S == WF_SAMPLER_ALIAS) {
-                    // the lanes whose hub fitted their own row replay Vose's
-                    // worklists on it, all at once
-                    if (q.coop == kCoopVose) {
-                        const double* row = L.lane_rows +
-                                            (blockIdx.x * static_cast<uint64_t>(kBlock) + threadIdx.x) * (2ull * kLaneRow);
-                        double split;
-                        uint32_t second;
-                        vose_bucket_scaled(q.cur_deg, [&](uint32_t i) { return row[i]; }, q.coop_pick,
-                                           const_cast<double*>(row) + kLaneRow, split, second);
-                        q.coop_pick = q.coop_k < unit_threshold(split) ? q.coop_pick : second;
-                        q.coop = kCoopPick;
-                    }
                 }
             }
         }

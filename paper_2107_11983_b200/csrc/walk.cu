@@ -155,21 +155,16 @@ void launch_walk(Session& s, const wf_query_spec& spec, const uint32_t* dev_sour
     int grid_needed = static_cast<int>(std::min<uint64_t>((lanes_needed + kBlock - 1) / kBlock, 1u << 30));
     grid = std::max(1, std::min(grid, grid_needed));
     if (s.kind == WF_SAMPLER_ALIAS && s.flow == kGathered && g.max_degree >= kCoopDegree) {
-        // rows for the cooperative hub steps (coop_step): a row per lane for
-        // hubs up to kLaneRow edges (the lanes replay Vose's worklists in
-        // parallel) and, when larger hubs exist, a row per warp (weights /
-        // scaled weights + Vose's park area each); lanes below kCoopDegree
-        // park in local memory
-        const uint64_t per_lane = 2ull * kLaneRow;
-        const uint64_t per_warp = g.max_degree > kLaneRow ? 2ull * g.max_degree : 0;
-        const uint64_t per_block = kBlock * per_lane + (kBlock / 32) * per_warp;
+        // a row per warp for the cooperative hub steps (coop_step): the hub's
+        // weights, then the compacted scaled weights Vose's replay runs over
+        // (vose_bucket_staged); lanes below kCoopDegree park in local memory
+        const uint64_t per_warp = 2ull * g.max_degree;
         const uint64_t budget = 16ull << 30;
-        grid = std::max(1, std::min<int>(grid, static_cast<int>(std::max<uint64_t>(1, budget / (per_block * 8)))));
-        const uint64_t lanes = static_cast<uint64_t>(grid) * kBlock;
-        const uint64_t need = lanes * per_lane + (per_warp ? static_cast<uint64_t>(grid) * (kBlock / 32) * per_warp : 0);
+        const uint64_t warps = std::max<uint64_t>(kBlock / 32, budget / (per_warp * 8));
+        grid = std::max(1, std::min<int>(grid, static_cast<int>(warps / (kBlock / 32))));
+        const uint64_t need = static_cast<uint64_t>(grid) * (kBlock / 32) * per_warp;
         if (s.scratch.size() < need) s.scratch.allocate(need);
-        L.lane_rows = s.scratch.get();
-        L.scratch = per_warp ? s.scratch.get() + lanes * per_lane : nullptr;
+        L.scratch = s.scratch.get();
         L.scratch_stride = g.max_degree;
     } else if (s.kind == WF_SAMPLER_ITS && s.flow == kGathered && g.max_degree >= kCoopDegree &&
                !(s.desc.kind == WF_PROGRAM_METAPATH && g.label_index_built)) {

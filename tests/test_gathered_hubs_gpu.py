@@ -163,3 +163,37 @@ def test_node2vec_merge_intersection_matches_reference(weighted, sampler):
     opts = ExecOptions(seed=31, sampler=int(sampler))
     spec = QuerySpec.one_per_vertex()
     same(E.run_sequential(dg, spec, prog, opts), rg.run(spec, prog, opts))
+
+
+def _big_hub_graph(kind):
+    """Hubs of 4500-13000 edges (several 128-entry staging batches per
+    cursor, both replay phases): their ALIAS gathers go through the warp's
+    staged replay (vose_bucket_staged).  `kind` picks the
+    weights: "u15" uniform [1, 5) f32, "wide" mixed scales with zeros, "int"
+    small integers (many exact ties with 1.0 after scaling)."""
+    rng = np.random.default_rng({"u15": 3, "wide": 5, "int": 7}[kind])
+    V = 1500
+    deg = np.array([4500, 6100, 9000, 13000] + list(rng.integers(2, 60, V - 4)))
+    lists = [np.sort(np.where(rng.random(d) < 0.3, rng.integers(0, 4, d), rng.integers(0, V, d))) for d in deg]
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    nbr = np.concatenate(lists).astype(np.uint32)
+    if kind == "u15":
+        w = rng.uniform(1, 5, nbr.size).astype(np.float32)
+    elif kind == "wide":
+        w = (rng.choice([0.0, 0.25, 1.0, 3.0, 1024.0], nbr.size) * rng.integers(1, 50, nbr.size)).astype(np.float32)
+    else:
+        w = rng.integers(1, 4, nbr.size).astype(np.float32)
+    labels = rng.integers(0, 3, nbr.size).astype(np.uint8)
+    return Graph(off, nbr, w, labels)
+
+
+@pytest.mark.parametrize("kind", ["u15", "wide", "int"])
+def test_alias_gather_above_lane_row_matches_reference(kind):
+    hg = _big_hub_graph(kind)
+    dg = E.DeviceGraph.from_host(hg)
+    rg = RefOracle().graph(hg)
+    opts = ExecOptions(seed=44, sampler=int(abi.Sampler.ALIAS), use_static_tables=False)
+    spec = QuerySpec.from_list(np.repeat(np.arange(8, dtype=np.uint32), 40))  # many walks through the hubs
+    for prog in [DeepWalkProgram(30, True), MetaPathProgram([i % 3 for i in range(25)]),
+                 Node2VecProgram(0.5, 2.0, 25, True)]:
+        same(E.run_sequential(dg, spec, prog, opts), rg.run(spec, prog, opts))
