@@ -747,70 +747,61 @@ __device__ __forceinline__ int orej_accept(const WalkLaunch& L, const Walker& q,
     }
 }
 
-// Vose's alias construction (sampler.hpp:89-120) for ONE bucket x, over the
-// weights produced by wfn(i), without the FIFO worklists: the small queue is
-// [initial smalls ascending] ++ [larges in demotion order] and larges are
-// demoted in ascending order, so three ascending cursors replay it exactly.
-// Demoted larges park their final scaled value in park[] until consumed.
-// Returns split of bucket x and its alias index (x itself when none).
-// `scaled(i)` = w_i * n / sum (sampler.hpp:97): computed on demand, or read
-// from a row the warp filled in parallel (vose_bucket_scaled).
-template <typename Scaled>
-__device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double* park, double& split_out,
-                                   uint32_t& second_out);
+// Vose's alias construction (sampler.hpp:89-120) for ONE bucket x, replayed
+// without the FIFO worklists: the small queue is [initial smalls ascending] ++
+// [larges in demotion order] and larges are demoted in ascending order, so
+// ascending cursors (or bitmasks) over the scaled weights w_i * n / sum
+// (sampler.hpp:97) reproduce it exactly; a demoted large's final value is
+// kept until it is consumed as a small.  Returns the split of bucket x and
+// its alias index (x itself when it is a leftover at probability 1).
 
-template <typename WFn>
-__device__ __forceinline__ void vose_bucket(uint32_t n, double sum, WFn wfn, uint32_t x, double* park,
-                                            double& split_out, uint32_t& second_out) {
-    vose_bucket_scaled(n, [&](uint32_t i) { return wfn(i) * n / sum; }, x, park, split_out, second_out);
-}
-
-template <typename Scaled>
-__device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double* park, double& split_out,
-                                   uint32_t& second_out) {
-    uint32_t a = 0;        // next initial-small candidate
-    uint32_t c = 0;        // next demoted-large candidate (trails the large cursor)
-    uint32_t demoted = 0;  // larges demoted so far
-    uint32_t consumed_demoted = 0;
-    uint32_t lcur = 0;     // current large
-    auto next_large = [&](uint32_t from) {
-        while (from < n && !(scaled(from) >= 1.0)) ++from;
-        return from;
-    };
-    auto next_small = [&](uint32_t from) {
-        while (from < n && !(scaled(from) < 1.0)) ++from;
-        return from;
-    };
-    lcur = next_large(0);
-    double lval = lcur < n ? scaled(lcur) : 0.0;
-    a = next_small(0);
-    while (lcur < n) {
-        uint32_t s;
-        double sval;
-        if (a < n) {
-            s = a;
-            sval = scaled(a);
-            a = next_small(a + 1);
-        } else if (consumed_demoted < demoted) {
-            c = next_large(c);
-            s = c;
-            sval = park[c];
-            c += 1;
-            consumed_demoted += 1;
-        } else {
-            break;
-        }
-        if (s == x) {
-            split_out = sval;
-            second_out = lcur;
-            return;
-        }
-        lval -= 1.0 - sval;
-        if (lval < 1.0) {
-            park[lcur] = lval;
-            demoted += 1;
-            lcur = next_large(lcur + 1);
-            if (lcur < n) lval = scaled(lcur);
+// The replay for a light vertex (d < kCoopDegree <= 64) whose
+// weights sit in a lane-local array: the scaled weights replace them in
+// place, the worklists are bitmasks (initial smalls, larges not yet head,
+// demoted larges — each consumed lowest index first, which is the FIFO order
+// since larges are demoted in ascending order), and a demoted large's final
+// value overwrites its own slot, so no scan ever re-reads a weight.
+__device__ __forceinline__ void vose_bucket_local(uint32_t n, double sum, double* w, uint32_t x, double& split_out,
+                                                  uint32_t& second_out) {
+    static_assert(kCoopDegree <= 64, "bitmask worklists");
+    uint64_t largem = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        w[i] = w[i] * n / sum;  // sampler.hpp:97
+        if (w[i] >= 1.0) largem |= 1ull << i;
+    }
+    uint64_t sq = (n == 64 ? ~0ull : (1ull << n) - 1) & ~largem;  // initial smalls not yet popped
+    uint64_t lq = largem;                                           // larges not yet head
+    uint64_t dq = 0;                                                // demoted larges not yet popped
+    if (lq) {
+        uint32_t l = __ffsll(static_cast<long long>(lq)) - 1;
+        lq &= lq - 1;
+        double lval = w[l];
+        for (;;) {  // sampler.hpp:103-111
+            uint32_t s;
+            if (sq) {
+                s = __ffsll(static_cast<long long>(sq)) - 1;
+                sq &= sq - 1;
+            } else if (dq) {
+                s = __ffsll(static_cast<long long>(dq)) - 1;
+                dq &= dq - 1;
+            } else {
+                break;
+            }
+            const double sval = w[s];
+            if (s == x) {
+                split_out = sval;
+                second_out = l;
+                return;
+            }
+            lval -= 1.0 - sval;
+            if (lval < 1.0) {
+                w[l] = lval;
+                dq |= 1ull << l;
+                if (!lq) break;
+                l = __ffsll(static_cast<long long>(lq)) - 1;
+                lq &= lq - 1;
+                lval = w[l];
+            }
         }
     }
     split_out = 1.0;  // leftover: probability exactly 1, no alias (sampler.hpp:112-119)
@@ -818,7 +809,7 @@ __device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double
 }
 
 // ---- Vose's worklists for a hub, by a warp ---------------------------------------
-// vose_bucket_scaled's replay for bucket x over a hub's weights (`row`, n
+// The replay for bucket x over a hub's weights (`row`, n
 // entries, summed to `total`), with the serial chain on one lane.  Vose's
 // pairing loop is an order-dependent fp64 chain (lval -= 1 - sval), so it
 // cannot be split; everything around it can.  The warp first turns the row
@@ -831,7 +822,7 @@ __device__ void vose_bucket_scaled(uint32_t n, Scaled scaled, uint32_t x, double
 // own subtraction), so a pairing is one subtraction and one compare — and
 // writes each demoted large's final value over its own slot, where the
 // second phase (demoted larges consumed as smalls, in demotion order) reads
-// it.  Same pairing sequence as vose_bucket_scaled.  `row` is overwritten.
+// it.  `row` is overwritten.
 constexpr uint32_t kVoseStage = 128;
 
 __device__ __forceinline__ void vose_bucket_staged(uint32_t n, double* __restrict__ row, double total, uint32_t x,
@@ -1112,9 +1103,15 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
         }
         double sum = 0.0, mx = 0.0;
         if (L.g.stats) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
+        // below kCoopDegree (hubs go through coop_step) the weights stay in a
+        // lane-local array, so each is evaluated (for Node2Vec: an adjacency
+        // test) once per step
+        double wl[kCoopDegree];
+        const bool local = d < kCoopDegree;
         for (uint32_t i = 0; i < d; ++i) {
             double w = P::weight(L, q, base + i);
             if (!weight_ok<P>(L, w)) return kFault;
+            if (local) wl[i] = w;
             sum += w;
             mx = w > mx ? w : mx;
         }
@@ -1124,19 +1121,15 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             double run = 0.0;
             pick = d - 1;
             for (uint32_t i = 0; i < d; ++i) {
-                run += P::weight(L, q, base + i);
+                run += local ? wl[i] : P::weight(L, q, base + i);
                 if (x < run) { pick = i; break; }
             }
         } else if constexpr (S == WF_SAMPLER_ALIAS) {
-            // below kCoopDegree (hubs go through coop_step): the demoted
-            // larges park in a lane-local array
             uint32_t x = q.rng.index(d);
             uint64_t k = q.rng.bits53();
-            double park[kCoopDegree];
             double split;
             uint32_t second;
-            vose_bucket(d, sum, [&](uint32_t i) { return P::weight(L, q, base + i); }, x,
-                        park, split, second);
+            vose_bucket_local(d, sum, wl, x, split, second);
             pick = k < unit_threshold(split) ? x : second;
         } else {  // REJ over the gathered weights, p* = max
             uint32_t t = 0;
@@ -1184,7 +1177,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
 //   ITS   the pick is the first i with x < cumulative[i]: a warp-wide inclusive
 //         scan per round of 32 weights, x drawn by the owner from its own stream;
 //   ALIAS the weights go to the warp's scratch row; the owner runs Vose's
-//         construction for its bucket over it (vose_bucket, no re-evaluation);
+//         construction for its bucket over it (vose_bucket_staged, no re-evaluation);
 //   REJ   p* = max weight (exact in any order); the owner runs the trials.
 // Bit-exactness: the reference sums in edge order.  A reordered fp64 sum is
 // the same number when every partial sum is exact, i.e. when all weights are
