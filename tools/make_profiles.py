@@ -7,7 +7,8 @@
                                      (gpu__time_duration, cold, serialised)
 * <round>_<config>_launch_share.json per-kernel totals and the walk kernel's share
 * <round>_<config>_walk_kernel.json  summary of the --set full capture
-* ncu_traffic.json                   per-config DRAM bytes per launch (bench.py)
+(profiles/ncu_traffic.json, the stamped per-config DRAM bytes bench.py reads,
+comes from tools/capture_traffic.py.)
 """
 import argparse
 import csv
@@ -50,7 +51,6 @@ def main():
     ap.add_argument("--config", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--full")
-    ap.add_argument("--moves", type=int, default=0, help="moves per launch (bytes/move)")
     args = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -63,17 +63,6 @@ def main():
         s = summarise(args.full)
         with open(os.path.join(prof, f"{tag}_walk_kernel.json"), "w") as f:
             json.dump(s, f, indent=1)
-        k = s[0]
-        traffic = (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"])
-        unit = k.get("dram__bytes_read.sum@unit", "byte")
-        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-        tpath = os.path.join(prof, "ncu_traffic.json")
-        t = json.load(open(tpath)) if os.path.exists(tpath) else {}
-        t[args.config] = traffic * mult
-        if args.moves:
-            t[args.config + "_bytes_per_move"] = traffic * mult / args.moves
-        with open(tpath, "w") as f:
-            json.dump(t, f, indent=1)
     print("ok", tag)
 
 
