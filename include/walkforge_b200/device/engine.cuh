@@ -40,7 +40,9 @@ constexpr int kMaxIndexedLabels = 6;  // 32 B label record: u64 base + 6 u32 gro
 
 enum Flow : int { kDirect = 0, kTables = 1, kGathered = 2 };
 enum WalkerTypeE : int { kUnbiased = 0, kStatic = 1, kDynamic = 2 };  // program.hpp:17
-enum MoveResult : int { kDead = 0, kMoved = 1, kFault = 2 };
+// kRetry: an O-REJ trial rejected; the walker stays and draws its next trial
+// in the kernel's next iteration (the same draws in the same order).
+enum MoveResult : int { kDead = 0, kMoved = 1, kFault = 2, kRetry = 3 };
 
 struct GraphView {
     uint32_t V;
@@ -159,6 +161,7 @@ struct Walker {
     uint32_t cur, prev;
     uint32_t cur_deg, prev_deg;
     uint32_t len;  // vertices on the path so far (moves + 1)
+    uint32_t trials;  // O-REJ: trials of the current move so far (the cap, sampler.hpp:27)
     // vertex word of the destination when the sampler's load carried it
     uint64_t nb_word;
     bool have_nb;
@@ -979,46 +982,49 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
         if constexpr (S == WF_SAMPLER_NAIVE) {
             pick = q.rng.index(d);
         } else {  // O-REJ
-            uint32_t t = 0;
-            for (;; ++t) {
-                if (t >= L.trial_cap) {
-                    raise_device(L, WF_ERR_REJECTION_CAP);
-                    return kFault;
-                }
-                if (L.g.stats) atomicAdd(L.g.stats, 1ull);
-                uint32_t x = q.rng.index(d);
-                double y = q.rng.real(L.prog.bound);
-                // one sector per trial: the candidate's id (and, with the
-                // decorated adjacency, its vertex word for the next step)
-                uint32_t dx;
-                uint64_t wx = 0;
-                if (L.adj8) {
-                    dx = adj8_unpack(ldr(reinterpret_cast<const uint64_t*>(L.adj8) + base + x), L.adj8_vbits,
-                                     L.adj8_dbits, wx);
-                } else if (L.adj) {
-                    uint4 a = ldr16(L.adj + base + x);
-                    dx = a.x;
-                    wx = (static_cast<uint64_t>(a.w) << 32) | a.z;
-                } else {
-                    dx = ldr(L.g.nbr + base + x);
-                }
-                if (L.g.stats && P::kind == WF_PROGRAM_NODE2VEC && q.len > 1 && dx != q.prev) {
-                    // instrumented runs: the reference's weight() binary-searches
-                    // adj(prev) on every such trial (ceil(log2(d_prev+1)) probes)
-                    atomicAdd(L.g.stats + 3, static_cast<unsigned long long>(32 - __clz(q.prev_deg)));
-                }
-                const int acc = orej_accept<P>(L, q, base + x, y, dx);
-                if (acc < 0) return kFault;
-                if (acc) {
-                    dst = dx;
-                    if constexpr (P::needs_edge) edge = base + x;
-                    if (L.adj || L.adj8) {
-                        q.nb_word = wx;
-                        q.have_nb = true;
-                    }
-                    return kMoved;
-                }
+            // One trial per call.  A rejected trial returns kRetry and the
+            // kernel's next iteration draws the next one: in a warp, a lane
+            // with a second trial (~6 % of Node2Vec moves, so most warp
+            // iterations on C3) no longer holds the other 31 at the loop's
+            // reconvergence point for a whole extra dependent chain.
+            if (q.trials >= L.trial_cap) {
+                raise_device(L, WF_ERR_REJECTION_CAP);
+                return kFault;
             }
+            ++q.trials;
+            if (L.g.stats) atomicAdd(L.g.stats, 1ull);
+            uint32_t x = q.rng.index(d);
+            double y = q.rng.real(L.prog.bound);
+            // one sector per trial: the candidate's id (and, with the
+            // decorated adjacency, its vertex word for the next step)
+            uint32_t dx;
+            uint64_t wx = 0;
+            if (L.adj8) {
+                dx = adj8_unpack(ldr(reinterpret_cast<const uint64_t*>(L.adj8) + base + x), L.adj8_vbits,
+                                 L.adj8_dbits, wx);
+            } else if (L.adj) {
+                uint4 a = ldr16(L.adj + base + x);
+                dx = a.x;
+                wx = (static_cast<uint64_t>(a.w) << 32) | a.z;
+            } else {
+                dx = ldr(L.g.nbr + base + x);
+            }
+            if (L.g.stats && P::kind == WF_PROGRAM_NODE2VEC && q.len > 1 && dx != q.prev) {
+                // instrumented runs: the reference's weight() binary-searches
+                // adj(prev) on every such trial (ceil(log2(d_prev+1)) probes)
+                atomicAdd(L.g.stats + 3, static_cast<unsigned long long>(32 - __clz(q.prev_deg)));
+            }
+            const int acc = orej_accept<P>(L, q, base + x, y, dx);
+            if (acc < 0) return kFault;
+            if (!acc) return kRetry;
+            q.trials = 0;
+            dst = dx;
+            if constexpr (P::needs_edge) edge = base + x;
+            if (L.adj || L.adj8) {
+                q.nb_word = wx;
+                q.have_nb = true;
+            }
+            return kMoved;
         }
     } else if constexpr (F == kTables) {
         if constexpr (S == WF_SAMPLER_ALIAS) {
@@ -1053,18 +1059,19 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
             double x = q.rng.real(__ldg(cum + d - 1));
             pick = upper_index(cum, d, x);
         } else {  // REJ with p* per vertex
-            double ps = __ldg(L.rej_pstar + q.cur);
-            uint32_t t = 0;
-            for (;; ++t) {
-                if (t >= L.trial_cap) {
-                    raise_device(L, WF_ERR_REJECTION_CAP);
-                    return kFault;
-                }
-                if (L.g.stats) atomicAdd(L.g.stats, 1ull);
-                uint32_t x = q.rng.index(d);
-                double y = q.rng.real(ps);
-                if (y < P::weight_static(L, q.cur, base + x)) { pick = x; break; }
+            // one trial per call, like O-REJ (kRetry)
+            if (q.trials >= L.trial_cap) {
+                raise_device(L, WF_ERR_REJECTION_CAP);
+                return kFault;
             }
+            ++q.trials;
+            if (L.g.stats) atomicAdd(L.g.stats, 1ull);
+            const double ps = __ldg(L.rej_pstar + q.cur);
+            uint32_t x = q.rng.index(d);
+            double y = q.rng.real(ps);
+            if (!(y < P::weight_static(L, q.cur, base + x))) return kRetry;
+            q.trials = 0;
+            pick = x;
         }
     } else {  // Gathered: gather (engine.hpp:134-184) without the scratch table
         if constexpr (P::kind == WF_PROGRAM_METAPATH && S == WF_SAMPLER_ITS) {
@@ -1747,6 +1754,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
     q.cur_deg = q.prev_deg = 0;
     q.cur_base = q.prev_base = 0;
     q.len = 0;
+    q.trials = 0;
     q.rng.s = 0;
     q.nb_word = 0;
     q.have_nb = false;
@@ -1859,6 +1867,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
                 q.cur = claim_src[wid][slot];
                 q.prev = 0xFFFFFFFFu;
                 q.len = 0;
+                q.trials = 0;
                 if (q.cur >= L.g.V) {
                     // QuerySpec validation (walker.cpp:8-109) on the device: the
                     // run reports ConfigError (its rows are not results)
@@ -1955,7 +1964,7 @@ __global__ void __launch_bounds__(kBlock, walk_min_blocks<P, S, F>()) walk_kerne
                     load_current<P, S, F>(L, q);
                 }
                 q.have_nb = false;
-            } else {
+            } else if (r != kRetry) {
                 finish(L, q, WF_WALK_DEAD_END, ps);
                 active = false;
             }
