@@ -1,4 +1,5 @@
-# round-2 evidence: traffic stamps, bench line, launch list, C5 full capture
+# Round evidence on a GPU box (gpurun): traffic stamps, the bench line, the C5 launch list and full capture.
+# Afterwards here: cp gpurun_out/ncu_traffic.json profiles/; tools/make_profiles.py --round N --config c5 ...
 set -x
 python tools/capture_traffic.py run > gpurun_out/capture_traffic.log 2>&1
 cp gpurun_out/ncu_traffic.json profiles/ncu_traffic.json
