@@ -1386,15 +1386,27 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         double running = 0.0;
         uint32_t pick = d - 1;
         if (wrow) __syncwarp();  // pass 1's weights are in the row
-        // with the row: four 32-weight rounds loaded at once, so a hub's scan
-        // waits on one load round trip per 128 weights instead of per 32
-        constexpr uint32_t kG = 4;
+        // with the row: eight 32-weight rounds loaded at once, so a hub's scan
+        // waits on one load round trip per 256 weights instead of per 32; a
+        // batch that ends below x is skipped on its total (one warp
+        // reduction) — only the batch holding the pick is scanned round by
+        // round.  Every partial sum is exact (the certificate), so the
+        // reordered totals are the cumulative sums the reference compares.
+        constexpr uint32_t kG = 8;
         for (uint32_t c0 = 0; wrow && c0 < d; c0 += 32 * kG) {
             double v[kG];
 #pragma unroll
             for (uint32_t k = 0; k < kG; ++k) {
                 const uint32_t i = c0 + 32 * k + lane;
                 v[k] = i < d ? wrow[i] : 0.0;
+            }
+            double tot = 0.0;
+#pragma unroll
+            for (uint32_t k = 0; k < kG; ++k) tot += v[k];
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+            if (!(x < running + tot) && c0 + 32 * kG < d) {
+                running += tot;
+                continue;
             }
             bool hit_any = false;
 #pragma unroll

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--graph", action="store_true", help="replay the launch as a captured CUDA graph")
     ap.add_argument("--flush", action="store_true", help="write 256 MiB between launches (cold L2, as bench.py)")
     ap.add_argument("--stride", type=int, default=0, help="path row stride override (vertices)")
+    ap.add_argument("--per-vertex", action="store_true",
+                    help="random-source configs: one walk per vertex in vertex order instead")
     args = ap.parse_args()
     import torch
 
@@ -42,6 +44,8 @@ def main():
                                                             layout_flags=args.layout, **bench.exec_extra(cfg)))
     if args.queries and cfg["queries"] == "random":
         cfg["n_queries"] = args.queries
+    if args.per_vertex:
+        cfg["queries"] = "per_vertex"
     spec, lo, hi = bench.query_plan(cfg, V, 0, 1)
     n = hi - lo
     stride = args.stride or bench.row_capacity(cfg)
