@@ -258,6 +258,23 @@ __device__ __forceinline__ uint4 ldr16_move(const uint4* p) {
     return (a & 16) ? hi : lo;
 }
 
+// The O-REJ trial's random adjacency entry, marked evict-first in L2 (and a
+// 64 B fetch): Node2Vec's pair filter (64 MiB, read at random by half the
+// trials) then keeps more of its lines against the 2 GB adjacency stream —
+// C3 6.55 -> 6.19 ms.  (Alone, without the policy, the 64 B fetch measured
+// slower; the policy on DeepWalk's bucket loads slowed C5, whose only other
+// L2 traffic is the path rows.)
+__device__ __forceinline__ uint4 ldr16_stream(const uint4* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    uint4 lo, hi;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm("ld.global.L2::cache_hint.L2::64B.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+        : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+        : "l"(a & ~static_cast<uintptr_t>(31)), "l"(pol));
+    return (a & 16) ? hi : lo;
+}
+
 // An edge's weight as the reference holds it (double, graph.hpp:102).
 __device__ __forceinline__ double edge_weight(const GraphView& g, uint64_t e) {
     return g.weights64 ? __ldg(g.weights64 + e) : static_cast<double>(ldr(g.weights + e));
@@ -1003,7 +1020,7 @@ __device__ __forceinline__ int move(const WalkLaunch& L, Walker& q, uint32_t& ds
                 dx = adj8_unpack(ldr(reinterpret_cast<const uint64_t*>(L.adj8) + base + x), L.adj8_vbits,
                                  L.adj8_dbits, wx);
             } else if (L.adj) {
-                uint4 a = ldr16(L.adj + base + x);
+                uint4 a = ldr16_stream(L.adj + base + x);
                 dx = a.x;
                 wx = (static_cast<uint64_t>(a.w) << 32) | a.z;
             } else {
