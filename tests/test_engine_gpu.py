@@ -672,3 +672,34 @@ def test_degenerate_inputs_match_reference():
                 streamed = E.Session(dg, prog, opts).run_to_numpy(spec)
                 assert streamed.walks.equals(want.walks), (V, prog, spec.mode)
                 assert streamed.metrics.total_steps == 0
+
+
+@pytest.mark.parametrize("cap", [1, 2, 3, 4, 6, 10, 40])
+@pytest.mark.parametrize("sampler", [abi.Sampler.OREJ, abi.Sampler.REJ])
+def test_trial_cap_outcome_matches_reference(rmat12, cap, sampler):
+    """The walk kernel makes one rejection trial per iteration and counts a
+    move's trials across iterations (Walker::trials): for every cap the run
+    either raises RejectionCapError exactly when the reference does, or gives
+    its walks (sampler.hpp:27, interleave.hpp:286-380)."""
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    dg, hg = rmat12
+    spec = QuerySpec.from_list(np.arange(0, hg.vertex_count, 7, dtype=np.uint32))
+    if sampler == abi.Sampler.OREJ:
+        prog = Node2VecProgram(0.25, 4.0, 12, True)  # acceptance as low as 1/16: caps below ~40 bind
+        opts = ExecOptions(seed=5, rej_trial_cap=cap)
+    else:
+        prog = DeepWalkProgram(12, True)
+        opts = ExecOptions(seed=5, sampler=int(sampler), rej_trial_cap=cap)
+    rg = RefOracle().graph(hg)
+    try:
+        want = rg.run(spec, prog, opts)
+    except abi.RejectionCapError:
+        want = None
+    if want is None:
+        with pytest.raises(abi.RejectionCapError):
+            E.run_sequential(dg, spec, prog, opts)
+    else:
+        got = E.run_sequential(dg, spec, prog, opts)
+        assert got.walks.first_mismatch(want.walks) is None
+        assert got.metrics.total_steps == want.metrics.total_steps
