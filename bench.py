@@ -745,7 +745,29 @@ def reference_arm(args, cfg, rank, world):
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit_line(line)
+
+
+# The JSON line is the only thing on stdout: native libraries that print there
+# (NCCL's version banner under torchrun) are pointed at stderr at the file
+# descriptor level, and the line itself goes to the saved stdout.
+_JSON_FD = None
+
+
+def _stdout_for_json_only():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit_line(line):
+    text = json.dumps(line) + "\n"
+    if _JSON_FD is None:
+        print(text, end="", flush=True)
+    else:
+        os.write(_JSON_FD, text.encode())
 
 
 def main():
@@ -775,10 +797,13 @@ def main():
     import torch
     dist = None
     if world > 1 or "RANK" in os.environ:  # any torchrun launch, even N=1
+        _stdout_for_json_only()
         # NCCL's init log names every rank of the communicators (the engine's
         # own for the visit counts and torch's for the barriers)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # ... on stderr: stdout carries only rank 0's JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
@@ -834,7 +859,7 @@ def main():
         torch.cuda.empty_cache()
         line["per_algorithm"] = extras(args, rank, world, local_rank, dist)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit_line(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
