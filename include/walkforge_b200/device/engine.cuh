@@ -966,6 +966,93 @@ __device__ __forceinline__ void vose_bucket_staged(uint32_t n, double* __restric
     }
 }
 
+// Index of the j-th (0-based) positive entry of row[0, n), by the warp: 256
+// entries per load batch, batches skipped on their ballot counts.
+__device__ __forceinline__ uint32_t warp_select_positive(const double* __restrict__ row, uint32_t n, uint64_t j) {
+    const int lane = threadIdx.x & 31;
+    uint64_t seen = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 256) {
+        unsigned m[8];
+        uint32_t tot = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t i = c0 + 32 * r + lane;
+            m[r] = __ballot_sync(kFull, i < n && row[i] > 0.0);
+            tot += __popc(m[r]);
+        }
+        if (seen + tot <= j) {
+            seen += tot;
+            continue;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t pc = __popc(m[r]);
+            if (seen + pc > j) return c0 + 32 * r + __fns(m[r], 0, static_cast<int>(j - seen) + 1);
+            seen += pc;
+        }
+    }
+    return n;  // not reached: j < the number of positive entries
+}
+
+// The replay in closed form when every positive weight has the same value
+// (MetaPath's 0/1 weights, unweighted programs).  Then every large starts at
+// c = w * n / sum (sampler.hpp:97, the same expression) and every small is a
+// zero, and the chain is exact arithmetic on multiples of ulp(c):
+//   phase 1 — each large absorbs K = floor(c) zeros (lval -= 1 exactly) and
+//     is demoted at f = c - K, so the zero of rank r pairs with the large of
+//     rank r / K;
+//   phase 2 — the D = Z / K larges demoted in phase 1 (Z zeros) are consumed
+//     in rank order, each with deficit t = 1 - f: head D (at c - Z mod K)
+//     takes a0 = floor((v0 - 1) / t) + 1 of them, every later head
+//     ac = floor((c - 1) / t) + 1, and the larges those heads demote queue
+//     behind them (position = rank), so the first D positions are consumed
+//     by that formula alone.
+// Returns false for the one case that needs the chain: x a large the first
+// phase did not demote.  Checked against the reference's tables and walks.
+__device__ __forceinline__ bool vose_bucket_uniform(uint32_t n, uint32_t m, double w, double total, uint32_t x,
+                                                    bool xpos, uint32_t xrank, const double* __restrict__ row,
+                                                    double& split_out, uint32_t& second_out) {
+    const double c = w * n / total;
+    if (m == n || !(c >= 1.0) || !(c < 4503599627370496.0)) {  // no smalls (c == 1): all leftovers
+        if (m != n) return false;
+        split_out = 1.0;
+        second_out = x;
+        return true;
+    }
+    const uint64_t K = static_cast<uint64_t>(c);
+    const double f = c - static_cast<double>(K);  // exact
+    const uint64_t Z = n - m;
+    if (!xpos) {  // phase 1
+        const uint64_t j = xrank / K;
+        if (j < m) {
+            split_out = 0.0;
+            second_out = warp_select_positive(row, n, j);
+        } else {
+            split_out = 1.0;
+            second_out = x;
+        }
+        return true;
+    }
+    const uint64_t D = Z / K;
+    if (xrank >= D) return false;
+    // phase 2 over the first-generation entries, in units of u = ulp(c)
+    const int e = ilogb(c) - 52;
+    const double t = 1.0 - f;
+    const double v0 = c - static_cast<double>(Z - D * K);
+    const uint64_t T = static_cast<uint64_t>(ldexp(t, -e));
+    const uint64_t a0 = static_cast<uint64_t>(ldexp(v0 - 1.0, -e)) / T + 1;
+    const uint64_t ac = static_cast<uint64_t>(ldexp(c - 1.0, -e)) / T + 1;
+    const uint64_t head = xrank < a0 ? D : D + 1 + (xrank - a0) / ac;
+    if (head < m) {
+        split_out = f;
+        second_out = warp_select_positive(row, n, head);
+    } else {
+        split_out = 1.0;
+        second_out = x;
+    }
+    return true;
+}
+
 // Deferred unpack of the current vertex word (Walker::pend): on for every
 // program but Node2Vec, whose O-REJ kernel measured 3 % slower with it.
 template <class P>
@@ -1330,11 +1417,28 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
     const uint64_t base = h.cur_base;
     double* wrow = wrow_warp;  // the warp's row: weights (ITS, ALIAS) + Vose's park area (ALIAS)
     if (L.g.stats && lane == leader) atomicAdd(L.g.stats + 2, static_cast<unsigned long long>(d));
-    // pass 1: weights, validity, partial sums, max, smallest quantum
+    // pass 1: weights, validity, partial sums, max, smallest quantum; for
+    // ALIAS also the positive weights' count and smallest value and the rank
+    // of bucket x (drawn next, peeked now) among the zero / positive weights
     double lsum = 0.0, lmax = 0.0;
     int qexp = 0x7FFFFFFF;
     bool bad = false;
     bool merged = false;
+    uint32_t xpeek = 0, npos = 0, nbefore = 0;
+    double pmin = 1.7976931348623157e308;
+    if constexpr (S == WF_SAMPLER_ALIAS) {
+        if (lane == leader) xpeek = static_cast<uint32_t>(__umul64hi(q.rng.peek(), static_cast<uint64_t>(d)));
+        xpeek = __shfl_sync(kFull, xpeek, leader);
+    }
+    auto alias_stats = [&](uint32_t i, double w) {
+        if constexpr (S == WF_SAMPLER_ALIAS) {
+            if (w > 0.0) {
+                ++npos;
+                pmin = w < pmin ? w : pmin;
+                nbefore += i < xpeek;
+            }
+        }
+    };
     if constexpr (P::kind == WF_PROGRAM_NODE2VEC) {
         if (h.len > 1 && L.g.sorted && h.prev_deg <= kMergeRatio * d) {
             const ProgParams& p = L.prog;
@@ -1346,6 +1450,7 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
                 if (w > 0.0) qexp = min(qexp, quantum_exp(w));
                 lsum += w;
                 lmax = w > lmax ? w : lmax;
+                alias_stats(i, w);
             });
             merged = true;
         }
@@ -1371,6 +1476,7 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
                 if (w > 0.0) qexp = min(qexp, quantum_exp(w));
                 lsum += w;
                 lmax = w > lmax ? w : lmax;
+                alias_stats(i, w);
             }
         }
     }
@@ -1483,7 +1589,19 @@ __device__ __forceinline__ void coop_step(const WalkLaunch& L, Walker& q, int le
         x = __shfl_sync(kFull, x, leader);
         double split;
         uint32_t second;
-        vose_bucket_staged(d, wrow, total, x, wrow + L.scratch_stride, split, second);
+        for (int o = 16; o > 0; o >>= 1) {
+            npos += __shfl_xor_sync(kFull, npos, o);
+            nbefore += __shfl_xor_sync(kFull, nbefore, o);
+            const double m2 = __shfl_xor_sync(kFull, pmin, o);
+            pmin = m2 < pmin ? m2 : pmin;
+        }
+        // every positive weight the same (MetaPath's 0/1, unweighted programs):
+        // the replay has a closed form (vose_bucket_uniform), else the chain
+        const uint32_t xi = (x & ~31u) | static_cast<uint32_t>(lane);
+        const bool xpos = __shfl_sync(kFull, xi < d ? wrow[xi] : 0.0, x & 31) > 0.0;
+        const uint32_t xrank = xpos ? nbefore : x - nbefore;
+        if (!(pmin == mx && vose_bucket_uniform(d, npos, mx, total, x, xpos, xrank, wrow, split, second)))
+            vose_bucket_staged(d, wrow, total, x, wrow + L.scratch_stride, split, second);
         if (lane == leader) {
             q.coop = kCoopPick;
             q.coop_pick = k < unit_threshold(split) ? x : second;

@@ -197,3 +197,26 @@ def test_alias_gather_above_lane_row_matches_reference(kind):
     for prog in [DeepWalkProgram(30, True), MetaPathProgram([i % 3 for i in range(25)]),
                  Node2VecProgram(0.5, 2.0, 25, True)]:
         same(E.run_sequential(dg, spec, prog, opts), rg.run(spec, prog, opts))
+
+
+@pytest.mark.parametrize("label_p", [0.03, 0.2, 0.5, 0.9, 1.0])
+def test_alias_gather_uniform_weights_closed_form(label_p):
+    """Every positive weight equal (MetaPath's 0/1 weights; unweighted
+    DeepWalk): the hub's Vose replay is a closed form (vose_bucket_uniform)
+    with the chain only for larges the first phase leaves; the share of
+    matching edges sets c = n/m (integer and fractional), both phases and the
+    leftovers."""
+    rng = np.random.default_rng(int(label_p * 100) + 3)
+    V = 1200
+    deg = np.array([40, 97, 256, 1000, 3001, 7000] + list(rng.integers(1, 50, V - 6)))
+    lists = [np.sort(rng.integers(0, V, d)) for d in deg]
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    nbr = np.concatenate(lists).astype(np.uint32)
+    labels = np.where(rng.random(nbr.size) < label_p, 1, 0).astype(np.uint8)
+    hg = Graph(off, nbr, rng.uniform(1, 5, nbr.size).astype(np.float32), labels)
+    dg = E.DeviceGraph.from_host(hg)
+    rg = RefOracle().graph(hg)
+    spec = QuerySpec.from_list(np.repeat(np.arange(6, dtype=np.uint32), 60))
+    opts = ExecOptions(seed=9, sampler=int(abi.Sampler.ALIAS), use_static_tables=False)
+    for prog in [MetaPathProgram([1] * 12), DeepWalkProgram(12, False)]:
+        same(E.run_sequential(dg, spec, prog, opts), rg.run(spec, prog, opts))
