@@ -848,7 +848,7 @@ constexpr uint32_t kVoseStage = 128;
 __device__ __forceinline__ void vose_bucket_staged(uint32_t n, double* __restrict__ row, double total, uint32_t x,
                                                    double* __restrict__ park, double& split_out,
                                                    uint32_t& second_out) {
-    __shared__ double vose_stage[kBlock / 32][2][kVoseStage];
+    __shared__ double vose_stage[kBlock / 32][2][kVoseStage + 2];
     const int lane = threadIdx.x & 31;
     double* tb = vose_stage[threadIdx.x >> 5][0];  // deficits: smalls (phase 1) / demoted larges (phase 2)
     double* lb = vose_stage[threadIdx.x >> 5][1];  // larges' initial values
@@ -921,21 +921,39 @@ __device__ __forceinline__ void vose_bucket_staged(uint32_t n, double* __restric
             uint32_t& cur = phase == 1 ? k : dq;
             const uint32_t stop_x = (phase == 1) == xs ? xr : 0xFFFFFFFFu;
             const uint32_t stop = min(tbase + tlen, stop_x);
-            const uint32_t lend = lbase + llen;
+            const uint32_t lend = lbase + llen;  // <= nl
+            // the next head's value is loaded ahead (off the chain's critical
+            // path); the chain itself is one subtraction and one compare
+            const double* tp = tb - tbase;
+            const double* lp = lb - lbase;
+            double* pj = park + (n - 1 - j);
+            double nv = j + 1 < lend ? lp[j + 1] : 0.0;
+            const uint32_t qcap = phase == 2 ? 0u : 0xFFFFFFFFu;  // phase 2: the queue may not pass j
+            uint32_t c = cur, jj = j;
             bool out = false;
-            while (cur < stop) {
-                lval -= tb[cur - tbase];
-                ++cur;
+            // deficits two ahead in registers, unrolled by two so each stays
+            // in its own register (tb has kVoseStage + 2 slots: the look-ahead
+            // never leaves the stage); the next head's value is loaded ahead
+            double ta = tp[c], tb2 = tp[c + 1];
+            auto pair = [&](double& tr) -> bool {  // one pairing; true: leave the batch
+                lval -= tr;
+                tr = tp[c + 2];
+                ++c;
                 if (lval < 1.0) {
-                    park[n - 1 - j] = lval;  // the demoted value, read back in phase 2
-                    ++j;
-                    if (j == nl || j >= lend || (phase == 2 && cur >= j)) {
-                        out = true;
-                        break;
-                    }
-                    lval = lb[j - lbase];
+                    *pj-- = lval;  // the demoted value, read back in phase 2
+                    ++jj;
+                    if (jj >= lend || (c >= jj && qcap == 0u)) return out = true;
+                    lval = nv;
+                    nv = jj + 1 < lend ? lp[jj + 1] : 0.0;
                 }
+                return false;
+            };
+            for (;;) {
+                if (c >= stop || pair(ta)) break;
+                if (c >= stop || pair(tb2)) break;
             }
+            cur = c;
+            j = jj;
             if (j == nl) {
                 done = true;  // no large left: every remaining bucket is a leftover
             } else if (!out && cur == stop_x) {
