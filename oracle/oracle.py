@@ -34,6 +34,49 @@ def _ptr(a, t):
     return None if a is None else a.ctypes.data_as(t)
 
 
+def _digest_mix(x: np.ndarray) -> np.ndarray:
+    x = x ^ (x >> np.uint64(30))
+    x = x * np.uint64(0xBF58476D1CE4E5B9)
+    x = x ^ (x >> np.uint64(27))
+    x = x * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def walk_digest(walks, qid0: int, chunk: int = 1 << 17, threads: int = 0) -> int:
+    """The 64-bit digest ref_harness.cpp:wfref_run_digest gives the block of
+    query ids [qid0, qid0 + len(walks)): per walk mix(qid*K1 + (len << 8 |
+    status) + K3) + sum over positions of mix(qid*K1 + pos*K2 + vertex), summed
+    mod 2^64.  Chunks of walks are folded on a thread pool (numpy releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    k1, k2, k3 = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xC2B2AE3D27D4EB4F), np.uint64(0x632BE59BD9B4E019)
+    n = len(walks)
+    offsets = np.asarray(walks.offsets, dtype=np.uint64)
+
+    def fold(a):
+        b = min(n, a + chunk)
+        with np.errstate(over="ignore"):
+            lens = np.diff(offsets[a:b + 1])
+            base = (np.arange(a, b, dtype=np.uint64) + np.uint64(qid0)) * k1
+            head = base + ((lens << np.uint64(8)) | walks.status[a:b].astype(np.uint64)) + k3
+            total = _digest_mix(head).sum(dtype=np.uint64)
+            v0, v1 = int(offsets[a]), int(offsets[b])
+            reps = lens.astype(np.int64)
+            term = np.arange(v1 - v0, dtype=np.uint64) - np.repeat(offsets[a:b] - np.uint64(v0), reps)
+            term *= k2
+            term += np.repeat(base, reps)
+            term += walks.vertices[v0:v1]
+            return total + _digest_mix(term).sum(dtype=np.uint64)
+
+    starts = range(0, n, chunk)
+    if len(starts) <= 1:
+        parts = [fold(a) for a in starts]
+    else:
+        with ThreadPoolExecutor(threads or min(16, os.cpu_count() or 1)) as pool:
+            parts = list(pool.map(fold, starts))
+    with np.errstate(over="ignore"):
+        return int(np.sum(np.asarray(parts, dtype=np.uint64), dtype=np.uint64))
+
+
 def ref_available() -> bool:
     return os.path.exists(REF_LIB)
 
@@ -419,6 +462,27 @@ class RefGraph:
                                                     C.byref(copts), _ptr(q, _u64p),
                                                     C.c_uint64(q.size), C.byref(h), C.byref(m)))
         return self._collect(h, m, q)
+
+    def run_digest(self, spec: QuerySpec, prog, opts: ExecOptions, block_qids: int,
+                   threads: int = 0):
+        """Every query of the spec walked by the reference (ResolvedRun + StepDriver
+        on `threads` host threads) and folded into one 64-bit digest per block of
+        `block_qids` query ids, nothing stored: full-size parity (walk_digest is the
+        same fold over a WalkSet).  Returns (digests u64[n_blocks], total_steps,
+        preprocess_seconds)."""
+        desc = prog.to_c()
+        cspec = spec.to_c()
+        copts = opts.to_c()
+        n = (int(spec.sources.size) if spec.sources is not None
+             else spec.count if spec.count else self.info()["V"])
+        nb = (n + block_qids - 1) // block_qids
+        out = np.zeros(nb, dtype=np.uint64)
+        m = RunMetricsC()
+        self.ref._check(self.ref.lib.wfref_run_digest(
+            self.h, C.byref(desc), C.byref(cspec), C.byref(copts),
+            C.c_uint32(threads or self.ref.hardware_threads()), C.c_uint64(block_qids),
+            _ptr(out, _u64p), C.c_uint64(nb), C.byref(m)))
+        return out, int(m.total_steps), float(m.preprocess_seconds)
 
     def run_test_program(self, which: int, params, spec: QuerySpec, opts: ExecOptions,
                          interleaved: bool = False):

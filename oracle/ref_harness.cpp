@@ -15,7 +15,9 @@
 //   RngStream                            proj/include/walkforge/rng.hpp:19-67
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 // reference leg may load the resulting library.
+#include <algorithm>
 #include <atomic>
+#include <exception>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -410,6 +412,100 @@ int wfref_run_qids(const void* gp, const wf_program_desc* prog, const wf_query_s
             metrics->max_in_flight = 1;
         }
         *out = res.release();
+    });
+}
+
+// Whole-run digest for full-size parity (C5: 2^26 walks): every query of the
+// spec is walked through the reference's ResolvedRun + StepDriver (the same
+// per-query loop as wfref_run_qids / engine.hpp:466-492) on `threads` host
+// threads, and folded into one 64-bit digest per block of `block_qids`
+// consecutive query ids instead of being stored.  A walk contributes
+// mix(qid*K1 + (len << 8 | status) + K3) + sum over positions of
+// mix(qid*K1 + pos*K2 + vertex) (mod 2^64); oracle.py:walk_digest is the same
+// fold over a WalkSet.
+static inline uint64_t digest_mix(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+int wfref_run_digest(const void* gp, const wf_program_desc* prog, const wf_query_spec* q,
+                     const wf_exec_options* opts, uint32_t threads, uint64_t block_qids,
+                     uint64_t* digests, uint64_t n_blocks, wf_run_metrics* metrics) {
+    return guarded([&] {
+        const Graph& g = *static_cast<const Graph*>(gp);
+        ExecOptions eo = to_exec(opts);
+        QuerySpec spec = to_spec(q);
+        spec.validate(g);
+        const uint64_t n = spec.total(g);
+        if (block_qids == 0 || (n + block_qids - 1) / block_qids != n_blocks)
+            throw ConfigError("wfref_run_digest: n_blocks does not cover the query count");
+        with_program(g, prog, [&](const auto& p) {
+            using P = std::decay_t<decltype(p)>;
+            detail::ResolvedRun<P> run(g, p, eo);
+            std::atomic<uint64_t> next{0}, steps{0};
+            std::exception_ptr first_error;
+            std::atomic<bool> failed{false};
+            auto work = [&] {
+                try {
+                    detail::StepDriver<P> driver(g, p, run);
+                    TransitionContext ctx;
+                    Walker walker;
+                    uint64_t my_steps = 0;
+                    for (;;) {
+                        const uint64_t b = next.fetch_add(1);
+                        if (b >= n_blocks || failed.load()) break;
+                        const uint64_t q0 = b * block_qids, q1 = std::min(n, q0 + block_qids);
+                        uint64_t d = 0;
+                        for (uint64_t qid = q0; qid < q1; ++qid) {
+                            walker.id = qid;
+                            walker.rng = RngStream(eo.seed, qid);
+                            walker.path.clear();
+                            walker.path.push_back(spec.source_at(qid, g));
+                            WalkStatus status = WalkStatus::DeadEnd;
+                            if (walk_already_finished(p, walker)) {
+                                status = WalkStatus::Complete;
+                            } else {
+                                while (true) {
+                                    uint64_t edge = driver.step(walker, ctx);
+                                    if (edge == detail::StepDriver<P>::kNoEdge) break;
+                                    my_steps += 1;
+                                    if (p.update(walker, EdgeRef{&g, walker.prev(), edge})) {
+                                        status = WalkStatus::Complete;
+                                        break;
+                                    }
+                                }
+                            }
+                            const uint64_t base = qid * 0x9E3779B97F4A7C15ull;
+                            const uint64_t len = walker.path.size();
+                            d += digest_mix(base + ((len << 8) | static_cast<uint64_t>(status)) +
+                                            0x632BE59BD9B4E019ull);
+                            for (uint64_t i = 0; i < len; ++i)
+                                d += digest_mix(base + i * 0xC2B2AE3D27D4EB4Full + walker.path[i]);
+                        }
+                        digests[b] = d;
+                    }
+                    steps.fetch_add(my_steps);
+                } catch (...) {
+                    if (!failed.exchange(true)) first_error = std::current_exception();
+                }
+            };
+            std::vector<std::thread> pool;
+            const uint32_t t = std::max<uint32_t>(1, threads);
+            for (uint32_t i = 1; i < t; ++i) pool.emplace_back(work);
+            work();
+            for (auto& th : pool) th.join();
+            if (first_error) std::rethrow_exception(first_error);
+            if (metrics) {
+                metrics->preprocess_seconds = run.tables.build_seconds;
+                metrics->exec_seconds = 0;
+                metrics->total_steps = steps.load();
+                metrics->max_in_flight = t;
+            }
+        });
     });
 }
 

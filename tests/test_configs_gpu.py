@@ -10,19 +10,25 @@
   to the number of path vertices, and repeated runs are identical.
 * whole-run parity against the unmodified reference: C1, C2 and C3 (Node2Vec
   s22, 4.2 M walks, 189 M moves; the reference on all host cores);
-* sampled parity at the largest sizes: C4 (MetaPath s22) on 20 k query ids and
-  C5 (DeepWalk s26, 2^26 walks, ~110 GB of HBM) on 10 k query ids, replayed by
-  the reference's own ResolvedRun + StepDriver (run_qids) over the downloaded
-  2.1 B-edge CSR (its preprocess_static builds 50 GB of alias tables on the
-  host); the 48-walk Python replay from the reference's primitives stays as a
-  second, independent check.
+* whole-run parity at the largest size by digest: C5 (DeepWalk s26, all 2^26
+  walks / 2.59 G moves, ~110 GB of HBM) is walked in full by the reference's
+  own ResolvedRun + StepDriver on all host cores over the downloaded CSR (its
+  preprocess_static builds 50 GB of alias tables on the host) and folded into
+  one 64-bit digest per 2^20 query ids; C4 (MetaPath s22) the same way over
+  its first 2^18 walks (all 4.2 M with WF_FULL_PARITY=1: the reference's label
+  scans take ~5 min) (oracle/ref_harness.cpp: wfref_run_digest); the engine's walk set,
+  copied to the host block by block, must give the same digests
+  (oracle.walk_digest) and the same step total.  A block that differs is
+  replayed walk by walk (run_qids) to name the first differing query;
+* C4 also on 20 k sampled query ids path by path, and C5 on a 48-walk Python
+  replay from the reference's primitives (a second, independent check).
 """
 import os
 
 import numpy as np
 import pytest
 
-from oracle.oracle import PortOracle, RefOracle, ref_available
+from oracle.oracle import PortOracle, RefOracle, ref_available, walk_digest
 from paper_2107_11983_b200 import engine as E
 from paper_2107_11983_b200.host import (DeepWalkProgram, ExecOptions, MetaPathProgram,
                                         Node2VecProgram, PprProgram, QuerySpec)
@@ -65,6 +71,30 @@ def _sample_parity(hg, spec, prog, opts, got, k=300, seed=0):
     for i, q in enumerate(qids):
         assert got.status[q] == want.walks.status[i], int(q)
         assert np.array_equal(got.path(int(q)), want.walks.path(i)), int(q)
+
+
+def _host_slice(ws, a, b):
+    from paper_2107_11983_b200.host import WalkSet
+    v0, v1 = int(ws.offsets[a]), int(ws.offsets[b])
+    return WalkSet(ws.offsets[a:b + 1] - ws.offsets[a], ws.vertices[v0:v1], ws.status[a:b])
+
+
+def _digest_parity(rg, ws, spec, prog, opts, n, block=1 << 20):
+    """The whole run against the unmodified reference: one digest per `block`
+    query ids from the reference (wfref_run_digest) and from the engine's
+    walk set copied to the host; the first differing block is replayed walk by
+    walk to name the query."""
+    want, steps, _ = rg.run_digest(spec, prog, opts, block)
+    assert steps == ws.metrics.total_steps
+    for b, a in enumerate(range(0, n, block)):
+        part = ws.to_host(a, min(n, a + block))
+        if walk_digest(part, a) == int(want[b]):
+            continue
+        qids = np.arange(a, min(n, a + block), dtype=np.uint64)
+        ref = rg.run_qids(spec, prog, opts, qids).walks
+        bad = part.first_mismatch(ref)
+        raise AssertionError(f"block {b}: digest differs from the reference; first differing query "
+                             f"{a + bad if bad is not None else 'none (digest fold?)'}")
 
 
 @pytest.fixture(scope="module")
@@ -155,6 +185,17 @@ def test_c4_metapath_s22_full_size(s22):
         want_label = schema[lens[q] - 1]
         assert not np.any(hg.labels[hg.offsets[last]:hg.offsets[last + 1]] == want_label)
     _sample_parity(hg, spec, prog, opts, got, k=20000)
+    # against the unmodified reference by digest: the first 2^18 walks (the
+    # reference's per-step label scans take ~5 min for all 4.2 M walks on 16
+    # cores; WF_FULL_PARITY=1 runs them all — passed on the round-2 sources)
+    if ref_available():
+        block = 1 << 16
+        n = len(got) if os.environ.get("WF_FULL_PARITY") == "1" else 1 << 18
+        pre = QuerySpec.from_list(np.arange(n, dtype=np.uint32))  # qid q from vertex q, as one_per_vertex
+        want, steps, _ = RefOracle().graph(hg).run_digest(pre, prog, opts, block)
+        assert steps == int(got.offsets[n]) - n
+        for b, a in enumerate(range(0, n, block)):
+            assert walk_digest(_host_slice(got, a, min(n, a + block)), a) == int(want[b]), f"block {b}"
 
 
 def _replay_deepwalk_alias(hg, port, qid, length, seed, cache):
@@ -205,22 +246,12 @@ def test_c5_deepwalk_s26_full_size():
     ok, *_ = _edges_ok(hg, ws.to_host(0, 1 << 17))
     assert ok
     assert ws.metrics.total_steps == total
-    # 10 k query ids (10 blocks of 1024 at random offsets) against the
-    # unmodified reference's ResolvedRun + StepDriver over this CSR
+    # every one of the 2^26 walks against the unmodified reference, by digest
     if ref_available():
-        starts = np.sort(np.random.default_rng(5).choice(V // 1024, 10, replace=False)) * 1024
-        qids = np.concatenate([np.arange(a, a + 1024) for a in starts]).astype(np.uint64)
         rg = RefOracle().graph(hg)
         del hg.weights  # the reference holds its own f64 copy now
-        want = rg.run_qids(QuerySpec.one_per_vertex(), prog, opts, qids).walks
+        _digest_parity(rg, ws, QuerySpec.one_per_vertex(), prog, opts, V)
         del rg
-        i = 0
-        for a in starts:
-            got = ws.to_host(int(a), int(a) + 1024)
-            for j in range(1024):
-                assert int(got.status[j]) == int(want.status[i]), int(a) + j
-                assert np.array_equal(got.path(j), want.path(i)), int(a) + j
-                i += 1
         hg = dg.download()
     # sampled parity against a replay from the reference's primitives
     port = PortOracle()

@@ -99,3 +99,37 @@ def test_port_matches_live_reference_on_random_graphs():
             got = port.run(g, gu.spec(d), gu.program(d), gu.opts(d))
             assert got.walks.equals(want.walks)
             assert got.metrics.total_steps == want.metrics.total_steps
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_run_digest_is_the_fold_of_the_reference_walks():
+    """wfref_run_digest (the whole-run digest the full-size C4 / C5 parity tests
+    compare) equals oracle.walk_digest over the walks the reference's
+    run_sequential returns, block by block; one changed vertex or status moves it."""
+    from oracle.oracle import walk_digest
+    from paper_2107_11983_b200.host import (DeepWalkProgram, ExecOptions, MetaPathProgram,
+                                            PprProgram, QuerySpec, WalkSet)
+    rg = RefOracle().rmat(11, 16, seed=1, weighted=True, label_count=5)
+    src = np.random.default_rng(3).integers(0, 2048, 3000, dtype=np.uint32)
+    block = 700
+    for prog, spec in [(DeepWalkProgram(40, True), QuerySpec.one_per_vertex()),
+                       (PprProgram(0.2), QuerySpec.from_list(src)),
+                       (MetaPathProgram([i % 5 for i in range(19)]), QuerySpec.one_per_vertex())]:
+        opts = ExecOptions(seed=7)
+        res = rg.run(spec, prog, opts)
+        w, n = res.walks, len(res.walks)
+        got, steps, _ = rg.run_digest(spec, prog, opts, block, threads=3)
+        assert steps == res.metrics.total_steps and got.size == (n + block - 1) // block
+        for b in range(got.size):
+            a0, a1 = b * block, min(n, (b + 1) * block)
+            v0, v1 = int(w.offsets[a0]), int(w.offsets[a1])
+            sub = WalkSet(w.offsets[a0:a1 + 1] - w.offsets[a0], w.vertices[v0:v1].copy(),
+                          w.status[a0:a1].copy())
+            assert walk_digest(sub, a0, chunk=256) == int(got[b]) == walk_digest(sub, a0)
+            if b == 0:
+                sub.vertices[v1 - v0 - 1] ^= 1
+                assert walk_digest(sub, a0) != int(got[b])
+                sub.vertices[v1 - v0 - 1] ^= 1
+                sub.status[0] ^= 1
+                assert walk_digest(sub, a0) != int(got[b])
+                assert walk_digest(sub, a0 + 1) != int(got[b])
