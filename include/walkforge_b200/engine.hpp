@@ -313,7 +313,8 @@ struct RunResult {
     RunMetrics metrics;
 };
 using BlockSink = std::function<void(uint32_t worker, WalkSet&& block)>;
-enum class PrefetchLevel : uint8_t { None, L1, L2, L3 };
+// prefetch.hpp:17 (same enumerators; software prefetch hints have no device meaning)
+enum class PrefetchLevel : uint8_t { L1, L2, L3, NonTemporal, Off };
 struct ExecOptions {
     uint32_t threads = 1;
     uint64_t seed = 0;
@@ -465,6 +466,40 @@ inline std::pair<uint64_t, uint64_t> worker_range(uint64_t n, uint32_t workers, 
     return {n * w / workers, n * (w + 1) / workers};  // engine.hpp:296-298
 }
 
+// RunMetrics::max_in_flight as the reference defines it (engine.hpp:68: peak
+// ring occupancy of any worker; 1 for run_sequential, engine.hpp:502): a
+// worker's ring holds min(k, its walks that were not already finished at
+// admission) (interleave.hpp:436-467) — a walk finished at admission is the
+// one stored Complete with its source alone.  The device's own residency
+// (resident walker lanes) is wf_run_metrics.max_in_flight of the C-ABI.
+struct RingPeak {
+    uint32_t k = 0;  // 0: run_sequential
+    uint32_t workers = 1;
+    uint64_t n = 0;
+    std::vector<uint64_t> live;
+    void init(uint32_t ring, uint32_t w, uint64_t total) {
+        k = ring;
+        workers = w;
+        n = total;
+        live.assign(w, 0);
+    }
+    void count(uint32_t worker, uint32_t rec) {  // rec: length | dead_end << 31
+        if (rec != 1u) live[worker] += 1;
+    }
+    uint32_t worker_of(uint64_t q) const {  // inverse of worker_range (engine.hpp:296-298)
+        uint32_t w = static_cast<uint32_t>(static_cast<unsigned __int128>(q) * workers / std::max<uint64_t>(n, 1));
+        while (w + 1 < workers && n * (w + 1) / workers <= q) ++w;
+        while (w > 0 && n * w / workers > q) --w;
+        return w;
+    }
+    uint32_t value() const {
+        if (k == 0) return 1;
+        uint64_t peak = 0;
+        for (uint64_t l : live) peak = std::max(peak, std::min<uint64_t>(k, l));
+        return static_cast<uint32_t>(peak);
+    }
+};
+
 // Turns the streamed records + vertices into WalkRecords as blocks land, and
 // hands the sink one block per worker range (engine.hpp:446-495: `workers` =
 // max(1, threads) contiguous qid ranges, sink(w, block) once each, in order).
@@ -480,6 +515,7 @@ struct StreamSink {
     WalkSet block;
     bool delivered = false;
     std::exception_ptr error;
+    RingPeak* ring = nullptr;
 
     void flush_empty_workers() {  // ranges with no queries still get their (empty) block
         while (sink && next_worker < workers && worker_range(n, workers, next_worker).second <= next_q) {
@@ -491,6 +527,7 @@ struct StreamSink {
         for (uint64_t q = next_q; q < q1; ++q) {
             const uint32_t rec = records[q];
             const uint32_t len = rec & 0x7FFFFFFFu;
+            if (ring) ring->count(ring->worker_of(q), rec);
             WalkRecord r{q, (rec >> 31) ? WalkStatus::DeadEnd : WalkStatus::Complete,
                          std::vector<VertexId>(vertices + next_v, vertices + next_v + len)};
             next_v += len;
@@ -548,7 +585,7 @@ inline void validate_spec(const Graph& g, const QuerySpec& spec) {
 // guess (each block is sized after its walks ran).
 template <typename P>
 RunResult run_blocks(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts,
-                     uint32_t n_devices) {
+                     uint32_t n_devices, uint32_t ring_k) {
     const wf_exec_options o = to_c(opts);
     std::vector<int32_t> devs;
     int32_t total = 1;
@@ -566,11 +603,14 @@ RunResult run_blocks(const Graph& g, const QuerySpec& spec, const P& prog, const
     const uint32_t workers = std::max<uint32_t>(1, opts.threads);
     RunResult r;
     if (!opts.sink) r.walks.resize(n);
+    RingPeak ring;
+    ring.init(ring_k, workers, n);
     struct Ctx {
         RunResult* r;
         const BlockSink* sink;
         std::exception_ptr error;
-    } ctx{&r, opts.sink ? &opts.sink : nullptr, nullptr};
+        RingPeak* ring;
+    } ctx{&r, opts.sink ? &opts.sink : nullptr, nullptr, &ring};
     auto on_shard = [](void* user, uint32_t w, uint64_t q0, uint64_t q1, const uint32_t* rec,
                        const uint32_t* verts, uint64_t) -> int {
         auto* c = static_cast<Ctx*>(user);
@@ -579,6 +619,7 @@ RunResult run_blocks(const Graph& g, const QuerySpec& spec, const P& prog, const
             uint64_t v = 0;
             for (uint64_t q = q0; q < q1; ++q) {
                 const uint32_t len = rec[q - q0] & 0x7FFFFFFFu;
+                c->ring->count(w, rec[q - q0]);
                 WalkRecord wr{q, (rec[q - q0] >> 31) ? WalkStatus::DeadEnd : WalkStatus::Complete,
                               std::vector<VertexId>(verts + v, verts + v + len)};
                 v += len;
@@ -597,12 +638,13 @@ RunResult run_blocks(const Graph& g, const QuerySpec& spec, const P& prog, const
     const int rc = wf_multi_run(m, &q, workers, on_shard, &ctx, nullptr, &mt);
     if (ctx.error) std::rethrow_exception(ctx.error);
     check(rc);
-    r.metrics = {mt.preprocess_seconds, mt.exec_seconds, mt.total_steps, mt.max_in_flight};
+    r.metrics = {mt.preprocess_seconds, mt.exec_seconds, mt.total_steps, ring.value()};
     return r;
 }
 
 template <typename P>
-RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts) {
+RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOptions& opts,
+              uint32_t ring_k = 0) {
     validate_spec(g, spec);
     const uint64_t n = spec.total(g);
     uint64_t per;
@@ -613,7 +655,7 @@ RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOp
     check(wf_device_count(&ndev));
     const uint32_t workers = std::max<uint32_t>(1, opts.threads);
     const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(workers, static_cast<uint32_t>(std::max(ndev, 1))));
-    if (G > 1 || per == 0) return run_blocks(g, spec, prog, opts, G);
+    if (G > 1 || per == 0) return run_blocks(g, spec, prog, opts, G, ring_k);
 
     // one device, bounded walks: the walks stream into host memory block by
     // block (wf_session_run_host_blocks) and become WalkRecords while later
@@ -637,6 +679,9 @@ RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOp
     st.vertices = vertices.get();
     st.n = n;
     st.workers = workers;
+    RingPeak ring;
+    ring.init(ring_k, workers, n);
+    st.ring = &ring;
     if (opts.sink) {
         st.sink = &opts.sink;
     } else {
@@ -649,7 +694,7 @@ RunResult run(const Graph& g, const QuerySpec& spec, const P& prog, const ExecOp
     if (st.error) std::rethrow_exception(st.error);
     check(rc);
     st.flush_empty_workers();
-    r.metrics = {m.preprocess_seconds, m.exec_seconds, m.total_steps, m.max_in_flight};
+    r.metrics = {m.preprocess_seconds, m.exec_seconds, m.total_steps, ring.value()};
     return r;
 }
 }  // namespace detail
@@ -665,7 +710,7 @@ RunResult run_interleaved(const Graph& g, const QuerySpec& spec, const P& prog, 
                           uint32_t k_prime, const ExecOptions& opts = {}) {
     if (k == 0) throw ConfigError("task ring size must be >= 1");
     if (k_prime == 0 || k_prime > k) throw ConfigError("search ring size must be in [1, k]");
-    return detail::run(g, spec, prog, opts);
+    return detail::run(g, spec, prog, opts, k);
 }
 
 // ---- tune_ring_sizes (tune.hpp:12-42, tune.cpp:46-111) -----------------------------------

@@ -1,0 +1,508 @@
+// The reference's own unit suites for the hot path — "engine"
+// (/root/reference/proj/tests/test_engine.cpp:62-262) and "interleave"
+// (/root/reference/proj/tests/test_interleave.cpp:47-191) — re-expressed against
+// the drop-in shim (WALKFORGE_B200_DROP_IN: namespace walkforge), case by case
+// under the reference's case names, with the reference's call patterns:
+// run_sequential / run_interleaved, ExecOptions, BlockSink, custom programs.
+// No doctest here (absent from the image): a case is a function, a failed
+// expectation prints its line, the process exits with the number of failed
+// cases.  Inputs are small graphs built through Graph::from_csr; the
+// reference's random fixtures are replaced by a seeded generator of this
+// file's own (the cases check invariants, not golden values — bit-exactness
+// against the reference is tests/test_engine_gpu.py's job).
+// The custom programs are the device versions in tests/programs/test_programs.cu.
+#define WALKFORGE_B200_DROP_IN
+#include "walkforge_b200/engine.hpp"
+
+#include <cstdio>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <optional>
+#include <string>
+#include <utility>
+#include <vector>
+
+using namespace walkforge;
+
+extern "C" const wf_program_ops* wf_test_counting_program(void);
+extern "C" const wf_program_ops* wf_test_avoid_vertex_program(void);
+extern "C" const wf_program_ops* wf_test_negative_weight_program(void);
+extern "C" unsigned long long* wf_test_counter_new(void);
+extern "C" unsigned long long wf_test_counter_read(const unsigned long long*);
+extern "C" void wf_test_counter_free(unsigned long long*);
+
+namespace {
+struct CountingObj {  // host mirrors of the device programs' layouts
+    uint32_t length;
+    unsigned long long* updates;
+};
+struct AvoidVertexObj {
+    uint32_t banned, length;
+};
+struct NegativeObj {
+    uint32_t unused;
+};
+
+int g_failed_checks = 0;
+#define EXPECT(cond)                                                         \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            std::printf("    line %d: expected %s\n", __LINE__, #cond);      \
+            ++g_failed_checks;                                               \
+        }                                                                    \
+    } while (0)
+#define EXPECT_THROWS(expr, Type)                                            \
+    do {                                                                     \
+        bool caught_ = false;                                                \
+        try {                                                                \
+            (void)(expr);                                                    \
+        } catch (const Type&) {                                              \
+            caught_ = true;                                                  \
+        } catch (const std::exception& e_) {                                 \
+            std::printf("    line %d: %s threw %s\n", __LINE__, #expr, e_.what()); \
+        }                                                                    \
+        if (!caught_) {                                                      \
+            std::printf("    line %d: expected %s from %s\n", __LINE__, #Type, #expr); \
+            ++g_failed_checks;                                               \
+        }                                                                    \
+    } while (0)
+
+using EdgeList = std::vector<std::pair<VertexId, VertexId>>;
+
+// directed edges as given, grouped by source in input order
+Graph graph_of(uint32_t n, const EdgeList& edges, const std::vector<double>& weights = {},
+               const std::vector<uint32_t>& labels = {}) {
+    std::vector<uint64_t> off(n + 1, 0);
+    for (auto& e : edges) off[e.first + 1] += 1;
+    for (uint32_t v = 0; v < n; ++v) off[v + 1] += off[v];
+    std::vector<uint64_t> at(off.begin(), off.end() - 1);
+    std::vector<VertexId> nbr(edges.size());
+    std::vector<double> w(weights.empty() ? 0 : edges.size());
+    std::vector<uint32_t> lab(labels.empty() ? 0 : edges.size());
+    for (size_t i = 0; i < edges.size(); ++i) {
+        const uint64_t p = at[edges[i].first]++;
+        nbr[p] = edges[i].second;
+        if (!weights.empty()) w[p] = weights[i];
+        if (!labels.empty()) lab[p] = labels[i];
+    }
+    return Graph::from_csr(off, nbr, w, lab);
+}
+Graph triangle() { return graph_of(3, {{0, 1}, {1, 2}, {2, 0}}); }  // 0 -> 1 -> 2 -> 0
+Graph line(uint32_t n) {                                               // 0 -> 1 -> ... -> n-1
+    EdgeList e;
+    for (uint32_t v = 0; v + 1 < n; ++v) e.push_back({v, v + 1});
+    return graph_of(n, e);
+}
+Graph clique(uint32_t n) {
+    EdgeList e;
+    for (uint32_t u = 0; u < n; ++u)
+        for (uint32_t v = 0; v < n; ++v)
+            if (u != v) e.push_back({u, v});
+    return graph_of(n, e);
+}
+// a skewed random multigraph (hubs at the low ids), every vertex with an out-edge
+Graph skewed_graph(uint32_t n, uint32_t m, uint64_t seed, bool weighted = false, uint32_t label_count = 0) {
+    uint64_t s = seed * 0x9E3779B97F4A7C15ull + 12345;
+    auto next = [&] {
+        s += 0x9E3779B97F4A7C15ull;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    };
+    auto skew = [&] {
+        const double u = static_cast<double>(next() >> 11) * 0x1.0p-53;
+        return static_cast<VertexId>(u * u * n);
+    };
+    EdgeList e;
+    std::vector<double> w;
+    std::vector<uint32_t> lab;
+    for (uint32_t i = 0; i < m; ++i) {
+        const VertexId u = i < n ? i : skew(), v = skew();
+        e.push_back({u, v});
+        e.push_back({v, u});
+        const double x = 1.0 + static_cast<double>(next() % 4000) / 1000.0;
+        const uint32_t l = label_count ? static_cast<uint32_t>(next() % label_count) : 0;
+        for (int r = 0; r < 2; ++r) {
+            if (weighted) w.push_back(x);
+            if (label_count) lab.push_back(l);
+        }
+    }
+    return graph_of(n, e, w, lab);
+}
+bool scan_edge(const Graph& g, VertexId u, VertexId v) {
+    for (VertexId x : g.neighbors(u))
+        if (x == v) return true;
+    return false;
+}
+bool adjacency_holds(const Graph& g, const WalkSet& walks) {
+    for (const WalkRecord& r : walks)
+        for (size_t i = 0; i + 1 < r.path.size(); ++i)
+            if (!scan_edge(g, r.path[i], r.path[i + 1])) return false;
+    return true;
+}
+
+// ---- suite "engine" (test_engine.cpp) -------------------------------------------------------
+void fixed_length_walks_hit_their_target_exactly() {  // :63
+    Graph g = triangle();
+    RunResult res = run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 12, false));
+    EXPECT(res.walks.size() == 3);
+    for (const WalkRecord& r : res.walks) {
+        EXPECT(r.status == WalkStatus::Complete);
+        EXPECT(r.path.size() == 12);
+    }
+    EXPECT(res.metrics.total_steps == 3 * 11);
+    EXPECT(adjacency_holds(g, res.walks));
+}
+void target_length_one_completes_without_a_single_move() {  // :75
+    Graph g = triangle();
+    RunResult res = run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 1, false));
+    EXPECT(res.walks.size() == 3);
+    for (const WalkRecord& r : res.walks) {
+        EXPECT(r.status == WalkStatus::Complete);
+        EXPECT(r.path.size() == 1);
+    }
+    EXPECT(res.metrics.total_steps == 0);
+}
+void dead_ends_emit_the_partial_path_with_the_right_status() {  // :85
+    Graph g = line(4);
+    RunResult res = run_sequential(g, QuerySpec::from_source(0, 1), DeepWalkProgram(g, 10, false));
+    EXPECT(res.walks.size() == 1);
+    EXPECT(res.walks[0].status == WalkStatus::DeadEnd);
+    EXPECT((res.walks[0].path == std::vector<VertexId>{0, 1, 2, 3}));
+}
+void results_are_invariant_to_thread_count() {  // :93
+    Graph g = skewed_graph(300, 1200, 8);
+    ExecOptions one, four;
+    one.threads = 1;
+    one.seed = 123;
+    four.threads = 4;
+    four.seed = 123;
+    RunResult a = run_sequential(g, QuerySpec::one_per_vertex(), PprProgram(0.2), one);
+    RunResult b = run_sequential(g, QuerySpec::one_per_vertex(), PprProgram(0.2), four);
+    EXPECT(a.walks == b.walks);
+    EXPECT(a.walks.size() == 300);
+}
+void static_tables_and_per_step_gather_agree_for_every_table_sampler() {  // :106
+    Graph g = skewed_graph(200, 800, 4, true);
+    DeepWalkProgram prog(g, 10, true);
+    for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej}) {
+        ExecOptions tables;
+        tables.sampler = kind;
+        tables.seed = 5;
+        ExecOptions gathered = tables;
+        gathered.use_static_tables = false;
+        RunResult a = run_sequential(g, QuerySpec::one_per_vertex(), prog, tables);
+        RunResult b = run_sequential(g, QuerySpec::one_per_vertex(), prog, gathered);
+        EXPECT(a.walks == b.walks);
+        EXPECT(a.metrics.preprocess_seconds >= 0.0);
+    }
+}
+void unbiased_programs_run_under_every_sampling_method_identically_in_law() {  // :123
+    Graph g = skewed_graph(100, 450, 2);
+    for (SamplerKind kind : {SamplerKind::Naive, SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej,
+                             SamplerKind::ORej}) {
+        ExecOptions opts;
+        opts.sampler = kind;
+        opts.seed = 31;
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 4000), PprProgram(0.2), opts);
+        const double mean = static_cast<double>(res.metrics.total_steps) / 4000.0;
+        EXPECT(mean > 4.0);
+        EXPECT(mean < 6.0);
+    }
+}
+void illegal_pairings_are_refused_up_front() {  // :143
+    Graph g = triangle();
+    ExecOptions naive;
+    naive.sampler = SamplerKind::Naive;
+    EXPECT_THROWS(run_sequential(g, QuerySpec::one_per_vertex(), DeepWalkProgram(g, 5, false), naive), ConfigError);
+    ExecOptions orej;
+    orej.sampler = SamplerKind::ORej;
+    unsigned long long* ctr = wf_test_counter_new();
+    DeviceProgram no_bound(wf_test_counting_program(), CountingObj{5, ctr});  // no max_weight()
+    EXPECT_THROWS(run_sequential(g, QuerySpec::one_per_vertex(), no_bound, orej), ConfigError);
+    wf_test_counter_free(ctr);
+    Graph labeled = graph_of(3, {{0, 1}, {1, 2}, {2, 0}}, {}, {0, 0, 0});
+    EXPECT_THROWS(run_sequential(labeled, QuerySpec::one_per_vertex(), MetaPathProgram(labeled, {0, 0}), orej),
+                  ConfigError);
+}
+void a_program_emitting_negative_weights_is_caught() {  // :164
+    Graph g = triangle();
+    DeviceProgram neg(wf_test_negative_weight_program(), NegativeObj{0});
+    EXPECT_THROWS(run_sequential(g, QuerySpec::one_per_vertex(), neg), ContractError);
+}
+void zero_weight_edges_are_never_traversed() {  // :171
+    Graph g = clique(4);
+    DeviceProgram prog(wf_test_avoid_vertex_program(), AvoidVertexObj{2, 16});
+    for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej}) {
+        ExecOptions opts;
+        opts.sampler = kind;
+        opts.seed = 7;
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 200), prog, opts);
+        EXPECT(res.walks.size() == 200);
+        for (const WalkRecord& r : res.walks) {
+            EXPECT(r.status == WalkStatus::Complete);
+            EXPECT(r.path.size() == 16);
+            for (VertexId v : r.path) EXPECT(v != 2);
+        }
+    }
+}
+void vertices_whose_weights_all_vanish_dead_end_their_walkers() {  // :188
+    Graph g = graph_of(3, {{0, 1}, {1, 2}});
+    DeviceProgram prog(wf_test_avoid_vertex_program(), AvoidVertexObj{2, 16});
+    ExecOptions opts;
+    opts.sampler = SamplerKind::Alias;
+    RunResult res = run_sequential(g, QuerySpec::from_source(0, 4), prog, opts);
+    EXPECT(res.walks.size() == 4);
+    for (const WalkRecord& r : res.walks) {
+        EXPECT(r.status == WalkStatus::DeadEnd);
+        EXPECT((r.path == std::vector<VertexId>{0, 1}));
+    }
+}
+void update_runs_exactly_once_per_completed_move() {  // :201
+    Graph g = triangle();
+    unsigned long long* ctr = wf_test_counter_new();
+    DeviceProgram prog(wf_test_counting_program(), CountingObj{9, ctr});
+    RunResult res = run_sequential(g, QuerySpec::one_per_vertex(), prog);
+    EXPECT(wf_test_counter_read(ctr) == res.metrics.total_steps);
+    EXPECT(res.metrics.total_steps == 3 * 8);
+    wf_test_counter_free(ctr);
+}
+void sink_mode_streams_the_same_records_the_walk_set_would_hold() {  // :210
+    Graph g = skewed_graph(120, 350, 3);
+    ExecOptions plain;
+    plain.threads = 3;
+    plain.seed = 17;
+    RunResult expected = run_sequential(g, QuerySpec::one_per_vertex(), PprProgram(0.3), plain);
+    std::map<uint32_t, WalkSet> blocks;
+    std::mutex mu;
+    ExecOptions streamed = plain;
+    streamed.sink = [&](uint32_t worker, WalkSet&& block) {
+        std::lock_guard lock(mu);
+        blocks[worker] = std::move(block);
+    };
+    RunResult res = run_sequential(g, QuerySpec::one_per_vertex(), PprProgram(0.3), streamed);
+    EXPECT(res.walks.empty());
+    EXPECT(blocks.size() == 3);
+    WalkSet merged;
+    for (auto& [worker, block] : blocks)
+        for (WalkRecord& r : block) merged.push_back(std::move(r));
+    EXPECT(merged == expected.walks);
+}
+void query_specs_validate_their_sources() {  // :236
+    Graph g = triangle();
+    EXPECT_THROWS(run_sequential(g, QuerySpec::from_source(9, 5), PprProgram(0.2)), ConfigError);
+    EXPECT(QuerySpec::one_per_vertex().total(g) == 3);
+    EXPECT(QuerySpec::from_source(0, 42).total(g) == 42);
+}
+void doubling_the_step_count_does_not_blow_past_linear_scaling() {  // :244
+    Graph g = skewed_graph(400, 2000, 6);
+    QuerySpec spec = QuerySpec::from_source(0, 3000);
+    bool ok = false;
+    for (int attempt = 0; attempt < 3 && !ok; ++attempt) {
+        auto time_for = [&](uint32_t length) {
+            RunResult res = run_sequential(g, spec, DeepWalkProgram(g, length, false));
+            return res.metrics.exec_seconds;
+        };
+        time_for(11);
+        const double t1 = time_for(11), t2 = time_for(21);
+        ok = t2 <= 2.5 * t1 + 1e-4;
+    }
+    EXPECT(ok);
+}
+
+// ---- suite "interleave" (test_interleave.cpp) ------------------------------------------------
+Graph matrix_graph() {
+    static Graph g = skewed_graph(160, 700, 11, true, 4);
+    return g;
+}
+template <typename P>
+void check_equivalence(const Graph& g, const P& prog, SamplerKind kind, bool use_tables = true) {  // :23
+    ExecOptions opts;
+    opts.sampler = kind;
+    opts.seed = 99;
+    opts.use_static_tables = use_tables;
+    QuerySpec spec = QuerySpec::one_per_vertex();
+    RunResult base = run_sequential(g, spec, prog, opts);
+    EXPECT(base.metrics.max_in_flight == 1);  // engine.hpp:502
+    for (uint32_t k : {1u, 3u, 8u, 64u}) {
+        for (uint32_t k_prime : {1u, std::max(1u, k / 2), k}) {
+            RunResult inter = run_interleaved(g, spec, prog, k, k_prime, opts);
+            EXPECT(inter.walks == base.walks);
+            EXPECT(inter.metrics.total_steps == base.metrics.total_steps);
+            EXPECT(inter.metrics.max_in_flight <= k);
+            EXPECT(inter.metrics.max_in_flight >= 1);
+        }
+    }
+}
+void interleaved_execution_replays_the_sequential_run_exactly() {  // :48
+    Graph g = matrix_graph();
+    {  // unbiased walks
+        PprProgram ppr(0.25);
+        for (SamplerKind kind : {SamplerKind::Naive, SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej,
+                                 SamplerKind::ORej})
+            check_equivalence(g, ppr, kind);
+    }
+    {  // statically weighted walks through tables
+        DeepWalkProgram dw(g, 14, true);
+        for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej, SamplerKind::ORej})
+            check_equivalence(g, dw, kind);
+    }
+    {  // statically weighted walks gathered per step
+        DeepWalkProgram dw(g, 14, true);
+        for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej})
+            check_equivalence(g, dw, kind, /*use_tables=*/false);
+    }
+    {  // dynamically weighted walks
+        Node2VecProgram n2v(g, {.a = 2.0, .b = 0.5, .target_length = 12}, true);
+        for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej, SamplerKind::ORej})
+            check_equivalence(g, n2v, kind);
+    }
+    {  // label-constrained walks
+        MetaPathProgram mp(g, {0, 1, 2, 1});
+        for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej})
+            check_equivalence(g, mp, kind);
+    }
+}
+void multi_threaded_interleaving_matches_as_well() {  // :91
+    Graph g = matrix_graph();
+    DeepWalkProgram dw(g, 14, true);
+    ExecOptions opts;
+    opts.seed = 5;
+    RunResult base = run_sequential(g, QuerySpec::one_per_vertex(), dw, opts);
+    ExecOptions threaded = opts;
+    threaded.threads = 4;
+    RunResult inter = run_interleaved(g, QuerySpec::one_per_vertex(), dw, 16, 8, threaded);
+    EXPECT(inter.walks == base.walks);
+    EXPECT(inter.metrics.max_in_flight <= 16);
+}
+void ring_sizes_are_validated() {  // :104
+    Graph g = triangle();
+    PprProgram ppr(0.5);
+    QuerySpec spec = QuerySpec::one_per_vertex();
+    EXPECT_THROWS(run_interleaved(g, spec, ppr, 0, 1), ConfigError);
+    EXPECT_THROWS(run_interleaved(g, spec, ppr, 4, 0), ConfigError);
+    EXPECT_THROWS(run_interleaved(g, spec, ppr, 4, 8), ConfigError);
+    RunResult ok = run_interleaved(g, spec, ppr, 4, 4);
+    EXPECT(ok.walks.size() == 3);
+}
+void rings_larger_than_the_query_set_stay_correct() {  // :114
+    Graph g = triangle();
+    DeepWalkProgram dw(g, 6, false);
+    RunResult base = run_sequential(g, QuerySpec::one_per_vertex(), dw);
+    RunResult inter = run_interleaved(g, QuerySpec::one_per_vertex(), dw, 256, 128);
+    EXPECT(inter.walks == base.walks);
+    EXPECT(inter.metrics.max_in_flight <= 3);
+}
+void prefetch_level_does_not_change_results() {  // :123
+    Graph g = matrix_graph();
+    DeepWalkProgram dw(g, 10, true);
+    std::optional<RunResult> previous;
+    for (PrefetchLevel level : {PrefetchLevel::L1, PrefetchLevel::L3, PrefetchLevel::Off}) {
+        ExecOptions opts;
+        opts.seed = 44;
+        opts.prefetch = level;
+        RunResult res = run_interleaved(g, QuerySpec::one_per_vertex(), dw, 32, 16, opts);
+        if (previous) EXPECT(res.walks == previous->walks);
+        previous = std::move(res);
+    }
+}
+void walks_of_target_length_one_bypass_the_rings() {  // :139
+    Graph g = triangle();
+    DeepWalkProgram dw(g, 1, false);
+    RunResult res = run_interleaved(g, QuerySpec::one_per_vertex(), dw, 8, 4);
+    EXPECT(res.walks.size() == 3);
+    for (const WalkRecord& r : res.walks) {
+        EXPECT(r.status == WalkStatus::Complete);
+        EXPECT(r.path.size() == 1);
+    }
+    EXPECT(res.metrics.total_steps == 0);
+    EXPECT(res.metrics.max_in_flight == 0);
+}
+void rejection_trial_caps_propagate() {  // :152
+    // the walker circles vertex 0, where one edge sits far below the vertex
+    // envelope: half of all trials reject, so a cap of 2 trips within a few steps
+    Graph g = graph_of(2, {{0, 0}, {0, 1}, {1, 1}}, {1.0, 1e-6, 1.0});
+    DeepWalkProgram dw(g, 50, true);
+    ExecOptions opts;
+    opts.sampler = SamplerKind::Rej;
+    opts.rej_trial_cap = 2;
+    bool threw_somewhere = false;
+    for (uint64_t seed = 0; seed < 8 && !threw_somewhere; ++seed) {
+        opts.seed = seed;
+        try {
+            run_interleaved(g, QuerySpec::one_per_vertex(), dw, 4, 2, opts);
+        } catch (const RejectionCapError&) {
+            threw_somewhere = true;
+        }
+    }
+    EXPECT(threw_somewhere);
+}
+void sink_mode_emits_ordered_blocks_identical_to_the_walk_set() {  // :173
+    Graph g = matrix_graph();
+    PprProgram ppr(0.3);
+    ExecOptions plain;
+    plain.seed = 12;
+    RunResult expected = run_interleaved(g, QuerySpec::one_per_vertex(), ppr, 16, 8, plain);
+    WalkSet streamed;
+    ExecOptions opts = plain;
+    opts.sink = [&](uint32_t, WalkSet&& block) {
+        for (WalkRecord& r : block) streamed.push_back(std::move(r));
+    };
+    RunResult res = run_interleaved(g, QuerySpec::one_per_vertex(), ppr, 16, 8, opts);
+    EXPECT(res.walks.empty());
+    EXPECT(streamed == expected.walks);
+}
+}  // namespace
+
+int main() {
+    const std::vector<std::pair<const char*, std::function<void()>>> cases = {
+        {"engine: fixed-length walks hit their target exactly", fixed_length_walks_hit_their_target_exactly},
+        {"engine: target length one completes without a single move",
+         target_length_one_completes_without_a_single_move},
+        {"engine: dead ends emit the partial path with the right status",
+         dead_ends_emit_the_partial_path_with_the_right_status},
+        {"engine: results are invariant to thread count", results_are_invariant_to_thread_count},
+        {"engine: static tables and per-step gather agree for every table sampler",
+         static_tables_and_per_step_gather_agree_for_every_table_sampler},
+        {"engine: unbiased programs run under every sampling method identically in law",
+         unbiased_programs_run_under_every_sampling_method_identically_in_law},
+        {"engine: illegal pairings are refused up front", illegal_pairings_are_refused_up_front},
+        {"engine: a program emitting negative weights is caught", a_program_emitting_negative_weights_is_caught},
+        {"engine: zero-weight edges are never traversed", zero_weight_edges_are_never_traversed},
+        {"engine: vertices whose weights all vanish dead-end their walkers",
+         vertices_whose_weights_all_vanish_dead_end_their_walkers},
+        {"engine: update runs exactly once per completed move", update_runs_exactly_once_per_completed_move},
+        {"engine: sink mode streams the same records the walk set would hold",
+         sink_mode_streams_the_same_records_the_walk_set_would_hold},
+        {"engine: query specs validate their sources", query_specs_validate_their_sources},
+        {"engine: doubling the step count does not blow past linear scaling",
+         doubling_the_step_count_does_not_blow_past_linear_scaling},
+        {"interleave: interleaved execution replays the sequential run exactly",
+         interleaved_execution_replays_the_sequential_run_exactly},
+        {"interleave: multi-threaded interleaving matches as well", multi_threaded_interleaving_matches_as_well},
+        {"interleave: ring sizes are validated", ring_sizes_are_validated},
+        {"interleave: rings larger than the query set stay correct", rings_larger_than_the_query_set_stay_correct},
+        {"interleave: prefetch level does not change results", prefetch_level_does_not_change_results},
+        {"interleave: walks of target length one bypass the rings", walks_of_target_length_one_bypass_the_rings},
+        {"interleave: rejection trial caps propagate", rejection_trial_caps_propagate},
+        {"interleave: sink mode emits ordered blocks identical to the walk set",
+         sink_mode_emits_ordered_blocks_identical_to_the_walk_set},
+    };
+    int failed = 0;
+    for (auto& [name, fn] : cases) {
+        const int before = g_failed_checks;
+        try {
+            fn();
+        } catch (const std::exception& e) {
+            std::printf("    unexpected exception: %s\n", e.what());
+            ++g_failed_checks;
+        }
+        const bool ok = g_failed_checks == before;
+        std::printf("%s %s\n", ok ? "ok  " : "FAIL", name);
+        failed += ok ? 0 : 1;
+    }
+    std::printf("%zu cases, %d failed\n", cases.size(), failed);
+    return failed;
+}

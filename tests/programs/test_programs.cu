@@ -85,3 +85,19 @@ WF_DEVICE_PROGRAM(AvoidVertexProgram, wf_test_avoid_vertex_program)
 WF_DEVICE_PROGRAM(NegativeWeightProgram, wf_test_negative_weight_program)
 WF_DEVICE_PROGRAM(LabelWeightProgram, wf_test_label_weight_program)
 WF_DEVICE_PROGRAM(LabelStopProgram, wf_test_label_stop_program)
+
+// A counting program owns device memory of its own: these let a plain C++
+// caller (tests/cpp/ref_suite.cpp, compiled with g++) create and read the
+// counter CountingProgram::updates points at.
+extern "C" unsigned long long* wf_test_counter_new(void) {
+    unsigned long long* p = nullptr;
+    if (cudaMalloc(&p, sizeof(*p)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, sizeof(*p));
+    return p;
+}
+extern "C" unsigned long long wf_test_counter_read(const unsigned long long* p) {
+    unsigned long long v = 0;
+    cudaMemcpy(&v, p, sizeof(v), cudaMemcpyDeviceToHost);
+    return v;
+}
+extern "C" void wf_test_counter_free(unsigned long long* p) { cudaFree(p); }
