@@ -207,6 +207,10 @@ int wf_graph_download(const wf_graph* g, uint64_t* offsets, uint32_t* neighbors,
 /* Membership test, Graph::has_edge (graph.cpp:182-188), batched on the device. */
 int wf_graph_has_edge(const wf_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
                       uint8_t* out);
+/* Which labels occur on some edge: out[l] = 1 for l in [0, 256), else 0 (all 0
+ * when unlabeled).  MetaPathProgram's constructor check (algorithms.hpp:151-160)
+ * without a scan: the flags are computed once at graph creation. */
+int wf_graph_labels_present(const wf_graph* g, uint8_t out[256]);
 void wf_graph_destroy(wf_graph* g);
 
 /* ---- graph ingest (graph.cpp:190-453) -------------------------------------- */

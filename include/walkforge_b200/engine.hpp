@@ -333,6 +333,7 @@ public:
             throw ConfigError("termination probability must be in (0, 1], got " + std::to_string(termination));
     }
     WalkerType walker_type() const { return WalkerType::Unbiased; }
+    double max_weight() const { return 1.0; }
     double termination() const { return stop_; }
     wf_program_desc to_desc() const {
         wf_program_desc d{};
@@ -351,8 +352,10 @@ public:
         : length_(target_length), weighted_(weighted) {
         if (target_length < 1) throw ConfigError("target length must be >= 1");
         if (weighted && !g.has_weights()) throw ConfigError("weighted walks need a graph with edge weights");
+        bound_ = weighted ? g.max_weight() : 1.0;  // algorithms.hpp:51
     }
     WalkerType walker_type() const { return WalkerType::Static; }
+    double max_weight() const { return bound_; }
     uint32_t target_length() const { return length_; }
     wf_program_desc to_desc() const {
         wf_program_desc d{};
@@ -365,6 +368,7 @@ public:
 private:
     uint32_t length_;
     bool weighted_;
+    double bound_ = 1.0;
 };
 
 struct Node2VecParams {
@@ -381,9 +385,12 @@ public:
         if (!(std::isfinite(params.b) && params.b > 0.0)) throw ConfigError("in-out parameter b must be positive and finite");
         if (params.target_length < 1) throw ConfigError("target length must be >= 1");
         if (weighted && !g.has_weights()) throw ConfigError("weighted walks need a graph with edge weights");
+        const double first = std::max({1.0 / params.a, 1.0, 1.0 / params.b});  // algorithms.hpp:95-98
+        bound_ = weighted ? first * g.max_weight() : first;
     }
     WalkerType walker_type() const { return WalkerType::Dynamic; }
     SamplerKind preferred_sampler() const { return SamplerKind::ORej; }
+    double max_weight() const { return bound_; }
     const Node2VecParams& params() const { return params_; }
     wf_program_desc to_desc() const {
         wf_program_desc d{};
@@ -398,6 +405,7 @@ public:
 private:
     Node2VecParams params_;
     bool weighted_;
+    double bound_ = 1.0;
 };
 
 class MetaPathProgram {
@@ -405,6 +413,12 @@ public:
     MetaPathProgram(const Graph& g, std::vector<uint32_t> schema) : schema_(std::move(schema)) {
         if (!g.has_labels()) throw ConfigError("meta-path walks need a graph with edge labels");
         if (schema_.empty()) throw ConfigError("meta-path schema must be non-empty");
+        // every schema label must occur in the graph (algorithms.hpp:151-160)
+        uint8_t present[256];
+        check(wf_graph_labels_present(g.handle(), present));
+        for (uint32_t l : schema_)
+            if (l > 255 || !present[l])
+                throw ConfigError("schema label " + std::to_string(l) + " does not occur in the graph");
     }
     WalkerType walker_type() const { return WalkerType::Dynamic; }
     const std::vector<uint32_t>& schema() const { return schema_; }
@@ -449,6 +463,7 @@ public:
         if (target_length < 1) throw ConfigError("target length must be >= 1");
     }
     WalkerType walker_type() const { return WalkerType::Unbiased; }
+    double max_weight() const { return 1.0; }
     wf_program_desc to_desc() const {
         wf_program_desc d{};
         d.kind = WF_PROGRAM_UNIFORM;
@@ -459,6 +474,21 @@ public:
 private:
     uint32_t length_;
 };
+
+// ---- program.hpp:28-36, 68-75: the sampling method a program runs under by default ------
+inline SamplerKind default_sampler(WalkerType type) {
+    switch (type) {
+        case WalkerType::Unbiased: return SamplerKind::Naive;
+        case WalkerType::Static: return SamplerKind::Alias;
+        case WalkerType::Dynamic: return SamplerKind::Its;
+    }
+    return SamplerKind::Its;
+}
+template <typename P>
+SamplerKind resolve_default_sampler(const P& prog) {
+    if constexpr (requires { prog.preferred_sampler(); }) return prog.preferred_sampler();
+    else return default_sampler(prog.walker_type());
+}
 
 // ---- run_sequential / run_interleaved (engine.hpp:440-504, interleave.hpp:391-556) ---
 namespace detail {

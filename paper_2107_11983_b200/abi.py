@@ -232,7 +232,7 @@ EXPORTED_SYMBOLS = [
     "wf_abi_version", "wf_last_error", "wf_kernel_launches", "wf_device_count",
     "wf_graph_create", "wf_graph_create_f64", "wf_graph_download_weights_f64",
     "wf_graph_create_device", "wf_graph_generate_rmat",
-    "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_destroy",
+    "wf_graph_info_get", "wf_graph_download", "wf_graph_has_edge", "wf_graph_labels_present", "wf_graph_destroy",
     "wf_graph_read_wfg1", "wf_graph_write_wfg1", "wf_graph_load_edge_list", "wf_graph_original_ids",
     "wf_session_create", "wf_session_describe", "wf_session_destroy", "wf_session_run",
     "wf_session_launch", "wf_session_sync", "wf_session_run_host", "wf_session_run_host_records",

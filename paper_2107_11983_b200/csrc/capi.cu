@@ -413,6 +413,13 @@ int wf_graph_has_edge(const wf_graph* g, const uint32_t* src, const uint32_t* ds
     });
 }
 
+int wf_graph_labels_present(const wf_graph* g, uint8_t out[256]) {
+    return guarded([&] {
+        require(g && out, "null argument");
+        for (int l = 0; l < 256; ++l) out[l] = g->g->has_labels() ? g->g->label_present[l] : 0;
+    });
+}
+
 int wf_graph_read_wfg1(const char* path, int device, wf_graph** out) {
     return guarded([&] {
         require(path && out, "null argument");

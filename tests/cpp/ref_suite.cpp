@@ -1,6 +1,9 @@
 // The reference's own unit suites for the hot path — "engine"
-// (/root/reference/proj/tests/test_engine.cpp:62-262) and "interleave"
-// (/root/reference/proj/tests/test_interleave.cpp:47-191) — re-expressed against
+// (/root/reference/proj/tests/test_engine.cpp:62-262), "interleave"
+// (/root/reference/proj/tests/test_interleave.cpp:47-191) and "algorithms"
+// (/root/reference/proj/tests/test_algorithms.cpp:13-215; where the reference
+// evaluates a program's weight() on the host, the case measures the same
+// transition through walks instead) — re-expressed against
 // the drop-in shim (WALKFORGE_B200_DROP_IN: namespace walkforge), case by case
 // under the reference's case names, with the reference's call patterns:
 // run_sequential / run_interleaved, ExecOptions, BlockSink, custom programs.
@@ -14,8 +17,10 @@
 #define WALKFORGE_B200_DROP_IN
 #include "walkforge_b200/engine.hpp"
 
+#include <cmath>
 #include <cstdio>
 #include <functional>
+#include <limits>
 #include <map>
 #include <mutex>
 #include <optional>
@@ -454,6 +459,198 @@ void sink_mode_emits_ordered_blocks_identical_to_the_walk_set() {  // :173
     EXPECT(res.walks.empty());
     EXPECT(streamed == expected.walks);
 }
+
+// ---- suite "algorithms" (test_algorithms.cpp) -------------------------------------------------
+Graph ring(uint32_t n) {  // v <-> v+1 (mod n)
+    EdgeList e;
+    for (uint32_t v = 0; v < n; ++v) {
+        e.push_back({v, (v + 1) % n});
+        e.push_back({v, (v + n - 1) % n});
+    }
+    return graph_of(n, e);
+}
+Graph fan(const std::vector<double>& weights) {  // 0 -> 1..n with the given weights
+    EdgeList e;
+    for (uint32_t i = 0; i < weights.size(); ++i) e.push_back({0, i + 1});
+    return graph_of(static_cast<uint32_t>(weights.size()) + 1, e, weights);
+}
+bool near(double x, double want, double rel) { return std::fabs(x - want) <= rel * std::fabs(want); }
+
+void restart_walks_stop_geometrically() {  // :14
+    Graph g = ring(64);
+    {  // probability one stops after the first move
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 500), PprProgram(1.0));
+        EXPECT(res.walks.size() == 500);
+        for (const WalkRecord& r : res.walks) {
+            EXPECT(r.status == WalkStatus::Complete);
+            EXPECT(r.path.size() == 2);
+        }
+    }
+    {  // mean step count approaches the geometric expectation
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 20000), PprProgram(0.2));
+        EXPECT(near(static_cast<double>(res.metrics.total_steps) / 20000.0, 5.0, 0.03));
+    }
+    {  // termination probability is validated
+        EXPECT_THROWS(PprProgram(0.0), ConfigError);
+        EXPECT_THROWS(PprProgram(-0.5), ConfigError);
+        EXPECT_THROWS(PprProgram(1.5), ConfigError);
+        EXPECT_THROWS(PprProgram(std::nan("")), ConfigError);
+    }
+}
+void fixed_length_walk_weights_follow_the_edge_weights() {  // :40
+    {  // target length and weighted mode are validated
+        Graph g = triangle();
+        EXPECT_THROWS(DeepWalkProgram(g, 0, false), ConfigError);
+        EXPECT_THROWS(DeepWalkProgram(g, 10, true), ConfigError);
+    }
+    {  // first-step frequencies match the weight ratio
+        Graph g = fan({1.0, 3.0});
+        DeepWalkProgram prog(g, 2, true);
+        EXPECT(prog.max_weight() == 3.0);
+        for (SamplerKind kind : {SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej}) {
+            ExecOptions opts;
+            opts.sampler = kind;
+            opts.seed = 21;
+            RunResult res = run_sequential(g, QuerySpec::from_source(0, 20000), prog, opts);
+            uint64_t heavy = 0;
+            for (const WalkRecord& r : res.walks) {
+                EXPECT(r.path.size() == 2);
+                heavy += r.path.size() == 2 && r.path[1] == 2;
+            }
+            EXPECT(near(static_cast<double>(heavy) / 20000.0, 0.75, 0.02));
+        }
+    }
+    {  // unweighted mode ignores stored weights
+        Graph g = fan({1.0, 99.0});
+        DeepWalkProgram prog(g, 2, false);
+        ExecOptions opts;
+        opts.sampler = SamplerKind::Alias;
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 20000), prog, opts);
+        uint64_t heavy = 0;
+        for (const WalkRecord& r : res.walks) heavy += r.path[1] == 2;
+        EXPECT(near(static_cast<double>(heavy) / 20000.0, 0.5, 0.05));
+    }
+}
+// share of the walks [0, 1, y] with y == 2 among those that went 0 -> 1 first
+double forward_share(const Graph& g, const Node2VecProgram& prog, SamplerKind kind, uint64_t& seen) {
+    ExecOptions opts;
+    opts.sampler = kind;
+    opts.seed = 77;
+    RunResult res = run_sequential(g, QuerySpec::from_source(0, 80000), prog, opts);
+    uint64_t via1 = 0, forward = 0;
+    for (const WalkRecord& r : res.walks) {
+        if (r.path.size() == 3 && r.path[1] == 1) {
+            via1 += 1;
+            forward += r.path[2] == 2;
+        }
+    }
+    seen = via1;
+    return via1 ? static_cast<double>(forward) / static_cast<double>(via1) : 0.0;
+}
+void second_order_walk_weights_depend_on_the_previous_vertex() {  // :80
+    // out of vertex 1 with the walk at [0, 1]: back to 0 scores 1/a = 0.5, on to
+    // 2 (adjoins 0) 1, on to 3 (does not) 1/b = 2 -> 1/7, 2/7, 4/7
+    Graph g = graph_of(4, {{0, 1}, {0, 2}, {1, 0}, {1, 2}, {1, 3}});
+    Node2VecProgram prog(g, {.a = 2.0, .b = 0.5, .target_length = 3}, false);
+    for (SamplerKind kind : {SamplerKind::ORej, SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej}) {
+        ExecOptions opts;
+        opts.sampler = kind;
+        opts.seed = 9;
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 80000), prog, opts);
+        uint64_t via1 = 0, to[4] = {0, 0, 0, 0};
+        for (const WalkRecord& r : res.walks)
+            if (r.path.size() == 3 && r.path[1] == 1) {
+                via1 += 1;
+                to[r.path[2]] += 1;
+            }
+        EXPECT(via1 > 30000);  // the first move scores every edge at the shared maximum: 1/2 each
+        EXPECT(near(static_cast<double>(via1) / 80000.0, 0.5, 0.03));
+        EXPECT(near(static_cast<double>(to[0]) / via1, 1.0 / 7.0, 0.05));
+        EXPECT(near(static_cast<double>(to[2]) / via1, 2.0 / 7.0, 0.04));
+        EXPECT(near(static_cast<double>(to[3]) / via1, 4.0 / 7.0, 0.03));
+    }
+    EXPECT(prog.max_weight() == 2.0);  // the weight bound covers every reachable weight
+    // parameters are validated
+    EXPECT_THROWS(Node2VecProgram(g, {.a = 0.0, .b = 0.5}, false), ConfigError);
+    EXPECT_THROWS(Node2VecProgram(g, {.a = 2.0, .b = -1.0}, false), ConfigError);
+    EXPECT_THROWS(Node2VecProgram(g, {.a = std::numeric_limits<double>::infinity(), .b = 1.0}, false), ConfigError);
+    EXPECT_THROWS(Node2VecProgram(g, {.target_length = 0}, false), ConfigError);
+    EXPECT_THROWS(Node2VecProgram(g, {}, true), ConfigError);
+}
+void second_order_transitions_match_the_hand_computed_distribution() {  // :117
+    // undirected triangle: from [0, 1] back to 0 (1/a = 0.5) or on to 2, a neighbor of 0 (1) -> 1/3 vs 2/3
+    Graph g = graph_of(3, {{0, 1}, {0, 2}, {1, 0}, {1, 2}, {2, 0}, {2, 1}});
+    Node2VecProgram prog(g, {.a = 2.0, .b = 0.5, .target_length = 3}, false);
+    for (SamplerKind kind : {SamplerKind::ORej, SamplerKind::Its}) {
+        uint64_t seen = 0;
+        const double share = forward_share(g, prog, kind, seen);
+        EXPECT(seen > 30000);
+        EXPECT(near(share, 2.0 / 3.0, 0.02));
+    }
+}
+void weighted_second_order_walks_scale_by_the_edge_weight() {  // :145
+    Graph g = graph_of(3, {{0, 1}, {0, 2}, {1, 0}, {1, 2}, {2, 0}, {2, 1}}, {1.0, 1.0, 2.0, 4.0, 1.0, 1.0});
+    Node2VecProgram prog(g, {.a = 2.0, .b = 0.5, .target_length = 3}, true);
+    EXPECT(prog.max_weight() == 2.0 * 4.0);
+    // from [0, 1]: back to 0 scores 0.5 * 2, on to 2 scores 1 * 4 -> 1/5 vs 4/5
+    for (SamplerKind kind : {SamplerKind::ORej, SamplerKind::Its, SamplerKind::Alias}) {
+        uint64_t seen = 0;
+        const double share = forward_share(g, prog, kind, seen);
+        EXPECT(seen > 30000);
+        EXPECT(near(share, 0.8, 0.02));
+    }
+}
+void label_constrained_walks_obey_the_schema() {  // :157
+    Graph g = graph_of(4, {{0, 1}, {0, 2}, {1, 2}, {2, 3}, {3, 0}}, {}, {0, 1, 1, 2, 0});
+    {  // a fully matching path completes
+        MetaPathProgram prog(g, {0, 1, 2});
+        RunResult res = run_sequential(g, QuerySpec::from_source(0, 50), prog);
+        EXPECT(res.walks.size() == 50);
+        for (const WalkRecord& r : res.walks) {
+            EXPECT(r.status == WalkStatus::Complete);
+            EXPECT((r.path == std::vector<VertexId>{0, 1, 2, 3}));
+        }
+    }
+    {  // a vertex with no edge of the wanted label dead-ends
+        MetaPathProgram prog(g, {0, 1, 2});
+        RunResult res = run_sequential(g, QuerySpec::from_source(1, 50), prog);
+        for (const WalkRecord& r : res.walks) {
+            EXPECT(r.status == WalkStatus::DeadEnd);
+            EXPECT((r.path == std::vector<VertexId>{1}));
+        }
+    }
+    {  // construction is validated
+        EXPECT_THROWS(MetaPathProgram(g, {}), ConfigError);
+        EXPECT_THROWS(MetaPathProgram(g, {0, 9}), ConfigError);
+        Graph bare = triangle();
+        EXPECT_THROWS(MetaPathProgram(bare, {0}), ConfigError);
+    }
+    {  // the unknown label is named in the error
+        bool named = false;
+        try {
+            MetaPathProgram prog(g, {0, 7, 2});
+        } catch (const ConfigError& e) {
+            named = std::string(e.what()).find('7') != std::string::npos;
+        }
+        EXPECT(named);
+    }
+}
+void uniform_fixed_length_walks_need_no_weights_at_all() {  // :196
+    Graph g = triangle();
+    UniformProgram prog(5);
+    RunResult res = run_sequential(g, QuerySpec::one_per_vertex(), prog);
+    EXPECT(res.walks.size() == 3);
+    for (const WalkRecord& r : res.walks) EXPECT(r.path.size() == 5);
+    EXPECT_THROWS(UniformProgram(0), ConfigError);
+}
+void each_program_lands_on_its_expected_default_sampling_method() {  // :206
+    Graph g = graph_of(4, {{0, 1}, {0, 2}, {1, 2}, {2, 3}, {3, 0}}, {}, {0, 1, 1, 2, 0});
+    EXPECT(resolve_default_sampler(PprProgram(0.2)) == SamplerKind::Naive);
+    EXPECT(resolve_default_sampler(DeepWalkProgram(g, 5, false)) == SamplerKind::Alias);
+    EXPECT(resolve_default_sampler(Node2VecProgram(g, {}, false)) == SamplerKind::ORej);
+    EXPECT(resolve_default_sampler(MetaPathProgram(g, {0, 1})) == SamplerKind::Its);
+    EXPECT(resolve_default_sampler(UniformProgram(3)) == SamplerKind::Naive);
+}
 }  // namespace
 
 int main() {
@@ -489,6 +686,20 @@ int main() {
         {"interleave: rejection trial caps propagate", rejection_trial_caps_propagate},
         {"interleave: sink mode emits ordered blocks identical to the walk set",
          sink_mode_emits_ordered_blocks_identical_to_the_walk_set},
+        {"algorithms: restart walks stop geometrically", restart_walks_stop_geometrically},
+        {"algorithms: fixed-length walk weights follow the edge weights",
+         fixed_length_walk_weights_follow_the_edge_weights},
+        {"algorithms: second-order walk weights depend on the previous vertex",
+         second_order_walk_weights_depend_on_the_previous_vertex},
+        {"algorithms: second-order transitions match the hand-computed distribution",
+         second_order_transitions_match_the_hand_computed_distribution},
+        {"algorithms: weighted second-order walks scale by the edge weight",
+         weighted_second_order_walks_scale_by_the_edge_weight},
+        {"algorithms: label-constrained walks obey the schema", label_constrained_walks_obey_the_schema},
+        {"algorithms: uniform fixed-length walks need no weights at all",
+         uniform_fixed_length_walks_need_no_weights_at_all},
+        {"algorithms: each program lands on its expected default sampling method",
+         each_program_lands_on_its_expected_default_sampling_method},
     };
     int failed = 0;
     for (auto& [name, fn] : cases) {
