@@ -221,6 +221,34 @@ inline LoadedGraph load_edge_list(const std::string& path, const EdgeListOptions
     return lg;
 }
 
+// ---- build_graph (graph.hpp:141-144, graph.cpp:289-305) -----------------------------------
+// CSR assembly from an unsorted edge set: edges ordered by (source,
+// destination), input order breaking ties, weights and labels following their
+// edges; then Graph::from_csr's validation.
+inline Graph build_graph(uint32_t vertex_count, std::vector<std::pair<VertexId, VertexId>> edges,
+                         std::vector<double> weights = {}, std::vector<uint32_t> labels = {}, int device = 0) {
+    if (!weights.empty() && weights.size() != edges.size()) throw ConfigError("weight array does not match edge count");
+    if (!labels.empty() && labels.size() != edges.size()) throw ConfigError("label array does not match edge count");
+    for (const auto& e : edges)
+        if (e.first >= vertex_count || e.second >= vertex_count) throw ConfigError("edge endpoint out of range");
+    std::vector<uint64_t> order(edges.size());
+    for (uint64_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return edges[a] < edges[b]; });
+    std::vector<uint64_t> offsets(static_cast<size_t>(vertex_count) + 1, 0);
+    std::vector<VertexId> neighbors(edges.size());
+    std::vector<double> w(weights.empty() ? 0 : edges.size());
+    std::vector<uint32_t> l(labels.empty() ? 0 : edges.size());
+    for (uint64_t p = 0; p < order.size(); ++p) {
+        const uint64_t i = order[p];
+        offsets[edges[i].first + 1] += 1;
+        neighbors[p] = edges[i].second;
+        if (!w.empty()) w[p] = weights[i];
+        if (!l.empty()) l[p] = labels[i];
+    }
+    for (uint32_t v = 0; v < vertex_count; ++v) offsets[v + 1] += offsets[v];
+    return Graph::from_csr(std::move(offsets), std::move(neighbors), std::move(w), std::move(l), device);
+}
+
 // ---- walker.hpp:47-84 ------------------------------------------------------------------
 struct WalkRecord {
     uint64_t query_id = 0;

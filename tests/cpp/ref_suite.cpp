@@ -1,9 +1,12 @@
 // The reference's own unit suites for the hot path — "engine"
 // (/root/reference/proj/tests/test_engine.cpp:62-262), "interleave"
-// (/root/reference/proj/tests/test_interleave.cpp:47-191) and "algorithms"
+// (/root/reference/proj/tests/test_interleave.cpp:47-191), "algorithms"
 // (/root/reference/proj/tests/test_algorithms.cpp:13-215; where the reference
 // evaluates a program's weight() on the host, the case measures the same
-// transition through walks instead) — re-expressed against
+// transition through walks instead) and "graph"
+// (/root/reference/proj/tests/test_graph.cpp:18-196; its two cases on the
+// reference's synthetic fixture generators are not part of the drop-in) —
+// re-expressed against
 // the drop-in shim (WALKFORGE_B200_DROP_IN: namespace walkforge), case by case
 // under the reference's case names, with the reference's call patterns:
 // run_sequential / run_interleaved, ExecOptions, BlockSink, custom programs.
@@ -19,7 +22,10 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <functional>
+#include <iterator>
 #include <limits>
 #include <map>
 #include <mutex>
@@ -75,23 +81,10 @@ int g_failed_checks = 0;
 
 using EdgeList = std::vector<std::pair<VertexId, VertexId>>;
 
-// directed edges as given, grouped by source in input order
+// the reference's build_graph (graph.hpp:143): adjacency sorted, attributes follow their edges
 Graph graph_of(uint32_t n, const EdgeList& edges, const std::vector<double>& weights = {},
                const std::vector<uint32_t>& labels = {}) {
-    std::vector<uint64_t> off(n + 1, 0);
-    for (auto& e : edges) off[e.first + 1] += 1;
-    for (uint32_t v = 0; v < n; ++v) off[v + 1] += off[v];
-    std::vector<uint64_t> at(off.begin(), off.end() - 1);
-    std::vector<VertexId> nbr(edges.size());
-    std::vector<double> w(weights.empty() ? 0 : edges.size());
-    std::vector<uint32_t> lab(labels.empty() ? 0 : edges.size());
-    for (size_t i = 0; i < edges.size(); ++i) {
-        const uint64_t p = at[edges[i].first]++;
-        nbr[p] = edges[i].second;
-        if (!weights.empty()) w[p] = weights[i];
-        if (!labels.empty()) lab[p] = labels[i];
-    }
-    return Graph::from_csr(off, nbr, w, lab);
+    return build_graph(n, edges, weights, labels);
 }
 Graph triangle() { return graph_of(3, {{0, 1}, {1, 2}, {2, 0}}); }  // 0 -> 1 -> 2 -> 0
 Graph line(uint32_t n) {                                               // 0 -> 1 -> ... -> n-1
@@ -651,9 +644,173 @@ void each_program_lands_on_its_expected_default_sampling_method() {  // :206
     EXPECT(resolve_default_sampler(MetaPathProgram(g, {0, 1})) == SamplerKind::Its);
     EXPECT(resolve_default_sampler(UniformProgram(3)) == SamplerKind::Naive);
 }
+
+// ---- suite "graph" (test_graph.cpp) ---------------------------------------------------------
+std::string g_tmp;  // scratch directory (argv[1])
+std::string tmp_file(const std::string& name) { return g_tmp + "/" + name; }
+void write_file(const std::string& path, const std::string& bytes) {
+    std::ofstream(path, std::ios::binary) << bytes;
+}
+std::string read_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    return std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+}
+Graph star(uint32_t leaves) {  // hub 0 connected both ways to leaves 1..n
+    EdgeList e;
+    for (uint32_t v = 1; v <= leaves; ++v) {
+        e.push_back({0, v});
+        e.push_back({v, 0});
+    }
+    return graph_of(leaves + 1, e);
+}
+
+void csr_assembly_sorts_adjacency_and_keeps_attributes_aligned() {  // :19
+    Graph g = build_graph(3, {{1, 2}, {0, 2}, {0, 1}, {2, 0}}, {12.0, 2.0, 1.0, 20.0});
+    EXPECT(g.vertex_count() == 3);
+    EXPECT(g.edge_count() == 4);
+    EXPECT(g.degree(0) == 2);
+    EXPECT(g.neighbors(0)[0] == 1);
+    EXPECT(g.neighbors(0)[1] == 2);
+    EXPECT(g.weight(g.edge_begin(0)) == 1.0);
+    EXPECT(g.weight(g.edge_begin(0) + 1) == 2.0);
+    EXPECT(g.weight(g.edge_begin(1)) == 12.0);
+    EXPECT(g.weight(g.edge_begin(2)) == 20.0);
+    EXPECT(g.adjacency_sorted());
+}
+void edge_existence_via_binary_search() {  // :36
+    Graph g = star(5);
+    EXPECT(g.has_edge(0, 3));
+    EXPECT(g.has_edge(3, 0));
+    EXPECT(!g.has_edge(1, 2));
+    EXPECT(!g.has_edge(2, 2));
+}
+void degree_zero_vertices_are_just_dead_ends_not_errors() {  // :44
+    Graph g = line(4);
+    EXPECT(g.degree(3) == 0);
+    EXPECT(g.neighbors(3).empty());
+}
+void from_csr_validates_structure() {  // :50
+    EXPECT_THROWS(Graph::from_csr({0}, {}), ConfigError);                   // zero vertices
+    EXPECT_THROWS(Graph::from_csr({0, 2}, {0}), ConfigError);               // framing
+    EXPECT_THROWS(Graph::from_csr({0, 2, 1}, {0, 0}), ConfigError);         // non-monotone
+    EXPECT_THROWS(Graph::from_csr({0, 1}, {5}), ConfigError);               // id range
+    EXPECT_THROWS(Graph::from_csr({0, 1}, {0}, {-1.0}), ConfigError);       // negative weight
+    EXPECT_THROWS(Graph::from_csr({0, 1}, {0}, {1.0, 2.0}), ConfigError);   // length
+    EXPECT_THROWS(Graph::from_csr({0, 1}, {0}, {}, {1, 2}), ConfigError);   // labels length
+}
+void binary_files_round_trip_bit_exactly() {  // :60
+    Graph g = build_graph(4, {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {0, 2}}, {1.0, 2.5, 3.25, 4.125, 0.5},
+                          {0, 1, 2, 3, 4});
+    const std::string a = tmp_file("a.wfg"), b = tmp_file("b.wfg");
+    g.write_binary(a);
+    Graph loaded = Graph::read_binary(a);
+    loaded.write_binary(b);
+    EXPECT(read_file(a) == read_file(b));
+    EXPECT(!read_file(a).empty());
+    EXPECT(loaded.vertex_count() == 4);
+    EXPECT(loaded.edge_count() == 5);
+    EXPECT(loaded.weight(1) == g.weight(1));
+    EXPECT(loaded.label(4) == g.label(4));
+}
+void binary_reader_rejects_corruption() {  // :76
+    Graph g = triangle();
+    const std::string path = tmp_file("g.wfg");
+    g.write_binary(path);
+    const std::string bytes = read_file(path);
+    std::string bad_magic = bytes;
+    bad_magic[0] = 'X';
+    write_file(tmp_file("magic.wfg"), bad_magic);
+    EXPECT_THROWS(Graph::read_binary(tmp_file("magic.wfg")), FormatError);
+    write_file(tmp_file("trunc.wfg"), bytes.substr(0, bytes.size() - 3));
+    EXPECT_THROWS(Graph::read_binary(tmp_file("trunc.wfg")), FormatError);
+    write_file(tmp_file("trail.wfg"), bytes + "xx");
+    EXPECT_THROWS(Graph::read_binary(tmp_file("trail.wfg")), FormatError);
+    EXPECT_THROWS(Graph::read_binary(tmp_file("missing.wfg")), IoError);
+}
+void edge_list_loader_handles_comments_blanks_and_weights() {  // :97
+    const std::string path = tmp_file("edges.txt");
+    write_file(path, "# comment line\n0 1 2.5\n\n1 2 0.5\n2 0 1.5\n");
+    EdgeListOptions options;
+    options.weights = WeightMode::FromFile;
+    LoadedGraph loaded = load_edge_list(path, options);
+    EXPECT(loaded.graph.vertex_count() == 3);
+    EXPECT(loaded.graph.edge_count() == 3);
+    EXPECT(loaded.graph.has_weights());
+    EXPECT(loaded.graph.weight(loaded.graph.edge_begin(0)) == 2.5);
+}
+void edge_list_loader_reports_the_offending_line() {  // :115
+    const std::string path = tmp_file("bad.txt");
+    write_file(path, "0 1\nnonsense here\n");
+    bool named = false;
+    try {
+        load_edge_list(path);
+    } catch (const ParseError& e) {
+        named = std::string(e.what()).find(":2") != std::string::npos;
+    }
+    EXPECT(named);
+    write_file(path, "0 1 1.0 2 9\n");
+    EXPECT_THROWS(load_edge_list(path), ParseError);
+    write_file(path, "# only comments\n");
+    EXPECT_THROWS(load_edge_list(path), ParseError);
+    write_file(path, "0 1\n");
+    EdgeListOptions needs_weights;
+    needs_weights.weights = WeightMode::FromFile;
+    EXPECT_THROWS(load_edge_list(path, needs_weights), ParseError);
+}
+void sparse_ids_are_remapped_densely_in_ascending_order() {  // :138
+    const std::string path = tmp_file("sparse.txt");
+    write_file(path, "100 7\n7 42\n42 100\n");
+    LoadedGraph loaded = load_edge_list(path);
+    EXPECT(loaded.graph.vertex_count() == 3);
+    EXPECT(loaded.original_ids.size() == 3);
+    if (loaded.original_ids.size() == 3) {
+        EXPECT(loaded.original_ids[0] == 7);
+        EXPECT(loaded.original_ids[1] == 42);
+        EXPECT(loaded.original_ids[2] == 100);
+    }
+    EXPECT(scan_edge(loaded.graph, 2, 0));  // 100 -> 7 becomes 2 -> 0
+}
+void undirected_mode_emits_both_directions() {  // :152
+    const std::string path = tmp_file("undirected.txt");
+    write_file(path, "0 1\n1 2\n");
+    EdgeListOptions options;
+    options.directedness = Directedness::Undirected;
+    LoadedGraph loaded = load_edge_list(path, options);
+    EXPECT(loaded.graph.edge_count() == 4);
+    EXPECT(scan_edge(loaded.graph, 1, 0));
+    EXPECT(scan_edge(loaded.graph, 2, 1));
+}
+void random_attributes_are_a_pure_function_of_the_seed() {  // :164
+    const std::string path = tmp_file("edges3.txt");
+    write_file(path, "0 1\n1 2\n2 0\n");
+    EdgeListOptions options;
+    options.weights = WeightMode::Random;
+    options.labels = LabelMode::Random;
+    options.label_count = 3;
+    options.seed = 99;
+    LoadedGraph first = load_edge_list(path, options);
+    LoadedGraph second = load_edge_list(path, options);
+    const std::string a = tmp_file("ra.wfg"), b = tmp_file("rb.wfg");
+    first.graph.write_binary(a);
+    second.graph.write_binary(b);
+    EXPECT(read_file(a) == read_file(b));
+    for (uint64_t e = 0; e < first.graph.edge_count(); ++e) {
+        const double w = first.graph.weight(e);
+        EXPECT(w >= 1.0);
+        EXPECT(w < 5.0);
+        EXPECT(first.graph.label(e) < 3);
+    }
+}
+void attribute_access_on_a_bare_graph_is_refused() {  // :190
+    Graph g = triangle();
+    EXPECT(!g.has_weights());
+    EXPECT_THROWS(g.weight(0), ConfigError);
+    EXPECT_THROWS(g.label(0), ConfigError);
+}
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+    g_tmp = argc > 1 ? argv[1] : "/tmp";
     const std::vector<std::pair<const char*, std::function<void()>>> cases = {
         {"engine: fixed-length walks hit their target exactly", fixed_length_walks_hit_their_target_exactly},
         {"engine: target length one completes without a single move",
@@ -700,6 +857,23 @@ int main() {
          uniform_fixed_length_walks_need_no_weights_at_all},
         {"algorithms: each program lands on its expected default sampling method",
          each_program_lands_on_its_expected_default_sampling_method},
+        {"graph: csr assembly sorts adjacency and keeps attributes aligned",
+         csr_assembly_sorts_adjacency_and_keeps_attributes_aligned},
+        {"graph: edge existence via binary search", edge_existence_via_binary_search},
+        {"graph: degree-zero vertices are just dead ends, not errors",
+         degree_zero_vertices_are_just_dead_ends_not_errors},
+        {"graph: from_csr validates structure", from_csr_validates_structure},
+        {"graph: binary files round-trip bit-exactly", binary_files_round_trip_bit_exactly},
+        {"graph: binary reader rejects corruption", binary_reader_rejects_corruption},
+        {"graph: edge list loader handles comments, blanks, and weights",
+         edge_list_loader_handles_comments_blanks_and_weights},
+        {"graph: edge list loader reports the offending line", edge_list_loader_reports_the_offending_line},
+        {"graph: sparse ids are remapped densely in ascending order",
+         sparse_ids_are_remapped_densely_in_ascending_order},
+        {"graph: undirected mode emits both directions", undirected_mode_emits_both_directions},
+        {"graph: random attributes are a pure function of the seed",
+         random_attributes_are_a_pure_function_of_the_seed},
+        {"graph: attribute access on a bare graph is refused", attribute_access_on_a_bare_graph_is_refused},
     };
     int failed = 0;
     for (auto& [name, fn] : cases) {

@@ -1,6 +1,6 @@
-"""The reference's own "engine", "interleave" and "algorithms" unit suites
-(/root/reference/proj/tests/test_engine.cpp, test_interleave.cpp,
-test_algorithms.cpp) re-expressed
+"""The reference's own "engine", "interleave", "algorithms" and "graph" unit
+suites (/root/reference/proj/tests/test_engine.cpp, test_interleave.cpp,
+test_algorithms.cpp, test_graph.cpp) re-expressed
 against the drop-in shim (tests/cpp/ref_suite.cpp: same case names and call
 patterns, custom programs as device programs) compiled with plain g++ the way a
 reference caller would, and run on the GPU."""
@@ -35,11 +35,12 @@ def test_ref_suite_compiles_cpu_only():
 def test_reference_engine_and_interleave_suites_pass_through_the_shim():
     with tempfile.TemporaryDirectory() as d:
         exe = build_suite(d)
-        p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+        p = subprocess.run([exe, d], capture_output=True, text=True, timeout=900)
     lines = p.stdout.strip().splitlines()
     failed = [ln for ln in lines if ln.startswith("FAIL") or ln.startswith("    ")]
     assert p.returncode == 0 and not failed, p.stdout[-4000:] + p.stderr[-2000:]
-    assert lines[-1] == "30 cases, 0 failed", lines[-1]
+    assert lines[-1] == "42 cases, 0 failed", lines[-1]
     assert sum((ln.startswith("ok") and " engine: " in ln) for ln in lines) == 14
     assert sum((ln.startswith("ok") and " interleave: " in ln) for ln in lines) == 8
     assert sum((ln.startswith("ok") and " algorithms: " in ln) for ln in lines) == 8
+    assert sum((ln.startswith("ok") and " graph: " in ln) for ln in lines) == 12
