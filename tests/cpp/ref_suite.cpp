@@ -20,6 +20,8 @@
 #define WALKFORGE_B200_DROP_IN
 #include "walkforge_b200/engine.hpp"
 
+#include "mini_check.hpp"
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -54,30 +56,6 @@ struct AvoidVertexObj {
 struct NegativeObj {
     uint32_t unused;
 };
-
-int g_failed_checks = 0;
-#define EXPECT(cond)                                                         \
-    do {                                                                     \
-        if (!(cond)) {                                                       \
-            std::printf("    line %d: expected %s\n", __LINE__, #cond);      \
-            ++g_failed_checks;                                               \
-        }                                                                    \
-    } while (0)
-#define EXPECT_THROWS(expr, Type)                                            \
-    do {                                                                     \
-        bool caught_ = false;                                                \
-        try {                                                                \
-            (void)(expr);                                                    \
-        } catch (const Type&) {                                              \
-            caught_ = true;                                                  \
-        } catch (const std::exception& e_) {                                 \
-            std::printf("    line %d: %s threw %s\n", __LINE__, #expr, e_.what()); \
-        }                                                                    \
-        if (!caught_) {                                                      \
-            std::printf("    line %d: expected %s from %s\n", __LINE__, #Type, #expr); \
-            ++g_failed_checks;                                               \
-        }                                                                    \
-    } while (0)
 
 using EdgeList = std::vector<std::pair<VertexId, VertexId>>;
 
@@ -875,19 +853,5 @@ int main(int argc, char** argv) {
          random_attributes_are_a_pure_function_of_the_seed},
         {"graph: attribute access on a bare graph is refused", attribute_access_on_a_bare_graph_is_refused},
     };
-    int failed = 0;
-    for (auto& [name, fn] : cases) {
-        const int before = g_failed_checks;
-        try {
-            fn();
-        } catch (const std::exception& e) {
-            std::printf("    unexpected exception: %s\n", e.what());
-            ++g_failed_checks;
-        }
-        const bool ok = g_failed_checks == before;
-        std::printf("%s %s\n", ok ? "ok  " : "FAIL", name);
-        failed += ok ? 0 : 1;
-    }
-    std::printf("%zu cases, %d failed\n", cases.size(), failed);
-    return failed;
+    return run_cases(cases);
 }

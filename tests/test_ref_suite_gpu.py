@@ -16,10 +16,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROGRAMS = os.path.join(ROOT, "tests", "programs")
 
 
-def build_suite(tmp):
-    exe = os.path.join(tmp, "ref_suite")
+def build_suite(tmp, name="ref_suite"):
+    exe = os.path.join(tmp, name)
     subprocess.check_call(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
-                           os.path.join(ROOT, "tests", "cpp", "ref_suite.cpp"), "-o", exe,
+                           os.path.join(ROOT, "tests", "cpp", name + ".cpp"), "-o", exe, "-lpthread",
                            "-L", os.path.dirname(E.LIB_PATH), "-lwalkforge_b200",
                            f"-Wl,-rpath,{os.path.dirname(E.LIB_PATH)}",
                            "-L", PROGRAMS, "-l:libwf_test_programs.so", f"-Wl,-rpath,{PROGRAMS}"])
@@ -44,3 +44,13 @@ def test_reference_engine_and_interleave_suites_pass_through_the_shim():
     assert sum((ln.startswith("ok") and " interleave: " in ln) for ln in lines) == 8
     assert sum((ln.startswith("ok") and " algorithms: " in ln) for ln in lines) == 8
     assert sum((ln.startswith("ok") and " graph: " in ln) for ln in lines) == 12
+
+
+def test_reference_output_suite_passes_on_the_shim_headers():
+    """test_output.cpp's ten cases against walkforge_b200/output.hpp (host-only: CPU suite)."""
+    with tempfile.TemporaryDirectory() as d:
+        exe = build_suite(d, "ref_output_suite")
+        p = subprocess.run([exe, d], capture_output=True, text=True, timeout=300)
+    lines = p.stdout.strip().splitlines()
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-1000:]
+    assert lines[-1] == "10 cases, 0 failed", lines[-1]
