@@ -75,6 +75,36 @@ enum class SamplerKind : uint8_t { Naive, Its, Alias, Rej, ORej };
 enum class WalkerType : uint8_t { Unbiased, Static, Dynamic };
 enum class WalkStatus : uint8_t { Complete, DeadEnd };
 
+// The reference's names for them (sampler.cpp:7-26, program.hpp:19-26,
+// walker.hpp:14-16): what its CLI prints and parses.
+inline const char* to_string(SamplerKind kind) {
+    switch (kind) {
+        case SamplerKind::Naive: return "naive";
+        case SamplerKind::Its: return "its";
+        case SamplerKind::Alias: return "alias";
+        case SamplerKind::Rej: return "rej";
+        case SamplerKind::ORej: return "orej";
+    }
+    return "?";
+}
+inline SamplerKind parse_sampler(const std::string& name) {
+    for (SamplerKind k : {SamplerKind::Naive, SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej, SamplerKind::ORej})
+        if (name == to_string(k)) return k;
+    if (name == "o-rej") return SamplerKind::ORej;
+    throw ConfigError("unknown sampler '" + name + "'");
+}
+inline const char* to_string(WalkerType type) {
+    switch (type) {
+        case WalkerType::Unbiased: return "unbiased";
+        case WalkerType::Static: return "static";
+        case WalkerType::Dynamic: return "dynamic";
+    }
+    return "?";
+}
+inline const char* to_string(WalkStatus status) { return status == WalkStatus::Complete ? "complete" : "dead_end"; }
+inline constexpr uint32_t kNoAlias = UINT32_MAX;      // sampler.hpp:26
+inline constexpr uint32_t kRejTrialCap = 1u << 20;    // sampler.hpp:27
+
 // ---- Graph (graph.hpp:17-107), resident in HBM ---------------------------------------
 class Graph {
 public:
@@ -343,13 +373,29 @@ struct RunResult {
 using BlockSink = std::function<void(uint32_t worker, WalkSet&& block)>;
 // prefetch.hpp:17 (same enumerators; software prefetch hints have no device meaning)
 enum class PrefetchLevel : uint8_t { L1, L2, L3, NonTemporal, Off };
+inline const char* to_string(PrefetchLevel level) {  // prefetch.hpp:30-39
+    switch (level) {
+        case PrefetchLevel::L1: return "l1";
+        case PrefetchLevel::L2: return "l2";
+        case PrefetchLevel::L3: return "l3";
+        case PrefetchLevel::NonTemporal: return "nta";
+        case PrefetchLevel::Off: return "off";
+    }
+    return "?";
+}
+inline PrefetchLevel parse_prefetch_level(const std::string& name) {  // prefetch.hpp:41-48
+    for (PrefetchLevel l : {PrefetchLevel::L1, PrefetchLevel::L2, PrefetchLevel::L3, PrefetchLevel::NonTemporal,
+                            PrefetchLevel::Off})
+        if (name == to_string(l)) return l;
+    throw ConfigError("unknown prefetch level '" + name + "' (l1|l2|l3|nta|off)");
+}
 struct ExecOptions {
     uint32_t threads = 1;
     uint64_t seed = 0;
     std::optional<SamplerKind> sampler;
     bool use_static_tables = true;
     PrefetchLevel prefetch = PrefetchLevel::L1;
-    uint32_t rej_trial_cap = 1u << 20;
+    uint32_t rej_trial_cap = kRejTrialCap;
     BlockSink sink;
 };
 

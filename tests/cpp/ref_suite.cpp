@@ -621,6 +621,16 @@ void each_program_lands_on_its_expected_default_sampling_method() {  // :206
     EXPECT(resolve_default_sampler(Node2VecProgram(g, {}, false)) == SamplerKind::ORej);
     EXPECT(resolve_default_sampler(MetaPathProgram(g, {0, 1})) == SamplerKind::Its);
     EXPECT(resolve_default_sampler(UniformProgram(3)) == SamplerKind::Naive);
+    // the names the reference CLI prints and parses (sampler.cpp:7-26, prefetch.hpp:30-48)
+    for (SamplerKind k : {SamplerKind::Naive, SamplerKind::Its, SamplerKind::Alias, SamplerKind::Rej, SamplerKind::ORej})
+        EXPECT(parse_sampler(to_string(k)) == k);
+    EXPECT(parse_sampler("o-rej") == SamplerKind::ORej);
+    EXPECT_THROWS(parse_sampler("fastest"), ConfigError);
+    EXPECT(parse_prefetch_level("nta") == PrefetchLevel::NonTemporal);
+    EXPECT_THROWS(parse_prefetch_level("l9"), ConfigError);
+    EXPECT(std::string(to_string(WalkStatus::DeadEnd)) == "dead_end");
+    EXPECT(std::string(to_string(WalkerType::Dynamic)) == "dynamic");
+    EXPECT(ExecOptions{}.rej_trial_cap == kRejTrialCap);
 }
 
 // ---- suite "graph" (test_graph.cpp) ---------------------------------------------------------
