@@ -79,17 +79,20 @@ class DeviceGraph:
     def from_host(cls, g: Graph, device: int = 0) -> "DeviceGraph":
         lib = load_library()
         h = _vp()
-        lab = None if g.labels is None else g.labels.astype(np.uint32)
-        if g.weights is not None and g.weights.dtype == np.float64:
+        # Graph::from_csr takes vectors: an empty attribute array means "absent"
+        # (graph.cpp:118-159), which only shows on a graph without edges
+        weights = g.weights if g.weights is not None and g.weights.size else None
+        lab = None if g.labels is None or g.labels.size == 0 else g.labels.astype(np.uint32)
+        if weights is not None and weights.dtype == np.float64:
             # the reference's f64 weights (wf_graph_create_f64)
-            w = np.ascontiguousarray(g.weights)
+            w = np.ascontiguousarray(weights)
             _check(lib.wf_graph_create_f64(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
                                            w.ctypes.data_as(C.POINTER(C.c_double)), _ptr(lab, _u32p),
                                            C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),
                                            C.c_int(device), C.byref(h)))
             return cls(h)
         _check(lib.wf_graph_create(_ptr(g.offsets, _u64p), _ptr(g.neighbors, _u32p),
-                                   _ptr(g.weights, _f32p), _ptr(lab, _u32p),
+                                   _ptr(weights, _f32p), _ptr(lab, _u32p),
                                    C.c_uint32(g.vertex_count), C.c_uint64(g.edge_count),
                                    C.c_int(device), C.byref(h)))
         return cls(h)

@@ -7,6 +7,8 @@
   engine (oracle/_ref) or the C restatement on the same CSR — bit-exact walks;
 * size-independent properties at full BASELINE sizes (tests/test_configs_gpu.py).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -703,3 +705,18 @@ def test_trial_cap_outcome_matches_reference(rmat12, cap, sampler):
         got = E.run_sequential(dg, spec, prog, opts)
         assert got.walks.first_mismatch(want.walks) is None
         assert got.metrics.total_steps == want.metrics.total_steps
+
+
+def test_randomised_differential_parity_sample():
+    """tools/fuzz_parity.py: random graphs (hubs, multi-edges, weight families,
+    labels) x programs x samplers x layouts x query specs against the
+    unmodified reference — outcome class, every walk, the step total.  A
+    sample here; profiles/r02_fuzz_parity.log holds the 15 k-case runs."""
+    import subprocess
+    import sys
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "--cases", "250",
+                        "--seed", "5"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "250 cases (seed 5), 0 differing" in p.stdout, p.stdout[-3000:] + p.stderr[-2000:]
