@@ -55,6 +55,32 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     return lib
 
 
+_nccl_preloaded = False
+
+
+def _preload_nccl() -> None:
+    """The library dlopens "libnccl.so.2" at the first multi-device / communicator
+    call and takes whatever is already loaded under that SONAME.  In a Python
+    process that later imports torch, loading the SYSTEM libnccl first would
+    leave torch resolving its own (newer) NCCL symbols against it and failing
+    to import: so load the NCCL torch ships (site-packages/nvidia/nccl) first
+    when it exists.  No torch NCCL: the system library, as before."""
+    global _nccl_preloaded
+    if _nccl_preloaded:
+        return
+    _nccl_preloaded = True
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations if spec else []):
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                C.CDLL(cand, mode=C.RTLD_GLOBAL)
+                return
+    except Exception:
+        pass
+
+
 def _check(rc: int) -> None:
     if rc != 0:
         raise_for(rc, (_lib.wf_last_error() or b"").decode())
@@ -535,6 +561,7 @@ class MultiDevice:
         self._copts = self.opts.to_c()
         devs = (C.c_int32 * len(devices))(*devices)
         h = _vp()
+        _preload_nccl()
         lib = load_library()
         if isinstance(prog, host_mod.DeviceProgram):
             _check(lib.wf_multi_create_custom(graph.h, devs, C.c_uint32(len(devices)), _vp(prog.ops),
@@ -567,6 +594,7 @@ class MultiDevice:
         offs = [np.zeros(1, np.uint64)]
         verts, stats, order = [], [], []
         err = []
+        total = [0]  # vertices delivered so far (a worker block may be empty)
 
         def tramp(_user, w, q0, q1, rec, vp, nv):
             try:
@@ -578,7 +606,8 @@ class MultiDevice:
                 o = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
                 if on_block is not None:
                     on_block(w, q0, q1, WalkSet(o, v, st))
-                offs.append(o[1:] + offs[-1][-1])
+                offs.append(o[1:] + np.uint64(total[0]))
+                total[0] += int(o[-1])
                 verts.append(v)
                 stats.append(st)
                 return 0
@@ -613,12 +642,14 @@ class Comm:
     @staticmethod
     def unique_id() -> bytes:
         buf = (C.c_uint8 * Comm.ID_BYTES)()
+        _preload_nccl()
         _check(load_library().wf_comm_unique_id(buf))
         return bytes(buf)
 
     def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
         buf = (C.c_uint8 * Comm.ID_BYTES)(*uid)
         h = _vp()
+        _preload_nccl()
         _check(load_library().wf_comm_create(buf, C.c_int32(nranks), C.c_int32(rank), C.c_int32(device),
                                              C.byref(h)))
         self.h = h
@@ -636,6 +667,7 @@ class Comm:
 
 
 def nccl_version() -> int:
+    _preload_nccl()
     v = C.c_int32()
     _check(load_library().wf_nccl_version(C.byref(v)))
     return v.value

@@ -116,3 +116,18 @@ def test_comm_allreduce_one_rank():
     comm.allreduce_u32(x.data_ptr(), x.numel(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert torch.equal(x.cpu(), torch.arange(1000, dtype=torch.int32))
+
+
+def test_more_workers_than_queries_delivers_empty_blocks(dg):
+    """worker_range gives some workers nothing when workers > queries (and all of
+    them nothing for an empty query set): every worker still gets its block, in
+    order, and the walks are the single-device run's (found by tools/fuzz_parity.py:
+    the Python block collector indexed into an empty offsets array)."""
+    prog, opts = DeepWalkProgram(12, True), ExecOptions(seed=9)
+    for spec, workers in [(QuerySpec.from_source(3, 2), 7), (QuerySpec.from_source(3, 0), 3),
+                          (QuerySpec.from_list(np.asarray([5, 1, 4], np.uint32)), 5)]:
+        m = E.MultiDevice(dg, [0, 0], prog, opts)
+        got, _, order = m.run(spec, workers=workers)
+        assert [w for w, _, _ in order] == list(range(workers))
+        want = E.run_sequential(dg, spec, prog, opts)
+        assert got.walks.first_mismatch(want.walks) is None and len(got.walks) == len(want.walks)

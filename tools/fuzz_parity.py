@@ -7,8 +7,9 @@ edges so the warp-cooperative gathered paths run, sorted or unsorted adjacency,
 multi-edges and self-loops, weights from several families — equal, small
 integers, U[1,5) f32, mixed scales, zeros, f64 not float32-exact — and labels),
 a program, a sampling method, static tables on/off, a query spec and a seed,
-runs it on the engine (device walk set and, every other case, the host-streaming
-records path) and on the reference, and compares outcome class (same exception
+runs it on the engine (device walk set; every third case also the host-streaming
+path with a random chunk size, every third the worker blocks over devices
+[0] / [0, 0] with PPR's visit counts) and on the reference, and compares outcome class (same exception
 or none), every walk and the step total.  Test infrastructure: the reference is
 the checker.  Exit code = number of differing cases.
 """
@@ -148,9 +149,15 @@ def main():
                                  abi.LAYOUT_NO_MP_SUCC]))
         opts = ExecOptions(seed=int(rng.integers(0, 1 << 40)), sampler=None if sampler is None else int(sampler),
                            use_static_tables=bool(rng.random() < 0.5),
-                           rej_trial_cap=int(rng.choice([1 << 20, 1 << 20, 64])), layout_flags=layout)
+                           rej_trial_cap=int(rng.choice([1 << 20, 1 << 20, 64])), layout_flags=layout,
+                           # PPR rows shorter than some walks: the overflow re-run path
+                           path_stride=int(rng.choice([0, 0, 4, 16])) if pname == "ppr" else 0)
+        chunk = int(rng.choice([0, 1, 256, 4096, 65536]))
+        workers = int(rng.integers(1, 8))
+        devices = [0, 0] if rng.random() < 0.5 else [0]
         desc = (f"case {case}: {meta} {pname} {sname} sampler={sampler} tables={opts.use_static_tables} "
-                f"cap={opts.rej_trial_cap} layout={layout} seed={opts.seed}")
+                f"cap={opts.rej_trial_cap} layout={layout} stride={opts.path_stride} chunk={chunk} workers={workers} "
+                f"devices={devices} seed={opts.seed}")
         try:
             rg = ref.graph(g)
             dg = E.DeviceGraph.from_host(g)
@@ -160,9 +167,19 @@ def main():
             if ok and want is not None:
                 ok = got.walks.first_mismatch(want.walks) is None and \
                     got.metrics.total_steps == want.metrics.total_steps
-            if ok and want is not None and case % 2 == 0:
-                herr, hres = outcome(lambda: E.Session(dg, prog, opts).run_to_numpy(spec))
+            if ok and want is not None and case % 3 == 0:  # host streaming (chunk = publication granularity)
+                herr, hres = outcome(lambda: E.Session(dg, prog, opts).run_to_numpy(spec, chunk))
                 ok = herr is None and hres.walks.first_mismatch(want.walks) is None
+            if ok and want is not None and case % 3 == 1:  # worker blocks over devices, in worker order
+                is_ppr = pname == "ppr"
+                merr, mres = outcome(lambda: E.MultiDevice(dg, devices, prog, opts).run(spec, workers, counts=is_ppr))
+                ok = merr is None
+                if ok:
+                    res, cnt, order = mres
+                    ok = res.walks.first_mismatch(want.walks) is None and \
+                        [w for w, _, _ in order] == list(range(workers))
+                    if ok and is_ppr:
+                        ok = np.array_equal(cnt, np.bincount(want.walks.vertices, minlength=meta["V"]))
             errors[rerr] = errors.get(rerr, 0) + 1
             if not ok:
                 bad += 1
