@@ -142,3 +142,17 @@ def test_wfg1_format_errors():
                 E.DeviceGraph.read_wfg1(p)
         with pytest.raises(abi.IoError):
             E.DeviceGraph.read_wfg1(os.path.join(d, "missing.wfg"))
+
+
+def test_randomised_edge_list_ingest_sample():
+    """tools/fuzz_ingest.py: random text edge lists (sparse 64-bit ids, comments,
+    blanks, CRLF, number formats, a malformed line in a third of them) through
+    the device loader and the reference's load_edge_list: the same error class
+    and message, or the same CSR, attributes, original ids and WFG1 bytes.  A
+    sample here; profiles/r02_fuzz_ingest.log holds the 8 k-case runs."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_ingest.py"), "--cases", "300",
+                        "--seed", "9"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "300 cases (seed 9), 0 differing" in p.stdout, p.stdout[-3000:] + p.stderr[-2000:]

@@ -9,13 +9,15 @@ integers, U[1,5) f32, mixed scales, zeros, f64 not float32-exact — and labels)
 a program, a sampling method, static tables on/off, a query spec and a seed,
 runs it on the engine (device walk set; every third case also the host-streaming
 path with a random chunk size, every third the worker blocks over devices
-[0] / [0, 0] with PPR's visit counts) and on the reference, and compares outcome class (same exception
+[0] / [0, 0] with PPR's visit counts, every fifth the encoded walk file,
+text or binary, against the reference writer's bytes) and on the reference, and compares outcome class (same exception
 or none), every walk and the step total.  Test infrastructure: the reference is
 the checker.  Exit code = number of differing cases.
 """
 import argparse
 import os
 import sys
+import tempfile
 import time
 import traceback
 
@@ -180,6 +182,12 @@ def main():
                         [w for w, _, _ in order] == list(range(workers))
                     if ok and is_ppr:
                         ok = np.array_equal(cnt, np.bincount(want.walks.vertices, minlength=meta["V"]))
+            if ok and want is not None and case % 5 == 2:  # the qid-ordered file (wf_walkset_write) vs the reference writer
+                fmt = int(case // 5) & 1
+                with tempfile.TemporaryDirectory() as td:
+                    fp = os.path.join(td, "walks.out")
+                    E.Session(dg, prog, opts).run(spec).write(fp, fmt)
+                    ok = open(fp, "rb").read() == rg.run_encoded(spec, prog, opts, fmt)
             errors[rerr] = errors.get(rerr, 0) + 1
             if not ok:
                 bad += 1
