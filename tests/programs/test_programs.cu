@@ -29,7 +29,8 @@ struct CountingProgram {
         atomicAdd(updates, 1ull);
         return q.path_size() >= length;
     }
-    __host__ __device__ uint32_t max_path_vertices() const { return length; }
+    // no finished(): a walk always makes one move, so length 1 still emits two vertices
+    __host__ __device__ uint32_t max_path_vertices() const { return length < 2 ? 2 : length; }
 };
 
 struct AvoidVertexProgram {
@@ -42,7 +43,8 @@ struct AvoidVertexProgram {
     }
     __device__ bool update(wfd::WalkerView& q, const wfd::EdgeRef&) const { return q.path_size() >= length; }
     __host__ __device__ double max_weight() const { return 1.0; }
-    __host__ __device__ uint32_t max_path_vertices() const { return length; }
+    // no finished(): a walk always makes one move, so length 1 still emits two vertices
+    __host__ __device__ uint32_t max_path_vertices() const { return length < 2 ? 2 : length; }
 };
 
 struct NegativeWeightProgram {

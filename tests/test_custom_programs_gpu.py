@@ -178,3 +178,14 @@ def test_custom_session_rejects_illegal_pairings(graphs):
         E.Session(dg, dyn, ExecOptions(sampler=int(abi.Sampler.NAIVE)))
     with pytest.raises(abi.ConfigError):  # O-REJ needs max_weight() (engine.hpp:103-114)
         E.Session(dg, dyn, ExecOptions(sampler=int(abi.Sampler.OREJ)))
+
+
+def test_randomised_custom_program_parity_sample():
+    """tools/fuzz_custom.py: the test programs on random graphs x samplers x
+    tables x specs against the reference running the same programs (walks, step
+    total, update() count).  A sample; profiles/r02_fuzz_custom.log holds 4000."""
+    import subprocess
+    import sys
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_custom.py"), "--cases", "200",
+                        "--seed", "7"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "200 cases (seed 7), 0 differing" in p.stdout, p.stdout[-3000:] + p.stderr[-2000:]
