@@ -198,6 +198,37 @@ def test_c4_metapath_s22_full_size(s22):
             assert walk_digest(_host_slice(got, a, min(n, a + block)), a) == int(want[b]), f"block {b}"
 
 
+@pytest.mark.parametrize("name", ["g1_node2vec_its", "g2_metapath_alias", "g3_deepwalk_alias_untabled"])
+def test_gathered_flows_on_s22_hubs_match_reference(s22, name):
+    """bench.py's gathered configs G1-G3 at their real size: per-step gathers over
+    R-MAT s22's hubs (up to ~160 k edges: many staging batches, long Vose chains,
+    the Node2Vec merge against hub lists) for 8192 walks from random sources,
+    walk by walk against the unmodified reference."""
+    from paper_2107_11983_b200 import abi
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    dg, hg = s22
+    assert np.diff(hg.offsets).max() > 100_000
+    prog, opts = {
+        "g1_node2vec_its": (Node2VecProgram(2.0, 0.5, 80, False), ExecOptions(seed=1, sampler=int(abi.Sampler.ITS))),
+        "g2_metapath_alias": (MetaPathProgram([i % 5 for i in range(79)]),
+                              ExecOptions(seed=1, sampler=int(abi.Sampler.ALIAS))),
+        "g3_deepwalk_alias_untabled": (DeepWalkProgram(80, True),
+                                       ExecOptions(seed=1, sampler=int(abi.Sampler.ALIAS), use_static_tables=False)),
+    }[name]
+    src = np.random.default_rng(22).integers(0, hg.vertex_count, 8192, dtype=np.uint32)
+    spec = QuerySpec.from_list(src)
+    sess = E.Session(dg, prog, opts)
+    assert sess.describe()[1] == abi.Flow.GATHERED
+    got = E.run_sequential(dg, spec, prog, opts)
+    want = RefOracle().graph(hg).run(spec, prog, ExecOptions(seed=1, sampler=opts.sampler,
+                                                             use_static_tables=opts.use_static_tables,
+                                                             threads=os.cpu_count()))
+    bad = got.walks.first_mismatch(want.walks)
+    assert bad is None, f"walk {bad} differs"
+    assert got.metrics.total_steps == want.metrics.total_steps
+
+
 def _replay_deepwalk_alias(hg, port, qid, length, seed, cache):
     """DeepWalk on static ALIAS tables (engine.hpp:379-384, 423-424; sampler.hpp
     89-120): x = uniform_index(d), y = uniform_real(1.0), first if y < split."""
