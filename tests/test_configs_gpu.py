@@ -282,6 +282,20 @@ def test_c5_deepwalk_s26_full_size():
         rg = RefOracle().graph(hg)
         del hg.weights  # the reference holds its own f64 copy now
         _digest_parity(rg, ws, QuerySpec.one_per_vertex(), prog, opts, V)
+        # per-step gathers at this graph's hubs (up to ~1 M edges: the warp rows
+        # are budgeted, the Vose chain runs over thousands of staging batches),
+        # 256 walks from random sources, walk by walk
+        from paper_2107_11983_b200 import abi
+        assert deg.max() > 500_000
+        gspec = QuerySpec.from_list(np.random.default_rng(7).integers(0, V, 256, dtype=np.uint32))
+        for sampler in (abi.Sampler.ALIAS, abi.Sampler.ITS, abi.Sampler.REJ):
+            gopts = ExecOptions(seed=3, sampler=int(sampler), use_static_tables=False)
+            gprog = DeepWalkProgram(40, True)
+            got = E.run_sequential(dg, gspec, gprog, gopts)
+            want = rg.run(gspec, gprog, ExecOptions(seed=3, sampler=int(sampler), use_static_tables=False,
+                                                    threads=os.cpu_count()))
+            bad = got.walks.first_mismatch(want.walks)
+            assert bad is None, f"gathered {sampler.name}: walk {bad} differs"
         del rg
         hg = dg.download()
     # sampled parity against a replay from the reference's primitives
