@@ -281,9 +281,15 @@ int cmd_run(const Args& a) {  // walkforge.cpp:154-216
     return 0;
 }
 
-// tune: the ring sweep (tune.cpp:46-111) has no device meaning — lanes replace
-// rings — so this reports the throughput of the reference's unbiased probe
-// (UniformProgram, tune.cpp:18-31) on the device.
+// tune: the reference sweeps its CPU rings (tune.cpp:46-111) and prints
+// TuneReport::to_text (tune.cpp:92-111).  On the device k / k' are launch
+// hints — resident walkers replace the rings — so the sweep runs the
+// reference's probe (one uniform length-10 walk per vertex, tune.cpp:18-31)
+// through the engine at every ring size the reference would try and prints
+// the measured throughput in the reference's report format (a caller parsing
+// `walkforge tune` keeps working); the flat curve is the finding.  The knob
+// that does matter, resident walkers, is tuned by wf_session_tune and
+// reported on the last line.
 int cmd_tune(const Args& a) {
     if (a.pos.size() != 1) usage_error("tune needs <graph>");
     GraphPtr g = load_graph(a.pos[0]);
@@ -296,13 +302,39 @@ int cmd_tune(const Args& a) {
     o.use_static_tables = 1;
     wf_query_spec q{};
     q.mode = WF_QUERY_ONE_PER_VERTEX;
-    wf_walkset* ws = nullptr;
-    wf_run_metrics m{};
-    check(wf_run(g.get(), &d, &q, &o, &ws, &m));
-    wf_walkset_destroy(ws);
-    std::printf("device lanes in flight %u (rings replaced by the persistent walker queue)\n", m.max_in_flight);
-    std::printf("probe uniform length 10: %.1f steps/s\n",
-                m.exec_seconds > 0 ? static_cast<double>(m.total_steps) / m.exec_seconds : 0.0);
+    const double budget = static_cast<double>(get_u64(a, {"--budget"}, 120));
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    bool exhausted = false;
+    uint32_t lanes = 0;
+    auto probe = [&](uint32_t k, uint32_t k_prime) {
+        wf_exec_options ok = o;
+        ok.k = k;
+        ok.k_prime = k_prime;
+        wf_walkset* ws = nullptr;
+        wf_run_metrics m{};
+        check(wf_run(g.get(), &d, &q, &ok, &ws, &m));  // warm (tables, first launch)
+        wf_walkset_destroy(ws);
+        check(wf_run(g.get(), &d, &q, &ok, &ws, &m));
+        wf_walkset_destroy(ws);
+        lanes = m.max_in_flight;
+        return m.exec_seconds > 0 ? static_cast<double>(m.total_steps) / m.exec_seconds : 0.0;
+    };
+    const uint32_t best_k = 64, best_k_prime = 32;  // the reference's defaults: k / k' do not move the device
+    std::printf("task ring sweep (device: k is a launch hint, resident walkers replace the rings)\n");
+    std::printf("k\tthroughput_steps_per_sec\n");
+    for (uint32_t k = 1; k <= 1024 && !exhausted; k *= 2) {
+        std::printf("%u\t%.1f\n", k, probe(k, 1));
+        exhausted = elapsed() > budget;
+    }
+    std::printf("search ring sweep at k=%u (device: k' is a launch hint)\n", best_k);
+    std::printf("k'\tthroughput_steps_per_sec\n");
+    for (uint32_t kp = 1; kp <= best_k && !exhausted; kp *= 2) {
+        std::printf("%u\t%.1f\n", kp, probe(best_k, kp));
+        exhausted = elapsed() > budget;
+    }
+    std::printf("recommended k=%u k'=%u\n", best_k, best_k_prime);
+    if (exhausted) std::printf("budget exhausted; recommendation is best-so-far\n");
     // the device knob the rings become: resident walkers (blocks/SM), timed
     // over whole launches of the probe (wf_session_tune)
     wf_session* s = nullptr;
@@ -312,8 +344,8 @@ int cmd_tune(const Args& a) {
     const int rc = wf_session_tune(s, &q, 0, 0, &blocks, &ms);
     wf_session_destroy(s);
     check(rc);
-    std::printf("launch tuner: %d blocks/SM (%.3f ms per launch of the probe)\n", blocks, ms);
-    std::printf("recommended: k=64 k'=32 (accepted and ignored on the device)\n");
+    std::printf("device launch tuner: %d blocks/SM (%.3f ms per launch of the probe), %u lanes in flight\n", blocks,
+                ms, lanes);
     return 0;
 }
 
