@@ -183,7 +183,7 @@ def test_custom_session_rejects_illegal_pairings(graphs):
 def test_randomised_custom_program_parity_sample():
     """tools/fuzz_custom.py: the test programs on random graphs x samplers x
     tables x specs against the reference running the same programs (walks, step
-    total, update() count).  A sample; profiles/r02_fuzz_custom.log holds 4000."""
+    total, update() count).  A sample; profiles/r02_fuzz_custom.log holds 8000."""
     import subprocess
     import sys
     p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_custom.py"), "--cases", "200",

@@ -711,7 +711,7 @@ def test_randomised_differential_parity_sample():
     """tools/fuzz_parity.py: random graphs (hubs, multi-edges, weight families,
     labels) x programs x samplers x layouts x query specs against the
     unmodified reference — outcome class, every walk, the step total.  A
-    sample here; profiles/r02_fuzz_parity.log holds the 21 k-case runs."""
+    sample here; profiles/r02_fuzz_parity.log holds the 33 k-case runs."""
     import subprocess
     import sys
     if not ref_available():

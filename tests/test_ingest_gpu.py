@@ -149,7 +149,7 @@ def test_randomised_edge_list_ingest_sample():
     blanks, CRLF, number formats, a malformed line in a third of them) through
     the device loader and the reference's load_edge_list: the same error class
     and message, or the same CSR, attributes, original ids and WFG1 bytes.  A
-    sample here; profiles/r02_fuzz_ingest.log holds the 8 k-case runs."""
+    sample here; profiles/r02_fuzz_ingest.log holds the 16 k-case runs."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
